@@ -1,0 +1,293 @@
+/*
+ * oracle.c -- sequential CPU oracle for JP-ADG (arXiv 2008.11321).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_2008_11321_b200/) never links, imports or calls
+ * it, and shares no code, header or constant table with it.
+ *
+ * Plain, slow, obviously correct, single-threaded C.  All arithmetic is
+ * integer (the method fixes no floating point: SURVEY.md §8c Q2).  Each
+ * function cites the passage of /root/reference/PAPER.md it follows.
+ *
+ * Readings of the paper:
+ *   Q1  threshold uses "<=" (Alg. 1 line R_def; proof 769)
+ *   Q2  eps = num/den, test den*D[v]*|U| <= (den+num)*S exactly (128-bit)
+ *   Q3  D is the residual degree in G[U]; S = sum of D over U
+ *   Q6  rounds are 1-based (Alg. 1 "l = 1")
+ *   Q8  later ADG round = higher priority; larger hash wins inside a round
+ *   Q9  rho_R(v) = splitmix64(seed XOR v) (first output of a SplitMix64
+ *       generator whose state is seed^v); compared unsigned
+ *   Q11 colors are 1-based, 0 = uncolored
+ *   Q12 isolated vertices count in |U| (Count(U))
+ *
+ * Pins (tests/test_oracle_*.py): Appendix B worked examples, the ADG and JP
+ * certificate characterisations, Lemma 1 / Lemma 4 / Corollary 1 bounds,
+ * exact degeneracy, brute-force chromatic number, published SplitMix64
+ * output vectors, exhaustive enumeration of all graphs on <= 6 vertices.
+ * The choice of hash (Q9) is a convention, not a paper fact: "parity
+ * unpinned" for the choice itself.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_EXPORT __attribute__((visibility("default")))
+
+/* ------------------------------------------------------------------------ */
+/* rho_R: SplitMix64.  Written from the published definition:
+ *   z = x + 0x9E3779B97F4A7C15; z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9;
+ *   z = (z ^ (z >> 27)) * 0x94D049BB133111EB; return z ^ (z >> 31).        */
+ORC_EXPORT uint64_t orc_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+/* ------------------------------------------------------------------------ */
+/* ADG -- Algorithm 1.
+ *
+ *   D = [deg(v_1) ... deg(v_n)];  l = 1;  U = V               (676-677)
+ *   while U != {}:                                             (679)
+ *     |U| = Count(U);  cnt = Reduce(U) = sum_{v in U} D[v]     (680-681)
+ *     delta = cnt/|U|                                          (682)
+ *     R = { u in U : D[u] <= (1+eps) * delta }                 (685)
+ *     UPDATE(U, R, D): for v in R, u in N_U(v): D[u] -= 1      (686, 692-696)
+ *     U = U \ R                                                (687)
+ *     rho_ADG(v) = l for v in R                                (688-689)
+ *     l = l + 1                                                (690)
+ *
+ * With eps = num/den the test D[u] <= (1+eps)*cnt/|U| is, multiplied by the
+ * positive den*|U|:  den * D[u] * |U| <= (den + num) * cnt, in 128 bits.
+ * UPDATE runs before U = U \ R, so (literally) R-R edges are decremented
+ * too; those D values are never read again.
+ *
+ * Returns T (number of rounds), -1 on bad arguments, -2 if a round selects
+ * nothing (cannot happen for eps > 0: min degree <= mean).  Optional stats:
+ *   stats[0] = T, stats[1] = sum_l |U_l|, stats[2] = X = number of decrements
+ *   applied to vertices that survive the round (cross-round edges),
+ *   stats[3] = total decrements including R-R ones.
+ * Optional per-round arrays (capacity cap): nU[l-1], S[l-1], nR[l-1].       */
+ORC_EXPORT int orc_adg(int64_t n, const int64_t* off, const int32_t* col, uint32_t num,
+                       uint32_t den, int32_t* round_out, int64_t* stats, int64_t cap,
+                       int64_t* per_nU, int64_t* per_S, int64_t* per_nR) {
+  if (n < 0 || num == 0 || den == 0) return -1;
+  int64_t* D = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  char* inU = (char*)malloc((size_t)n + 1);
+  char* inR = (char*)malloc((size_t)n + 1);
+  int64_t* U = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));   /* list of U */
+  int64_t sizeU = n;
+  for (int64_t v = 0; v < n; ++v) {
+    D[v] = off[v + 1] - off[v];
+    inU[v] = 1;
+    inR[v] = 0;
+    U[v] = v;
+    round_out[v] = 0;
+  }
+  int64_t l = 1, sum_active = 0, cross = 0, all_dec = 0;
+  while (sizeU > 0) {
+    /* Count and Reduce over U (680-681) */
+    int64_t countU = 0;
+    uint64_t cnt = 0;
+    for (int64_t i = 0; i < sizeU; ++i) {
+      countU += 1;
+      cnt += (uint64_t)D[U[i]];
+    }
+    sum_active += countU;
+    /* R = { u in U : D[u] <= (1+eps) * cnt / |U| }  (685), exact */
+    int64_t sizeR = 0;
+    for (int64_t i = 0; i < sizeU; ++i) {
+      int64_t u = U[i];
+      unsigned __int128 lhs = (unsigned __int128)den * (uint64_t)D[u] * (uint64_t)countU;
+      unsigned __int128 rhs = ((unsigned __int128)den + num) * cnt;
+      if (lhs <= rhs) { inR[u] = 1; ++sizeR; }
+    }
+    if (sizeR == 0) {   /* impossible by Lemma 1 (the minimum is <= the mean); guard */
+      free(D); free(inU); free(inR); free(U);
+      return -2;
+    }
+    if (l - 1 < cap) {
+      if (per_nU) per_nU[l - 1] = countU;
+      if (per_S) per_S[l - 1] = (int64_t)cnt;
+      if (per_nR) per_nR[l - 1] = sizeR;
+    }
+    /* UPDATE(U, R, D) (692-696): for v in R, for u in N_U(v): DecrementAndFetch(D[u]) */
+    for (int64_t i = 0; i < sizeU; ++i) {
+      int64_t v = U[i];
+      if (!inR[v]) continue;
+      for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+        int64_t u = col[e];
+        if (inU[u]) {
+          D[u] -= 1;
+          all_dec += 1;
+          if (!inR[u]) cross += 1;
+        }
+      }
+    }
+    /* U = U \ R (687); rho_ADG(v) = l for v in R (688-689) */
+    int64_t k = 0;
+    for (int64_t i = 0; i < sizeU; ++i) {
+      int64_t v = U[i];
+      if (inR[v]) {
+        inU[v] = 0;
+        inR[v] = 0;
+        round_out[v] = (int32_t)l;
+      } else {
+        U[k++] = v;
+      }
+    }
+    sizeU = k;
+    l += 1;   /* (690) */
+  }
+  free(D);
+  free(inU);
+  free(inR);
+  free(U);
+  if (stats) {
+    stats[0] = l - 1;
+    stats[1] = sum_active;
+    stats[2] = cross;
+    stats[3] = all_dec;
+  }
+  return (int)(l - 1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* JP priority rho = <rho_ADG, rho_R>, lexicographic (PAPER.md:1073-1078,
+ * 1095-1096): u has higher priority than v iff
+ *   round[u] > round[v], or round[u] == round[v] and h(u) > h(v),
+ * with h(x) = splitmix64(seed ^ x) compared as unsigned 64-bit.              */
+static uint64_t g_seed;
+static const int32_t* g_round;
+
+static int higher(int64_t u, int64_t v) {
+  if (g_round[u] != g_round[v]) return g_round[u] > g_round[v];
+  return orc_splitmix64(g_seed ^ (uint64_t)u) > orc_splitmix64(g_seed ^ (uint64_t)v);
+}
+
+static int cmp_desc(const void* a, const void* b) {
+  int64_t u = *(const int64_t*)a, v = *(const int64_t*)b;
+  if (u == v) return 0;
+  return higher(u, v) ? -1 : 1;
+}
+
+/* JP (Algorithm 3) evaluated as sequential greedy in
+ * decreasing priority: every predecessor of v (pred[v] = {u in N(v) :
+ * rho(u) > rho(v)}, 1118) precedes v, so when v is reached all of pred[v]
+ * is colored and GetColor (1135-1138) returns
+ *   min({1, ..., |pred[v]|+1} \ {C[u] : u in pred[v]}).
+ * This equals JP's output because JPColor colors v exactly once, after all
+ * of pred[v] (Join on count[v], 1130-1133), from pred colors alone.
+ *
+ * Returns K = max color (0 for n = 0), -1 on bad arguments.  Optional
+ * level_out[v] = 1 + max level over pred[v] (the JP DAG depth; J = max).   */
+ORC_EXPORT int orc_jp(int64_t n, const int64_t* off, const int32_t* col, const int32_t* round,
+                      uint64_t seed, int32_t* color_out, int32_t* level_out, int64_t* J_out) {
+  if (n < 0) return -1;
+  g_seed = seed;
+  g_round = round;
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t v = 0; v < n; ++v) order[v] = v;
+  qsort(order, (size_t)n, sizeof(int64_t), cmp_desc);
+  int64_t* stamp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 2));
+  for (int64_t i = 0; i < n + 2; ++i) stamp[i] = -1;
+  for (int64_t v = 0; v < n; ++v) color_out[v] = 0;   /* C = [0 0 ... 0] (1115) */
+  int32_t K = 0;
+  int64_t J = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t v = order[i];
+    int64_t npred = 0, lvl = 0;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+      int64_t u = col[e];
+      if (higher(u, v)) {                  /* u in pred[v] */
+        npred += 1;
+        stamp[color_out[u]] = i;           /* C = C - {C[u]} */
+        if (level_out && level_out[u] > lvl) lvl = level_out[u];
+      }
+    }
+    int64_t c = 1;                         /* min of {1..|pred|+1} \ used */
+    while (c <= npred + 1 && stamp[c] == i) ++c;
+    color_out[v] = (int32_t)c;
+    if (c > K) K = (int32_t)c;
+    if (level_out) {
+      level_out[v] = (int32_t)(lvl + 1);
+      if (lvl + 1 > J) J = lvl + 1;
+    }
+  }
+  free(order);
+  free(stamp);
+  if (J_out) *J_out = J;
+  return K;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Exact degeneracy d: the smallest-last peel of Matula and
+ * Beck -- repeatedly remove a vertex of minimum residual degree; d is the
+ * largest minimum seen.  Bucket queue, O(n + m).                          */
+ORC_EXPORT int64_t orc_degeneracy(int64_t n, const int64_t* off, const int32_t* col) {
+  if (n <= 0) return 0;
+  int64_t maxdeg = 0;
+  int64_t* deg = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  for (int64_t v = 0; v < n; ++v) {
+    deg[v] = off[v + 1] - off[v];
+    if (deg[v] > maxdeg) maxdeg = deg[v];
+  }
+  /* bucket sort vertices by degree: bin[d] = start of degree-d block */
+  int64_t* bin = (int64_t*)calloc((size_t)maxdeg + 2, sizeof(int64_t));
+  int64_t* pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t* vert = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  for (int64_t v = 0; v < n; ++v) bin[deg[v]]++;
+  int64_t start = 0;
+  for (int64_t d = 0; d <= maxdeg; ++d) { int64_t c = bin[d]; bin[d] = start; start += c; }
+  for (int64_t v = 0; v < n; ++v) { pos[v] = bin[deg[v]]; vert[pos[v]] = v; bin[deg[v]]++; }
+  for (int64_t d = maxdeg; d >= 1; --d) bin[d] = bin[d - 1];
+  bin[0] = 0;
+  int64_t dgn = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t v = vert[i];            /* a vertex of minimum residual degree */
+    if (deg[v] > dgn) dgn = deg[v];
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+      int64_t u = col[e];
+      if (deg[u] > deg[v]) {        /* u not yet removed: move it down one bucket */
+        int64_t du = deg[u], pu = pos[u], pw = bin[du], w = vert[pw];
+        if (u != w) { pos[u] = pw; vert[pu] = w; pos[w] = pu; vert[pw] = u; }
+        bin[du]++;
+        deg[u]--;
+      }
+    }
+  }
+  free(deg);
+  free(bin);
+  free(pos);
+  free(vert);
+  return dgn;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Brute-force chromatic number (north star): the smallest k
+ * for which a backtracking search finds a proper k-coloring.  n <= 16.      */
+static int bt(int64_t v, int64_t n, const int64_t* off, const int32_t* col, int k, int* c) {
+  if (v == n) return 1;
+  for (int x = 1; x <= k; ++x) {
+    int ok = 1;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e)
+      if (col[e] < v && c[col[e]] == x) { ok = 0; break; }
+    if (!ok) continue;
+    c[v] = x;
+    if (bt(v + 1, n, off, col, k, c)) return 1;
+    c[v] = 0;
+  }
+  return 0;
+}
+
+ORC_EXPORT int orc_brute_chi(int64_t n, const int64_t* off, const int32_t* col) {
+  if (n < 0 || n > 16) return -1;
+  if (n == 0) return 0;
+  int c[16];
+  for (int k = 1; k <= n; ++k) {
+    memset(c, 0, sizeof(c));
+    if (bt(0, n, off, col, k, c)) return k;
+  }
+  return (int)n;
+}
