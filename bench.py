@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py -- JP-ADG (ADG ordering + Jones-Plassmann coloring) on B200.
+
+Metric (BASELINE.json): JP-ADG edges/sec (ADG+JP, 1 B200) and % HBM roofline;
+#colors.  One "step" = one full pgc_color_jp_adg call (every SURVEY.md §8(a)
+row: init, ADG rounds with fused JP Part 1, priority order, JP coloring) on a
+device-resident synthetic graph.  Default workload: R-MAT scale 24, edge
+factor 16, eps = 1/10 (BASELINE.json configs[3], the headline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat24] [--impl pgc|reference]
+
+N > 1 runs one independent replica per GPU (the path does not shard, DESIGN.md
+"Multi-GPU"): value = total edges colored by all ranks / max-over-ranks time.
+The reference arm (--impl reference) times the CPU oracle (oracle/), as it
+stands, on a bounded sample of the workload (see REF_SAMPLE).
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import graphgen as gg  # noqa: E402  (input harness: no method arithmetic)
+
+METRIC = "JP-ADG edges/sec (ADG+JP, 1 B200) and % HBM roofline; #colors"
+REF_SAMPLE = {"rmat24": ("rmat22", lambda: gg.rmat(22, 16, seed=1))}
+PROFILES = os.path.join(ROOT, "profiles")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["pgc", "reference"], default="pgc")
+    ap.add_argument("--config", default="rmat24", choices=sorted(gg.CONFIGS))
+    ap.add_argument("--eps", default=None, help="num/den (default: the config's first eps)")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline (for ncu runs)")
+    return ap.parse_args()
+
+
+def eps_of(args):
+    if args.eps:
+        a, b = args.eps.split("/")
+        return int(a), int(b)
+    return gg.CONFIGS[args.config][1][0]
+
+
+# ------------------------------------------------------------------ graph ---
+def _gen_hash():
+    h = hashlib.sha1(open(os.path.join(ROOT, "graphgen", "graphgen.c"), "rb").read())
+    h.update(open(os.path.join(ROOT, "graphgen", "__init__.py"), "rb").read())
+    return h.hexdigest()[:12]
+
+
+def load_graph(name, local_rank=0, barrier=None):
+    """Generate the config graph; ranks of one node share it via a /tmp cache
+    (setup only -- no timing or result depends on the cache)."""
+    path = f"/tmp/pgc_graph_{name}_{_gen_hash()}.npz"
+    if local_rank == 0 and not os.path.exists(path):
+        g = gg.config_graph(name)
+        tmp = path + f".{os.getpid()}.tmp.npz"
+        np.savez(tmp, off=g.off, col=g.col)
+        os.replace(tmp, path)
+    if barrier:
+        barrier()
+    if local_rank == 0 and name in gg._cache:
+        return gg._cache[name]
+    z = np.load(path)
+    return gg.Graph(int(len(z["off"]) - 1), z["off"], z["col"], name)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ model ---
+def algorithmic_bytes(n, nnz, m, X, sum_active):
+    """Bytes each kernel group must move (each logical access once, at its size,
+    no sector inflation, no cache credit).  DESIGN.md "Roofline model"."""
+    return {
+        "init": 8 * n + 12 * n,                                  # read off; write D, round, color
+        "select": 12 * sum_active + 20 * n,                      # U list + D + list write; round + offsets of R
+        "update": 24 * n + 8 * nnz + 8 * X + 4 * m,              # R entry+offsets+npred; col+round per arc; RED; pred write
+        "order": 56 * n,                                         # key/npred reads x3, atomics x2, order write/read/write
+        "jp": 20 * n + 8 * m,                                    # order, npred, off, color store; pred id + pred color
+    }
+
+
+def peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary, if any."""
+    p = os.path.join(PROFILES, "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ arms ----
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as O
+    num, den = eps_of(args)
+    sample_name, make = REF_SAMPLE.get(args.config, (args.config, lambda: gg.config_graph(args.config)))
+    g = make()
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r, _ = O.adg(g, num, den)
+        O.jp(g, r, args.seed)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = statistics.mean(times)
+    v = g.m / t
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+           "data": "synthetic",
+           "config": {"workload": f"{args.config}-eps{num}/{den}", "sample": sample_name,
+                      "eps": f"{num}/{den}", "seed": args.seed},
+           "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
+                            "sample": f"sequential C oracle (oracle/oracle.c), full JP-ADG on the "
+                                      f"{sample_name} graph (same recipe, eps, seed) per step"},
+           "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_pgc(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    barrier = (lambda: dist.barrier()) if dist else None
+
+    import paper_2008_11321_b200 as pgc
+
+    num, den = eps_of(args)
+    g = load_graph(args.config, local_rank, barrier)
+    n, nnz, m = g.n, g.nnz, g.m
+    dev = torch.device("cuda", local_rank)
+    off = torch.from_numpy(g.off).to(dev)
+    col = torch.from_numpy(g.col).to(dev)
+    rnd = torch.empty(n, dtype=torch.int32, device=dev)
+    color = torch.empty(n, dtype=torch.int32, device=dev)
+
+    def step():
+        return pgc.color_jp_adg(off, col, num, den, args.seed, round_out=rnd, color_out=color)
+
+    pgc.set_tuning("timing", 0)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- timed region A: the headline (no per-launch events) ----
+    launches = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        if barrier:
+            barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, _, T, K = step()
+            launches += pgc.last_stats()["kernel_launches"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    st = pgc.last_stats()
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- timed region B: same steps with per-launch CUDA events (attribution) ----
+    pgc.set_tuning("timing", 1)
+    groups = {"t_select_ms": [], "t_update_ms": [], "t_adg_other_ms": [], "t_order_ms": [],
+              "t_jp_ms": [], "t_total_ms": []}
+    for _ in range(args.steps):
+        step()
+        s = pgc.last_stats()
+        for k in groups:
+            groups[k].append(s[k])
+    pgc.set_tuning("timing", 0)
+    gmean = {k: statistics.mean(v) for k, v in groups.items()}
+
+    X, sum_active = st["cross_edges"], st["sum_active"]
+    model = algorithmic_bytes(n, nnz, m, X, sum_active)
+    peak, peak_kind = peak_gbs()
+    kern = {"update": ("k_update_light+k_update_heavy", gmean["t_update_ms"], model["update"]),
+            "jp": ("k_jp_color", gmean["t_jp_ms"], model["jp"]),
+            "select": ("k_adg_select", gmean["t_select_ms"], model["select"]),
+            "order": ("order (bucket sort)", gmean["t_order_ms"], model["order"])}
+    dom = max(kern, key=lambda k: kern[k][1])
+    kname, kms, kbytes = kern[dom]
+    achieved = kbytes / (kms * 1e-3) / 1e9
+    traffic = ncu_traffic(kname)
+    path_bytes = sum(model.values())
+
+    out = {
+        "metric": METRIC, "value": world * m / (ms * 1e-3), "unit": "edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{args.config}-eps{num}/{den}", "n": n, "m": m, "nnz": nnz,
+                   "eps": f"{num}/{den}", "seed": args.seed, "graph_seed": 1,
+                   "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+                   "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB L2); no flush" %
+                         ((8 * (n + 1) + 4 * nnz) / 1e9)},
+        "colors": K, "rounds": T, "cross_edges": X, "sum_active": sum_active,
+        "heavy_vertices": st["heavy_vertices"],
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "bytes_per_launch": kbytes, "ms_per_launch": kms,
+                     "path_bytes": path_bytes,
+                     "path_frac": path_bytes / (ms * 1e-3) / 1e9 / peak},
+        "breakdown_ms": {k[2:-3]: v for k, v in gmean.items()},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+
+    # ---- end to end through the host-buffer C-ABI call ----
+    if not (args.no_e2e or args.quick):
+        h_off = torch.from_numpy(g.off).pin_memory()
+        h_col = torch.from_numpy(g.col).pin_memory()
+        h_r = torch.empty(n, dtype=torch.int32).pin_memory()
+        h_c = torch.empty(n, dtype=torch.int32).pin_memory()
+        pgc.color_jp_adg_host(h_off, h_col, num, den, args.seed, h_r, h_c)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if barrier:
+            barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            pgc.color_jp_adg_host(h_off, h_col, num, den, args.seed, h_r, h_c)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        if dist:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        out["e2e"] = {"value": world * m / (ems * 1e-3), "unit": "edges/s",
+                      "h2d_bytes_per_step": 8 * (n + 1) + 4 * nnz, "d2h_bytes_per_step": 8 * n,
+                      "ms_per_step": ems}
+        parity_ok = bool(torch.equal(h_r, rnd.cpu()) and torch.equal(h_c, color.cpu()))
+        out["e2e"]["matches_device_api"] = parity_ok
+
+    # ---- CPU oracle baseline (rank 0, N=1) + parity of this run ----
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
+        import oracle as O
+        t0 = time.perf_counter()
+        r_or, _ = O.adg(g, num, den)
+        t1 = time.perf_counter()
+        c_or, K_or = O.jp(g, r_or, args.seed)
+        t2 = time.perf_counter()
+        out["cpu_baseline"] = {"value": m / (t2 - t0), "unit": "edges/s", "cores": 1,
+                               "kind": "oracle",
+                               "sample": f"full {args.config} workload, one JP-ADG run of the "
+                                         f"sequential C oracle (ADG {t1 - t0:.1f}s + greedy JP "
+                                         f"{t2 - t1:.1f}s)"}
+        out["parity"] = {"round": bool(np.array_equal(rnd.cpu().numpy(), r_or)),
+                         "color": bool(np.array_equal(color.cpu().numpy(), c_or)),
+                         "K": K == K_or}
+
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_pgc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

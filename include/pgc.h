@@ -1,0 +1,166 @@
+/*
+ * pgc.h -- C ABI of the B200-native JP-ADG graph-coloring library.
+ *
+ * Method: Besta et al., "High-Performance Parallel Graph Coloring with Strong
+ * Guarantees on Work, Depth, and Quality", SC'20 (arXiv 2008.11321);
+ * /root/reference/PAPER.md.  This library implements the data-parallel hot
+ * path of JP-ADG on one NVIDIA B200 (sm_100a):
+ *
+ *   ADG  (Algorithm 1): approximate degeneracy ordering.
+ *        Round l removes every remaining vertex whose residual degree is at
+ *        most (1+eps) times the remaining graph's average degree
+ *        (PAPER.md:685), then decrements its neighbours' degrees (UPDATE,
+ *        PAPER.md:692-696).  rho_ADG(v) = l.
+ *   JP   (Algorithm 3) with the priority
+ *        rho = <rho_ADG, rho_R>: a vertex is colored
+ *        with the smallest color (>= 1) not used by any higher-priority
+ *        neighbour (GetColor).
+ *
+ * Conventions shared by every entry point:
+ *   - eps = eps_num / eps_den with eps_num >= 1, eps_den >= 1; the selection
+ *     test is the exact integer form  den*D[v]*|U| <= (den+num)*sum_U D
+ *     ("<=" per Alg. 1).  No floating point anywhere.
+ *   - Rounds are 1-based.  A later round is a HIGHER priority
+ *     (the dense core is colored first).  Inside a round the larger
+ *     h(v) = splitmix64(seed ^ (uint64)v) wins (unsigned compare); h is a
+ *     bijection, so the priority is a total order.
+ *   - Colors are 1-based; num_colors = K = max color.
+ *
+ * Graph input (all entry points): an undirected simple graph in CSR,
+ *   row_offsets : int64[n+1], row_offsets[0] = 0, nondecreasing, [n] = nnz
+ *   col_indices : int32[nnz], each row strictly ascending, symmetric
+ *                 (v in N(u) <=> u in N(v)), no self-loops.
+ * These invariants are NOT checked on the hot path (pgc_check_graph checks
+ * them in O(n+m)); results on an invalid graph are undefined.
+ *
+ * Memory ownership: the caller owns the graph, every output and the
+ * workspace.  The library allocates nothing on the device, keeps no pointer
+ * after a call returns, and has no global mutable state besides the
+ * thread-local error string, statistics and tuning values.  Calls with
+ * distinct workspaces on distinct streams are independent.
+ *
+ * Synchrony: work is enqueued on `cuda_stream` (a cudaStream_t, NULL = the
+ * legacy default stream); each call blocks until its work has finished,
+ * because T and K are returned in host memory.
+ *
+ * Errors: every entry point returns one of the PGC_* codes below; on a
+ * nonzero return the contents of the outputs are unspecified and
+ * pgc_last_error() describes the failure.  No C++ exception crosses the ABI.
+ */
+#ifndef PGC_H
+#define PGC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGC_VERSION 1
+
+enum pgc_status {
+  PGC_OK = 0,          /* success                                                  */
+  PGC_EINVAL = 1,      /* NULL pointer, n < 0, n >= INT32_MAX, nnz < 0, nnz >= 2^40,
+                          eps_num == 0 or eps_den == 0, bad round[] range           */
+  PGC_EWORKSPACE = 2,  /* workspace too small or not 256-byte aligned              */
+  PGC_ECUDA = 3,       /* a CUDA runtime error (message in pgc_last_error)         */
+  PGC_EINTERNAL = 4    /* an internal invariant failed (a bug): e.g. an empty ADG
+                          round or an inconsistent compaction count                */
+};
+
+/* Graph in caller-owned DEVICE memory (see "Graph input" above). */
+typedef struct pgc_graph {
+  int64_t n;                   /* number of vertices, 0 <= n < INT32_MAX              */
+  int64_t nnz;                 /* number of arcs = 2m = row_offsets[n], < 2^40        */
+  const int64_t* row_offsets;  /* device, n+1 entries                                 */
+  const int32_t* col_indices;  /* device, nnz entries                                 */
+} pgc_graph;
+
+/* Statistics of this thread's last successful call (pgc_last_stats). */
+typedef struct pgc_stats {
+  int32_t rounds;          /* T, number of ADG rounds (0 for pgc_jp_color)                */
+  int32_t num_colors;      /* K (0 for pgc_adg_order)                                     */
+  int64_t sum_active;      /* sum over rounds of |U_l| (Lemma 2 work term)  */
+  int64_t cross_edges;     /* X: decrements applied to surviving vertices, over all rounds */
+  int64_t pred_arcs;       /* sum_v |pred(v)|; equals m for a valid graph                 */
+  int64_t heavy_vertices;  /* vertices colored by the warp-per-vertex path (|pred| > 62)  */
+  int32_t kernel_launches; /* CUDA kernels this call launched                             */
+  int32_t host_syncs;      /* stream synchronisations this call performed                 */
+  /* Device time per kernel group, from CUDA events on the call's stream; all -1
+   * unless pgc_set_tuning("timing", 1).  Groups: ADG select (a2/a3), ADG UPDATE
+   * with fused JP Part 1 (a4/a7), other ADG kernels (init, finalize), the
+   * priority-order sort, JP coloring (a8/a9), and the whole call. */
+  float t_select_ms, t_update_ms, t_adg_other_ms, t_order_ms, t_jp_ms, t_total_ms;
+} pgc_stats;
+
+/* Bytes of device workspace the entry points below need for a graph with n
+ * vertices and nnz arcs (the same size serves all three).  The workspace must
+ * be 256-byte aligned.  Returns 0 for invalid sizes. */
+size_t pgc_workspace_bytes(int64_t n, int64_t nnz);
+
+/* ADG ordering only (Algorithm 1).
+ *   round_out  : device int32[n], receives rho_ADG(v) in [1, T]
+ *   num_rounds : host int32*, receives T (0 for n = 0)
+ * ADG uses no randomness, so there is no seed. */
+int pgc_adg_order(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int32_t* round_out,
+                  int32_t* num_rounds, void* workspace, size_t workspace_bytes,
+                  void* cuda_stream);
+
+/* JP coloring (Algorithm 3) for the priority
+ * <round[v], splitmix64(seed ^ v)>, lexicographic.  round[] may be ANY int32
+ * array whose value range (max - min) is below n + 65536, e.g. rho_ADG
+ * (JP-ADG), a constant (JP-R) or the degree (JP-LF).
+ *   round      : device int32[n], read only
+ *   color_out  : device int32[n], receives colors in [1, K]
+ *   num_colors : host int32*, receives K */
+int pgc_jp_color(const pgc_graph* g, const int32_t* round, uint64_t seed, int32_t* color_out,
+                 int32_t* num_colors, void* workspace, size_t workspace_bytes, void* cuda_stream);
+
+/* JP-ADG, the whole hot path: ADG then JP with <rho_ADG, rho_R>.  JP Part 1
+ * (pred counts / DAG) is fused into ADG's UPDATE.
+ *   round_out, color_out : device int32[n]
+ *   num_rounds, num_colors : host int32* */
+int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uint64_t seed,
+                     int32_t* round_out, int32_t* color_out, int32_t* num_rounds,
+                     int32_t* num_colors, void* workspace, size_t workspace_bytes,
+                     void* cuda_stream);
+
+/* JP-ADG end to end from HOST memory: copies the CSR host->device on
+ * `cuda_stream`, runs pgc_color_jp_adg, copies round[] and color[] back.
+ * Host buffers should be pinned (cudaHostAlloc) for full copy bandwidth.
+ *   h_row_offsets : host int64[n+1];  h_col_indices : host int32[nnz]
+ *   h_round_out, h_color_out : host int32[n]
+ *   workspace : DEVICE buffer of pgc_host_workspace_bytes(n, nnz) bytes */
+size_t pgc_host_workspace_bytes(int64_t n, int64_t nnz);
+int pgc_color_jp_adg_host(int64_t n, int64_t nnz, const int64_t* h_row_offsets,
+                          const int32_t* h_col_indices, uint32_t eps_num, uint32_t eps_den,
+                          uint64_t seed, int32_t* h_round_out, int32_t* h_color_out,
+                          int32_t* num_rounds, int32_t* num_colors, void* workspace,
+                          size_t workspace_bytes, void* cuda_stream);
+
+/* O(n+m) validation of the CSR invariants on the device.  Returns PGC_OK or
+ * PGC_EINVAL with the first offending vertex named in pgc_last_error(). */
+int pgc_check_graph(const pgc_graph* g, void* workspace, size_t workspace_bytes,
+                    void* cuda_stream);
+
+/* Statistics of this thread's last successful call; PGC_EINVAL if out is NULL. */
+int pgc_last_stats(pgc_stats* out);
+
+/* Thread-local, NUL-terminated description of the last nonzero return. */
+const char* pgc_last_error(void);
+
+/* Thread-local tuning knobs (results never depend on them; tests sweep them to
+ * prove it).  Keys: "timing" (0/1: per-phase events), "rounds_per_sync"
+ * (>= 1), "heavy_degree" (>= 32), "block_threads" (64..1024, multiple of 32).
+ * Returns PGC_EINVAL for an unknown key or out-of-range value. */
+int pgc_set_tuning(const char* key, int64_t value);
+
+/* PGC_VERSION of the loaded library. */
+int pgc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGC_H */

@@ -1,0 +1,402 @@
+// adg.cu -- ADG (Algorithm 1) on the B200, plus the arc
+// classification kernels shared with JP Part 1 (Algorithm 3).
+//
+// Per round l (host loop, kernels read every size from device memory):
+//   k_adg_select   Count/Reduce are cached (S_l, |U_l| carried in State,
+//                  PAPER.md:2353-2365); Dmax_l = floor((den+num)*S_l/(den*|U_l|))
+//                  once per block in 128-bit; R_l = {v in U_l : D[v] <= Dmax_l}
+//                  (exact); round[v] = l (688-689); block-level
+//                  ballot compaction of R_l (light list + heavy edge chunks)
+//                  and U_{l+1} (U = U \ R, 687).
+//   k_update_*     UPDATE (692-696): for v in R_l, u in N(v) with round[u]==0:
+//                  D[u] -= 1 (RED, result unused), cut += 1.  Fused JP Part 1
+//                  (PAPER.md:2259-2271): pred(v) = {u alive} U {u in R_l :
+//                  h(u) > h(v)} is written into v's own CSR slot of P[] and
+//                  npred[v] = |pred(v)| (= count[v] of Alg. 3).
+//   k_adg_finalize S_{l+1} = S_l - sum_{R_l} D - cut_l; |U_{l+1}| = |U_l| - |R_l|.
+#include <cstdio>
+
+#include "pgc_internal.cuh"
+
+namespace pgc {
+
+__global__ void k_zero_i32(int32_t* p, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0;
+}
+__global__ void k_zero_i32_dev(int32_t* p, const int* len, int extra) {
+  int64_t L = (int64_t)*len + extra;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0;
+}
+
+// a1: D[v] = deg(v); round[v] = 0 (v in U); optional color[v] = 0 (uncolored,
+// PAPER.md:1115).  Thread 0 initialises the round state: S_1 = nnz, |U_1| = n.
+__global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ off,
+                           int32_t* __restrict__ D, int32_t* __restrict__ round,
+                           int32_t* __restrict__ color, State* st) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    D[v] = (int32_t)(off[v + 1] - off[v]);
+    round[v] = 0;
+    if (color) color[v] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    State s = {};
+    s.S = (unsigned long long)nnz;
+    s.nU = n;
+    s.done = (n == 0);
+    s.rmin = 1;
+    s.rmax = 0;
+    *st = s;
+  }
+}
+
+// a2+a3: threshold, select, compact.
+__global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
+                             const int32_t* __restrict__ D, int32_t* __restrict__ round,
+                             const int32_t* __restrict__ Uin, int32_t* __restrict__ Uout,
+                             int32_t* __restrict__ Rl, int2* __restrict__ chunks,
+                             int32_t* __restrict__ npred, State* st, int heavy_deg,
+                             int64_t chunk_cap) {
+  __shared__ int sm[33];
+  __shared__ long long s_dmax;
+  __shared__ unsigned long long s_red[32];
+  if (st->done) return;
+  const long long count = st->nU;
+  if (threadIdx.x == 0) {
+    // Dmax = floor((den+num) * S / (den * |U|)); den*|U| < 2^63, numerator < 2^97.
+    unsigned __int128 numer = (unsigned __int128)((unsigned long long)den + num) * st->S;
+    unsigned long long denom = (unsigned long long)den * (unsigned long long)count;
+    unsigned __int128 q = numer / denom;
+    s_dmax = q > (unsigned __int128)0x7fffffff ? 0x7fffffffLL : (long long)q;
+  }
+  __syncthreads();
+  const long long dmax = s_dmax;
+  unsigned long long my_sumD = 0;
+  unsigned long long my_nR = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < count; base += stride) {
+    const long long i = base + threadIdx.x;
+    const bool valid = i < count;
+    int v = 0, d = 0;
+    if (valid) {
+      v = Uin ? Uin[i] : (int)i;
+      d = D[v];
+    }
+    const bool sel = valid && d <= dmax;
+    bool light = false, heavy = false;
+    if (sel) {
+      round[v] = l;
+      my_sumD += (unsigned long long)d;
+      my_nR += 1;
+      const long long deg = off[v + 1] - off[v];
+      light = deg <= heavy_deg;
+      heavy = !light;
+      if (heavy) {
+        const int nch = (int)((deg + kChunk - 1) / kChunk);
+        const int b = atomicAdd(&st->nChunks, nch);
+        if (b + (long long)nch > chunk_cap) {
+          st->err = 3;
+        } else {
+          for (int k = 0; k < nch; ++k) chunks[b + k] = make_int2(v, k);
+        }
+        npred[v] = 0;
+      }
+    }
+    block_append(light, v, Rl, &st->nLight, sm);
+    block_append(valid && !sel, v, Uout, &st->nUnext, sm);
+  }
+  unsigned long long t = block_sum(my_sumD, s_red);
+  if (threadIdx.x == 0 && t) atomicAdd(&st->sumDR, t);
+  t = block_sum(my_nR, s_red);
+  if (threadIdx.x == 0 && t) atomicAdd(&st->nR, (int)t);
+}
+
+// Arc classifier.  MODE 0: ADG only; 1: ADG with fused JP Part 1; 2: JP Part 1
+// for an arbitrary first key (pgc_jp_color).
+template <int MODE>
+struct Arc {
+  int l;
+  uint64_t seed;
+  const int32_t* __restrict__ round;
+  int32_t* __restrict__ D;
+  // returns true iff u in pred(v); counts cut arcs
+  __device__ __forceinline__ bool classify(int u, int rv, uint64_t hv, unsigned long long& cut) const {
+    const int ru = round[u];
+    if (MODE == 2) {
+      if (ru != rv) return ru > rv;
+      return prio_hash(seed, (uint32_t)u) > hv;
+    }
+    if (ru == 0) {                      // u in U \ R: DecrementAndFetch(D[u])
+      atomicSub(&D[u], 1);              // result unused -> RED
+      cut += 1;
+      return MODE == 1;                 // u gets a later round: higher priority
+    }
+    if (MODE == 1 && ru == l) return prio_hash(seed, (uint32_t)u) > hv;  // same round: hash
+    return false;                       // removed earlier: lower priority
+  }
+};
+
+// UPDATE for light vertices (deg <= heavy_deg): a warp takes 32 list entries
+// and walks their concatenated adjacencies 32 arcs at a time (warp-level merge
+// path: each arc finds its owner by a 5-step shuffle search over the inclusive
+// degree scan).  Pred slots come from per-owner shared-memory counters.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t* __restrict__ off,
+                                                      const int32_t* __restrict__ col,
+                                                      const int32_t* __restrict__ Rl,
+                                                      int32_t* __restrict__ npred,
+                                                      int32_t* __restrict__ P, State* st) {
+  __shared__ int s_cnt[8][32];
+  __shared__ unsigned long long s_red[32];
+  if (MODE != 2 && st->done) return;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int nL = st->nLight;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long cut = 0, preds = 0;
+  for (int b = wg * 32; b < nL; b += nwarps * 32) {
+    const int i = b + lane;
+    const bool valid = i < nL;
+    int v = 0, rv = 0, deg = 0;
+    long long o = 0;
+    if (valid) {
+      v = Rl[i];
+      o = off[v];
+      deg = (int)(off[v + 1] - o);
+      if (MODE == 2) rv = A.round[v];
+    }
+    const uint64_t hv = (MODE != 0 && valid) ? prio_hash(A.seed, (uint32_t)v) : 0;
+    int incl = deg;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, incl, s);
+      if (lane >= s) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - deg;
+    if (MODE != 0) s_cnt[warp][lane] = 0;
+    __syncwarp();
+    for (int t = 0; t < total; t += 32) {
+      const int a = t + lane;
+      // owner = number of lanes whose inclusive prefix is <= a
+      int lo = 0;
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) {
+        int x = __shfl_sync(0xffffffffu, incl, lo + s - 1);
+        if (x <= a) lo += s;
+      }
+      const int owner = lo > 31 ? 31 : lo;
+      const long long oo = __shfl_sync(0xffffffffu, o, owner);
+      const int oe = __shfl_sync(0xffffffffu, excl, owner);
+      const uint64_t oh = __shfl_sync(0xffffffffu, hv, owner);
+      const int orv = __shfl_sync(0xffffffffu, rv, owner);
+      if (a < total) {
+        const int u = col[oo + (a - oe)];
+        const bool pred = A.classify(u, orv, oh, cut);
+        if (MODE != 0 && pred) {
+          const int k = atomicAdd(&s_cnt[warp][owner], 1);
+          P[oo + k] = u;
+        }
+      }
+    }
+    __syncwarp();
+    if (MODE != 0 && valid) {
+      const int k = s_cnt[warp][lane];
+      npred[v] = k;
+      preds += (unsigned long long)k;
+    }
+    __syncwarp();
+  }
+  unsigned long long t = block_sum(cut, s_red);
+  if (threadIdx.x == 0 && t) atomicAdd(&st->cut, t);
+  if (MODE != 0) {
+    t = block_sum(preds, s_red);
+    if (threadIdx.x == 0 && t) atomicAdd(&st->pred_arcs, t);
+  }
+}
+
+// UPDATE for heavy vertices: one warp per kChunk-arc work item; pred slots via
+// one warp-aggregated atomicAdd on npred[v] per 32 arcs.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int64_t* __restrict__ off,
+                                                      const int32_t* __restrict__ col,
+                                                      const int2* __restrict__ chunks,
+                                                      int32_t* __restrict__ npred,
+                                                      int32_t* __restrict__ P, State* st) {
+  __shared__ unsigned long long s_red[32];
+  if (MODE != 2 && st->done) return;
+  const int lane = lane_id();
+  const int nC = st->nChunks;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long cut = 0, preds = 0;
+  for (int ci = wg; ci < nC; ci += nwarps) {
+    const int2 ck = chunks[ci];
+    const int v = ck.x;
+    const long long o = off[v], end = off[v + 1];
+    const long long s = o + (long long)ck.y * kChunk;
+    const long long e = min(end, s + kChunk);
+    const uint64_t hv = MODE != 0 ? prio_hash(A.seed, (uint32_t)v) : 0;
+    const int rv = MODE == 2 ? A.round[v] : 0;
+    for (long long a0 = s; a0 < e; a0 += 32) {
+      const long long a = a0 + lane;
+      bool pred = false;
+      int u = 0;
+      if (a < e) {
+        u = col[a];
+        pred = A.classify(u, rv, hv, cut);
+      }
+      if (MODE != 0) {
+        const unsigned bal = __ballot_sync(0xffffffffu, pred);
+        if (bal) {
+          int base = 0;
+          if (lane == 0) {
+            base = atomicAdd(&npred[v], __popc(bal));
+            preds += (unsigned long long)__popc(bal);
+          }
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (pred) P[o + base + __popc(bal & lanemask_lt())] = u;
+        }
+      }
+    }
+  }
+  unsigned long long t = block_sum(cut, s_red);
+  if (threadIdx.x == 0 && t) atomicAdd(&st->cut, t);
+  if (MODE != 0) {
+    t = block_sum(preds, s_red);
+    if (threadIdx.x == 0 && t) atomicAdd(&st->pred_arcs, t);
+  }
+}
+
+// a2/a5: carry the cached degree sum and |U| to the next round (Q5 reading of
+// PAPER.md:2359-2361), record statistics, detect termination.
+__global__ void k_adg_finalize(int l, State* st, long long* per_round) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (st->done) return;
+  const int nR = st->nR;
+  if (nR == 0) {            // impossible for eps > 0 (Lemma 1): min degree <= mean
+    st->err = 1;
+    st->done = 1;
+    return;
+  }
+  if (l - 1 < kMaxRoundStats) {
+    per_round[3 * (l - 1) + 0] = st->nU;
+    per_round[3 * (l - 1) + 1] = (long long)st->S;
+    per_round[3 * (l - 1) + 2] = nR;
+  }
+  st->sum_active += st->nU;
+  st->cross += st->cut;
+  const long long nU1 = st->nU - nR;
+  if (st->nUnext != nU1) st->err = 2;
+  st->S = st->S - st->sumDR - st->cut;
+  st->nU = nU1;
+  st->T = l;
+  st->rmax = l;
+  st->sumDR = 0;
+  st->cut = 0;
+  st->nR = 0;
+  st->nLight = 0;
+  st->nUnext = 0;
+  st->nChunks = 0;
+  if (nU1 == 0) st->done = 1;
+}
+
+// JP Part 1 work lists for an arbitrary key (pgc_jp_color): every vertex is
+// classified, light ones into Rl, heavy ones into edge chunks.
+__global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int32_t* __restrict__ Rl,
+                              int2* __restrict__ chunks, int32_t* __restrict__ npred, State* st,
+                              int heavy_deg, int64_t chunk_cap) {
+  __shared__ int sm[33];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const long long i = base + threadIdx.x;
+    const bool valid = i < n;
+    bool light = false;
+    if (valid) {
+      const int v = (int)i;
+      const long long deg = off[v + 1] - off[v];
+      light = deg <= heavy_deg;
+      if (!light) {
+        const int nch = (int)((deg + kChunk - 1) / kChunk);
+        const int b = atomicAdd(&st->nChunks, nch);
+        if (b + (long long)nch > chunk_cap) st->err = 3;
+        else
+          for (int k = 0; k < nch; ++k) chunks[b + k] = make_int2(v, k);
+        npred[v] = 0;
+      }
+    }
+    block_append(light, (int)i, Rl, &st->nLight, sm);
+  }
+}
+
+__global__ void k_state_reset_jp(State* st) {
+  State s = {};
+  s.rmin = 0x7fffffff;
+  s.rmax = (int)0x80000000;
+  *st = s;
+}
+
+static int grid_for(const Ctx& c, int per_sm) { return c.nsm * per_sm; }
+
+template <int MODE>
+static int launch_update(Ctx& c, const Arc<MODE>& A) {
+  const int G = grid_for(c, 8);
+  PGC_LAUNCH(c, kGUpdate, "k_update_light",
+             k_update_light<MODE><<<G, 256, 0, c.st>>>(A, c.off, c.col, c.Rl, c.npred, c.P, c.state));
+  PGC_LAUNCH(c, kGUpdate, "k_update_heavy",
+             k_update_heavy<MODE><<<G, 256, 0, c.st>>>(A, c.off, c.col, c.chunks, c.npred, c.P,
+                                                       c.state));
+  return 0;
+}
+
+int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
+            int32_t* color_zero) {
+  const int B = 256;
+  const int G = grid_for(c, 8);
+  PGC_LAUNCH(c, kGAdgOther, "k_adg_init",
+             k_adg_init<<<G, B, 0, c.st>>>(c.n, c.nnz, c.off, c.D, round, color_zero, c.state));
+  if (c.n == 0) return sync_state(c);
+  int l = 1;
+  const int batch = c.tune.rounds_per_sync < 1 ? 1 : c.tune.rounds_per_sync;
+  for (;;) {
+    for (int j = 0; j < batch; ++j, ++l) {
+      const int32_t* Uin = l == 1 ? nullptr : c.U[l & 1];
+      int32_t* Uout = c.U[(l + 1) & 1];
+      PGC_LAUNCH(c, kGSelect, "k_adg_select",
+                 k_adg_select<<<G, B, 0, c.st>>>(l, num, den, c.off, c.D, round, Uin, Uout, c.Rl,
+                                                 c.chunks, c.npred, c.state, c.tune.heavy_degree,
+                                                 c.lay.chunk_cap));
+      if (mode == kAdgFused) {
+        if (int e = launch_update(c, Arc<1>{l, seed, round, c.D})) return e;
+      } else {
+        if (int e = launch_update(c, Arc<0>{l, seed, round, c.D})) return e;
+      }
+      PGC_LAUNCH(c, kGAdgOther, "k_adg_finalize",
+                 k_adg_finalize<<<1, 32, 0, c.st>>>(l, c.state, c.per_round));
+    }
+    if (int e = sync_state(c)) return e;
+    if (c.h_state->err) return fail(4, "ADG internal invariant failed (code %d)", c.h_state->err);
+    if (c.h_state->done) break;
+    if ((int64_t)l > c.n + 2) return fail(4, "ADG did not terminate within n rounds");
+  }
+  return 0;
+}
+
+int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color_zero) {
+  const int G = grid_for(c, 8);
+  PGC_LAUNCH(c, kGAdgOther, "k_state_reset_jp", k_state_reset_jp<<<1, 1, 0, c.st>>>(c.state));
+  if (color_zero) {
+    PGC_LAUNCH(c, kGAdgOther, "k_zero_i32", k_zero_i32<<<G, 256, 0, c.st>>>(color_zero, c.n));
+  }
+  if (c.n == 0) return 0;
+  PGC_LAUNCH(c, kGUpdate, "k_jp_classify",
+             k_jp_classify<<<G, 256, 0, c.st>>>(c.n, c.off, c.Rl, c.chunks, c.npred, c.state,
+                                                c.tune.heavy_degree, c.lay.chunk_cap));
+  return launch_update(c, Arc<2>{0, seed, round, nullptr});
+}
+
+}  // namespace pgc

@@ -1,0 +1,365 @@
+// capi.cu -- the C ABI declared in include/pgc.h: argument validation,
+// workspace carving, thread-local error/statistics/tuning, phase sequencing.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "pgc.h"
+#include "pgc_internal.cuh"
+
+namespace pgc {
+
+static thread_local char g_err[512] = "";
+static thread_local pgc_stats g_stats = {};
+static thread_local Tuning g_tune;
+static thread_local State* g_hstate = nullptr;
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(PGC_ECUDA, "CUDA error '%s' (%s) at %s", cudaGetErrorString(e), cudaGetErrorName(e),
+              where);
+}
+
+static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout make_layout(int64_t n, int64_t nnz) {
+  Layout L = {};
+  size_t a = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = a;
+    a = a256(a + (bytes ? bytes : 1));
+    return o;
+  };
+  const size_t un = (size_t)n, unnz = (size_t)nnz;
+  L.state = take(sizeof(State));
+  L.per_round = take(sizeof(long long) * 3 * kMaxRoundStats);
+  L.D = take(4 * un);
+  L.npred = take(4 * un);
+  L.P = take(4 * unnz);
+  L.U0 = take(4 * un);
+  L.U1 = take(4 * un);
+  L.Rl = take(4 * un);
+  // heavy vertices have degree > heavy_degree >= 32, so at most nnz/33 of them
+  L.chunk_cap = nnz / kChunk + (nnz / 33 < n ? nnz / 33 : n) + 2;
+  L.chunks = take(sizeof(int2) * (size_t)L.chunk_cap);
+  L.order = take(4 * un);
+  L.range_cap = n + 65536;
+  L.hist1 = take(4 * (size_t)(2 * L.range_cap));
+  L.base1 = take(4 * (size_t)(2 * L.range_cap + 1));
+  // sum over keys of pow2ceil(ceil(cnt/8)) <= n/4 + 2 * (nonempty keys) <= n/4 + 2n
+  L.nb_cap = n / 4 + 2 * n + 2;
+  L.bcnt = take(4 * (size_t)(L.nb_cap + 1));
+  L.bstart = take(4 * (size_t)(L.nb_cap + 1));
+  const int64_t big = L.nb_cap > 2 * L.range_cap + 1 ? L.nb_cap : 2 * L.range_cap + 1;
+  L.scan_tmp_cap = big / kScanTile + 4;
+  L.scan_tmp = take(4 * (size_t)L.scan_tmp_cap);
+  L.total = a;
+  return L;
+}
+
+static bool sizes_ok(int64_t n, int64_t nnz) {
+  return n >= 0 && n < ((int64_t)1 << 29) && nnz >= 0 && nnz < ((int64_t)1 << 40);
+}
+
+static int check_graph_args(const pgc_graph* g) {
+  if (!g) return fail(PGC_EINVAL, "graph is NULL");
+  if (!sizes_ok(g->n, g->nnz))
+    return fail(PGC_EINVAL, "bad sizes n=%lld nnz=%lld (need 0 <= n < 2^29, 0 <= nnz < 2^40)",
+                (long long)g->n, (long long)g->nnz);
+  if (!g->row_offsets) return fail(PGC_EINVAL, "row_offsets is NULL");
+  if (g->nnz > 0 && !g->col_indices) return fail(PGC_EINVAL, "col_indices is NULL");
+  return 0;
+}
+
+static int check_ws(const pgc_graph* g, void* ws, size_t bytes) {
+  if (!ws) return fail(PGC_EWORKSPACE, "workspace is NULL");
+  if (((uintptr_t)ws & 255) != 0) return fail(PGC_EWORKSPACE, "workspace not 256-byte aligned");
+  const size_t need = make_layout(g->n, g->nnz).total;
+  if (bytes < need)
+    return fail(PGC_EWORKSPACE, "workspace too small: %zu < %zu bytes", bytes, need);
+  return 0;
+}
+
+static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
+  c.n = g->n;
+  c.nnz = g->nnz;
+  c.off = g->row_offsets;
+  c.col = g->col_indices;
+  c.st = (cudaStream_t)stream;
+  c.tune = g_tune;
+  int dev = 0;
+  PGC_CUDA(cudaGetDevice(&dev));
+  PGC_CUDA(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev));
+  c.lay = make_layout(g->n, g->nnz);
+  char* b = (char*)ws;
+  c.state = (State*)(b + c.lay.state);
+  c.per_round = (long long*)(b + c.lay.per_round);
+  c.D = (int32_t*)(b + c.lay.D);
+  c.npred = (int32_t*)(b + c.lay.npred);
+  c.P = (int32_t*)(b + c.lay.P);
+  c.U[0] = (int32_t*)(b + c.lay.U0);
+  c.U[1] = (int32_t*)(b + c.lay.U1);
+  c.Rl = (int32_t*)(b + c.lay.Rl);
+  c.chunks = (int2*)(b + c.lay.chunks);
+  c.order = (int32_t*)(b + c.lay.order);
+  c.hist1 = (int32_t*)(b + c.lay.hist1);
+  c.base1 = (int32_t*)(b + c.lay.base1);
+  c.bcnt = (int32_t*)(b + c.lay.bcnt);
+  c.bstart = (int32_t*)(b + c.lay.bstart);
+  c.scan_tmp = (int32_t*)(b + c.lay.scan_tmp);
+  if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));
+  c.h_state = g_hstate;
+  return 0;
+}
+
+// Per-group device timing: one event pair around every launch when enabled.
+// Events are pooled per thread and reused across calls.
+struct EventLog {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<int> groups;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void reset(bool on_, cudaStream_t s) {
+    on = on_;
+    st = s;
+    used = 0;
+    groups.clear();
+  }
+};
+static thread_local EventLog g_log;
+static thread_local cudaEvent_t g_total[2] = {nullptr, nullptr};
+
+void log_begin(Ctx& c, int group) {
+  if (!g_log.on) return;
+  g_log.groups.push_back(group);
+  cudaEventRecord(g_log.get(), c.st);
+}
+void log_end(Ctx& c) {
+  if (!g_log.on) return;
+  cudaEventRecord(g_log.get(), c.st);
+}
+
+int sync_state(Ctx& c) {
+  PGC_CUDA(cudaMemcpyAsync(c.h_state, c.state, sizeof(State), cudaMemcpyDeviceToHost, c.st));
+  PGC_CUDA(cudaStreamSynchronize(c.st));
+  ++c.syncs;
+  return 0;
+}
+
+static void call_begin(Ctx& c) {
+  g_log.reset(c.tune.timing != 0, c.st);
+  if (g_log.on) {
+    if (!g_total[0]) {
+      cudaEventCreate(&g_total[0]);
+      cudaEventCreate(&g_total[1]);
+    }
+    cudaEventRecord(g_total[0], c.st);
+  }
+}
+
+// Called after the call's final synchronisation.
+static void call_end(Ctx& c, int rounds, int colors, long long sum_active,
+                     unsigned long long cross, unsigned long long preds, int nheavy) {
+  g_stats.rounds = rounds;
+  g_stats.num_colors = colors;
+  g_stats.sum_active = sum_active;
+  g_stats.cross_edges = (int64_t)cross;
+  g_stats.pred_arcs = (int64_t)preds;
+  g_stats.heavy_vertices = nheavy;
+  g_stats.kernel_launches = c.launches;
+  g_stats.host_syncs = c.syncs;
+  float t[kNumGroups] = {-1.f, -1.f, -1.f, -1.f, -1.f};
+  float total = -1.f;
+  if (g_log.on) {
+    cudaEventRecord(g_total[1], c.st);
+    cudaEventSynchronize(g_total[1]);
+    for (int g = 0; g < kNumGroups; ++g) t[g] = 0.f;
+    for (size_t i = 0; i < g_log.groups.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, g_log.pool[2 * i], g_log.pool[2 * i + 1]);
+      t[g_log.groups[i]] += ms;
+    }
+    cudaEventElapsedTime(&total, g_total[0], g_total[1]);
+  }
+  g_stats.t_select_ms = t[kGSelect];
+  g_stats.t_update_ms = t[kGUpdate];
+  g_stats.t_adg_other_ms = t[kGAdgOther];
+  g_stats.t_order_ms = t[kGOrder];
+  g_stats.t_jp_ms = t[kGJp];
+  g_stats.t_total_ms = total;
+}
+
+}  // namespace pgc
+
+using namespace pgc;
+
+extern "C" {
+
+size_t pgc_workspace_bytes(int64_t n, int64_t nnz) {
+  if (!sizes_ok(n, nnz)) return 0;
+  return make_layout(n, nnz).total;
+}
+
+int pgc_adg_order(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int32_t* round_out,
+                  int32_t* num_rounds, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (eps_num == 0 || eps_den == 0) return fail(PGC_EINVAL, "eps must be num/den with num, den >= 1");
+  if (!num_rounds || (g->n > 0 && !round_out)) return fail(PGC_EINVAL, "output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  if (int e = adg_run(c, eps_num, eps_den, 0, round_out, kAdgOnly, nullptr)) return e;
+  *num_rounds = c.h_state->T;
+  call_end(c, c.h_state->T, 0, c.h_state->sum_active, c.h_state->cross, 0, 0);
+  return PGC_OK;
+}
+
+int pgc_jp_color(const pgc_graph* g, const int32_t* round, uint64_t seed, int32_t* color_out,
+                 int32_t* num_colors, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (!num_colors || (g->n > 0 && (!color_out || !round)))
+    return fail(PGC_EINVAL, "input/output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  if (int e = jp_setup_run(c, round, seed, color_out)) return e;
+  if (int e = jp_order_run(c, round, seed, false)) return e;
+  if (int e = jp_color_run(c, color_out)) return e;
+  *num_colors = c.h_state->K;
+  call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.h_state->nheavy);
+  return PGC_OK;
+}
+
+int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uint64_t seed,
+                     int32_t* round_out, int32_t* color_out, int32_t* num_rounds,
+                     int32_t* num_colors, void* workspace, size_t workspace_bytes,
+                     void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (eps_num == 0 || eps_den == 0) return fail(PGC_EINVAL, "eps must be num/den with num, den >= 1");
+  if (!num_rounds || !num_colors || (g->n > 0 && (!round_out || !color_out)))
+    return fail(PGC_EINVAL, "output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  if (int e = adg_run(c, eps_num, eps_den, seed, round_out, kAdgFused, color_out)) return e;
+  const int T = c.h_state->T;
+  const long long sum_active = c.h_state->sum_active;
+  const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
+  if (int e = jp_order_run(c, round_out, seed, true)) return e;
+  if (int e = jp_color_run(c, color_out)) return e;
+  *num_rounds = T;
+  *num_colors = c.h_state->K;
+  call_end(c, T, c.h_state->K, sum_active, cross, preds, c.h_state->nheavy);
+  return PGC_OK;
+}
+
+size_t pgc_host_workspace_bytes(int64_t n, int64_t nnz) {
+  if (!sizes_ok(n, nnz)) return 0;
+  return a256(8 * (size_t)(n + 1)) + a256(4 * (size_t)nnz) + 2 * a256(4 * (size_t)n) +
+         make_layout(n, nnz).total;
+}
+
+int pgc_color_jp_adg_host(int64_t n, int64_t nnz, const int64_t* h_row_offsets,
+                          const int32_t* h_col_indices, uint32_t eps_num, uint32_t eps_den,
+                          uint64_t seed, int32_t* h_round_out, int32_t* h_color_out,
+                          int32_t* num_rounds, int32_t* num_colors, void* workspace,
+                          size_t workspace_bytes, void* cuda_stream) {
+  if (!sizes_ok(n, nnz)) return fail(PGC_EINVAL, "bad sizes n=%lld nnz=%lld", (long long)n, (long long)nnz);
+  if (!h_row_offsets || (nnz > 0 && !h_col_indices) || (n > 0 && (!h_round_out || !h_color_out)))
+    return fail(PGC_EINVAL, "host pointer is NULL");
+  if (!workspace) return fail(PGC_EWORKSPACE, "workspace is NULL");
+  if (((uintptr_t)workspace & 255) != 0) return fail(PGC_EWORKSPACE, "workspace not 256-byte aligned");
+  if (workspace_bytes < pgc_host_workspace_bytes(n, nnz))
+    return fail(PGC_EWORKSPACE, "workspace too small: %zu < %zu bytes", workspace_bytes,
+                pgc_host_workspace_bytes(n, nnz));
+  char* b = (char*)workspace;
+  int64_t* d_off = (int64_t*)b;
+  b += a256(8 * (size_t)(n + 1));
+  int32_t* d_col = (int32_t*)b;
+  b += a256(4 * (size_t)nnz);
+  int32_t* d_round = (int32_t*)b;
+  b += a256(4 * (size_t)n);
+  int32_t* d_color = (int32_t*)b;
+  b += a256(4 * (size_t)n);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  PGC_CUDA(cudaMemcpyAsync(d_off, h_row_offsets, 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, st));
+  if (nnz > 0)
+    PGC_CUDA(cudaMemcpyAsync(d_col, h_col_indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice, st));
+  pgc_graph g = {n, nnz, d_off, d_col};
+  if (int e = pgc_color_jp_adg(&g, eps_num, eps_den, seed, d_round, d_color, num_rounds,
+                               num_colors, b, workspace_bytes - (size_t)(b - (char*)workspace),
+                               cuda_stream))
+    return e;
+  if (n > 0) {
+    PGC_CUDA(cudaMemcpyAsync(h_round_out, d_round, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    PGC_CUDA(cudaMemcpyAsync(h_color_out, d_color, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  }
+  PGC_CUDA(cudaStreamSynchronize(st));
+  return PGC_OK;
+}
+
+int pgc_check_graph(const pgc_graph* g, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  int64_t bad = -1;
+  if (int e = check_graph_run(c, &bad)) return e;
+  if (bad >= 0)
+    return fail(PGC_EINVAL, "CSR invariant violated at vertex %lld (offsets, range, order, self-loop or symmetry)",
+                (long long)bad);
+  return PGC_OK;
+}
+
+int pgc_last_stats(pgc_stats* out) {
+  if (!out) return fail(PGC_EINVAL, "out is NULL");
+  *out = g_stats;
+  return PGC_OK;
+}
+
+const char* pgc_last_error(void) { return g_err; }
+
+int pgc_set_tuning(const char* key, int64_t value) {
+  if (!key) return fail(PGC_EINVAL, "key is NULL");
+  if (!strcmp(key, "timing") && (value == 0 || value == 1)) {
+    g_tune.timing = (int)value;
+    return PGC_OK;
+  }
+  if (!strcmp(key, "rounds_per_sync") && value >= 1 && value <= 1 << 16) {
+    g_tune.rounds_per_sync = (int)value;
+    return PGC_OK;
+  }
+  if (!strcmp(key, "heavy_degree") && value >= 32 && value <= (1 << 30)) {
+    g_tune.heavy_degree = (int)value;
+    return PGC_OK;
+  }
+  if (!strcmp(key, "block_threads") && value >= 64 && value <= 1024 && value % 32 == 0) {
+    g_tune.block_threads = (int)value;
+    return PGC_OK;
+  }
+  return fail(PGC_EINVAL, "unknown tuning key or value out of range: %s=%lld", key, (long long)value);
+}
+
+int pgc_version(void) { return PGC_VERSION; }
+
+}  // extern "C"

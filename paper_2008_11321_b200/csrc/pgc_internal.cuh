@@ -1,0 +1,217 @@
+// pgc_internal.cuh -- shared internals of the B200 JP-ADG library (product path).
+//
+// Nothing here is shared with oracle/ (the CPU oracle is test infrastructure;
+// the two share no code, header or constant table).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pgc {
+
+constexpr int kWarp = 32;
+constexpr int kChunk = 2048;          // arcs per heavy-vertex work item (ADG UPDATE / JP setup)
+constexpr int kLightPredMax = 62;     // JP: lane-per-vertex when |pred(v)| <= this (colors fit a u64 mask)
+constexpr int kHeavyWin = 2048;       // JP heavy path: colors per bitmap window (64 x u32 words)
+constexpr int kPendCap = 256;         // JP heavy path: pending-pred list capacity per warp (smem)
+constexpr int kMaxRoundStats = 4096;  // per-round statistics kept in the workspace
+constexpr int kBucketTarget = 8;      // mean bucket occupancy target of the priority-order sort
+constexpr int kScanTile = 4096;       // elements per block in the device-wide scan
+
+// Device-resident scalars of one call.  Lives at the head of the workspace.
+struct State {
+  // ADG round state (Alg. 1)
+  unsigned long long S;        // sum_{v in U} D[v] for the current round
+  long long nU;                // |U| for the current round
+  int done;                    // 1 once U is empty
+  int err;                     // internal invariant failure code (0 = none)
+  int T;                       // rounds completed
+  int pad0;
+  // counters of the current round, reset by k_adg_finalize
+  unsigned long long sumDR;    // sum of D over R_l
+  unsigned long long cut;      // arcs from R_l into U_{l+1}
+  int nR, nLight, nUnext, nChunks;
+  // totals
+  long long sum_active;        // sum_l |U_l|
+  unsigned long long cross;    // X
+  unsigned long long pred_arcs;  // sum_v |pred(v)|
+  // priority-order sort
+  int rmin, rmax;              // range of the first priority key
+  int nbuckets;                // buckets in use
+  int nheavy;                  // vertices with |pred| > kLightPredMax (they lead the order)
+  int sorted;                  // total placed by the scan (== n)
+  // JP dataflow
+  int ticket_heavy, ticket_light;
+  int K;
+};
+
+// Byte offsets of every workspace region (each 256-byte aligned).
+struct Layout {
+  size_t state, per_round, D, npred, P, U0, U1, Rl, chunks, order, hist1, base1, bcnt, bstart,
+      scan_tmp, total;
+  int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap;
+};
+
+Layout make_layout(int64_t n, int64_t nnz);
+
+struct Tuning {
+  int timing = 0;
+  int rounds_per_sync = 8;
+  int heavy_degree = 1024;
+  int block_threads = 256;
+};
+
+// Kernel groups for per-group device timing (pgc_stats.t_*_ms).
+enum Group { kGSelect = 0, kGUpdate = 1, kGAdgOther = 2, kGOrder = 3, kGJp = 4, kNumGroups = 5 };
+
+// Everything a phase needs; built by the C-ABI layer from the caller's arguments.
+struct Ctx {
+  int launches = 0;  // kernels launched by this call
+  int syncs = 0;     // host synchronisations by this call
+  int64_t n, nnz;
+  const int64_t* off;
+  const int32_t* col;
+  cudaStream_t st;
+  int nsm;
+  Tuning tune;
+  Layout lay;
+  State* state;
+  long long* per_round;  // [kMaxRoundStats][3] = (|U_l|, S_l, |R_l|)
+  int32_t* D;
+  int32_t* npred;
+  int32_t* P;
+  int32_t* U[2];
+  int32_t* Rl;
+  int2* chunks;
+  int32_t* order;
+  int32_t* hist1;
+  int32_t* base1;
+  int32_t* bcnt;
+  int32_t* bstart;
+  int32_t* scan_tmp;
+  State* h_state;  // pinned host mirror
+};
+
+// ---- phases (host orchestration; return 0 or a PGC_* code) -----------------
+enum AdgMode { kAdgOnly = 0, kAdgFused = 1 };
+int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
+            int32_t* color_zero);
+int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color_zero);
+int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known);
+int jp_color_run(Ctx& c, int32_t* color);
+int check_graph_run(Ctx& c, int64_t* bad_vertex);
+
+// error reporting helper implemented in capi.cu
+int fail(int code, const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* where);
+// per-group event timing (no-ops unless timing is enabled); capi.cu
+void log_begin(Ctx& c, int group);
+void log_end(Ctx& c);
+// copy State to the pinned host mirror and wait for the stream; capi.cu
+int sync_state(Ctx& c);
+
+// Launch a kernel (variadic so the <<<...>>> commas survive), check the launch,
+// account it and time it in `group`.
+#define PGC_LAUNCH(c, group, name, ...)                         \
+  do {                                                          \
+    ::pgc::log_begin(c, group);                                 \
+    __VA_ARGS__;                                                \
+    cudaError_t e_ = cudaGetLastError();                        \
+    if (e_ != cudaSuccess) return ::pgc::cuda_fail(e_, name);   \
+    ::pgc::log_end(c);                                          \
+    ++(c).launches;                                             \
+  } while (0)
+
+#define PGC_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return ::pgc::cuda_fail(e_, #call); \
+  } while (0)
+
+#define PGC_LAUNCHED(name)                                        \
+  do {                                                            \
+    cudaError_t e_ = cudaGetLastError();                          \
+    if (e_ != cudaSuccess) return ::pgc::cuda_fail(e_, name);     \
+  } while (0)
+
+// ---- device helpers ---------------------------------------------------------
+// rho_R(v) = splitmix64(seed ^ v): the first output of a SplitMix64 generator
+// whose state is seed^v (published constants).
+__device__ __forceinline__ uint64_t prio_hash(uint64_t seed, uint32_t v) {
+  uint64_t z = (seed ^ (uint64_t)v) + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ int ld_relaxed(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
+  asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ int warp_max(int x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// Block-wide stream compaction: every thread with `flag` appends `val` to
+// out[] at a position reserved with ONE atomicAdd per block (order inside the
+// list is arbitrary -- all consumers treat the lists as sets).  Must be called
+// by all threads of the block; `sm` needs (blockDim/32 + 1) ints.
+__device__ __forceinline__ void block_append(bool flag, int val, int32_t* out, int* counter,
+                                             int* sm) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned b = __ballot_sync(0xffffffffu, flag);
+  if (lane == 0) sm[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      int c = sm[w];
+      sm[w] = tot;
+      tot += c;
+    }
+    sm[nw] = tot ? atomicAdd(counter, tot) : 0;
+  }
+  __syncthreads();
+  if (flag) out[sm[nw] + sm[warp] + __popc(b & lanemask_lt())] = val;
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T x, T* sm) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  x = warp_sum(x);
+  if (lane == 0) sm[warp] = x;
+  __syncthreads();
+  T t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < nw; ++w) t += sm[w];
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+// ---- shared kernels (defined in adg.cu) -----------------------------------
+__global__ void k_zero_i32(int32_t* p, int64_t len);
+__global__ void k_zero_i32_dev(int32_t* p, const int* len, int extra);
+
+
+}  // namespace pgc

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Everything is integer, so the bar is bit-exactness: identical round[] and
+color[] per vertex, identical T and K (and identical ADG statistics).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import graphgen as gg
+import oracle as O
+from _refcheck import all_graphs
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def dev(g):
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    off = torch.from_numpy(g.off).cuda()
+    col = torch.from_numpy(g.col).cuda() if g.nnz else torch.empty(0, dtype=torch.int32, device="cuda")
+    return pgc, off, col
+
+
+def run_gpu(g, num, den, seed):
+    pgc, off, col = dev(g)
+    rnd, color, T, K = pgc.color_jp_adg(off, col, num, den, seed)
+    torch.cuda.synchronize()
+    return rnd.cpu().numpy(), color.cpu().numpy(), T, K, pgc.last_stats()
+
+
+def assert_parity(g, num, den, seed, stats=True):
+    r_gpu, c_gpu, T, K, st = run_gpu(g, num, den, seed)
+    r_or, st_or = O.adg(g, num, den)
+    c_or, K_or = O.jp(g, r_or, seed)
+    assert T == st_or["T"]
+    bad = np.nonzero(r_gpu != r_or)[0]
+    assert len(bad) == 0, f"round mismatch at {bad[:10]} gpu={r_gpu[bad[:10]]} cpu={r_or[bad[:10]]}"
+    bad = np.nonzero(c_gpu != c_or)[0]
+    assert len(bad) == 0, f"color mismatch at {bad[:10]} gpu={c_gpu[bad[:10]]} cpu={c_or[bad[:10]]}"
+    assert K == K_or
+    if stats:
+        assert st["rounds"] == T and st["num_colors"] == K
+        assert st["sum_active"] == st_or["sum_active"]
+        assert st["cross_edges"] == st_or["cross_edges"]
+        assert st["pred_arcs"] == g.m
+    return T, K
+
+
+def test_appendix_b_cases():
+    cases = json.load(open(os.path.join(GOLDEN, "appendix_b.json")))["cases"]
+    for c in cases:
+        g = gg.from_edges(c["n"], c["edges"])
+        for seed in (1, 2, 0xDEADBEEFCAFEF00D):
+            T, K = assert_parity(g, c["eps"][0], c["eps"][1], seed)
+            assert T == c["T"]
+
+
+def test_zoo_all_graphs_up_to_5():
+    # disjoint union of every labelled graph on <= 5 vertices
+    edges, n = [], 0
+    for k in range(1, 6):
+        for es in all_graphs(k):
+            edges += [(a + n, b + n) for a, b in es]
+            n += k
+    g = gg.from_edges(n, edges)
+    for num, den in [(1, 100), (1, 10), (1, 2), (1, 1), (4294967295, 1)]:
+        assert_parity(g, num, den, 7)
+
+
+@pytest.mark.parametrize("seed", range(1, 9))
+def test_random_er_rmat(seed):
+    for g in (gg.er(3000, 15000 + 1000 * seed, seed), gg.rmat(8 + seed % 7, 8, seed=seed)):
+        for num, den in [(1, 100), (1, 10), (1, 2)]:
+            assert_parity(g, num, den, seed * 31 + 1)
+
+
+def test_heavy_paths_cliques_and_hubs():
+    # K_n: every vertex has up to n-1 preds -> heavy JP path; n > 2049 -> several color windows
+    for n in (70, 300, 2100):
+        g = gg.from_edges(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+        T, K = assert_parity(g, 1, 10, 3)
+        assert T == 1 and K == n
+    # star with a 5000-leaf hub -> heavy ADG UPDATE chunks
+    g = gg.from_edges(5001, [(0, i) for i in range(1, 5001)])
+    assert_parity(g, 1, 10, 3)
+    # hub joined to a clique
+    n = 400
+    edges = [(i, j) for i in range(1, n) for j in range(i + 1, n)] + [(0, i) for i in range(1, 20000)]
+    g = gg.from_edges(20000, edges)
+    assert_parity(g, 1, 100, 5)
+
+
+def test_edge_cases():
+    pgc, off, col = dev(gg.from_edges(0, []))
+    r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 1)
+    assert T == 0 and K == 0 and r.numel() == 0
+    for n in (1, 2, 33, 1000):
+        assert_parity(gg.from_edges(n, []), 1, 10, 1)   # edgeless: one round, all color 1
+
+
+@pytest.mark.parametrize("name", ["er", "rmat20", "grid"])
+def test_config_parity(name):
+    g = gg.config_graph(name)
+    for num, den in gg.CONFIGS[name][1]:
+        assert_parity(g, num, den, 1)
+
+
+@pytest.mark.parametrize("name", ["rmat24", "cl"])
+def test_config_parity_large(name):
+    g = gg.config_graph(name)
+    for num, den in gg.CONFIGS[name][1]:
+        assert_parity(g, num, den, 1)
+
+
+def test_adg_order_only_and_jp_generic_keys():
+    g = gg.rmat(13, 8, seed=4)
+    pgc, off, col = dev(g)
+    for num, den in [(1, 100), (1, 2)]:
+        rnd, T = pgc.adg_order(off, col, num, den)
+        r_or, st = O.adg(g, num, den)
+        assert T == st["T"] and np.array_equal(rnd.cpu().numpy(), r_or)
+        assert pgc.last_stats()["cross_edges"] == st["cross_edges"]
+    seed = 11
+    keys = {
+        "adg": torch.from_numpy(O.adg(g, 1, 10)[0]).cuda(),
+        "const(JP-R)": torch.full((g.n,), 5, dtype=torch.int32, device="cuda"),
+        "degree(JP-LF)": torch.from_numpy(g.degrees().astype(np.int32)).cuda(),
+        "negative": torch.from_numpy(-(np.arange(g.n) % 97).astype(np.int32)).cuda(),
+    }
+    for name, key in keys.items():
+        color, K = pgc.jp_color(off, col, key, seed)
+        c_or, K_or = O.jp(g, key.cpu().numpy(), seed)
+        assert K == K_or and np.array_equal(color.cpu().numpy(), c_or), name
+        assert pgc.last_stats()["pred_arcs"] == g.m
+
+
+def test_jp_key_range_error():
+    g = gg.er(100, 300, 1)
+    pgc, off, col = dev(g)
+    key = torch.zeros(g.n, dtype=torch.int32, device="cuda")
+    key[0] = 2**31 - 1
+    key[1] = -(2**31)
+    with pytest.raises(pgc.PGCError) as e:
+        pgc.jp_color(off, col, key, 1)
+    assert e.value.code == pgc.PGC_EINVAL
+
+
+def test_determinism_across_tuning():
+    g = gg.rmat(14, 16, seed=2)
+    pgc, off, col = dev(g)
+    ref = None
+    try:
+        for hd in (32, 100, 1024, 1 << 20):
+            for rps in (1, 3, 8):
+                pgc.set_tuning("heavy_degree", hd)
+                pgc.set_tuning("rounds_per_sync", rps)
+                for _ in range(2):
+                    r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 9)
+                    out = (r.cpu().numpy(), c.cpu().numpy(), T, K)
+                    if ref is None:
+                        ref = out
+                    assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
+                    assert out[2:] == ref[2:]
+    finally:
+        pgc.set_tuning("heavy_degree", 1024)
+        pgc.set_tuning("rounds_per_sync", 8)
+    r_or, _ = O.adg(g, 1, 10)
+    c_or, _ = O.jp(g, r_or, 9)
+    assert np.array_equal(ref[0], r_or) and np.array_equal(ref[1], c_or)
+
+
+def test_host_api_matches_device_api():
+    g = gg.rmat(12, 16, seed=6)
+    pgc, off, col = dev(g)
+    r_d, c_d, T_d, K_d = pgc.color_jp_adg(off, col, 1, 10, 3)
+    h_off = torch.from_numpy(g.off).pin_memory()
+    h_col = torch.from_numpy(g.col).pin_memory()
+    h_r = torch.empty(g.n, dtype=torch.int32).pin_memory()
+    h_c = torch.empty(g.n, dtype=torch.int32).pin_memory()
+    T, K = pgc.color_jp_adg_host(h_off, h_col, 1, 10, 3, h_r, h_c)
+    assert (T, K) == (T_d, K_d)
+    assert torch.equal(h_r, r_d.cpu()) and torch.equal(h_c, c_d.cpu())
+
+
+def test_check_graph():
+    g = gg.rmat(10, 8, seed=1)
+    pgc, off, col = dev(g)
+    pgc.check_graph(off, col)
+    bad = col.clone()
+    # break symmetry: redirect one arc of the first nonempty row
+    v = int(np.nonzero(g.degrees())[0][0])
+    e = int(g.off[v])
+    bad[e] = (bad[e] + 1) % g.n if int(bad[e] + 1) % g.n != v else (bad[e] + 2) % g.n
+    with pytest.raises(pgc.PGCError) as ei:
+        pgc.check_graph(off, bad)
+    assert ei.value.code == pgc.PGC_EINVAL
+
+
+def test_timing_stats():
+    g = gg.rmat(12, 16, seed=6)
+    pgc, off, col = dev(g)
+    pgc.set_tuning("timing", 1)
+    try:
+        pgc.color_jp_adg(off, col, 1, 10, 3)
+        st = pgc.last_stats()
+        for k in ("t_select_ms", "t_update_ms", "t_order_ms", "t_jp_ms", "t_total_ms"):
+            assert st[k] > 0, k
+        parts = st["t_select_ms"] + st["t_update_ms"] + st["t_adg_other_ms"] + st["t_order_ms"] + st["t_jp_ms"]
+        assert parts <= st["t_total_ms"] * 1.01
+        assert st["kernel_launches"] > 10 and st["host_syncs"] >= 2
+    finally:
+        pgc.set_tuning("timing", 0)
