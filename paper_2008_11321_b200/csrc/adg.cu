@@ -35,11 +35,12 @@ __global__ void k_zero_i32_dev(int32_t* p, const int* len, int extra) {
 // a1: D[v] = deg(v); round[v] = 0 (v in U); optional color[v] = 0 (uncolored,
 // PAPER.md:1115).  Thread 0 initialises the round state: S_1 = nnz, |U_1| = n.
 __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ off,
-                           int32_t* __restrict__ D, int32_t* __restrict__ round,
-                           int32_t* __restrict__ color, State* st) {
+                           int32_t* __restrict__ D, uint8_t* __restrict__ rs,
+                           int32_t* __restrict__ round, int32_t* __restrict__ color, State* st) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     D[v] = (int32_t)(off[v + 1] - off[v]);
+    rs[v] = 0;
     round[v] = 0;
     if (color) color[v] = 0;
   }
@@ -57,9 +58,10 @@ __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ o
 // a2+a3: threshold, select, compact.
 __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
                              const int32_t* __restrict__ D, int32_t* __restrict__ round,
+                             uint8_t* __restrict__ rs,
                              const int32_t* __restrict__ Uin, int32_t* __restrict__ Uout,
                              int32_t* __restrict__ Rl, int2* __restrict__ chunks,
-                             int32_t* __restrict__ npred, State* st, int heavy_deg,
+                             int32_t* __restrict__ npred, State* st, int heavy_deg, int chunk,
                              int64_t chunk_cap) {
   __shared__ int sm[33];
   __shared__ long long s_dmax;
@@ -87,24 +89,25 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
       d = D[v];
     }
     const bool sel = valid && d <= dmax;
-    bool light = false, heavy = false;
+    bool light = false;
+    int nch = 0;
     if (sel) {
       round[v] = l;
+      rs[v] = (uint8_t)((l - 1) % 255 + 1);
       my_sumD += (unsigned long long)d;
       my_nR += 1;
       const long long deg = off[v + 1] - off[v];
       light = deg <= heavy_deg;
-      heavy = !light;
-      if (heavy) {
-        const int nch = (int)((deg + kChunk - 1) / kChunk);
-        const int b = atomicAdd(&st->nChunks, nch);
-        if (b + (long long)nch > chunk_cap) {
-          st->err = 3;
-        } else {
-          for (int k = 0; k < nch; ++k) chunks[b + k] = make_int2(v, k);
-        }
+      if (!light) {
+        nch = (int)((deg + chunk - 1) / chunk);
         npred[v] = 0;
       }
+    }
+    const int cb = block_reserve(nch, &st->nChunks, sm);
+    if (nch) {
+      if (cb + (long long)nch > chunk_cap) st->err = 3;
+      else
+        for (int k = 0; k < nch; ++k) chunks[cb + k] = make_int2(v, k);
     }
     block_append(light, v, Rl, &st->nLight, sm);
     block_append(valid && !sel, v, Uout, &st->nUnext, sm);
@@ -123,19 +126,35 @@ struct Arc {
   uint64_t seed;
   const int32_t* __restrict__ round;
   int32_t* __restrict__ D;
-  // returns true iff u in pred(v); counts cut arcs
-  __device__ __forceinline__ bool classify(int u, int rv, uint64_t hv, unsigned long long& cut) const {
-    const int ru = round[u];
+  const uint8_t* __restrict__ rs;
+  // Round state of u.  MODE 0/1: 0 = alive (u in U), 1 = removed in this
+  // round, 2 = removed earlier; read from the 1-byte rs[] while l <= 255
+  // (exact: rs = ((round-1) mod 255) + 1), from round[] afterwards.
+  __device__ __forceinline__ int state(int u) const {
+    if (l <= 255) {
+      const int b = rs[u];
+      return b == 0 ? 0 : (b == l ? 1 : 2);
+    }
+    const int r = round[u];
+    return r == 0 ? 0 : (r == l ? 1 : 2);
+  }
+  // the per-arc gather: MODE 2 the key round[u], else the round state
+  __device__ __forceinline__ int gather(int u) const { return MODE == 2 ? round[u] : state(u); }
+  // true iff u in pred(v); performs UPDATE's decrement and counts cut arcs.
+  // g = gather(u).
+  __device__ __forceinline__ bool classify(int u, int g, int rv, uint64_t hv,
+                                          unsigned long long& cut) const {
     if (MODE == 2) {
-      if (ru != rv) return ru > rv;
+      if (g != rv) return g > rv;
       return prio_hash(seed, (uint32_t)u) > hv;
     }
-    if (ru == 0) {                      // u in U \ R: DecrementAndFetch(D[u])
+    const int su = g;
+    if (su == 0) {                      // u in U \ R: DecrementAndFetch(D[u])
       atomicSub(&D[u], 1);              // result unused -> RED
       cut += 1;
       return MODE == 1;                 // u gets a later round: higher priority
     }
-    if (MODE == 1 && ru == l) return prio_hash(seed, (uint32_t)u) > hv;  // same round: hash
+    if (MODE == 1 && su == 1) return prio_hash(seed, (uint32_t)u) > hv;  // same round: hash
     return false;                       // removed earlier: lower priority
   }
 };
@@ -195,11 +214,11 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t
       const uint64_t oh = __shfl_sync(0xffffffffu, hv, owner);
       const int orv = __shfl_sync(0xffffffffu, rv, owner);
       if (a < total) {
-        const int u = col[oo + (a - oe)];
-        const bool pred = A.classify(u, orv, oh, cut);
+        const int u = ld_stream(col + oo + (a - oe));
+        const bool pred = A.classify(u, A.gather(u), orv, oh, cut);
         if (MODE != 0 && pred) {
           const int k = atomicAdd(&s_cnt[warp][owner], 1);
-          P[oo + k] = u;
+          st_stream(P + oo + k, u);
         }
       }
     }
@@ -219,14 +238,15 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t
   }
 }
 
-// UPDATE for heavy vertices: one warp per kChunk-arc work item; pred slots via
+// UPDATE for chunked vertices: one warp per `chunk`-arc work item; pred slots via
 // one warp-aggregated atomicAdd on npred[v] per 32 arcs.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int64_t* __restrict__ off,
                                                       const int32_t* __restrict__ col,
                                                       const int2* __restrict__ chunks,
                                                       int32_t* __restrict__ npred,
-                                                      int32_t* __restrict__ P, State* st) {
+                                                      int32_t* __restrict__ P, State* st,
+                                                      int chunk) {
   __shared__ unsigned long long s_red[32];
   if (MODE != 2 && st->done) return;
   const int lane = lane_id();
@@ -238,28 +258,35 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int64_t
     const int2 ck = chunks[ci];
     const int v = ck.x;
     const long long o = off[v], end = off[v + 1];
-    const long long s = o + (long long)ck.y * kChunk;
-    const long long e = min(end, s + kChunk);
+    const long long s = o + (long long)ck.y * chunk;
+    const long long e = min(end, s + chunk);
     const uint64_t hv = MODE != 0 ? prio_hash(A.seed, (uint32_t)v) : 0;
     const int rv = MODE == 2 ? A.round[v] : 0;
-    for (long long a0 = s; a0 < e; a0 += 32) {
-      const long long a = a0 + lane;
-      bool pred = false;
-      int u = 0;
-      if (a < e) {
-        u = col[a];
-        pred = A.classify(u, rv, hv, cut);
+    for (long long a0 = s; a0 < e; a0 += 128) {
+      // 4 strips of 32 arcs: 4 independent col loads, then 4 state gathers in flight
+      int u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long long a = a0 + 32 * k + lane;
+        u[k] = a < e ? ld_stream(col + a) : -1;
       }
-      if (MODE != 0) {
-        const unsigned bal = __ballot_sync(0xffffffffu, pred);
-        if (bal) {
-          int base = 0;
-          if (lane == 0) {
-            base = atomicAdd(&npred[v], __popc(bal));
-            preds += (unsigned long long)__popc(bal);
+      int g[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut);
+        if (MODE != 0) {
+          const unsigned bal = __ballot_sync(0xffffffffu, pred);
+          if (bal) {
+            int base = 0;
+            if (lane == 0) {
+              base = atomicAdd(&npred[v], __popc(bal));
+              preds += (unsigned long long)__popc(bal);
+            }
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (pred) st_stream(P + o + base + __popc(bal & lanemask_lt()), u[k]);
           }
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (pred) P[o + base + __popc(bal & lanemask_lt())] = u;
         }
       }
     }
@@ -309,25 +336,28 @@ __global__ void k_adg_finalize(int l, State* st, long long* per_round) {
 // classified, light ones into Rl, heavy ones into edge chunks.
 __global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int32_t* __restrict__ Rl,
                               int2* __restrict__ chunks, int32_t* __restrict__ npred, State* st,
-                              int heavy_deg, int64_t chunk_cap) {
+                              int heavy_deg, int chunk, int64_t chunk_cap) {
   __shared__ int sm[33];
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
     const long long i = base + threadIdx.x;
     const bool valid = i < n;
     bool light = false;
+    int nch = 0;
     if (valid) {
       const int v = (int)i;
       const long long deg = off[v + 1] - off[v];
       light = deg <= heavy_deg;
       if (!light) {
-        const int nch = (int)((deg + kChunk - 1) / kChunk);
-        const int b = atomicAdd(&st->nChunks, nch);
-        if (b + (long long)nch > chunk_cap) st->err = 3;
-        else
-          for (int k = 0; k < nch; ++k) chunks[b + k] = make_int2(v, k);
+        nch = (int)((deg + chunk - 1) / chunk);
         npred[v] = 0;
       }
+    }
+    const int cb = block_reserve(nch, &st->nChunks, sm);
+    if (nch) {
+      if (cb + (long long)nch > chunk_cap) st->err = 3;
+      else
+        for (int k = 0; k < nch; ++k) chunks[cb + k] = make_int2((int)i, k);
     }
     block_append(light, (int)i, Rl, &st->nLight, sm);
   }
@@ -349,7 +379,7 @@ static int launch_update(Ctx& c, const Arc<MODE>& A) {
              k_update_light<MODE><<<G, 256, 0, c.st>>>(A, c.off, c.col, c.Rl, c.npred, c.P, c.state));
   PGC_LAUNCH(c, kGUpdate, "k_update_heavy",
              k_update_heavy<MODE><<<G, 256, 0, c.st>>>(A, c.off, c.col, c.chunks, c.npred, c.P,
-                                                       c.state));
+                                                       c.state, c.tune.chunk_arcs));
   return 0;
 }
 
@@ -358,7 +388,8 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
   const int B = 256;
   const int G = grid_for(c, 8);
   PGC_LAUNCH(c, kGAdgOther, "k_adg_init",
-             k_adg_init<<<G, B, 0, c.st>>>(c.n, c.nnz, c.off, c.D, round, color_zero, c.state));
+             k_adg_init<<<G, B, 0, c.st>>>(c.n, c.nnz, c.off, c.D, c.rs, round, color_zero,
+                                           c.state));
   if (c.n == 0) return sync_state(c);
   int l = 1;
   const int batch = c.tune.rounds_per_sync < 1 ? 1 : c.tune.rounds_per_sync;
@@ -367,13 +398,13 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
       const int32_t* Uin = l == 1 ? nullptr : c.U[l & 1];
       int32_t* Uout = c.U[(l + 1) & 1];
       PGC_LAUNCH(c, kGSelect, "k_adg_select",
-                 k_adg_select<<<G, B, 0, c.st>>>(l, num, den, c.off, c.D, round, Uin, Uout, c.Rl,
+                 k_adg_select<<<G, B, 0, c.st>>>(l, num, den, c.off, c.D, round, c.rs, Uin, Uout, c.Rl,
                                                  c.chunks, c.npred, c.state, c.tune.heavy_degree,
-                                                 c.lay.chunk_cap));
+                                                 c.tune.chunk_arcs, c.lay.chunk_cap));
       if (mode == kAdgFused) {
-        if (int e = launch_update(c, Arc<1>{l, seed, round, c.D})) return e;
+        if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs})) return e;
       } else {
-        if (int e = launch_update(c, Arc<0>{l, seed, round, c.D})) return e;
+        if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs})) return e;
       }
       PGC_LAUNCH(c, kGAdgOther, "k_adg_finalize",
                  k_adg_finalize<<<1, 32, 0, c.st>>>(l, c.state, c.per_round));
@@ -395,8 +426,9 @@ int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color_zer
   if (c.n == 0) return 0;
   PGC_LAUNCH(c, kGUpdate, "k_jp_classify",
              k_jp_classify<<<G, 256, 0, c.st>>>(c.n, c.off, c.Rl, c.chunks, c.npred, c.state,
-                                                c.tune.heavy_degree, c.lay.chunk_cap));
-  return launch_update(c, Arc<2>{0, seed, round, nullptr});
+                                                c.tune.heavy_degree, c.tune.chunk_arcs,
+                                                c.lay.chunk_cap));
+  return launch_update(c, Arc<2>{0, seed, round, nullptr, nullptr});
 }
 
 }  // namespace pgc

@@ -42,13 +42,15 @@ Layout make_layout(int64_t n, int64_t nnz) {
   L.state = take(sizeof(State));
   L.per_round = take(sizeof(long long) * 3 * kMaxRoundStats);
   L.D = take(4 * un);
+  L.rs = take(un);
   L.npred = take(4 * un);
   L.P = take(4 * unnz);
   L.U0 = take(4 * un);
   L.U1 = take(4 * un);
   L.Rl = take(4 * un);
-  // heavy vertices have degree > heavy_degree >= 32, so at most nnz/33 of them
-  L.chunk_cap = nnz / kChunk + (nnz / 33 < n ? nnz / 33 : n) + 2;
+  // chunked vertices have degree > heavy_degree >= 32 (at most nnz/33 of them)
+  // and need ceil(deg/chunk) <= deg/kMinChunk + 1 items each
+  L.chunk_cap = nnz / kMinChunk + (nnz / 33 < n ? nnz / 33 : n) + 2;
   L.chunks = take(sizeof(int2) * (size_t)L.chunk_cap);
   L.order = take(4 * un);
   L.range_cap = n + 65536;
@@ -103,6 +105,7 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.state = (State*)(b + c.lay.state);
   c.per_round = (long long*)(b + c.lay.per_round);
   c.D = (int32_t*)(b + c.lay.D);
+  c.rs = (uint8_t*)(b + c.lay.rs);
   c.npred = (int32_t*)(b + c.lay.npred);
   c.P = (int32_t*)(b + c.lay.P);
   c.U[0] = (int32_t*)(b + c.lay.U0);
@@ -351,6 +354,18 @@ int pgc_set_tuning(const char* key, int64_t value) {
   }
   if (!strcmp(key, "heavy_degree") && value >= 32 && value <= (1 << 30)) {
     g_tune.heavy_degree = (int)value;
+    return PGC_OK;
+  }
+  if (!strcmp(key, "chunk_arcs") && value >= kMinChunk && value <= (1 << 24)) {
+    g_tune.chunk_arcs = (int)value;
+    return PGC_OK;
+  }
+  if (!strcmp(key, "jp_heavy_sleep_max") && value >= 0 && value <= 1000000) {
+    g_tune.jp_heavy_sleep_max = (int)value;
+    return PGC_OK;
+  }
+  if (!strcmp(key, "jp_light_sleep_max") && value >= 0 && value <= 1000000) {
+    g_tune.jp_light_sleep_max = (int)value;
     return PGC_OK;
   }
   if (!strcmp(key, "block_threads") && value >= 64 && value <= 1024 && value % 32 == 0) {

@@ -347,12 +347,54 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) 
 // ------------------------------------------------------------- color --------
 constexpr int kJpBlock = 256;
 constexpr int kHeavyWarps = 2;  // warps 0..1 of each block take heavy vertices
+constexpr int kLightBatch = 8;  // pred loads in flight per light lane
+
+// OR color cc into the window bitmap (colors wbase+1 .. wbase+kHeavyWin).
+__device__ __forceinline__ void bm_set(unsigned* bm, int cc, int wbase) {
+  if (cc > wbase && cc <= wbase + kHeavyWin) {
+    const int bit = cc - wbase - 1;
+    atomicOr(&bm[bit >> 5], 1u << (bit & 31));
+  }
+}
+
+// Heavy path, one warp per vertex: examine preds [from, np) in strips of 4x32
+// (4 independent loads in flight per lane), OR colored ones into the window,
+// queue pending ones in the warp's list.  Returns the index to resume from when
+// the pending list is full, np when every pred was examined.
+__device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t pb, int np,
+                                          int from, const int32_t* color, unsigned* bm, int wbase,
+                                          int* plist, int& npend) {
+  const int lane = lane_id();
+  for (int i0 = from; i0 < np; i0 += 128) {
+    int u[4], cc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + 32 * k + lane;
+      u[k] = i < np ? __ldg(P + pb + i) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool pend = u[k] >= 0 && cc[k] == 0;
+      if (u[k] >= 0 && cc[k]) bm_set(bm, cc[k], wbase);
+      const unsigned bal = __ballot_sync(0xffffffffu, pend);
+      const int cnt = __popc(bal);
+      if (npend + cnt > kPendCap) return i0 + 32 * k;  // strips before k are complete
+      if (pend) plist[npend + __popc(bal & lanemask_lt())] = u[k];
+      npend += cnt;
+    }
+  }
+  return np;
+}
 
 __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t* __restrict__ off,
                                                       const int32_t* __restrict__ P,
                                                       const int32_t* __restrict__ npred,
                                                       const int32_t* __restrict__ order,
-                                                      int32_t* color, State* st) {
+                                                      int32_t* color, State* st,
+                                                      unsigned heavy_sleep_max,
+                                                      unsigned light_sleep_max) {
   __shared__ unsigned s_bm[kHeavyWarps][kHeavyWin / 32];
   __shared__ int s_pend[kHeavyWarps][kPendCap];
   const int lane = lane_id(), warp = threadIdx.x >> 5;
@@ -375,31 +417,10 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
         bm[lane + 32] = 0;
         __syncwarp();
         int npend = 0;
-        int over = 0;  // next pred index not yet examined (overflow rescan point); np = none
-        // examine preds [from, np): OR colors into the window, queue pending ones
-        auto pass = [&](int from) {
-          int i0 = from;
-          for (; i0 < np; i0 += 32) {
-            const int i = i0 + lane;
-            int u = 0, cc = 1;
-            if (i < np) {
-              u = P[pb + i];
-              cc = ld_relaxed(color + u);
-            }
-            const bool pend = i < np && cc == 0;
-            if (i < np && cc > wbase && cc <= wbase + kHeavyWin) {
-              const int bit = cc - wbase - 1;
-              atomicOr(&bm[bit >> 5], 1u << (bit & 31));
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, pend);
-            const int k = __popc(bal);
-            if (npend + k > kPendCap) return i0;  // resume here later
-            if (pend) plist[npend + __popc(bal & lanemask_lt())] = u;
-            npend += k;
-          }
-          return np;
-        };
-        over = pass(0);
+        int over = heavy_scan(P, pb, np, 0, color, bm, wbase, plist, npend);
+        // poll the pending preds until every one is colored (never blocks: a
+        // pass either makes progress or sleeps briefly and retries)
+        unsigned sleep_ns = 16;
         while (npend > 0 || over < np) {
           bool progress = false;
           int keep = 0;
@@ -411,10 +432,7 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
               cc = ld_relaxed(color + u);
             }
             const bool still = j < npend && cc == 0;
-            if (j < npend && cc > wbase && cc <= wbase + kHeavyWin) {
-              const int bit = cc - wbase - 1;
-              atomicOr(&bm[bit >> 5], 1u << (bit & 31));
-            }
+            if (j < npend && cc) bm_set(bm, cc, wbase);
             const unsigned bal = __ballot_sync(0xffffffffu, still);
             if (__ballot_sync(0xffffffffu, j < npend && cc != 0)) progress = true;
             __syncwarp();
@@ -425,29 +443,30 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
           __syncwarp();
           if (over < np) {
             const int before = over;
-            over = pass(over);
+            over = heavy_scan(P, pb, np, over, color, bm, wbase, plist, npend);
             if (over != before) progress = true;
           }
           if (npend == 0 && over >= np) break;
-          if (!progress) __nanosleep(32);
+          if (progress) {
+            sleep_ns = 16;
+          } else {
+            __nanosleep(sleep_ns);
+            sleep_ns = min(sleep_ns * 2, heavy_sleep_max);
+          }
         }
         __syncwarp();
-        // mex inside this window: first zero bit
+        // GetColor inside this window: the first zero bit
         const unsigned z0 = ~bm[lane], z1 = ~bm[lane + 32];
         const unsigned b0 = __ballot_sync(0xffffffffu, z0 != 0);
         const unsigned b1 = __ballot_sync(0xffffffffu, z1 != 0);
-        int cfound = 0;
         if (b0) {
           const int w = __ffs(b0) - 1;
           const unsigned z = __shfl_sync(0xffffffffu, z0, w);
-          cfound = wbase + 32 * w + __ffs(z);
+          found = wbase + 32 * w + __ffs(z);
         } else if (b1) {
           const int w = __ffs(b1) - 1;
           const unsigned z = __shfl_sync(0xffffffffu, z1, w);
-          cfound = wbase + 32 * (w + 32) + __ffs(z);
-        }
-        if (cfound) {
-          found = cfound;
+          found = wbase + 32 * (w + 32) + __ffs(z);
         }
         __syncwarp();
       }
@@ -463,36 +482,82 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
       if (t >= nlight) break;
       const int64_t pos = nheavy + (int64_t)t + lane;
       const bool valid = pos < n;
-      int v = 0, np = 0, idx = 0;
+      int v = 0, np = 0;
       int64_t pb = 0;
-      unsigned long long mask = 1ull;  // bit 0 reserved: colors start at 1
+      unsigned long long mask = 1ull;  // used colors; bit 0 reserved (colors start at 1)
+      unsigned long long pend = 0ull;  // indices of preds still uncolored (np <= 62)
       if (valid) {
         v = order[pos];
         np = npred[v];
         pb = off[v];
       }
+      // first pass over every pred, kLightBatch loads in flight
+      for (int j0 = 0; j0 < np; j0 += kLightBatch) {
+        int u[kLightBatch], cc[kLightBatch];
+#pragma unroll
+        for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? __ldg(P + pb + j0 + k) : -1;
+#pragma unroll
+        for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+#pragma unroll
+        for (int k = 0; k < kLightBatch; ++k) {
+          if (u[k] < 0) continue;
+          if (cc[k] == 0) pend |= 1ull << (j0 + k);
+          else if (cc[k] < 64) mask |= 1ull << cc[k];
+        }
+      }
+      // Waiting: each lane watches ONE pending pred (its lowest pending index)
+      // with a single load per poll; only when the watched pred is colored does
+      // it re-examine the remaining pending preds in one batched pass.
+      int watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
+      int watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
       bool done = !valid;
+      unsigned sleep_ns = 32;
       for (;;) {
         bool progress = false;
-        if (!done) {
-          while (idx < np) {
-            const int u = P[pb + idx];
-            const int cc = ld_relaxed(color + u);
-            if (cc == 0) break;
-            if (cc < 64) mask |= 1ull << cc;
-            ++idx;
+        if (!done && watch_u >= 0) {
+          const int cw = ld_relaxed(color + watch_u);
+          if (cw) {
+            if (cw < 64) mask |= 1ull << cw;
+            pend &= ~(1ull << watch_j);
             progress = true;
-          }
-          if (idx == np) {
-            const int cc = __ffsll((long long)~mask) - 1;
-            st_relaxed(color + v, cc);
-            kmax = max(kmax, cc);
-            done = true;
-            progress = true;
+            // batched re-poll of the other pending preds
+            unsigned long long p = pend;
+            while (p) {
+              int js[kLightBatch], u[kLightBatch], cc[kLightBatch];
+#pragma unroll
+              for (int k = 0; k < kLightBatch; ++k) {
+                js[k] = p ? __ffsll((long long)p) - 1 : -1;
+                p &= p - 1;
+              }
+#pragma unroll
+              for (int k = 0; k < kLightBatch; ++k) u[k] = js[k] >= 0 ? __ldg(P + pb + js[k]) : -1;
+#pragma unroll
+              for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 0;
+#pragma unroll
+              for (int k = 0; k < kLightBatch; ++k)
+                if (cc[k]) {
+                  if (cc[k] < 64) mask |= 1ull << cc[k];
+                  pend &= ~(1ull << js[k]);
+                }
+            }
+            watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
+            watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
           }
         }
+        if (!done && watch_u < 0) {  // GetColor: smallest color unused by the preds
+          const int cc = __ffsll((long long)~mask) - 1;
+          st_relaxed(color + v, cc);
+          kmax = max(kmax, cc);
+          done = true;
+          progress = true;
+        }
         if (__ballot_sync(0xffffffffu, !done) == 0) break;
-        if (__ballot_sync(0xffffffffu, progress) == 0) __nanosleep(64);
+        if (__ballot_sync(0xffffffffu, progress)) {
+          sleep_ns = 32;
+        } else {
+          __nanosleep(sleep_ns);
+          sleep_ns = min(sleep_ns * 2, light_sleep_max);
+        }
       }
     }
   }
@@ -515,8 +580,9 @@ int jp_color_run(Ctx& c, int32_t* color) {
       if (occ < 1) occ = 1;
     }
     PGC_LAUNCH(c, kGJp, "k_jp_color",
-               k_jp_color<<<c.nsm * occ, kJpBlock, 0, c.st>>>(c.n, c.off, c.P, c.npred, c.order,
-                                                              color, c.state));
+               k_jp_color<<<c.nsm * occ, kJpBlock, 0, c.st>>>(
+                   c.n, c.off, c.P, c.npred, c.order, color, c.state,
+                   (unsigned)c.tune.jp_heavy_sleep_max, (unsigned)c.tune.jp_light_sleep_max));
   }
   if (int e = sync_state(c)) return e;
   if (c.n > 0 && c.h_state->sorted != c.n)

@@ -11,7 +11,7 @@
 namespace pgc {
 
 constexpr int kWarp = 32;
-constexpr int kChunk = 2048;          // arcs per heavy-vertex work item (ADG UPDATE / JP setup)
+constexpr int kMinChunk = 256;        // smallest allowed arcs-per-work-item for chunked vertices
 constexpr int kLightPredMax = 62;     // JP: lane-per-vertex when |pred(v)| <= this (colors fit a u64 mask)
 constexpr int kHeavyWin = 2048;       // JP heavy path: colors per bitmap window (64 x u32 words)
 constexpr int kPendCap = 256;         // JP heavy path: pending-pred list capacity per warp (smem)
@@ -48,7 +48,7 @@ struct State {
 
 // Byte offsets of every workspace region (each 256-byte aligned).
 struct Layout {
-  size_t state, per_round, D, npred, P, U0, U1, Rl, chunks, order, hist1, base1, bcnt, bstart,
+  size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, order, hist1, base1, bcnt, bstart,
       scan_tmp, total;
   int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap;
 };
@@ -58,7 +58,10 @@ Layout make_layout(int64_t n, int64_t nnz);
 struct Tuning {
   int timing = 0;
   int rounds_per_sync = 8;
-  int heavy_degree = 1024;
+  int heavy_degree = 32;    // vertices with more arcs are split into edge chunks
+  int chunk_arcs = 1024;    // arcs per chunk work item
+  int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
+  int jp_light_sleep_max = 2048;  // ns, same for light warps
   int block_threads = 256;
 };
 
@@ -79,6 +82,7 @@ struct Ctx {
   State* state;
   long long* per_round;  // [kMaxRoundStats][3] = (|U_l|, S_l, |R_l|)
   int32_t* D;
+  uint8_t* rs;  // 1-byte round state: 0 = alive, else ((round-1) % 255) + 1 (L2-resident)
   int32_t* npred;
   int32_t* P;
   int32_t* U[2];
@@ -153,6 +157,11 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
 __device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// streaming (evict-first) accesses for data touched once: keeps the L2 for the
+// randomly gathered per-vertex state (rs, D, colors).
+__device__ __forceinline__ int ld_stream(const int32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(int32_t* p, int v) { __stcs(p, v); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -194,6 +203,34 @@ __device__ __forceinline__ void block_append(bool flag, int val, int32_t* out, i
   __syncthreads();
   if (flag) out[sm[nw] + sm[warp] + __popc(b & lanemask_lt())] = val;
   __syncthreads();
+}
+
+// Block-wide reservation: each thread asks for `cnt` slots; returns the
+// thread's first slot, reserved with ONE atomicAdd per block.  All threads of
+// the block must call it; `sm` needs (blockDim/32 + 1) ints.
+__device__ __forceinline__ int block_reserve(int cnt, int* counter, int* sm) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= s) incl += y;
+  }
+  if (lane == 31) sm[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      int c = sm[w];
+      sm[w] = tot;
+      tot += c;
+    }
+    sm[nw] = tot ? atomicAdd(counter, tot) : 0;
+  }
+  __syncthreads();
+  const int base = sm[nw] + sm[warp] + incl - cnt;
+  __syncthreads();
+  return base;
 }
 
 template <typename T>
