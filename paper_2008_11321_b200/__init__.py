@@ -27,7 +27,8 @@ PGC_OK, PGC_EINVAL, PGC_EWORKSPACE, PGC_ECUDA, PGC_EINTERNAL = 0, 1, 2, 3, 4
 
 EXPORTS = ["pgc_workspace_bytes", "pgc_adg_order", "pgc_jp_color", "pgc_color_jp_adg",
            "pgc_host_workspace_bytes", "pgc_color_jp_adg_host", "pgc_check_graph",
-           "pgc_last_stats", "pgc_last_error", "pgc_set_tuning", "pgc_version"]
+           "pgc_last_stats", "pgc_last_error", "pgc_set_tuning", "pgc_version",
+           "pgc_debug_set_trace"]
 
 
 class Graph(ctypes.Structure):
@@ -72,6 +73,8 @@ _lib.pgc_set_tuning.restype = ctypes.c_int
 _lib.pgc_set_tuning.argtypes = [ctypes.c_char_p, _i64]
 _lib.pgc_version.restype = ctypes.c_int
 _lib.pgc_version.argtypes = []
+_lib.pgc_debug_set_trace.restype = ctypes.c_int
+_lib.pgc_debug_set_trace.argtypes = [_vp, _vp, _i64]
 
 
 class PGCError(RuntimeError):
@@ -104,6 +107,15 @@ def host_workspace_bytes(n: int, nnz: int) -> int:
 
 def set_tuning(key: str, value: int):
     _check(_lib.pgc_set_tuning(key.encode(), int(value)))
+
+
+def debug_set_trace(t_grab=None, t_done=None):
+    """Diagnostics (include/pgc_debug.h): record per-vertex JP grab/done
+    %globaltimer stamps into two CUDA int64 tensors of n entries; None = off."""
+    if t_grab is None:
+        _check(_lib.pgc_debug_set_trace(None, None, 0))
+    else:
+        _check(_lib.pgc_debug_set_trace(t_grab.data_ptr(), t_done.data_ptr(), t_grab.numel()))
 
 
 def last_stats() -> dict:

@@ -238,8 +238,11 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t
   }
 }
 
-// UPDATE for chunked vertices: one warp per `chunk`-arc work item; pred slots via
-// one warp-aggregated atomicAdd on npred[v] per 32 arcs.
+// UPDATE for chunked vertices: one warp per `chunk`-arc work item.  The preds
+// found in each 512-arc sub-chunk are staged in shared memory and written as
+// one coalesced run after a single atomicAdd on npred[v] (no per-strip atomic
+// round trip on the critical path).
+constexpr int kSub = 512;
 template <int MODE>
 __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int64_t* __restrict__ off,
                                                       const int32_t* __restrict__ col,
@@ -248,8 +251,9 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int64_t
                                                       int32_t* __restrict__ P, State* st,
                                                       int chunk) {
   __shared__ unsigned long long s_red[32];
+  __shared__ int s_buf[MODE != 0 ? 8 : 1][MODE != 0 ? kSub : 1];
   if (MODE != 2 && st->done) return;
-  const int lane = lane_id();
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
   const int nC = st->nChunks;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -262,32 +266,37 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int64_t
     const long long e = min(end, s + chunk);
     const uint64_t hv = MODE != 0 ? prio_hash(A.seed, (uint32_t)v) : 0;
     const int rv = MODE == 2 ? A.round[v] : 0;
-    for (long long a0 = s; a0 < e; a0 += 128) {
-      // 4 strips of 32 arcs: 4 independent col loads, then 4 state gathers in flight
-      int u[4];
+    for (long long s0 = s; s0 < e; s0 += kSub) {
+      const long long e0 = min(e, s0 + kSub);
+      int cnt = 0;  // preds staged in s_buf[warp]
+      for (long long a0 = s0; a0 < e0; a0 += 128) {
+        // 4 strips of 32 arcs: 4 independent col loads, then 4 state gathers in flight
+        int u[4], g[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const long long a = a0 + 32 * k + lane;
-        u[k] = a < e ? ld_stream(col + a) : -1;
-      }
-      int g[4];
+        for (int k = 0; k < 4; ++k) {
+          const long long a = a0 + 32 * k + lane;
+          u[k] = a < e0 ? ld_stream(col + a) : -1;
+        }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
+        for (int k = 0; k < 4; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut);
-        if (MODE != 0) {
-          const unsigned bal = __ballot_sync(0xffffffffu, pred);
-          if (bal) {
-            int base = 0;
-            if (lane == 0) {
-              base = atomicAdd(&npred[v], __popc(bal));
-              preds += (unsigned long long)__popc(bal);
-            }
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (pred) st_stream(P + o + base + __popc(bal & lanemask_lt()), u[k]);
+        for (int k = 0; k < 4; ++k) {
+          const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut);
+          if (MODE != 0) {
+            const unsigned bal = __ballot_sync(0xffffffffu, pred);
+            if (pred) s_buf[warp][cnt + __popc(bal & lanemask_lt())] = u[k];
+            cnt += __popc(bal);
           }
         }
+      }
+      if (MODE != 0 && cnt) {
+        __syncwarp();
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&npred[v], cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane; i < cnt; i += 32) st_stream(P + o + base + i, s_buf[warp][i]);
+        if (lane == 0) preds += (unsigned long long)cnt;
+        __syncwarp();
       }
     }
   }

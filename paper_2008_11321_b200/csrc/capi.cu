@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "pgc.h"
+#include "pgc_debug.h"
 #include "pgc_internal.cuh"
 
 namespace pgc {
@@ -14,6 +15,9 @@ static thread_local char g_err[512] = "";
 static thread_local pgc_stats g_stats = {};
 static thread_local Tuning g_tune;
 static thread_local State* g_hstate = nullptr;
+static thread_local unsigned long long* g_trace_grab = nullptr;
+static thread_local unsigned long long* g_trace_done = nullptr;
+static thread_local int64_t g_trace_n = -1;
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -120,6 +124,10 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.scan_tmp = (int32_t*)(b + c.lay.scan_tmp);
   if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));
   c.h_state = g_hstate;
+  if (g_trace_grab && g_trace_n == g->n) {
+    c.trace_grab = g_trace_grab;
+    c.trace_done = g_trace_done;
+  }
   return 0;
 }
 
@@ -360,6 +368,10 @@ int pgc_set_tuning(const char* key, int64_t value) {
     g_tune.chunk_arcs = (int)value;
     return PGC_OK;
   }
+  if (!strcmp(key, "jp_heavy_warps") && value >= 1 && value <= 7) {
+    g_tune.jp_heavy_warps = (int)value;
+    return PGC_OK;
+  }
   if (!strcmp(key, "jp_heavy_sleep_max") && value >= 0 && value <= 1000000) {
     g_tune.jp_heavy_sleep_max = (int)value;
     return PGC_OK;
@@ -376,5 +388,13 @@ int pgc_set_tuning(const char* key, int64_t value) {
 }
 
 int pgc_version(void) { return PGC_VERSION; }
+
+int pgc_debug_set_trace(uint64_t* t_grab, uint64_t* t_done, int64_t n) {
+  if (n < 0 || (!t_grab) != (!t_done)) return fail(PGC_EINVAL, "trace: need both pointers and n >= 0");
+  g_trace_grab = (unsigned long long*)t_grab;
+  g_trace_done = (unsigned long long*)t_done;
+  g_trace_n = t_grab ? n : -1;
+  return PGC_OK;
+}
 
 }  // extern "C"

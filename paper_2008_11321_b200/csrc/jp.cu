@@ -255,38 +255,81 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round,
 }
 
 // Sort every bucket by h descending (bucket = same class and round, same top
-// hash bits).  Warp per bucket; <= 32 entries: rank by 32 shuffles.
+// hash bits).  One lane per bucket (insertion sort in registers, <= 16
+// entries, the common case at mean occupancy 4..8); larger buckets are
+// ranked by a whole warp afterwards.
+constexpr int kLaneSortMax = 16;
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
                               int32_t* __restrict__ order, uint64_t seed) {
   const int lane = lane_id();
   const int nb = st->nbuckets;
-  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int b = wg; b < nb; b += nwarps) {
-    const int s0 = bstart[b], s = bstart[b + 1] - s0;
-    if (s <= 1) continue;
-    if (s <= 32) {
-      const int v = lane < s ? order[s0 + lane] : 0;
-      const uint64_t h = lane < s ? prio_hash(seed, (uint32_t)v) : 0;
-      int rank = 0;
-      for (int j = 0; j < s; ++j) {
-        const uint64_t hj = __shfl_sync(0xffffffffu, h, j);
-        rank += hj > h;
-      }
-      __syncwarp();
-      if (lane < s) order[s0 + rank] = v;
-      __syncwarp();
-    } else if (lane == 0) {  // rare: insertion sort in place
-      for (int i = 1; i < s; ++i) {
-        const int x = order[s0 + i];
-        const uint64_t hx = prio_hash(seed, (uint32_t)x);
-        int j = i - 1;
-        while (j >= 0 && prio_hash(seed, (uint32_t)order[s0 + j]) < hx) {
-          order[s0 + j + 1] = order[s0 + j];
-          --j;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthreads = gridDim.x * blockDim.x;
+  for (int b0 = tid - lane; b0 < nb; b0 += nthreads) {
+    const int b = b0 + lane;
+    int s0 = 0, s = 0;
+    if (b < nb) {
+      s0 = bstart[b];
+      s = bstart[b + 1] - s0;
+    }
+    if (s >= 2 && s <= kLaneSortMax) {
+      int vv[kLaneSortMax];
+      uint64_t hh[kLaneSortMax];
+#pragma unroll
+      for (int i = 0; i < kLaneSortMax; ++i)
+        if (i < s) {
+          vv[i] = order[s0 + i];
+          hh[i] = prio_hash(seed, (uint32_t)vv[i]);
         }
-        order[s0 + j + 1] = x;
+#pragma unroll
+      for (int i = 1; i < kLaneSortMax; ++i) {
+        if (i < s) {
+          const int x = vv[i];
+          const uint64_t hx = hh[i];
+          int j = i - 1;
+#pragma unroll
+          for (int k = kLaneSortMax - 2; k >= 0; --k) {  // shift larger-priority-later entries
+            if (k <= j && k < i && hh[k] < hx) {
+              hh[k + 1] = hh[k];
+              vv[k + 1] = vv[k];
+              hh[k] = hx;
+              vv[k] = x;
+            }
+          }
+        }
       }
+#pragma unroll
+      for (int i = 0; i < kLaneSortMax; ++i)
+        if (i < s) order[s0 + i] = vv[i];
+    }
+    // rare large buckets: the whole warp ranks them, one bucket at a time
+    unsigned big = __ballot_sync(0xffffffffu, s > kLaneSortMax);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int bs0 = __shfl_sync(0xffffffffu, s0, src);
+      const int bs = __shfl_sync(0xffffffffu, s, src);
+      if (bs <= 32) {
+        const int v = lane < bs ? order[bs0 + lane] : 0;
+        const uint64_t h = lane < bs ? prio_hash(seed, (uint32_t)v) : 0;
+        int rank = 0;
+        for (int j = 0; j < bs; ++j) rank += __shfl_sync(0xffffffffu, h, j) > h;
+        __syncwarp();
+        if (lane < bs) order[bs0 + rank] = v;
+        __syncwarp();
+      } else if (lane == 0) {  // very rare: insertion sort in place
+        for (int i = 1; i < bs; ++i) {
+          const int x = order[bs0 + i];
+          const uint64_t hx = prio_hash(seed, (uint32_t)x);
+          int j = i - 1;
+          while (j >= 0 && prio_hash(seed, (uint32_t)order[bs0 + j]) < hx) {
+            order[bs0 + j + 1] = order[bs0 + j];
+            --j;
+          }
+          order[bs0 + j + 1] = x;
+        }
+      }
+      __syncwarp();
     }
   }
 }
@@ -346,8 +389,9 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) 
 
 // ------------------------------------------------------------- color --------
 constexpr int kJpBlock = 256;
-constexpr int kHeavyWarps = 2;  // warps 0..1 of each block take heavy vertices
-constexpr int kLightBatch = 8;  // pred loads in flight per light lane
+constexpr int kJpWarps = kJpBlock / 32;
+constexpr int kPendCap = 256;          // pending-pred list capacity per heavy warp (smem)
+constexpr int kLightBatch = 8;         // pred loads in flight per light lane
 
 // OR color cc into the window bitmap (colors wbase+1 .. wbase+kHeavyWin).
 __device__ __forceinline__ void bm_set(unsigned* bm, int cc, int wbase) {
@@ -393,14 +437,18 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
                                                       const int32_t* __restrict__ npred,
                                                       const int32_t* __restrict__ order,
                                                       int32_t* color, State* st,
+                                                      int heavy_warps,
                                                       unsigned heavy_sleep_max,
-                                                      unsigned light_sleep_max) {
-  __shared__ unsigned s_bm[kHeavyWarps][kHeavyWin / 32];
-  __shared__ int s_pend[kHeavyWarps][kPendCap];
+                                                      unsigned light_sleep_max,
+                                                      unsigned long long* tr_grab,
+                                                      unsigned long long* tr_done) {
+  // heavy-warp state: window bitmap + pending preds, per warp
+  __shared__ unsigned s_bm[kJpWarps][kHeavyWin / 32];
+  __shared__ int s_pend[kJpWarps][kPendCap];
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const int nheavy = st->nheavy;
   int kmax = 0;
-  if (warp < kHeavyWarps) {
+  if (warp < heavy_warps) {
     unsigned* bm = s_bm[warp];
     int* plist = s_pend[warp];
     for (;;) {
@@ -411,6 +459,7 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
       const int v = order[t];
       const int np = npred[v];
       const int64_t pb = off[v];
+      if (tr_grab && lane == 0) tr_grab[v] = globaltimer();
       int found = 0;
       for (int wbase = 0; !found; wbase += kHeavyWin) {
         bm[lane] = 0;
@@ -470,7 +519,10 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
         }
         __syncwarp();
       }
-      if (lane == 0) st_relaxed(color + v, found);
+      if (lane == 0) {
+        st_relaxed(color + v, found);
+        if (tr_done) tr_done[v] = globaltimer();
+      }
       kmax = max(kmax, found);
     }
   } else {
@@ -490,6 +542,7 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
         v = order[pos];
         np = npred[v];
         pb = off[v];
+        if (tr_grab) tr_grab[v] = globaltimer();
       }
       // first pass over every pred, kLightBatch loads in flight
       for (int j0 = 0; j0 < np; j0 += kLightBatch) {
@@ -547,6 +600,7 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
         if (!done && watch_u < 0) {  // GetColor: smallest color unused by the preds
           const int cc = __ffsll((long long)~mask) - 1;
           st_relaxed(color + v, cc);
+          if (tr_done) tr_done[v] = globaltimer();
           kmax = max(kmax, cc);
           done = true;
           progress = true;
@@ -581,8 +635,9 @@ int jp_color_run(Ctx& c, int32_t* color) {
     }
     PGC_LAUNCH(c, kGJp, "k_jp_color",
                k_jp_color<<<c.nsm * occ, kJpBlock, 0, c.st>>>(
-                   c.n, c.off, c.P, c.npred, c.order, color, c.state,
-                   (unsigned)c.tune.jp_heavy_sleep_max, (unsigned)c.tune.jp_light_sleep_max));
+                   c.n, c.off, c.P, c.npred, c.order, color, c.state, c.tune.jp_heavy_warps,
+                   (unsigned)c.tune.jp_heavy_sleep_max, (unsigned)c.tune.jp_light_sleep_max,
+                   c.trace_grab, c.trace_done));
   }
   if (int e = sync_state(c)) return e;
   if (c.n > 0 && c.h_state->sorted != c.n)

@@ -14,7 +14,6 @@ constexpr int kWarp = 32;
 constexpr int kMinChunk = 256;        // smallest allowed arcs-per-work-item for chunked vertices
 constexpr int kLightPredMax = 62;     // JP: lane-per-vertex when |pred(v)| <= this (colors fit a u64 mask)
 constexpr int kHeavyWin = 2048;       // JP heavy path: colors per bitmap window (64 x u32 words)
-constexpr int kPendCap = 256;         // JP heavy path: pending-pred list capacity per warp (smem)
 constexpr int kMaxRoundStats = 4096;  // per-round statistics kept in the workspace
 constexpr int kBucketTarget = 8;      // mean bucket occupancy target of the priority-order sort
 constexpr int kScanTile = 4096;       // elements per block in the device-wide scan
@@ -60,8 +59,9 @@ struct Tuning {
   int rounds_per_sync = 8;
   int heavy_degree = 32;    // vertices with more arcs are split into edge chunks
   int chunk_arcs = 1024;    // arcs per chunk work item
+  int jp_heavy_warps = 2;         // warps per 8-warp JP block serving heavy vertices (1..7)
   int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
-  int jp_light_sleep_max = 2048;  // ns, same for light warps
+  int jp_light_sleep_max = 8192;  // ns, same for light warps
   int block_threads = 256;
 };
 
@@ -95,6 +95,8 @@ struct Ctx {
   int32_t* bstart;
   int32_t* scan_tmp;
   State* h_state;  // pinned host mirror
+  unsigned long long* trace_grab = nullptr;  // pgc_debug_set_trace (diagnostics)
+  unsigned long long* trace_done = nullptr;
 };
 
 // ---- phases (host orchestration; return 0 or a PGC_* code) -----------------
@@ -161,6 +163,12 @@ __device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
 // randomly gathered per-vertex state (rs, D, colors).
 __device__ __forceinline__ int ld_stream(const int32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(int32_t* p, int v) { __stcs(p, v); }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

@@ -18,7 +18,7 @@ import torch  # noqa: E402
 
 import graphgen as gg  # noqa: E402
 
-KEYS = {"heavy_sleep": "jp_heavy_sleep_max", "light_sleep": "jp_light_sleep_max",
+KEYS = {"hw": "jp_heavy_warps", "heavy_sleep": "jp_heavy_sleep_max", "light_sleep": "jp_light_sleep_max",
         "chunk": "chunk_arcs", "heavy_deg": "heavy_degree", "rps": "rounds_per_sync"}
 
 
