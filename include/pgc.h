@@ -153,7 +153,8 @@ const char* pgc_last_error(void);
 /* Thread-local tuning knobs (results never depend on them; tests sweep them to
  * prove it).  Keys: "timing" (0/1: per-phase events), "rounds_per_sync"
  * (>= 1), "heavy_degree" (>= 32), "chunk_arcs"
- * (>= 256), "jp_heavy_warps" (1..7), "jp_heavy_sleep_max" / "jp_light_sleep_max" (ns, >= 0), "block_threads" (64..1024, multiple of 32).
+ * (>= 256), "jp_heavy_warps" (1..7), "jp_heavy_sleep_max" / "jp_light_sleep_max" (ns, >= 0), "jp_watchdog_ms" (a stalled JP
+ * kernel returns PGC_EINTERNAL after this long, default 20000), "block_threads" (64..1024, multiple of 32).
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

@@ -14,7 +14,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libpgc.so")
+# PGC_LIB may point at another build of the same ABI (A/B experiments only)
+SO_PATH = os.environ.get("PGC_LIB") or os.path.join(_HERE, "libpgc.so")
 
 if not os.path.exists(SO_PATH):
     raise ImportError(f"libpgc.so not found at {SO_PATH}: build it with "
@@ -73,8 +74,9 @@ _lib.pgc_set_tuning.restype = ctypes.c_int
 _lib.pgc_set_tuning.argtypes = [ctypes.c_char_p, _i64]
 _lib.pgc_version.restype = ctypes.c_int
 _lib.pgc_version.argtypes = []
-_lib.pgc_debug_set_trace.restype = ctypes.c_int
-_lib.pgc_debug_set_trace.argtypes = [_vp, _vp, _i64]
+if hasattr(_lib, "pgc_debug_set_trace"):
+    _lib.pgc_debug_set_trace.restype = ctypes.c_int
+    _lib.pgc_debug_set_trace.argtypes = [_vp, _vp, _i64]
 
 
 class PGCError(RuntimeError):

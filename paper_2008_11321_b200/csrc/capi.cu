@@ -372,6 +372,10 @@ int pgc_set_tuning(const char* key, int64_t value) {
     g_tune.jp_heavy_warps = (int)value;
     return PGC_OK;
   }
+  if (!strcmp(key, "jp_watchdog_ms") && value >= 1 && value <= 3600000) {
+    g_tune.jp_watchdog_ms = (int)value;
+    return PGC_OK;
+  }
   if (!strcmp(key, "jp_heavy_sleep_max") && value >= 0 && value <= 1000000) {
     g_tune.jp_heavy_sleep_max = (int)value;
     return PGC_OK;

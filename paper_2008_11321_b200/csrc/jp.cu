@@ -401,6 +401,19 @@ __device__ __forceinline__ void bm_set(unsigned* bm, int cc, int wbase) {
   }
 }
 
+__device__ __forceinline__ int vload(const int* p) { return *(volatile const int*)p; }
+
+// Watchdog: a JP kernel running past its budget reports a stall (st->err = 5)
+// instead of hanging the device.  Idle spin iterations check only the local
+// %globaltimer (no memory traffic on the polling path).
+__device__ __forceinline__ bool stalled(State* st, unsigned long long deadline) {
+  if (globaltimer() > deadline) {
+    st->err = 5;
+    return true;
+  }
+  return false;
+}
+
 // Heavy path, one warp per vertex: examine preds [from, np) in strips of 4x32
 // (4 independent loads in flight per lane), OR colored ones into the window,
 // queue pending ones in the warp's list.  Returns the index to resume from when
@@ -441,7 +454,9 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
                                                       unsigned heavy_sleep_max,
                                                       unsigned light_sleep_max,
                                                       unsigned long long* tr_grab,
-                                                      unsigned long long* tr_done) {
+                                                      unsigned long long* tr_done,
+                                                      unsigned long long watchdog_ns) {
+  const unsigned long long deadline = globaltimer() + watchdog_ns;
   // heavy-warp state: window bitmap + pending preds, per warp
   __shared__ unsigned s_bm[kJpWarps][kHeavyWin / 32];
   __shared__ int s_pend[kJpWarps][kPendCap];
@@ -499,11 +514,16 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
           if (progress) {
             sleep_ns = 16;
           } else {
+            if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+              found = -1;
+              break;
+            }
             __nanosleep(sleep_ns);
             sleep_ns = min(sleep_ns * 2, heavy_sleep_max);
           }
         }
         __syncwarp();
+        if (found < 0) break;  // stalled (watchdog)
         // GetColor inside this window: the first zero bit
         const unsigned z0 = ~bm[lane], z1 = ~bm[lane + 32];
         const unsigned b0 = __ballot_sync(0xffffffffu, z0 != 0);
@@ -519,6 +539,7 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
         }
         __syncwarp();
       }
+      if (found < 0) break;  // stalled: the host reports PGC_EINTERNAL
       if (lane == 0) {
         st_relaxed(color + v, found);
         if (tr_done) tr_done[v] = globaltimer();
@@ -531,7 +552,7 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
       int t = 0;
       if (lane == 0) t = atomicAdd(&st->ticket_light, 32);
       t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= nlight) break;
+      if (t >= nlight || globaltimer() > deadline) break;
       const int64_t pos = nheavy + (int64_t)t + lane;
       const bool valid = pos < n;
       int v = 0, np = 0;
@@ -609,6 +630,7 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
         if (__ballot_sync(0xffffffffu, progress)) {
           sleep_ns = 32;
         } else {
+          if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) break;
           __nanosleep(sleep_ns);
           sleep_ns = min(sleep_ns * 2, light_sleep_max);
         }
@@ -637,9 +659,11 @@ int jp_color_run(Ctx& c, int32_t* color) {
                k_jp_color<<<c.nsm * occ, kJpBlock, 0, c.st>>>(
                    c.n, c.off, c.P, c.npred, c.order, color, c.state, c.tune.jp_heavy_warps,
                    (unsigned)c.tune.jp_heavy_sleep_max, (unsigned)c.tune.jp_light_sleep_max,
-                   c.trace_grab, c.trace_done));
+                   c.trace_grab, c.trace_done, (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
   }
   if (int e = sync_state(c)) return e;
+  if (c.h_state->err == 5)
+    return fail(4, "JP coloring stalled: no progress within %d ms (watchdog)", c.tune.jp_watchdog_ms);
   if (c.n > 0 && c.h_state->sorted != c.n)
     return fail(4, "priority order placed %d of %lld vertices", c.h_state->sorted,
                 (long long)c.n);

@@ -62,6 +62,7 @@ struct Tuning {
   int jp_heavy_warps = 2;         // warps per 8-warp JP block serving heavy vertices (1..7)
   int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
   int jp_light_sleep_max = 8192;  // ns, same for light warps
+  int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
   int block_threads = 256;
 };
 
