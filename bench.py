@@ -254,7 +254,7 @@ def run_pgc(args):
     # ---- timed region B: same steps with per-launch CUDA events (attribution) ----
     pgc.set_tuning("timing", 1)
     groups = {"t_select_ms": [], "t_update_ms": [], "t_adg_other_ms": [], "t_order_ms": [],
-              "t_jp_ms": [], "t_total_ms": []}
+              "t_core_ms": [], "t_jp_ms": [], "t_total_ms": []}
     for _ in range(args.steps):
         step()
         s = pgc.last_stats()
@@ -267,7 +267,7 @@ def run_pgc(args):
     model = algorithmic_bytes(n, nnz, m, X, sum_active)
     peak, peak_kind = peak_gbs()
     kern = {"update": ("k_update_light+k_update_heavy", gmean["t_update_ms"], model["update"]),
-            "jp": ("k_jp_color", gmean["t_jp_ms"], model["jp"]),
+            "jp": ("k_jp_bulk", gmean["t_jp_ms"], model["jp"]),
             "select": ("k_adg_select", gmean["t_select_ms"], model["select"]),
             "order": ("order (bucket sort)", gmean["t_order_ms"], model["order"])}
     dom = max(kern, key=lambda k: kern[k][1])
@@ -286,7 +286,7 @@ def run_pgc(args):
                    "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB L2); no flush" %
                          ((8 * (n + 1) + 4 * nnz) / 1e9)},
         "colors": K, "rounds": T, "cross_edges": X, "sum_active": sum_active,
-        "heavy_vertices": st["heavy_vertices"],
+        "core_vertices": st["core_vertices"], "core_ctas": st["core_ctas"],
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "bytes_per_launch": kbytes, "ms_per_launch": kms,

@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define PGC_VERSION 1
+#define PGC_VERSION 2
 
 enum pgc_status {
   PGC_OK = 0,          /* success                                                  */
@@ -84,14 +84,18 @@ typedef struct pgc_stats {
   int64_t sum_active;      /* sum over rounds of |U_l| (Lemma 2 work term)  */
   int64_t cross_edges;     /* X: decrements applied to surviving vertices, over all rounds */
   int64_t pred_arcs;       /* sum_v |pred(v)|; equals m for a valid graph                 */
-  int64_t heavy_vertices;  /* vertices colored by the warp-per-vertex path (|pred| > 62)  */
+  int64_t core_vertices;   /* JP: length of the priority prefix colored by the cluster
+                              "core" engine (0 = everything by the bulk dataflow)         */
   int32_t kernel_launches; /* CUDA kernels this call launched                             */
   int32_t host_syncs;      /* stream synchronisations this call performed                 */
+  int32_t core_ctas;       /* JP: thread-block cluster size of the core engine (0 = none) */
+  int32_t pad0;
   /* Device time per kernel group, from CUDA events on the call's stream; all -1
    * unless pgc_set_tuning("timing", 1).  Groups: ADG select (a2/a3), ADG UPDATE
    * with fused JP Part 1 (a4/a7), other ADG kernels (init, finalize), the
-   * priority-order sort, JP coloring (a8/a9), and the whole call. */
-  float t_select_ms, t_update_ms, t_adg_other_ms, t_order_ms, t_jp_ms, t_total_ms;
+   * priority-order sort, the JP core (selection, list rewrite, cluster kernel),
+   * the JP bulk dataflow (a8/a9), and the whole call. */
+  float t_select_ms, t_update_ms, t_adg_other_ms, t_order_ms, t_core_ms, t_jp_ms, t_total_ms;
 } pgc_stats;
 
 /* Bytes of device workspace the entry points below need for a graph with n
@@ -151,10 +155,16 @@ int pgc_last_stats(pgc_stats* out);
 const char* pgc_last_error(void);
 
 /* Thread-local tuning knobs (results never depend on them; tests sweep them to
- * prove it).  Keys: "timing" (0/1: per-phase events), "rounds_per_sync"
- * (>= 1), "heavy_degree" (>= 32), "chunk_arcs"
- * (>= 256), "jp_heavy_warps" (1..7), "jp_heavy_sleep_max" / "jp_light_sleep_max" (ns, >= 0), "jp_watchdog_ms" (a stalled JP
- * kernel returns PGC_EINTERNAL after this long, default 20000), "block_threads" (64..1024, multiple of 32).
+ * prove it).  Keys and ranges:
+ *   "timing" 0/1 (per-kernel-group CUDA events), "rounds_per_sync" >= 1,
+ *   "heavy_degree" >= 32 (ADG UPDATE edge-chunks rows longer than this),
+ *   "chunk_arcs" >= 256, "block_threads" 64..1024 (multiple of 32),
+ *   "jp_sleep_max" ns >= 0 (backoff cap of idle JP warps), "jp_watchdog_ms"
+ *   (a stalled JP kernel returns PGC_EINTERNAL after this long; default 20000),
+ *   "core_max" 0..65535 (JP core size cap; 0 disables the core engine),
+ *   "core_min_avg" (min mean |pred| of the core prefix), "core_min_n",
+ *   "core_ctas" 0..16 (cluster size; 0 = automatic), "core_arc_cap",
+ *   "core_arcs_per_cta".
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

@@ -40,11 +40,13 @@ class Graph(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("rounds", ctypes.c_int32), ("num_colors", ctypes.c_int32),
                 ("sum_active", ctypes.c_int64), ("cross_edges", ctypes.c_int64),
-                ("pred_arcs", ctypes.c_int64), ("heavy_vertices", ctypes.c_int64),
+                ("pred_arcs", ctypes.c_int64), ("core_vertices", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int32), ("host_syncs", ctypes.c_int32),
+                ("core_ctas", ctypes.c_int32), ("pad0", ctypes.c_int32),
                 ("t_select_ms", ctypes.c_float), ("t_update_ms", ctypes.c_float),
                 ("t_adg_other_ms", ctypes.c_float), ("t_order_ms", ctypes.c_float),
-                ("t_jp_ms", ctypes.c_float), ("t_total_ms", ctypes.c_float)]
+                ("t_core_ms", ctypes.c_float), ("t_jp_ms", ctypes.c_float),
+                ("t_total_ms", ctypes.c_float)]
 
 
 _vp, _i64, _u32, _u64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_size_t

@@ -160,19 +160,25 @@ struct Arc {
 };
 
 // UPDATE for light vertices (deg <= heavy_deg): a warp takes 32 list entries
-// and walks their concatenated adjacencies 32 arcs at a time (warp-level merge
-// path: each arc finds its owner by a 5-step shuffle search over the inclusive
-// degree scan).  Pred slots come from per-owner shared-memory counters.
+// and walks their concatenated adjacencies (warp-level merge path: each arc
+// finds its owner by a 5-step shuffle search over the inclusive degree scan),
+// kStrips strips of 32 arcs in flight (col loads, then state gathers, then
+// classification) so each warp keeps 4 independent requests outstanding.
+// Pred slots: the arcs of one owner are contiguous in a strip, so an arc's
+// rank among its owner's preds is a popc of the pred ballot over the owner's
+// segment; each lane keeps its own vertex's running count in a register (no
+// shared-memory atomics).
+constexpr int kStrips = 4;
 template <int MODE>
 __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t* __restrict__ off,
                                                       const int32_t* __restrict__ col,
                                                       const int32_t* __restrict__ Rl,
                                                       int32_t* __restrict__ npred,
                                                       int32_t* __restrict__ P, State* st) {
-  __shared__ int s_cnt[8][32];
   __shared__ unsigned long long s_red[32];
   if (MODE != 2 && st->done) return;
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int lane = lane_id();
+  const unsigned lt = lanemask_lt();
   const int nL = st->nLight;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -197,38 +203,54 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int excl = incl - deg;
-    if (MODE != 0) s_cnt[warp][lane] = 0;
-    __syncwarp();
-    for (int t = 0; t < total; t += 32) {
-      const int a = t + lane;
-      // owner = number of lanes whose inclusive prefix is <= a
-      int lo = 0;
+    int cnt = 0;  // preds of this lane's vertex found so far
+    for (int t0 = 0; t0 < total; t0 += 32 * kStrips) {
+      int u[kStrips], ow[kStrips], g[kStrips];
+      long long oo[kStrips];
 #pragma unroll
-      for (int s = 16; s > 0; s >>= 1) {
-        int x = __shfl_sync(0xffffffffu, incl, lo + s - 1);
-        if (x <= a) lo += s;
+      for (int k = 0; k < kStrips; ++k) {
+        const int a = t0 + 32 * k + lane;
+        // owner = number of lanes whose inclusive prefix is <= a
+        int lo = 0;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+          int x = __shfl_sync(0xffffffffu, incl, lo + s - 1);
+          if (x <= a) lo += s;
+        }
+        ow[k] = lo > 31 ? 31 : lo;
+        oo[k] = __shfl_sync(0xffffffffu, o, ow[k]);
+        const int oe = __shfl_sync(0xffffffffu, excl, ow[k]);
+        u[k] = a < total ? ld_stream(col + oo[k] + (a - oe)) : -1;
       }
-      const int owner = lo > 31 ? 31 : lo;
-      const long long oo = __shfl_sync(0xffffffffu, o, owner);
-      const int oe = __shfl_sync(0xffffffffu, excl, owner);
-      const uint64_t oh = __shfl_sync(0xffffffffu, hv, owner);
-      const int orv = __shfl_sync(0xffffffffu, rv, owner);
-      if (a < total) {
-        const int u = ld_stream(col + oo + (a - oe));
-        const bool pred = A.classify(u, A.gather(u), orv, oh, cut);
-        if (MODE != 0 && pred) {
-          const int k = atomicAdd(&s_cnt[warp][owner], 1);
-          st_stream(P + oo + k, u);
+#pragma unroll
+      for (int k = 0; k < kStrips; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
+#pragma unroll
+      for (int k = 0; k < kStrips; ++k) {
+        const int ts = t0 + 32 * k;  // first arc of this strip
+        const uint64_t oh = MODE != 0 ? __shfl_sync(0xffffffffu, hv, ow[k]) : 0;
+        const int orv = MODE == 2 ? __shfl_sync(0xffffffffu, rv, ow[k]) : 0;
+        const bool pred = u[k] >= 0 && A.classify(u[k], g[k], orv, oh, cut);
+        if (MODE != 0) {
+          const unsigned pb = __ballot_sync(0xffffffffu, pred);
+          const int base = __shfl_sync(0xffffffffu, cnt, ow[k]);
+          const int oe = __shfl_sync(0xffffffffu, excl, ow[k]);
+          const int seg0 = max(0, oe - ts);  // first lane of the owner's segment
+          if (pred) {
+            const int rank = __popc(pb & lt & ~((1u << seg0) - 1u));
+            st_stream(P + oo[k] + base + rank, u[k]);
+          }
+          // own segment in this strip: lanes [lo, hi)
+          const int lo = min(32, max(0, excl - ts)), hi = min(32, max(0, incl - ts));
+          const unsigned mhi = hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u);
+          const unsigned mlo = lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u);
+          cnt += __popc(pb & mhi & ~mlo);
         }
       }
     }
-    __syncwarp();
     if (MODE != 0 && valid) {
-      const int k = s_cnt[warp][lane];
-      npred[v] = k;
-      preds += (unsigned long long)k;
+      npred[v] = cnt;
+      preds += (unsigned long long)cnt;
     }
-    __syncwarp();
   }
   unsigned long long t = block_sum(cut, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(&st->cut, t);
@@ -383,11 +405,12 @@ static int grid_for(const Ctx& c, int per_sm) { return c.nsm * per_sm; }
 
 template <int MODE>
 static int launch_update(Ctx& c, const Arc<MODE>& A) {
-  const int G = grid_for(c, 8);
+  const int GL = wave_grid(c, k_update_light<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_light",
-             k_update_light<MODE><<<G, 256, 0, c.st>>>(A, c.off, c.col, c.Rl, c.npred, c.P, c.state));
+             k_update_light<MODE><<<GL, 256, 0, c.st>>>(A, c.off, c.col, c.Rl, c.npred, c.P, c.state));
+  const int GH = wave_grid(c, k_update_heavy<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_heavy",
-             k_update_heavy<MODE><<<G, 256, 0, c.st>>>(A, c.off, c.col, c.chunks, c.npred, c.P,
+             k_update_heavy<MODE><<<GH, 256, 0, c.st>>>(A, c.off, c.col, c.chunks, c.npred, c.P,
                                                        c.state, c.tune.chunk_arcs));
   return 0;
 }

@@ -34,6 +34,20 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// Resident blocks per SM of a kernel (cached per thread; a handful of entries).
+int occupancy_cached(const void* kernel, int block, size_t smem) {
+  struct E { const void* k; int block; size_t smem; int occ; };
+  static thread_local std::vector<E> cache;
+  for (const E& e : cache)
+    if (e.k == kernel && e.block == block && e.smem == smem) return e.occ;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem) != cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  cache.push_back({kernel, block, smem, occ});
+  return occ;
+}
+
 Layout make_layout(int64_t n, int64_t nnz) {
   Layout L = {};
   size_t a = 0;
@@ -67,6 +81,9 @@ Layout make_layout(int64_t n, int64_t nnz) {
   const int64_t big = L.nb_cap > 2 * L.range_cap + 1 ? L.nb_cap : 2 * L.range_cap + 1;
   L.scan_tmp_cap = big / kScanTile + 4;
   L.scan_tmp = take(4 * (size_t)L.scan_tmp_cap);
+  const size_t ncore = (size_t)(n < kCoreCap ? n : kCoreCap);
+  L.cbase = take(8 * ncore);
+  L.cnp = take(4 * ncore);
   L.total = a;
   return L;
 }
@@ -122,6 +139,8 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.bcnt = (int32_t*)(b + c.lay.bcnt);
   c.bstart = (int32_t*)(b + c.lay.bstart);
   c.scan_tmp = (int32_t*)(b + c.lay.scan_tmp);
+  c.cbase = (int64_t*)(b + c.lay.cbase);
+  c.cnp = (int32_t*)(b + c.lay.cnp);
   if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));
   c.h_state = g_hstate;
   if (g_trace_grab && g_trace_n == g->n) {
@@ -187,16 +206,17 @@ static void call_begin(Ctx& c) {
 
 // Called after the call's final synchronisation.
 static void call_end(Ctx& c, int rounds, int colors, long long sum_active,
-                     unsigned long long cross, unsigned long long preds, int nheavy) {
+                     unsigned long long cross, unsigned long long preds, int ncore) {
   g_stats.rounds = rounds;
   g_stats.num_colors = colors;
   g_stats.sum_active = sum_active;
   g_stats.cross_edges = (int64_t)cross;
   g_stats.pred_arcs = (int64_t)preds;
-  g_stats.heavy_vertices = nheavy;
+  g_stats.core_vertices = ncore;
+  g_stats.core_ctas = c.core_ctas;
   g_stats.kernel_launches = c.launches;
   g_stats.host_syncs = c.syncs;
-  float t[kNumGroups] = {-1.f, -1.f, -1.f, -1.f, -1.f};
+  float t[kNumGroups] = {-1.f, -1.f, -1.f, -1.f, -1.f, -1.f};
   float total = -1.f;
   if (g_log.on) {
     cudaEventRecord(g_total[1], c.st);
@@ -213,6 +233,7 @@ static void call_end(Ctx& c, int rounds, int colors, long long sum_active,
   g_stats.t_update_ms = t[kGUpdate];
   g_stats.t_adg_other_ms = t[kGAdgOther];
   g_stats.t_order_ms = t[kGOrder];
+  g_stats.t_core_ms = t[kGCore];
   g_stats.t_jp_ms = t[kGJp];
   g_stats.t_total_ms = total;
 }
@@ -252,11 +273,13 @@ int pgc_jp_color(const pgc_graph* g, const int32_t* round, uint64_t seed, int32_
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
   call_begin(c);
+  c.round_key = round;
+  c.seed = seed;
   if (int e = jp_setup_run(c, round, seed, color_out)) return e;
   if (int e = jp_order_run(c, round, seed, false)) return e;
   if (int e = jp_color_run(c, color_out)) return e;
   *num_colors = c.h_state->K;
-  call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.h_state->nheavy);
+  call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.h_state->core_n);
   return PGC_OK;
 }
 
@@ -276,11 +299,13 @@ int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uin
   const int T = c.h_state->T;
   const long long sum_active = c.h_state->sum_active;
   const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
+  c.round_key = round_out;
+  c.seed = seed;
   if (int e = jp_order_run(c, round_out, seed, true)) return e;
   if (int e = jp_color_run(c, color_out)) return e;
   *num_rounds = T;
   *num_colors = c.h_state->K;
-  call_end(c, T, c.h_state->K, sum_active, cross, preds, c.h_state->nheavy);
+  call_end(c, T, c.h_state->K, sum_active, cross, preds, c.h_state->core_n);
   return PGC_OK;
 }
 
@@ -368,22 +393,23 @@ int pgc_set_tuning(const char* key, int64_t value) {
     g_tune.chunk_arcs = (int)value;
     return PGC_OK;
   }
-  if (!strcmp(key, "jp_heavy_warps") && value >= 1 && value <= 7) {
-    g_tune.jp_heavy_warps = (int)value;
-    return PGC_OK;
-  }
-  if (!strcmp(key, "jp_watchdog_ms") && value >= 1 && value <= 3600000) {
-    g_tune.jp_watchdog_ms = (int)value;
-    return PGC_OK;
-  }
-  if (!strcmp(key, "jp_heavy_sleep_max") && value >= 0 && value <= 1000000) {
-    g_tune.jp_heavy_sleep_max = (int)value;
-    return PGC_OK;
-  }
-  if (!strcmp(key, "jp_light_sleep_max") && value >= 0 && value <= 1000000) {
-    g_tune.jp_light_sleep_max = (int)value;
-    return PGC_OK;
-  }
+  struct Key { const char* name; long long lo, hi; long long* l; int* i; };
+  const Key keys[] = {
+      {"jp_watchdog_ms", 1, 3600000, nullptr, &g_tune.jp_watchdog_ms},
+      {"jp_sleep_max", 0, 1000000, nullptr, &g_tune.jp_sleep_max},
+      {"core_max", 0, 65535, nullptr, &g_tune.core_max},
+      {"core_min_avg", 0, 1 << 30, nullptr, &g_tune.core_min_avg},
+      {"core_min_n", 1, 65535, nullptr, &g_tune.core_min_n},
+      {"core_ctas", 0, 16, nullptr, &g_tune.core_ctas},
+      {"core_arc_cap", 0, 1ll << 40, &g_tune.core_arc_cap, nullptr},
+      {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
+  };
+  for (const Key& k : keys)
+    if (!strcmp(key, k.name) && value >= k.lo && value <= k.hi) {
+      if (k.l) *k.l = value;
+      else *k.i = (int)value;
+      return PGC_OK;
+    }
   if (!strcmp(key, "block_threads") && value >= 64 && value <= 1024 && value % 32 == 0) {
     g_tune.block_threads = (int)value;
     return PGC_OK;

@@ -5,27 +5,26 @@
 // ADG's fused UPDATE (adg.cu) or by jp_setup_run: pred(v) lives in v's own
 // CSR slot P[off[v] .. off[v] + npred[v]).
 //
-// JP Part 2 runs as a sync-free dataflow instead of level-synchronous
-// frontiers: vertices are placed in one priority order (a topological order
-// of the DAG G_rho) and handed to warps by an atomic
-// ticket; a vertex is colored by GetColor (1135-1138) as soon as every
-// predecessor's color is nonzero -- the Join of line 1132 observed by polling
-// the predecessor's color instead of decrementing a counter.  Deadlock
-// freedom: tickets are taken in priority order and a warp never blocks, so the
-// highest-priority uncolored vertex always belongs to a running warp whose
-// predecessors are all colored.
-//
-// Priority order = stable two-level bucket sort by key
-//   (class, round desc, h desc), class 0 = |pred| > kLightPredMax ("heavy").
-// Both classes are priority-ordered; heavy vertices are colored warp-per-
-// vertex (bitmap windows in shared memory), light ones lane-per-vertex (a
-// 64-bit used-color mask in registers).
+// JP Part 2 (lines 1123-1133) runs without level barriers:
+//   1. jp_order_run  -- the exact priority order (a topological order of the
+//                       DAG G_rho) by a two-level bucket sort.
+//   2. k_jp_core     -- the dense priority prefix ("core", where the long
+//                       dependency chains live) on one thread-block cluster
+//                       with a shared-memory color replica per CTA (DSMEM).
+//   3. k_jp_bulk     -- everything else as a lane-per-vertex dataflow: the
+//                       Join of line 1132 is observed by polling the
+//                       predecessors' colors instead of decrementing a counter.
+// GetColor (lines 1135-1138) = first zero bit of a used-color bitmap window.
 #include <climits>
 #include <cstdio>
+
+#include <cooperative_groups.h>
 
 #include "pgc_internal.cuh"
 
 namespace pgc {
+
+namespace cg = cooperative_groups;
 
 // ------------------------------------------------------------- scan ---------
 __global__ void k_scan_reduce(const int32_t* __restrict__ in, const int* len_ptr, int64_t len_h,
@@ -152,6 +151,11 @@ static int scan_ex(Ctx& c, const int32_t* in, int32_t* out, const int* len_ptr, 
 }
 
 // ------------------------------------------------------------- order --------
+// Exact priority order: round descending, then h = splitmix64(seed ^ v)
+// descending (a topological order of G_rho).
+// Two-level bucket sort: key (round) histogram -> per-round bucket count ~
+// |round| / kBucketTarget (a power of two, indexed by the top hash bits) ->
+// scatter -> sort every bucket by h.
 __global__ void k_key_range(int64_t n, const int32_t* __restrict__ round, State* st) {
   int mn = INT_MAX, mx = INT_MIN;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
@@ -171,9 +175,6 @@ __global__ void k_key_range(int64_t n, const int32_t* __restrict__ round, State*
   }
 }
 
-__device__ __forceinline__ int key_index(int cls, int r, int rmax, int range) {
-  return cls * range + (rmax - r);  // class-major, then round descending
-}
 __device__ __forceinline__ int bucket_count_for(int cnt) {
   if (cnt <= 0) return 0;
   int want = (cnt + kBucketTarget - 1) / kBucketTarget;
@@ -182,31 +183,24 @@ __device__ __forceinline__ int bucket_count_for(int cnt) {
   return b;
 }
 
-// hist1[key index] += 1; privatised in shared memory when the key range is small.
-__global__ void k_hist1(int64_t n, const int32_t* __restrict__ round,
-                        const int32_t* __restrict__ npred, const State* st, int range,
-                        int32_t* __restrict__ hist1, int* nheavy) {
+// hist1[rmax - round[v]] += 1; privatised in shared memory when the key range is small.
+__global__ void k_hist1(int64_t n, const int32_t* __restrict__ round, const State* st, int range,
+                        int32_t* __restrict__ hist1) {
   extern __shared__ int sh[];
   const int rmax = st->rmax;
-  const int L = 2 * range;
-  const bool priv = L <= 8192;
+  const bool priv = range <= 8192;
   if (priv)
-    for (int i = threadIdx.x; i < L; i += blockDim.x) sh[i] = 0;
+    for (int i = threadIdx.x; i < range; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  int heavy = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int cls = npred[v] > kLightPredMax ? 0 : 1;
-    heavy += 1 - cls;
-    const int k = key_index(cls, round[v], rmax, range);
+    const int k = rmax - round[v];
     if (priv) atomicAdd(&sh[k], 1);
     else atomicAdd(&hist1[k], 1);
   }
-  heavy = warp_sum(heavy);
-  if ((threadIdx.x & 31) == 0 && heavy) atomicAdd(nheavy, heavy);
   __syncthreads();
   if (priv)
-    for (int i = threadIdx.x; i < L; i += blockDim.x)
+    for (int i = threadIdx.x; i < range; i += blockDim.x)
       if (sh[i]) atomicAdd(&hist1[i], sh[i]);
 }
 
@@ -215,10 +209,10 @@ __global__ void k_bucket_sizes(int L, const int32_t* __restrict__ hist1, int32_t
     bsz[i] = bucket_count_for(hist1[i]);
 }
 
-__device__ __forceinline__ int bucket_of(int v, int r, int cls, uint64_t seed, int rmax, int range,
+__device__ __forceinline__ int bucket_of(int v, int r, uint64_t seed, int rmax,
                                          const int32_t* __restrict__ hist1,
                                          const int32_t* __restrict__ base1) {
-  const int k = key_index(cls, r, rmax, range);
+  const int k = rmax - r;
   const int B = bucket_count_for(hist1[k]);
   const int lg = 31 - __clz(B);
   const uint64_t h = prio_hash(seed, (uint32_t)v);
@@ -226,38 +220,34 @@ __device__ __forceinline__ int bucket_of(int v, int r, int cls, uint64_t seed, i
   return base1[k] + (B - 1 - hb);  // larger hash -> earlier bucket
 }
 
-__global__ void k_hist2(int64_t n, const int32_t* __restrict__ round,
-                        const int32_t* __restrict__ npred, uint64_t seed, const State* st,
-                        int range, const int32_t* __restrict__ hist1,
+__global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, uint64_t seed,
+                        const State* st, const int32_t* __restrict__ hist1,
                         const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt) {
   const int rmax = st->rmax;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int cls = npred[v] > kLightPredMax ? 0 : 1;
-    const int b = bucket_of((int)v, round[v], cls, seed, rmax, range, hist1, base1);
+    const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
     atomicAdd(&bcnt[b], 1);
   }
 }
 
-__global__ void k_scatter(int64_t n, const int32_t* __restrict__ round,
-                          const int32_t* __restrict__ npred, uint64_t seed, const State* st,
-                          int range, const int32_t* __restrict__ hist1,
+__global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, uint64_t seed,
+                          const State* st, const int32_t* __restrict__ hist1,
                           const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
                           const int32_t* __restrict__ bstart, int32_t* __restrict__ order) {
   const int rmax = st->rmax;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int cls = npred[v] > kLightPredMax ? 0 : 1;
-    const int b = bucket_of((int)v, round[v], cls, seed, rmax, range, hist1, base1);
+    const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
     const int pos = bstart[b] + atomicSub(&bcnt[b], 1) - 1;
     order[pos] = (int)v;
   }
 }
 
-// Sort every bucket by h descending (bucket = same class and round, same top
-// hash bits).  One lane per bucket (insertion sort in registers, <= 16
-// entries, the common case at mean occupancy 4..8); larger buckets are
-// ranked by a whole warp afterwards.
+// Sort every bucket by h descending (bucket = same round, same top hash
+// bits).  One lane per bucket (insertion sort in registers, <= 16 entries, the
+// common case at mean occupancy 4..8); larger buckets are ranked by a whole
+// warp afterwards.
 constexpr int kLaneSortMax = 16;
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
                               int32_t* __restrict__ order, uint64_t seed) {
@@ -339,7 +329,6 @@ __global__ void k_order_setup(State* st, int rmax_host, int use_host) {
     st->rmin = 1;
     st->rmax = rmax_host;
   }
-  st->nheavy = 0;
   st->nbuckets = 0;
   st->sorted = 0;
 }
@@ -362,47 +351,30 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) 
   const int64_t range = (int64_t)rmax - rmin + 1;
   if (range < 1 || range > c.lay.range_cap)
     return fail(1, "round[] value range %lld exceeds n + 65536", (long long)range);
-  const int L = (int)(2 * range);
+  const int L = (int)range;
   PGC_LAUNCH(c, kGOrder, "k_zero_i32", k_zero_i32<<<G, 256, 0, c.st>>>(c.hist1, L));
   const size_t shb = L <= 8192 ? (size_t)L * sizeof(int) : 0;
   PGC_LAUNCH(c, kGOrder, "k_hist1",
-             k_hist1<<<G, 256, shb, c.st>>>(c.n, round, c.npred, c.state, (int)range, c.hist1,
-                                            &c.state->nheavy));
+             k_hist1<<<G, 256, shb, c.st>>>(c.n, round, c.state, L, c.hist1));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sizes",
              k_bucket_sizes<<<G, 256, 0, c.st>>>(L, c.hist1, c.base1));
   if (int e = scan_ex(c, c.base1, c.base1, nullptr, L, L, &c.state->nbuckets)) return e;
   PGC_LAUNCH(c, kGOrder, "k_zero_i32_dev",
              k_zero_i32_dev<<<G, 256, 0, c.st>>>(c.bcnt, &c.state->nbuckets, 1));
   PGC_LAUNCH(c, kGOrder, "k_hist2",
-             k_hist2<<<G, 256, 0, c.st>>>(c.n, round, c.npred, seed, c.state, (int)range, c.hist1,
-                                          c.base1, c.bcnt));
+             k_hist2<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt));
   if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
                       &c.state->sorted))
     return e;
   PGC_LAUNCH(c, kGOrder, "k_scatter",
-             k_scatter<<<G, 256, 0, c.st>>>(c.n, round, c.npred, seed, c.state, (int)range, c.hist1,
-                                            c.base1, c.bcnt, c.bstart, c.order));
+             k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
+                                            c.bstart, c.order));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
              k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.order, seed));
   return 0;
 }
 
-// ------------------------------------------------------------- color --------
-constexpr int kJpBlock = 256;
-constexpr int kJpWarps = kJpBlock / 32;
-constexpr int kPendCap = 256;          // pending-pred list capacity per heavy warp (smem)
-constexpr int kLightBatch = 8;         // pred loads in flight per light lane
-
-// OR color cc into the window bitmap (colors wbase+1 .. wbase+kHeavyWin).
-__device__ __forceinline__ void bm_set(unsigned* bm, int cc, int wbase) {
-  if (cc > wbase && cc <= wbase + kHeavyWin) {
-    const int bit = cc - wbase - 1;
-    atomicOr(&bm[bit >> 5], 1u << (bit & 31));
-  }
-}
-
-__device__ __forceinline__ int vload(const int* p) { return *(volatile const int*)p; }
-
+// ------------------------------------------------------------- shared -------
 // Watchdog: a JP kernel running past its budget reports a stall (st->err = 5)
 // instead of hanging the device.  Idle spin iterations check only the local
 // %globaltimer (no memory traffic on the polling path).
@@ -414,227 +386,401 @@ __device__ __forceinline__ bool stalled(State* st, unsigned long long deadline) 
   return false;
 }
 
-// Heavy path, one warp per vertex: examine preds [from, np) in strips of 4x32
-// (4 independent loads in flight per lane), OR colored ones into the window,
-// queue pending ones in the warp's list.  Returns the index to resume from when
-// the pending list is full, np when every pred was examined.
-__device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t pb, int np,
-                                          int from, const int32_t* color, unsigned* bm, int wbase,
-                                          int* plist, int& npend) {
+// ------------------------------------------------------------- core ---------
+// JP on the "core": the longest prefix of the priority order whose vertices
+// average >= core_min_avg preds (the dense, deep part of G_rho: on R-MAT 24 the
+// top 55K vertices carry 4 146 of the 4 625 JP levels).  A priority prefix is
+// closed under pred (preds have higher priority), so the core is colored
+// before and independently of everything else.  It runs on ONE thread-block
+// cluster: every CTA keeps a u16 replica of all core colors in shared memory;
+// a vertex is colored by a warp of CTA (p mod C) (p = its core position), which
+// reads its pred list -- rewritten to u16 core positions by k_core_lists -- and
+// looks every pred color up in its LOCAL replica, waits on uncolored preds by
+// polling local shared memory, takes GetColor from a
+// 2048-color bitmap window, and publishes the color to all C replicas with
+// DSMEM stores (plus the global color[]).  A dependency hop thus costs one
+// DSMEM store + a local shared-memory poll instead of an L2 round trip.
+constexpr int kCoreBlock = 1024;
+constexpr int kCoreWarps = kCoreBlock / 32;
+constexpr int kCoreWin = 2048;   // colors per bitmap window (64 x u32)
+constexpr int kCorePend = 256;   // pending-pred list capacity per warp
+
+// One block: NC = the longest prefix p <= min(n, core_max) of the priority
+// order with sum(npred) >= min_avg * p and sum(npred) <= arc_cap.
+__global__ void __launch_bounds__(1024) k_core_select(int64_t n, const int32_t* __restrict__ order,
+                                                      const int32_t* __restrict__ npred, State* st,
+                                                      int core_max, int min_avg,
+                                                      long long arc_cap) {
+  __shared__ long long s_w[32];
+  __shared__ unsigned long long s_best;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int L = (int)(n < (int64_t)core_max ? n : (int64_t)core_max);
+  const int per = (L + blockDim.x - 1) / blockDim.x;
+  const int t0 = threadIdx.x * per;
+  if (threadIdx.x == 0) s_best = 0;
+  long long loc = 0;
+  for (int k = 0; k < per; ++k)
+    if (t0 + k < L) loc += npred[order[t0 + k]];
+  long long incl = loc;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    long long y = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= s) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    long long w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+    long long wi = w;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, wi, s);
+      if (lane >= s) wi += y;
+    }
+    s_w[lane] = wi - w;
+  }
+  __syncthreads();
+  long long run = s_w[warp] + incl - loc;
+  unsigned long long best = 0;
+  for (int k = 0; k < per; ++k) {
+    const int p = t0 + k;
+    if (p >= L) break;
+    run += npred[order[p]];  // sum over the prefix of length p + 1
+    if (run >= (long long)min_avg * (p + 1) && run <= arc_cap)
+      best = ((unsigned long long)(p + 1) << 32) | (unsigned long long)run;
+  }
+  atomicMax(&s_best, best);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->core_n = (int)(s_best >> 32);
+    st->core_arcs = (long long)(s_best & 0xffffffffull);
+  }
+}
+
+__global__ void k_core_pos(const int32_t* __restrict__ order, const State* st,
+                           int32_t* __restrict__ pos) {
+  const int NC = st->core_n;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < NC; p += gridDim.x * blockDim.x)
+    pos[order[p]] = p;
+}
+
+// Warp per core vertex: rewrite its pred list in place (P slot, int32 ids ->
+// u16 core positions at the start of the same slot) and record (slot, |pred|).
+__global__ void k_core_lists(const int64_t* __restrict__ off, const int32_t* __restrict__ order,
+                             const int32_t* __restrict__ npred, const int32_t* __restrict__ pos,
+                             int32_t* P, int64_t* __restrict__ cbase, int32_t* __restrict__ cnp,
+                             const State* st) {
   const int lane = lane_id();
+  const int NC = st->core_n;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < NC; p += nw) {
+    const int v = order[p];
+    const int np = npred[v];
+    const int64_t b = off[v];
+    if (lane == 0) {
+      cbase[p] = b;
+      cnp[p] = np;
+    }
+    uint16_t* L = reinterpret_cast<uint16_t*>(P + b);
+    for (int i0 = 0; i0 < np; i0 += 32) {
+      const int i = i0 + lane;
+      const int y = i < np ? pos[P[b + i]] : 0;
+      __syncwarp();  // every lane has read its int32 entry before any u16 lands
+      if (i < np) L[i] = (uint16_t)y;
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ int ld_vol_u16(const uint16_t* p) {
+  return *(volatile const uint16_t*)p;
+}
+
+// OR color cc into the window bitmap (colors wbase+1 .. wbase+kCoreWin).
+__device__ __forceinline__ void bm_set(unsigned* bm, int cc, int wbase) {
+  const int bit = cc - wbase - 1;
+  if (bit >= 0 && bit < kCoreWin) atomicOr(&bm[bit >> 5], 1u << (bit & 31));
+}
+
+// Examine core preds [from, np) in strips of 4x32: colored ones go into the
+// window, uncolored ones into the warp's pending list.  Returns where to resume
+// when the list is full, np when every pred was examined.
+__device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np, int from,
+                                         const uint16_t* cc, unsigned* bm, int wbase,
+                                         uint16_t* plist, int& npend) {
+  const int lane = lane_id();
+  const unsigned lt = lanemask_lt();
   for (int i0 = from; i0 < np; i0 += 128) {
-    int u[4], cc[4];
+    int q[4], c[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int i = i0 + 32 * k + lane;
-      u[k] = i < np ? __ldg(P + pb + i) : -1;
+      q[k] = i < np ? (int)__ldg(L + i) : -1;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+    for (int k = 0; k < 4; ++k) c[k] = q[k] >= 0 ? ld_vol_u16(cc + q[k]) : 1;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const bool pend = u[k] >= 0 && cc[k] == 0;
-      if (u[k] >= 0 && cc[k]) bm_set(bm, cc[k], wbase);
+      const bool pend = q[k] >= 0 && c[k] == 0;
+      if (q[k] >= 0 && c[k]) bm_set(bm, c[k], wbase);
       const unsigned bal = __ballot_sync(0xffffffffu, pend);
       const int cnt = __popc(bal);
-      if (npend + cnt > kPendCap) return i0 + 32 * k;  // strips before k are complete
-      if (pend) plist[npend + __popc(bal & lanemask_lt())] = u[k];
+      if (npend + cnt > kCorePend) return i0 + 32 * k;  // strips before k are complete
+      if (pend) plist[npend + __popc(bal & lt)] = (uint16_t)q[k];
       npend += cnt;
     }
   }
   return np;
 }
 
-__global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t* __restrict__ off,
-                                                      const int32_t* __restrict__ P,
-                                                      const int32_t* __restrict__ npred,
-                                                      const int32_t* __restrict__ order,
-                                                      int32_t* color, State* st,
-                                                      int heavy_warps,
-                                                      unsigned heavy_sleep_max,
-                                                      unsigned light_sleep_max,
-                                                      unsigned long long* tr_grab,
-                                                      unsigned long long* tr_done,
-                                                      unsigned long long watchdog_ns) {
-  const unsigned long long deadline = globaltimer() + watchdog_ns;
-  // heavy-warp state: window bitmap + pending preds, per warp
-  __shared__ unsigned s_bm[kJpWarps][kHeavyWin / 32];
-  __shared__ int s_pend[kJpWarps][kPendCap];
+__global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int32_t* __restrict__ order,
+                                                           const int64_t* __restrict__ cbase,
+                                                           const int32_t* __restrict__ cnp,
+                                                           const int32_t* __restrict__ P,
+                                                           int32_t* color, State* st,
+                                                           unsigned long long watchdog_ns) {
+  extern __shared__ __align__(16) uint16_t s_cc[];  // [NC] color replica (0 = uncolored)
+  __shared__ unsigned s_bm[kCoreWarps][kCoreWin / 32];
+  __shared__ uint16_t s_pend[kCoreWarps][kCorePend];
+  __shared__ int s_ticket;
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int NC = st->core_n;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const int nheavy = st->nheavy;
+  const unsigned lt = lanemask_lt();
+  for (int i = threadIdx.x; i < NC; i += blockDim.x) s_cc[i] = 0;
+  if (threadIdx.x == 0) s_ticket = 0;
+  cl.sync();  // every replica is zeroed before any color is published
+  uint16_t* remote = lane < C ? cl.map_shared_rank(s_cc, lane) : nullptr;
+  const unsigned long long deadline = globaltimer() + watchdog_ns;
+  unsigned* bm = s_bm[warp];
+  uint16_t* plist = s_pend[warp];
   int kmax = 0;
-  if (warp < heavy_warps) {
-    unsigned* bm = s_bm[warp];
-    int* plist = s_pend[warp];
-    for (;;) {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&st->ticket_heavy, 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= nheavy) break;
-      const int v = order[t];
-      const int np = npred[v];
-      const int64_t pb = off[v];
-      if (tr_grab && lane == 0) tr_grab[v] = globaltimer();
-      int found = 0;
-      for (int wbase = 0; !found; wbase += kHeavyWin) {
-        bm[lane] = 0;
-        bm[lane + 32] = 0;
-        __syncwarp();
-        int npend = 0;
-        int over = heavy_scan(P, pb, np, 0, color, bm, wbase, plist, npend);
-        // poll the pending preds until every one is colored (never blocks: a
-        // pass either makes progress or sleeps briefly and retries)
-        unsigned sleep_ns = 16;
-        while (npend > 0 || over < np) {
-          bool progress = false;
-          int keep = 0;
-          for (int j0 = 0; j0 < npend; j0 += 32) {
-            const int j = j0 + lane;
-            int u = 0, cc = 1;
-            if (j < npend) {
-              u = plist[j];
-              cc = ld_relaxed(color + u);
-            }
-            const bool still = j < npend && cc == 0;
-            if (j < npend && cc) bm_set(bm, cc, wbase);
-            const unsigned bal = __ballot_sync(0xffffffffu, still);
-            if (__ballot_sync(0xffffffffu, j < npend && cc != 0)) progress = true;
-            __syncwarp();
-            if (still) plist[keep + __popc(bal & lanemask_lt())] = u;
-            keep += __popc(bal);
-          }
-          npend = keep;
-          __syncwarp();
-          if (over < np) {
-            const int before = over;
-            over = heavy_scan(P, pb, np, over, color, bm, wbase, plist, npend);
-            if (over != before) progress = true;
-          }
-          if (npend == 0 && over >= np) break;
-          if (progress) {
-            sleep_ns = 16;
-          } else {
-            if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
-              found = -1;
-              break;
-            }
-            __nanosleep(sleep_ns);
-            sleep_ns = min(sleep_ns * 2, heavy_sleep_max);
-          }
-        }
-        __syncwarp();
-        if (found < 0) break;  // stalled (watchdog)
-        // GetColor inside this window: the first zero bit
-        const unsigned z0 = ~bm[lane], z1 = ~bm[lane + 32];
-        const unsigned b0 = __ballot_sync(0xffffffffu, z0 != 0);
-        const unsigned b1 = __ballot_sync(0xffffffffu, z1 != 0);
-        if (b0) {
-          const int w = __ffs(b0) - 1;
-          const unsigned z = __shfl_sync(0xffffffffu, z0, w);
-          found = wbase + 32 * w + __ffs(z);
-        } else if (b1) {
-          const int w = __ffs(b1) - 1;
-          const unsigned z = __shfl_sync(0xffffffffu, z1, w);
-          found = wbase + 32 * (w + 32) + __ffs(z);
-        }
-        __syncwarp();
-      }
-      if (found < 0) break;  // stalled: the host reports PGC_EINTERNAL
-      if (lane == 0) {
-        st_relaxed(color + v, found);
-        if (tr_done) tr_done[v] = globaltimer();
-      }
-      kmax = max(kmax, found);
-    }
-  } else {
-    const int64_t nlight = n - nheavy;
-    for (;;) {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&st->ticket_light, 32);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= nlight || globaltimer() > deadline) break;
-      const int64_t pos = nheavy + (int64_t)t + lane;
-      const bool valid = pos < n;
-      int v = 0, np = 0;
-      int64_t pb = 0;
-      unsigned long long mask = 1ull;  // used colors; bit 0 reserved (colors start at 1)
-      unsigned long long pend = 0ull;  // indices of preds still uncolored (np <= 62)
-      if (valid) {
-        v = order[pos];
-        np = npred[v];
-        pb = off[v];
-        if (tr_grab) tr_grab[v] = globaltimer();
-      }
-      // first pass over every pred, kLightBatch loads in flight
-      for (int j0 = 0; j0 < np; j0 += kLightBatch) {
-        int u[kLightBatch], cc[kLightBatch];
-#pragma unroll
-        for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? __ldg(P + pb + j0 + k) : -1;
-#pragma unroll
-        for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
-#pragma unroll
-        for (int k = 0; k < kLightBatch; ++k) {
-          if (u[k] < 0) continue;
-          if (cc[k] == 0) pend |= 1ull << (j0 + k);
-          else if (cc[k] < 64) mask |= 1ull << cc[k];
-        }
-      }
-      // Waiting: each lane watches ONE pending pred (its lowest pending index)
-      // with a single load per poll; only when the watched pred is colored does
-      // it re-examine the remaining pending preds in one batched pass.
-      int watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
-      int watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
-      bool done = !valid;
-      unsigned sleep_ns = 32;
-      for (;;) {
+  bool stall = false;
+  while (!stall) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(&s_ticket, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    const int p = rank + C * k;
+    if (p >= NC) break;
+    const int np = cnp[p];
+    const uint16_t* L = reinterpret_cast<const uint16_t*>(P + cbase[p]);
+    int found = 0;
+    for (int wbase = 0; !found && !stall; wbase += kCoreWin) {
+      bm[lane] = 0;
+      bm[lane + 32] = 0;
+      __syncwarp();
+      int npend = 0;
+      int over = core_scan(L, np, 0, s_cc, bm, wbase, plist, npend);
+      unsigned sleep_ns = 0;
+      while (npend > 0 || over < np) {
         bool progress = false;
-        if (!done && watch_u >= 0) {
-          const int cw = ld_relaxed(color + watch_u);
-          if (cw) {
-            if (cw < 64) mask |= 1ull << cw;
-            pend &= ~(1ull << watch_j);
-            progress = true;
-            // batched re-poll of the other pending preds
-            unsigned long long p = pend;
-            while (p) {
-              int js[kLightBatch], u[kLightBatch], cc[kLightBatch];
-#pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) {
-                js[k] = p ? __ffsll((long long)p) - 1 : -1;
-                p &= p - 1;
-              }
-#pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) u[k] = js[k] >= 0 ? __ldg(P + pb + js[k]) : -1;
-#pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 0;
-#pragma unroll
-              for (int k = 0; k < kLightBatch; ++k)
-                if (cc[k]) {
-                  if (cc[k] < 64) mask |= 1ull << cc[k];
-                  pend &= ~(1ull << js[k]);
-                }
-            }
-            watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
-            watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
+        int keep = 0;
+        for (int j0 = 0; j0 < npend; j0 += 32) {
+          const int j = j0 + lane;
+          int q = 0, cc = 1;
+          if (j < npend) {
+            q = plist[j];
+            cc = ld_vol_u16(s_cc + q);
           }
+          const bool still = j < npend && cc == 0;
+          if (j < npend && cc) bm_set(bm, cc, wbase);
+          const unsigned bal = __ballot_sync(0xffffffffu, still);
+          if (__ballot_sync(0xffffffffu, j < npend && cc != 0)) progress = true;
+          __syncwarp();
+          if (still) plist[keep + __popc(bal & lt)] = (uint16_t)q;
+          keep += __popc(bal);
         }
-        if (!done && watch_u < 0) {  // GetColor: smallest color unused by the preds
-          const int cc = __ffsll((long long)~mask) - 1;
-          st_relaxed(color + v, cc);
-          if (tr_done) tr_done[v] = globaltimer();
-          kmax = max(kmax, cc);
-          done = true;
-          progress = true;
+        npend = keep;
+        __syncwarp();
+        if (over < np) {
+          const int before = over;
+          over = core_scan(L, np, over, s_cc, bm, wbase, plist, npend);
+          if (over != before) progress = true;
         }
-        if (__ballot_sync(0xffffffffu, !done) == 0) break;
-        if (__ballot_sync(0xffffffffu, progress)) {
-          sleep_ns = 32;
+        if (npend == 0 && over >= np) break;
+        if (progress) {
+          sleep_ns = 0;
         } else {
-          if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) break;
-          __nanosleep(sleep_ns);
-          sleep_ns = min(sleep_ns * 2, light_sleep_max);
+          if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+            stall = true;
+            break;
+          }
+          if (sleep_ns) __nanosleep(sleep_ns);
+          sleep_ns = sleep_ns ? min(sleep_ns * 2, 64u) : 8u;
         }
       }
+      __syncwarp();
+      if (stall) break;
+      // GetColor inside this window: the first zero bit
+      const unsigned z0 = ~bm[lane], z1 = ~bm[lane + 32];
+      const unsigned b0 = __ballot_sync(0xffffffffu, z0 != 0);
+      const unsigned b1 = __ballot_sync(0xffffffffu, z1 != 0);
+      if (b0) {
+        const int w = __ffs(b0) - 1;
+        found = wbase + 32 * w + __ffs(__shfl_sync(0xffffffffu, z0, w));
+      } else if (b1) {
+        const int w = __ffs(b1) - 1;
+        found = wbase + 32 * (w + 32) + __ffs(__shfl_sync(0xffffffffu, z1, w));
+      }
+      __syncwarp();
+    }
+    if (stall) break;
+    if (lane < C) *(volatile uint16_t*)(remote + p) = (uint16_t)found;  // publish to every replica
+    if (lane == 0) st_relaxed(color + order[p], found);
+    kmax = max(kmax, found);
+  }
+  kmax = warp_max(kmax);
+  if (lane == 0 && kmax) atomicMax(&st->K, kmax);
+  cl.sync();  // no CTA leaves while a peer may still store into its replica
+}
+
+// ------------------------------------------------------------- bulk ---------
+// JP on the rest of the priority order as a sync-free dataflow, one vertex per
+// lane.  Tickets are taken in priority order (a topological order of G_rho) by
+// free lanes; a lane scans its vertex's preds once (colors of colored preds go
+// into a lane-private 512-color bitmap in shared memory, uncolored preds are
+// compacted in place at the front of the vertex's own P slot), then watches
+// the lowest-priority pending pred with one load per poll; when it is colored
+// the pending list is re-examined.  With no pending pred, GetColor is the
+// first zero bit; the lane stores the color and takes a
+// new ticket.  Deadlock freedom: the highest-priority uncolored vertex has all
+// preds colored, and if it is not held by a lane then no later ticket was
+// handed out either, so some lane is free to take it; no lane ever blocks.
+constexpr int kBulkBlock = 256;
+constexpr int kBulkWords = 16;  // 512-color window per lane
+constexpr int kBulkWin = 32 * kBulkWords;
+constexpr int kBulkBatch = 8;   // pred loads in flight per lane
+
+struct BulkLane {
+  int v = -1, np = 0, wbase = 0, npend = 0, watch = -1;
+  int64_t pb = 0;
+  bool scan = false;
+};
+
+// priority key of u (larger = higher priority): round, then hash
+__device__ __forceinline__ bool lower_prio(int ru, uint64_t hu, int rw, uint64_t hw) {
+  return ru != rw ? ru < rw : hu < hw;
+}
+
+__global__ void __launch_bounds__(kBulkBlock) k_jp_bulk(int64_t n, const int64_t* __restrict__ off,
+                                                       int32_t* P, const int32_t* __restrict__ npred,
+                                                       const int32_t* __restrict__ order,
+                                                       const int32_t* __restrict__ round,
+                                                       uint64_t seed, int32_t* color, State* st,
+                                                       unsigned sleep_max,
+                                                       unsigned long long* tr_grab,
+                                                       unsigned long long* tr_done,
+                                                       unsigned long long watchdog_ns) {
+  __shared__ unsigned s_bm[kBulkWords][kBulkBlock];  // word-major: lane-private, conflict-free
+  const unsigned long long deadline = globaltimer() + watchdog_ns;
+  const int lane = lane_id();
+  const unsigned lt = lanemask_lt();
+  const int NC = st->core_n;
+  const int64_t nb = n - NC;
+  BulkLane s;
+  bool exhausted = false;
+  int kmax = 0;
+  unsigned sleep_ns = 32;
+  auto bm = [&](int w) -> unsigned& { return s_bm[w][threadIdx.x]; };
+  // Re-examine pending preds P[pb, pb+npend): OR colored ones into the
+  // window, compact the rest in place, watch the lowest-priority one.
+  auto recheck = [&]() {
+    int keep = 0, wr = 0x7fffffff;
+    uint64_t wh = ~0ull;
+    s.watch = -1;
+    for (int j0 = 0; j0 < s.npend; j0 += kBulkBatch) {
+      int u[kBulkBatch], c[kBulkBatch];
+#pragma unroll
+      for (int k = 0; k < kBulkBatch; ++k) u[k] = j0 + k < s.npend ? P[s.pb + j0 + k] : -1;
+#pragma unroll
+      for (int k = 0; k < kBulkBatch; ++k) c[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+#pragma unroll
+      for (int k = 0; k < kBulkBatch; ++k) {
+        if (u[k] < 0) continue;
+        if (c[k]) {
+          const int bit = c[k] - s.wbase - 1;
+          if (bit >= 0 && bit < kBulkWin) bm(bit >> 5) |= 1u << (bit & 31);
+        } else {
+          P[s.pb + keep++] = u[k];
+          const int ru = round[u[k]];
+          const uint64_t hu = prio_hash(seed, (uint32_t)u[k]);
+          if (s.watch < 0 || lower_prio(ru, hu, wr, wh)) {
+            s.watch = u[k];
+            wr = ru;
+            wh = hu;
+          }
+        }
+      }
+    }
+    s.npend = keep;
+  };
+  for (;;) {
+    // 1. free lanes take the next tickets (one atomic per warp)
+    const unsigned want = __ballot_sync(0xffffffffu, s.v < 0 && !exhausted);
+    if (want) {
+      const int leader = __ffs(want) - 1;
+      long long t0 = 0;
+      if (lane == leader) t0 = atomicAdd(&st->ticket, (unsigned long long)__popc(want));
+      t0 = __shfl_sync(0xffffffffu, t0, leader);
+      if (s.v < 0 && !exhausted) {
+        const long long t = t0 + __popc(want & lt);
+        if (t < nb) {
+          s.v = order[NC + t];
+          s.np = npred[s.v];
+          s.pb = off[s.v];
+          s.wbase = 0;
+          s.scan = true;
+          if (tr_grab) tr_grab[s.v] = globaltimer();
+        } else {
+          exhausted = true;
+        }
+      }
+    }
+    if (__ballot_sync(0xffffffffu, s.v >= 0) == 0) break;  // all lanes free and out of tickets
+    bool progress = false;
+    // 2. first pass over every pred (or a new color window)
+    if (s.v >= 0 && s.scan) {
+#pragma unroll
+      for (int w = 0; w < kBulkWords; ++w) bm(w) = 0;
+      s.npend = s.np;  // every pred is "pending" until examined
+      recheck();
+      s.scan = false;
+      progress = true;
+    }
+    // 3. poll the watched pred; when it is colored, re-examine the others
+    if (s.v >= 0 && s.npend > 0) {
+      if (ld_relaxed(color + s.watch)) {
+        recheck();
+        progress = true;
+      }
+    }
+    // 4. GetColor once nothing is pending
+    if (s.v >= 0 && !s.scan && s.npend == 0) {
+      int found = 0;
+#pragma unroll
+      for (int w = 0; w < kBulkWords; ++w) {
+        const unsigned z = ~bm(w);
+        if (!found && z) found = s.wbase + 32 * w + __ffs(z);
+      }
+      if (found) {
+        st_relaxed(color + s.v, found);
+        if (tr_done) tr_done[s.v] = globaltimer();
+        kmax = max(kmax, found);
+        s.v = -1;
+      } else {  // all kBulkWin colors of this window used: next window
+        s.wbase += kBulkWin;
+        s.scan = true;
+      }
+      progress = true;
+    }
+    if (__ballot_sync(0xffffffffu, progress)) {
+      sleep_ns = 32;
+    } else {
+      if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) break;
+      __nanosleep(sleep_ns);
+      sleep_ns = min(sleep_ns * 2, sleep_max);
     }
   }
   kmax = warp_max(kmax);
@@ -642,24 +788,107 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_color(int64_t n, const int64_t*
 }
 
 __global__ void k_jp_reset(State* st) {
-  st->ticket_heavy = 0;
-  st->ticket_light = 0;
+  st->ticket = 0;
   st->K = 0;
+  st->core_n = 0;
+  st->core_arcs = 0;
+}
+
+// Largest cluster size (power of two <= want) that k_jp_core can launch with
+// `smem` dynamic bytes; 0 if none.
+static int core_cluster_size(int want, size_t smem) {
+  static thread_local int attr_done = 0;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_done = 1;
+  }
+  if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  for (int C = want; C >= 1; C >>= 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kCoreBlock);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, k_jp_core, &cfg) == cudaSuccess && nclusters >= 1)
+      return C;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+static int pow2_floor(int x) {
+  int p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
 }
 
 int jp_color_run(Ctx& c, int32_t* color) {
   PGC_LAUNCH(c, kGJp, "k_jp_reset", k_jp_reset<<<1, 1, 0, c.st>>>(c.state));
   if (c.n > 0) {
-    static thread_local int occ = 0;
-    if (occ == 0) {
-      PGC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_jp_color, kJpBlock, 0));
-      if (occ < 1) occ = 1;
+    // --- core ---
+    if (c.tune.core_max > 0) {
+      PGC_LAUNCH(c, kGCore, "k_core_select",
+                 k_core_select<<<1, 1024, 0, c.st>>>(c.n, c.order, c.npred, c.state,
+                                                      c.tune.core_max, c.tune.core_min_avg,
+                                                      c.tune.core_arc_cap));
+      if (int e = sync_state(c)) return e;
+      const int NC = c.h_state->core_n;
+      const long long arcs = c.h_state->core_arcs;
+      int C = 0;
+      const size_t smem = ((size_t)NC * 2 + 15) & ~(size_t)15;
+      if (NC >= c.tune.core_min_n) {
+        int want = c.tune.core_ctas > 0
+                       ? c.tune.core_ctas
+                       : (int)((arcs + c.tune.core_arcs_per_cta - 1) / c.tune.core_arcs_per_cta);
+        want = pow2_floor(want < 1 ? 1 : (want > 16 ? 16 : want));
+        C = core_cluster_size(want, smem);
+      }
+      if (C == 0) {
+        PGC_CUDA(cudaMemsetAsync(&c.state->core_n, 0, sizeof(int), c.st));
+      } else {
+        c.core_ctas = C;
+        const int G = c.nsm * 4;
+        PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.order, c.state, c.D));
+        PGC_LAUNCH(c, kGCore, "k_core_lists",
+                   k_core_lists<<<G * 2, 256, 0, c.st>>>(c.off, c.order, c.npred, c.D, c.P,
+                                                         c.cbase, c.cnp, c.state));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(C);
+        cfg.blockDim = dim3(kCoreBlock);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = c.st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = C;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const unsigned long long wd = (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull;
+        PGC_LAUNCH(c, kGCore, "k_jp_core",
+                   PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int32_t*)c.order,
+                                               (const int64_t*)c.cbase, (const int32_t*)c.cnp,
+                                               (const int32_t*)c.P, color, c.state, wd)));
+      }
     }
-    PGC_LAUNCH(c, kGJp, "k_jp_color",
-               k_jp_color<<<c.nsm * occ, kJpBlock, 0, c.st>>>(
-                   c.n, c.off, c.P, c.npred, c.order, color, c.state, c.tune.jp_heavy_warps,
-                   (unsigned)c.tune.jp_heavy_sleep_max, (unsigned)c.tune.jp_light_sleep_max,
-                   c.trace_grab, c.trace_done, (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
+    // --- bulk ---
+    const int G = wave_grid(c, k_jp_bulk, kBulkBlock);
+    PGC_LAUNCH(c, kGJp, "k_jp_bulk",
+               k_jp_bulk<<<G, kBulkBlock, 0, c.st>>>(
+                   c.n, c.off, c.P, c.npred, c.order, c.round_key, c.seed, color, c.state,
+                   (unsigned)c.tune.jp_sleep_max, c.trace_grab, c.trace_done,
+                   (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
   }
   if (int e = sync_state(c)) return e;
   if (c.h_state->err == 5)

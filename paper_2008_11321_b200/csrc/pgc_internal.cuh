@@ -12,9 +12,8 @@ namespace pgc {
 
 constexpr int kWarp = 32;
 constexpr int kMinChunk = 256;        // smallest allowed arcs-per-work-item for chunked vertices
-constexpr int kLightPredMax = 62;     // JP: lane-per-vertex when |pred(v)| <= this (colors fit a u64 mask)
-constexpr int kHeavyWin = 2048;       // JP heavy path: colors per bitmap window (64 x u32 words)
 constexpr int kMaxRoundStats = 4096;  // per-round statistics kept in the workspace
+constexpr int kCoreCap = 65536;       // JP core: at most this many vertices (u16 positions)
 constexpr int kBucketTarget = 8;      // mean bucket occupancy target of the priority-order sort
 constexpr int kScanTile = 4096;       // elements per block in the device-wide scan
 
@@ -38,17 +37,18 @@ struct State {
   // priority-order sort
   int rmin, rmax;              // range of the first priority key
   int nbuckets;                // buckets in use
-  int nheavy;                  // vertices with |pred| > kLightPredMax (they lead the order)
   int sorted;                  // total placed by the scan (== n)
-  // JP dataflow
-  int ticket_heavy, ticket_light;
+  // JP
+  int core_n;                  // |core| = length of the priority prefix colored by k_jp_core
   int K;
+  long long core_arcs;         // sum of |pred| over the core
+  unsigned long long ticket;   // next bulk ticket
 };
 
 // Byte offsets of every workspace region (each 256-byte aligned).
 struct Layout {
   size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, order, hist1, base1, bcnt, bstart,
-      scan_tmp, total;
+      scan_tmp, cbase, cnp, total;
   int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap;
 };
 
@@ -57,17 +57,22 @@ Layout make_layout(int64_t n, int64_t nnz);
 struct Tuning {
   int timing = 0;
   int rounds_per_sync = 8;
-  int heavy_degree = 32;    // vertices with more arcs are split into edge chunks
+  int heavy_degree = 128;   // vertices with more arcs are split into edge chunks
   int chunk_arcs = 1024;    // arcs per chunk work item
-  int jp_heavy_warps = 2;         // warps per 8-warp JP block serving heavy vertices (1..7)
-  int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
-  int jp_light_sleep_max = 8192;  // ns, same for light warps
+  int jp_sleep_max = 2048;  // ns, exponential backoff cap of idle bulk JP warps
   int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
+  int core_max = 65535;           // JP core: max vertices (0 disables the core engine)
+  int core_min_avg = 32;          // JP core: min mean |pred| over the prefix
+  int core_min_n = 256;           // JP core: smaller cores are left to the bulk kernel
+  int core_ctas = 0;              // JP core: cluster size (0 = from core_arcs_per_cta)
+  long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
+  long long core_arcs_per_cta = 4 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
 };
 
 // Kernel groups for per-group device timing (pgc_stats.t_*_ms).
-enum Group { kGSelect = 0, kGUpdate = 1, kGAdgOther = 2, kGOrder = 3, kGJp = 4, kNumGroups = 5 };
+enum Group { kGSelect = 0, kGUpdate = 1, kGAdgOther = 2, kGOrder = 3, kGCore = 4, kGJp = 5,
+             kNumGroups = 6 };
 
 // Everything a phase needs; built by the C-ABI layer from the caller's arguments.
 struct Ctx {
@@ -95,6 +100,11 @@ struct Ctx {
   int32_t* bcnt;
   int32_t* bstart;
   int32_t* scan_tmp;
+  int64_t* cbase;  // JP core: P slot of core position p
+  int32_t* cnp;    // JP core: |pred| of core position p
+  const int32_t* round_key = nullptr;  // JP first priority key (rho_ADG for JP-ADG)
+  uint64_t seed = 0;                   // JP tie-break seed
+  int core_ctas = 0;                   // cluster size used by the last k_jp_core (0 = none)
   State* h_state;  // pinned host mirror
   unsigned long long* trace_grab = nullptr;  // pgc_debug_set_trace (diagnostics)
   unsigned long long* trace_done = nullptr;
@@ -253,6 +263,14 @@ __device__ __forceinline__ T block_sum(T x, T* sm) {
     for (int w = 0; w < nw; ++w) t += sm[w];
   __syncthreads();
   return t;  // valid in thread 0
+}
+
+// Grid of exactly one wave: SMs x resident blocks of `kernel` (cached per kernel).
+// Grid-stride kernels sized this way never run a second, serialised wave.
+int occupancy_cached(const void* kernel, int block, size_t smem);  // capi.cu
+template <typename K>
+inline int wave_grid(const Ctx& c, K kernel, int block, size_t smem = 0) {
+  return c.nsm * occupancy_cached((const void*)kernel, block, smem);
 }
 
 // ---- shared kernels (defined in adg.cu) -----------------------------------

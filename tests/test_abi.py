@@ -39,7 +39,9 @@ def test_exports_are_extern_c():
 
 
 def test_version_and_workspace_sizes():
-    assert pgc.version() == 1
+    hdr = open(os.path.join(ROOT, "include", "pgc.h")).read()
+    declared = int(re.search(r"#define PGC_VERSION (\d+)", hdr).group(1))
+    assert pgc.version() == declared
     assert pgc.workspace_bytes(0, 0) > 0
     a = pgc.workspace_bytes(1000, 10000)
     b = pgc.workspace_bytes(2000, 10000)

@@ -117,6 +117,54 @@ def test_config_parity_large(name):
         assert_parity(g, num, den, 1)
 
 
+@pytest.fixture
+def tuning():
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    touched = {}
+
+    def set_(k, v):
+        touched[k] = True
+        pgc.set_tuning(k, v)
+    yield set_
+    defaults = {"core_max": 65535, "core_min_avg": 32, "core_min_n": 256, "core_ctas": 0,
+                "core_arc_cap": 1 << 30, "core_arcs_per_cta": 4 << 20, "jp_sleep_max": 2048,
+                "heavy_degree": 128, "rounds_per_sync": 8}
+    for k in touched:
+        pgc.set_tuning(k, defaults[k])
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 4, 8, 16])
+def test_core_engine_cluster_sizes(ctas, tuning):
+    """The cluster core engine (DSMEM color replicas) at every cluster size,
+    forced onto graphs with a deep dense prefix, against the oracle."""
+    tuning("core_ctas", ctas)
+    tuning("core_min_n", 1)
+    for g, (num, den) in ((gg.rmat(14, 16, seed=5), (1, 10)), (gg.rmat(13, 32, seed=8), (1, 100))):
+        assert_parity(g, num, den, 11)
+        st = pgc_stats()
+        assert st["core_vertices"] > 0 and st["core_ctas"] >= 1
+
+
+def test_core_engine_whole_graph_and_windows(tuning):
+    """Every vertex in the core (min_avg 0) incl. K_n with > 2048 colors (several
+    bitmap windows), and a core/bulk split right inside a round."""
+    tuning("core_min_avg", 0)
+    tuning("core_min_n", 1)
+    n = 2100
+    g = gg.from_edges(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+    T, K = assert_parity(g, 1, 10, 3)
+    assert K == n and pgc_stats()["core_vertices"] == n
+    for cap in (1, 37, 1000):
+        tuning("core_max", cap)
+        assert_parity(gg.rmat(12, 16, seed=2), 1, 10, 4)
+        assert pgc_stats()["core_vertices"] == cap
+
+
+def pgc_stats():
+    import paper_2008_11321_b200 as pgc
+    return pgc.last_stats()
+
+
 def test_adg_order_only_and_jp_generic_keys():
     g = gg.rmat(13, 8, seed=4)
     pgc, off, col = dev(g)
@@ -150,25 +198,23 @@ def test_jp_key_range_error():
     assert e.value.code == pgc.PGC_EINVAL
 
 
-def test_determinism_across_tuning():
+def test_determinism_across_tuning(tuning):
     g = gg.rmat(14, 16, seed=2)
     pgc, off, col = dev(g)
     ref = None
-    try:
-        for hd in (32, 100, 1024, 1 << 20):
-            for rps in (1, 3, 8):
-                pgc.set_tuning("heavy_degree", hd)
-                pgc.set_tuning("rounds_per_sync", rps)
-                for _ in range(2):
-                    r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 9)
-                    out = (r.cpu().numpy(), c.cpu().numpy(), T, K)
-                    if ref is None:
-                        ref = out
-                    assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
-                    assert out[2:] == ref[2:]
-    finally:
-        pgc.set_tuning("heavy_degree", 1024)
-        pgc.set_tuning("rounds_per_sync", 8)
+    for hd, rps, core, sleep in ((32, 1, 0, 0), (100, 3, 65535, 64), (1024, 8, 500, 8192),
+                                 (1 << 20, 8, 65535, 2048), (128, 2, 0, 100000)):
+        tuning("heavy_degree", hd)
+        tuning("rounds_per_sync", rps)
+        tuning("core_max", core)
+        tuning("jp_sleep_max", sleep)
+        for _ in range(2):
+            r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 9)
+            out = (r.cpu().numpy(), c.cpu().numpy(), T, K)
+            if ref is None:
+                ref = out
+            assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
+            assert out[2:] == ref[2:]
     r_or, _ = O.adg(g, 1, 10)
     c_or, _ = O.jp(g, r_or, 9)
     assert np.array_equal(ref[0], r_or) and np.array_equal(ref[1], c_or)
@@ -210,7 +256,8 @@ def test_timing_stats():
         st = pgc.last_stats()
         for k in ("t_select_ms", "t_update_ms", "t_order_ms", "t_jp_ms", "t_total_ms"):
             assert st[k] > 0, k
-        parts = st["t_select_ms"] + st["t_update_ms"] + st["t_adg_other_ms"] + st["t_order_ms"] + st["t_jp_ms"]
+        parts = (st["t_select_ms"] + st["t_update_ms"] + st["t_adg_other_ms"] + st["t_order_ms"]
+                 + st["t_core_ms"] + st["t_jp_ms"])
         assert parts <= st["t_total_ms"] * 1.01
         assert st["kernel_launches"] > 10 and st["host_syncs"] >= 2
     finally:

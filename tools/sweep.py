@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Tuning sweep on one config: per-group device times for each knob setting.
 
-  python tools/sweep.py --config rmat24 --reps 3 heavy_sleep=0,64,256 light_sleep=512,2048
+  python tools/sweep.py --config rmat24 --reps 3 sleep=512,2048 ctas=0,4,16
 Results never depend on the knobs (checked here against the first setting).
 """
 import argparse
@@ -18,8 +18,9 @@ import torch  # noqa: E402
 
 import graphgen as gg  # noqa: E402
 
-KEYS = {"hw": "jp_heavy_warps", "heavy_sleep": "jp_heavy_sleep_max", "light_sleep": "jp_light_sleep_max",
-        "chunk": "chunk_arcs", "heavy_deg": "heavy_degree", "rps": "rounds_per_sync"}
+KEYS = {"sleep": "jp_sleep_max", "chunk": "chunk_arcs", "heavy_deg": "heavy_degree",
+        "rps": "rounds_per_sync", "core": "core_max", "ctas": "core_ctas", "avg": "core_min_avg",
+        "apc": "core_arcs_per_cta"}
 
 
 def main():
@@ -53,6 +54,8 @@ def main():
             ref = out
         same = bool(np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1]))
         med = {k: float(np.median([x[k] for x in rows])) for k in rows[0] if k.startswith("t_")}
+        med["core_vertices"] = rows[-1]["core_vertices"]
+        med["core_ctas"] = rows[-1]["core_ctas"]
         print(json.dumps({"config": a.config, "knobs": dict(combo), "same": same,
                           "edges_per_s": g.m / (med["t_total_ms"] * 1e-3), **med}), flush=True)
 

@@ -54,9 +54,10 @@ def main():
     tg = tg.cpu().numpy().astype(np.int64)
     td = td.cpu().numpy().astype(np.int64)
     r = rnd.cpu().numpy().astype(np.int64)
-    t0 = tg.min()
-    tg -= t0
-    td -= t0
+    core = tg == 0            # colored by the cluster core engine (not traced)
+    t0 = tg[~core].min() if (~core).any() else 0
+    tg = np.where(core, 0, tg - t0)
+    td = np.where(core, 0, td - t0)
     # oracle levels (JP DAG depth)
     _, _, lvl, J = O.jp(g, rnd.cpu().numpy(), a.seed, levels=True)
     # pred relation and ready time = max done over preds
@@ -78,7 +79,8 @@ def main():
     wait_grab = tg - ready  # >0: the vertex was grabbed after it became ready
     out = {"config": a.config, "tune": a.tune, "n": n, "J": J, "T": T, "K": K,
            "jp_ms": st["t_jp_ms"], "span_ms": float(td.max() / 1e6),
-           "heavy": int(heavy.sum())}
+           "heavy": int(heavy.sum()), "core_vertices": int(core.sum()),
+           "core_ms": st["t_core_ms"]}
     # chain pace: time when each level finished (max done over the level)
     lv_done = np.zeros(J + 1, dtype=np.int64)
     np.maximum.at(lv_done, lvl, td)
@@ -86,7 +88,7 @@ def main():
     marks = sorted(set([1, 10, 100, J // 4, J // 2, 3 * J // 4, J - 50, J - 10, J]))
     out["level_done_us"] = {int(L): float(lv_done[L] / 1e3) for L in marks if 0 < L <= J}
     out["ns_per_level"] = float(lv_done[J] / max(J, 1))
-    for name, m in (("heavy", heavy & has_pred), ("light", ~heavy & has_pred)):
+    for name, m in (("heavy", heavy & has_pred & ~core), ("light", ~heavy & has_pred & ~core)):
         out[f"step_ns_{name}"] = pct(step[m])
         out[f"grab_after_ready_ns_{name}"] = pct(wait_grab[m])
         out[f"done_minus_grab_ns_{name}"] = pct((td - tg)[m])
