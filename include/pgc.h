@@ -159,11 +159,14 @@ const char* pgc_last_error(void);
  *   "timing" 0/1 (per-kernel-group CUDA events), "rounds_per_sync" >= 1,
  *   "heavy_degree" >= 32 (ADG UPDATE edge-chunks rows longer than this),
  *   "chunk_arcs" >= 256, "block_threads" 64..1024 (multiple of 32),
- *   "jp_sleep_max" ns >= 0 (backoff cap of idle JP warps), "jp_watchdog_ms"
+ *   "jp_heavy_warps" 1..7 (warps per 8-warp bulk JP block serving vertices with
+ *   more than 62 preds), "jp_heavy_sleep_max" / "jp_light_sleep_max" ns >= 0
+ *   (backoff caps of waiting bulk JP warps), "jp_watchdog_ms"
  *   (a stalled JP kernel returns PGC_EINTERNAL after this long; default 20000),
  *   "core_max" 0..65535 (JP core size cap; 0 disables the core engine),
  *   "core_min_avg" (min mean |pred| of the core prefix), "core_min_n",
- *   "core_ctas" 0..16 (cluster size; 0 = automatic), "core_arc_cap",
+ *   "core_ctas" 0..16 (cluster size; 0 = automatic), "core_spin_ns" (backoff cap
+ *   of a core warp several preds away from ready), "core_arc_cap",
  *   "core_arcs_per_cta".
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);

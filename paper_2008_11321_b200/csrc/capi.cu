@@ -279,7 +279,7 @@ int pgc_jp_color(const pgc_graph* g, const int32_t* round, uint64_t seed, int32_
   if (int e = jp_order_run(c, round, seed, false)) return e;
   if (int e = jp_color_run(c, color_out)) return e;
   *num_colors = c.h_state->K;
-  call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.h_state->core_n);
+  call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.core_n);
   return PGC_OK;
 }
 
@@ -305,7 +305,7 @@ int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uin
   if (int e = jp_color_run(c, color_out)) return e;
   *num_rounds = T;
   *num_colors = c.h_state->K;
-  call_end(c, T, c.h_state->K, sum_active, cross, preds, c.h_state->core_n);
+  call_end(c, T, c.h_state->K, sum_active, cross, preds, c.core_n);
   return PGC_OK;
 }
 
@@ -396,11 +396,14 @@ int pgc_set_tuning(const char* key, int64_t value) {
   struct Key { const char* name; long long lo, hi; long long* l; int* i; };
   const Key keys[] = {
       {"jp_watchdog_ms", 1, 3600000, nullptr, &g_tune.jp_watchdog_ms},
-      {"jp_sleep_max", 0, 1000000, nullptr, &g_tune.jp_sleep_max},
+      {"jp_heavy_warps", 1, 7, nullptr, &g_tune.jp_heavy_warps},
+      {"jp_heavy_sleep_max", 0, 1000000, nullptr, &g_tune.jp_heavy_sleep_max},
+      {"jp_light_sleep_max", 0, 1000000, nullptr, &g_tune.jp_light_sleep_max},
       {"core_max", 0, 65535, nullptr, &g_tune.core_max},
       {"core_min_avg", 0, 1 << 30, nullptr, &g_tune.core_min_avg},
       {"core_min_n", 1, 65535, nullptr, &g_tune.core_min_n},
       {"core_ctas", 0, 16, nullptr, &g_tune.core_ctas},
+      {"core_spin_ns", 0, 100000, nullptr, &g_tune.core_spin_ns},
       {"core_arc_cap", 0, 1ll << 40, &g_tune.core_arc_cap, nullptr},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };

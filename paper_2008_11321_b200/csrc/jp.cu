@@ -26,6 +26,20 @@ namespace pgc {
 
 namespace cg = cooperative_groups;
 
+// PGC_PROBE builds (tools/micro/build_probe.sh, never the product library)
+// stamp per-vertex phase times into the trace arrays ([4*v + k]) for the
+// core engine's hop breakdown (tools/micro/hop_probe.py).
+#ifdef PGC_PROBE
+#define PROBE_STAMP(arr, v, k) \
+  do {                          \
+    if ((arr) && lane == 0) (arr)[4 * (v) + (k)] = clock64(); \
+  } while (0)
+#else
+#define PROBE_STAMP(arr, v, k) \
+  do {                          \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------- scan ---------
 __global__ void k_scan_reduce(const int32_t* __restrict__ in, const int* len_ptr, int64_t len_h,
                               int32_t* __restrict__ tmp) {
@@ -135,17 +149,17 @@ __global__ void __launch_bounds__(1024) k_scan_down(const int32_t* in, const int
 }
 
 static int scan_ex(Ctx& c, const int32_t* in, int32_t* out, const int* len_ptr, int64_t len_h,
-                   int64_t cap, int* total_out) {
+                   int64_t cap, int* total_out, int group = kGOrder) {
   const int64_t ntiles_cap = (cap + kScanTile - 1) / kScanTile + 1;
   if (ntiles_cap > c.lay.scan_tmp_cap) return fail(4, "scan temp too small");
   const int64_t grid = len_h >= 0 ? (len_h + kScanTile - 1) / kScanTile : ntiles_cap;
   if (grid > 0)
-    PGC_LAUNCH(c, kGOrder, "k_scan_reduce",
+    PGC_LAUNCH(c, group, "k_scan_reduce",
                k_scan_reduce<<<(unsigned)grid, 256, 0, c.st>>>(in, len_ptr, len_h, c.scan_tmp));
-  PGC_LAUNCH(c, kGOrder, "k_scan_tmp",
+  PGC_LAUNCH(c, group, "k_scan_tmp",
              k_scan_tmp<<<1, 1024, 0, c.st>>>(c.scan_tmp, ntiles_cap, len_ptr, len_h, out, total_out));
   if (grid > 0)
-    PGC_LAUNCH(c, kGOrder, "k_scan_down",
+    PGC_LAUNCH(c, group, "k_scan_down",
                k_scan_down<<<(unsigned)grid, 1024, 0, c.st>>>(in, len_ptr, len_h, c.scan_tmp, out));
   return 0;
 }
@@ -386,6 +400,33 @@ __device__ __forceinline__ bool stalled(State* st, unsigned long long deadline) 
   return false;
 }
 
+// ------------------------------------------------------------- byte maps ---
+// GetColor's used-color set as a BYTE map per warp in shared memory: marking
+// color c is a plain st.shared.u8 of 1 (idempotent, so lanes marking colors
+// that share a word never lose an update and need no atomics -- a shared
+// atomicOr costs 2 cycles per lane); the first zero byte is found 32 bytes per
+// ballot.
+__device__ __forceinline__ void bmap_clear(uint8_t* bm, int bytes) {
+  uint4* w = reinterpret_cast<uint4*>(bm);
+  for (int i = lane_id(); i < bytes / 16; i += 32) w[i] = make_uint4(0, 0, 0, 0);
+}
+__device__ __forceinline__ void bmap_mark(uint8_t* bm, int cc, int wbase, int bytes) {
+  const int b = cc - wbase - 1;
+  if (b >= 0 && b < bytes) bm[b] = 1;
+}
+// Index of the first zero byte at or after `from` in the warp's map (BYTES if
+// none); warp-wide.  32 consecutive bytes per probe (conflict-free).
+template <int BYTES>
+__device__ __forceinline__ int bmap_next_zero(const uint8_t* bm, int from) {
+  const int lane = lane_id();
+  for (int b0 = from; b0 < BYTES; b0 += 32) {
+    const int b = b0 + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, b < BYTES && bm[b] == 0);
+    if (m) return b0 + __ffs(m) - 1;
+  }
+  return BYTES;
+}
+
 // ------------------------------------------------------------- core ---------
 // JP on the "core": the longest prefix of the priority order whose vertices
 // average >= core_min_avg preds (the dense, deep part of G_rho: on R-MAT 24 the
@@ -402,8 +443,11 @@ __device__ __forceinline__ bool stalled(State* st, unsigned long long deadline) 
 // DSMEM store + a local shared-memory poll instead of an L2 round trip.
 constexpr int kCoreBlock = 1024;
 constexpr int kCoreWarps = kCoreBlock / 32;
-constexpr int kCoreWin = 2048;   // colors per bitmap window (64 x u32)
-constexpr int kCorePend = 256;   // pending-pred list capacity per warp
+constexpr int kCoreWin = 1024;   // colors per byte-map window
+constexpr int kCorePend = 512;   // pending-pred list capacity per warp
+constexpr int kCoreRun = 32;     // consecutive core positions per CTA run
+// dynamic shared memory ahead of the color replica: bitmaps + pending lists
+constexpr int kCoreFixedSmem = kCoreWarps * kCoreWin + kCoreWarps * kCorePend * 2;
 
 // One block: NC = the longest prefix p <= min(n, core_max) of the priority
 // order with sum(npred) >= min_avg * p and sum(npred) <= arc_cap.
@@ -496,38 +540,47 @@ __device__ __forceinline__ int ld_vol_u16(const uint16_t* p) {
   return *(volatile const uint16_t*)p;
 }
 
-// OR color cc into the window bitmap (colors wbase+1 .. wbase+kCoreWin).
-__device__ __forceinline__ void bm_set(unsigned* bm, int cc, int wbase) {
-  const int bit = cc - wbase - 1;
-  if (bit >= 0 && bit < kCoreWin) atomicOr(&bm[bit >> 5], 1u << (bit & 31));
-}
 
-// Examine core preds [from, np) in strips of 4x32: colored ones go into the
-// window, uncolored ones into the warp's pending list.  Returns where to resume
-// when the list is full, np when every pred was examined.
+// Examine core preds [from, np) (from even) in strips of 32 u16 pairs, 4 strips
+// (256 preds) in flight: colored ones go into the window, uncolored ones into
+// the warp's pending list; qmax tracks the largest pending core position (the
+// lowest-priority pending pred, i.e. the one expected to be colored last).
+// Returns where to resume when the list is full, np when every pred was examined.
 __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np, int from,
-                                         const uint16_t* cc, unsigned* bm, int wbase,
-                                         uint16_t* plist, int& npend) {
+                                         const uint16_t* cc, uint8_t* bm, int wbase,
+                                         uint16_t* plist, int& npend, int& qmax) {
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
-  for (int i0 = from; i0 < np; i0 += 128) {
-    int q[4], c[4];
+  const uint32_t* L2 = reinterpret_cast<const uint32_t*>(L);  // P slots are 4-byte aligned
+  for (int i0 = from; i0 < np; i0 += 256) {
+    uint32_t w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int i = i0 + 32 * k + lane;
-      q[k] = i < np ? (int)__ldg(L + i) : -1;
+      const int i = i0 + 64 * k + 2 * lane;
+      w[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = q[k] >= 0 ? ld_vol_u16(cc + q[k]) : 1;
-#pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const bool pend = q[k] >= 0 && c[k] == 0;
-      if (q[k] >= 0 && c[k]) bm_set(bm, c[k], wbase);
-      const unsigned bal = __ballot_sync(0xffffffffu, pend);
-      const int cnt = __popc(bal);
-      if (npend + cnt > kCorePend) return i0 + 32 * k;  // strips before k are complete
-      if (pend) plist[npend + __popc(bal & lt)] = (uint16_t)q[k];
-      npend += cnt;
+      const int i = i0 + 64 * k + 2 * lane;
+      const int qa = i < np ? (int)(w[k] & 0xffffu) : -1;
+      const int qb = i + 1 < np ? (int)(w[k] >> 16) : -1;
+      const int ca = qa >= 0 ? ld_vol_u16(cc + qa) : 1;
+      const int cb = qb >= 0 ? ld_vol_u16(cc + qb) : 1;
+      const unsigned ba = __ballot_sync(0xffffffffu, qa >= 0 && ca == 0);
+      const unsigned bb = __ballot_sync(0xffffffffu, qb >= 0 && cb == 0);
+      if (npend + __popc(ba) + __popc(bb) > kCorePend) return i0 + 64 * k;  // strips before k are complete
+      if (qa >= 0 && ca) bmap_mark(bm, ca, wbase, kCoreWin);
+      if (qb >= 0 && cb) bmap_mark(bm, cb, wbase, kCoreWin);
+      if (qa >= 0 && ca == 0) {
+        plist[npend + __popc(ba & lt)] = (uint16_t)qa;
+        qmax = max(qmax, qa);
+      }
+      npend += __popc(ba);
+      if (qb >= 0 && cb == 0) {
+        plist[npend + __popc(bb & lt)] = (uint16_t)qb;
+        qmax = max(qmax, qb);
+      }
+      npend += __popc(bb);
     }
   }
   return np;
@@ -538,10 +591,15 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int32_t* __rest
                                                            const int32_t* __restrict__ cnp,
                                                            const int32_t* __restrict__ P,
                                                            int32_t* color, State* st,
+                                                           unsigned long long* tr_grab,
+                                                           unsigned long long* tr_done,
+                                                           unsigned spin_ns,
                                                            unsigned long long watchdog_ns) {
-  extern __shared__ __align__(16) uint16_t s_cc[];  // [NC] color replica (0 = uncolored)
-  __shared__ unsigned s_bm[kCoreWarps][kCoreWin / 32];
-  __shared__ uint16_t s_pend[kCoreWarps][kCorePend];
+  // dynamic shared memory: bitmaps | pending lists | color replica [NC] (0 = uncolored)
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  uint8_t* s_bm = s_dyn;
+  uint16_t* s_pend = reinterpret_cast<uint16_t*>(s_dyn + kCoreFixedSmem - kCoreWarps * kCorePend * 2);
+  uint16_t* s_cc = reinterpret_cast<uint16_t*>(s_dyn + kCoreFixedSmem);
   __shared__ int s_ticket;
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();
@@ -554,81 +612,140 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int32_t* __rest
   cl.sync();  // every replica is zeroed before any color is published
   uint16_t* remote = lane < C ? cl.map_shared_rank(s_cc, lane) : nullptr;
   const unsigned long long deadline = globaltimer() + watchdog_ns;
-  unsigned* bm = s_bm[warp];
-  uint16_t* plist = s_pend[warp];
+  uint8_t* bm = s_bm + warp * kCoreWin;
+  uint16_t* plist = s_pend + warp * kCorePend;
   int kmax = 0;
   bool stall = false;
   while (!stall) {
     int k = 0;
     if (lane == 0) k = atomicAdd(&s_ticket, 1);
     k = __shfl_sync(0xffffffffu, k, 0);
-    const int p = rank + C * k;
+    // runs of kCoreRun consecutive positions per CTA, runs dealt round-robin:
+    // chain hops inside a run stay in local shared memory
+    const int p = (rank + C * (k / kCoreRun)) * kCoreRun + (k % kCoreRun);
     if (p >= NC) break;
     const int np = cnp[p];
     const uint16_t* L = reinterpret_cast<const uint16_t*>(P + cbase[p]);
+    const int vcore = order[p];  // loaded early: the color store must not wait on it
+#ifdef PGC_PROBE
+    const int vprobe = order[p];
+    PROBE_STAMP(tr_done, vprobe, 0);
+#else
+    if (tr_grab && lane == 0) tr_grab[order[p]] = globaltimer();
+#endif
     int found = 0;
     for (int wbase = 0; !found && !stall; wbase += kCoreWin) {
-      bm[lane] = 0;
-      bm[lane + 32] = 0;
+      bmap_clear(bm, kCoreWin);
       __syncwarp();
-      int npend = 0;
-      int over = core_scan(L, np, 0, s_cc, bm, wbase, plist, npend);
-      unsigned sleep_ns = 0;
-      while (npend > 0 || over < np) {
-        bool progress = false;
-        int keep = 0;
-        for (int j0 = 0; j0 < npend; j0 += 32) {
-          const int j = j0 + lane;
-          int q = 0, cc = 1;
-          if (j < npend) {
-            q = plist[j];
-            cc = ld_vol_u16(s_cc + q);
-          }
-          const bool still = j < npend && cc == 0;
-          if (j < npend && cc) bm_set(bm, cc, wbase);
-          const unsigned bal = __ballot_sync(0xffffffffu, still);
-          if (__ballot_sync(0xffffffffu, j < npend && cc != 0)) progress = true;
+      int npend = 0, qmax = -1;
+      int over = core_scan(L, np, 0, s_cc, bm, wbase, plist, npend, qmax);
+      __syncwarp();
+      // zi = the GetColor candidate (first unused color of the window, 0-based),
+      // kept current as pending colors arrive so that the last arrival costs
+      // one compare
+      int zi = bmap_next_zero<kCoreWin>(bm, 0);
+      PROBE_STAMP(tr_done, vprobe, 1);
+      unsigned sleep_ns = 0, polls = 0;
+      // reduce the pending set until at most the last pred is left
+      for (;;) {
+        if (npend == 0) {
+          if (over >= np) break;
+          over = core_scan(L, np, over, s_cc, bm, wbase, plist, npend, qmax);
           __syncwarp();
-          if (still) plist[keep + __popc(bal & lt)] = (uint16_t)q;
-          keep += __popc(bal);
+          zi = bmap_next_zero<kCoreWin>(bm, zi);
+          continue;
         }
+        if (npend == 1 && over >= np) break;  // the tail below takes the last one
+        // Several preds pending.  Preds get colored roughly in position order,
+        // so the second-largest pending position is the one whose coloring
+        // leaves this vertex waiting on its last pred: spin on it, then one pass
+        // drops the colored entries and (usually) hands over to the tail.
+        {
+          qmax = warp_max(qmax);
+          int q2 = -1;
+          for (int j0 = 0; j0 < npend; j0 += 32) {  // second-largest pending position
+            const int j = j0 + lane;
+            const int q = j < npend ? (int)plist[j] : -1;
+            q2 = max(q2, q < qmax ? q : -1);
+          }
+          q2 = warp_max(q2);
+          if (q2 < 0) q2 = qmax;
+          for (int k = 0; k < 64 && ld_vol_u16(s_cc + q2) == 0; ++k) {
+            if (sleep_ns) __nanosleep(sleep_ns);
+          }
+          if (ld_vol_u16(s_cc + q2) == 0)
+            sleep_ns = sleep_ns ? min(sleep_ns * 2, (unsigned)spin_ns) : (spin_ns ? 32u : 0u);
+        }
+        if ((++polls & 255u) == 0 && __shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+          stall = true;
+          break;
+        }
+        int keep = 0, nq = -1;
+        for (int j0 = 0; j0 < npend; j0 += 128) {
+          int q[4], cc[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int j = j0 + 32 * k + lane;
+            q[k] = j < npend ? (int)plist[j] : -1;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cc[k] = q[k] >= 0 ? ld_vol_u16(s_cc + q[k]) : 1;
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool still = q[k] >= 0 && cc[k] == 0;
+            if (q[k] >= 0 && cc[k]) bmap_mark(bm, cc[k], wbase, kCoreWin);
+            const unsigned bal = __ballot_sync(0xffffffffu, still);
+            if (still) {
+              plist[keep + __popc(bal & lt)] = (uint16_t)q[k];
+              nq = max(nq, q[k]);
+            }
+            keep += __popc(bal);
+          }
+        }
+        const bool moved = keep < npend;
         npend = keep;
+        qmax = nq;
         __syncwarp();
-        if (over < np) {
-          const int before = over;
-          over = core_scan(L, np, over, s_cc, bm, wbase, plist, npend);
-          if (over != before) progress = true;
-        }
-        if (npend == 0 && over >= np) break;
-        if (progress) {
+        if (moved) {
+          zi = bmap_next_zero<kCoreWin>(bm, zi);
           sleep_ns = 0;
-        } else {
-          if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+        }
+      }
+      if (stall) break;
+      if (npend == 1) {
+        // Tail -- the critical path of a dependency chain.  Everything that
+        // does not need the last color is done before waiting: the candidate
+        // for "the last color takes the current candidate" is found now, so
+        // after the (warp-uniform) spin only a compare-and-select remains.
+        const int q = plist[0];
+        const int zi_next = bmap_next_zero<kCoreWin>(bm, zi + 1);
+        int c;
+        while ((c = ld_vol_u16(s_cc + q)) == 0) {
+          if ((++polls & 65535u) == 0 && globaltimer() > deadline) {
+            st->err = 5;
             stall = true;
             break;
           }
-          if (sleep_ns) __nanosleep(sleep_ns);
-          sleep_ns = sleep_ns ? min(sleep_ns * 2, 64u) : 8u;
         }
+        PROBE_STAMP(tr_grab, vprobe, 0);
+        zi = (c - wbase - 1 == zi) ? zi_next : zi;
+        npend = 0;
+        PROBE_STAMP(tr_grab, vprobe, 1);
       }
-      __syncwarp();
-      if (stall) break;
-      // GetColor inside this window: the first zero bit
-      const unsigned z0 = ~bm[lane], z1 = ~bm[lane + 32];
-      const unsigned b0 = __ballot_sync(0xffffffffu, z0 != 0);
-      const unsigned b1 = __ballot_sync(0xffffffffu, z1 != 0);
-      if (b0) {
-        const int w = __ffs(b0) - 1;
-        found = wbase + 32 * w + __ffs(__shfl_sync(0xffffffffu, z0, w));
-      } else if (b1) {
-        const int w = __ffs(b1) - 1;
-        found = wbase + 32 * (w + 32) + __ffs(__shfl_sync(0xffffffffu, z1, w));
-      }
-      __syncwarp();
+      if (stall) break;  // warp-uniform: every lane read the same timer in the same instruction
+      if (zi < kCoreWin) found = wbase + zi + 1;  // GetColor (else: next window)
     }
+    PROBE_STAMP(tr_grab, vprobe, 2);
     if (stall) break;
     if (lane < C) *(volatile uint16_t*)(remote + p) = (uint16_t)found;  // publish to every replica
-    if (lane == 0) st_relaxed(color + order[p], found);
+    PROBE_STAMP(tr_grab, vprobe, 3);
+    if (lane == 0) {
+      st_relaxed(color + vcore, found);
+#ifndef PGC_PROBE
+      if (tr_done) tr_done[vcore] = globaltimer();
+#endif
+    }
     kmax = max(kmax, found);
   }
   kmax = warp_max(kmax);
@@ -637,150 +754,280 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int32_t* __rest
 }
 
 // ------------------------------------------------------------- bulk ---------
-// JP on the rest of the priority order as a sync-free dataflow, one vertex per
-// lane.  Tickets are taken in priority order (a topological order of G_rho) by
-// free lanes; a lane scans its vertex's preds once (colors of colored preds go
-// into a lane-private 512-color bitmap in shared memory, uncolored preds are
-// compacted in place at the front of the vertex's own P slot), then watches
-// the lowest-priority pending pred with one load per poll; when it is colored
-// the pending list is re-examined.  With no pending pred, GetColor is the
-// first zero bit; the lane stores the color and takes a
-// new ticket.  Deadlock freedom: the highest-priority uncolored vertex has all
-// preds colored, and if it is not held by a lane then no later ticket was
-// handed out either, so some lane is free to take it; no lane ever blocks.
-constexpr int kBulkBlock = 256;
-constexpr int kBulkWords = 16;  // 512-color window per lane
-constexpr int kBulkWin = 32 * kBulkWords;
-constexpr int kBulkBatch = 8;   // pred loads in flight per lane
+// JP on the rest of the priority order (positions >= core_n) as a sync-free
+// dataflow.  The rest is split (stably, so each class stays in priority order)
+// into heavy vertices (|pred| > kLightPredMax), colored warp-per-vertex with a
+// 2048-color shared-memory bitmap window, and light ones, colored
+// lane-per-vertex with a 64-bit used-color mask in registers.  Each class is
+// handed out by its own atomic ticket in priority order; a vertex is colored
+// by GetColor as soon as every pred's color is nonzero --
+// the Join of line 1132 observed by polling.  Deadlock freedom: per class, the
+// highest-priority uncolored vertex has all preds colored, and if it is not
+// held then no later ticket of its class was handed out either, so a worker of
+// its class is free to take it; no worker ever blocks.
+constexpr int kLightPredMax = 62;  // light: colors 1..63 fit a u64 mask
+constexpr int kJpBlock = 256;
+constexpr int kJpWarps = kJpBlock / 32;
+constexpr int kHeavyWin = 2048;    // colors per heavy byte-map window
+constexpr int kPendCap = 256;      // pending-pred list capacity per heavy warp (smem)
+constexpr int kLightBatch = 8;     // pred loads in flight per light lane
 
-struct BulkLane {
-  int v = -1, np = 0, wbase = 0, npend = 0, watch = -1;
-  int64_t pb = 0;
-  bool scan = false;
-};
-
-// priority key of u (larger = higher priority): round, then hash
-__device__ __forceinline__ bool lower_prio(int ru, uint64_t hu, int rw, uint64_t hw) {
-  return ru != rw ? ru < rw : hu < hw;
+__global__ void k_bulk_flags(int64_t n, const int32_t* __restrict__ order,
+                             const int32_t* __restrict__ npred, const State* st,
+                             int32_t* __restrict__ flag) {
+  const int NC = st->core_n;
+  for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    flag[p - NC] = npred[order[p]] > kLightPredMax ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(kBulkBlock) k_jp_bulk(int64_t n, const int64_t* __restrict__ off,
-                                                       int32_t* P, const int32_t* __restrict__ npred,
-                                                       const int32_t* __restrict__ order,
-                                                       const int32_t* __restrict__ round,
-                                                       uint64_t seed, int32_t* color, State* st,
-                                                       unsigned sleep_max,
-                                                       unsigned long long* tr_grab,
-                                                       unsigned long long* tr_done,
-                                                       unsigned long long watchdog_ns) {
-  __shared__ unsigned s_bm[kBulkWords][kBulkBlock];  // word-major: lane-private, conflict-free
-  const unsigned long long deadline = globaltimer() + watchdog_ns;
+__global__ void k_bulk_scatter(int64_t n, const int32_t* __restrict__ order,
+                               const int32_t* __restrict__ npred, const State* st,
+                               const int32_t* __restrict__ hpos, int32_t* __restrict__ hlist,
+                               int32_t* __restrict__ llist) {
+  const int NC = st->core_n;
+  for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int v = order[p];
+    const int64_t i = p - NC;
+    const int h = hpos[i];
+    if (npred[v] > kLightPredMax) hlist[h] = v;
+    else llist[i - h] = v;
+  }
+}
+
+
+// Heavy path, one warp per vertex: examine preds [from, np) in strips of 4x32
+// (4 independent loads in flight per lane), OR colored ones into the window,
+// queue pending ones in the warp's list.  Returns the index to resume from when
+// the pending list is full, np when every pred was examined.
+__device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t pb, int np,
+                                          int from, const int32_t* color, uint8_t* bm, int wbase,
+                                          int* plist, int& npend) {
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
-  const int NC = st->core_n;
-  const int64_t nb = n - NC;
-  BulkLane s;
-  bool exhausted = false;
+  for (int i0 = from; i0 < np; i0 += 128) {
+    int u[4], cc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + 32 * k + lane;
+      u[k] = i < np ? __ldg(P + pb + i) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool pend = u[k] >= 0 && cc[k] == 0;
+      if (u[k] >= 0 && cc[k]) bmap_mark(bm, cc[k], wbase, kHeavyWin);
+      const unsigned bal = __ballot_sync(0xffffffffu, pend);
+      const int cnt = __popc(bal);
+      if (npend + cnt > kPendCap) return i0 + 32 * k;  // strips before k are complete
+      if (pend) plist[npend + __popc(bal & lt)] = u[k];
+      npend += cnt;
+    }
+  }
+  return np;
+}
+
+__global__ void __launch_bounds__(kJpBlock) k_jp_bulk(const int64_t* __restrict__ off,
+                                                     const int32_t* __restrict__ P,
+                                                     const int32_t* __restrict__ npred,
+                                                     const int32_t* __restrict__ hlist,
+                                                     const int32_t* __restrict__ llist,
+                                                     int64_t nbulk, int32_t* color, State* st,
+                                                     int heavy_warps, unsigned heavy_sleep_max,
+                                                     unsigned light_sleep_max,
+                                                     unsigned long long* tr_grab,
+                                                     unsigned long long* tr_done,
+                                                     unsigned long long watchdog_ns) {
+  const unsigned long long deadline = globaltimer() + watchdog_ns;
+  __shared__ __align__(16) uint8_t s_bm[kJpWarps][kHeavyWin];
+  __shared__ int s_pend[kJpWarps][kPendCap];
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  const int nheavy = st->nheavy;
   int kmax = 0;
-  unsigned sleep_ns = 32;
-  auto bm = [&](int w) -> unsigned& { return s_bm[w][threadIdx.x]; };
-  // Re-examine pending preds P[pb, pb+npend): OR colored ones into the
-  // window, compact the rest in place, watch the lowest-priority one.
-  auto recheck = [&]() {
-    int keep = 0, wr = 0x7fffffff;
-    uint64_t wh = ~0ull;
-    s.watch = -1;
-    for (int j0 = 0; j0 < s.npend; j0 += kBulkBatch) {
-      int u[kBulkBatch], c[kBulkBatch];
-#pragma unroll
-      for (int k = 0; k < kBulkBatch; ++k) u[k] = j0 + k < s.npend ? P[s.pb + j0 + k] : -1;
-#pragma unroll
-      for (int k = 0; k < kBulkBatch; ++k) c[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
-#pragma unroll
-      for (int k = 0; k < kBulkBatch; ++k) {
-        if (u[k] < 0) continue;
-        if (c[k]) {
-          const int bit = c[k] - s.wbase - 1;
-          if (bit >= 0 && bit < kBulkWin) bm(bit >> 5) |= 1u << (bit & 31);
-        } else {
-          P[s.pb + keep++] = u[k];
-          const int ru = round[u[k]];
-          const uint64_t hu = prio_hash(seed, (uint32_t)u[k]);
-          if (s.watch < 0 || lower_prio(ru, hu, wr, wh)) {
-            s.watch = u[k];
-            wr = ru;
-            wh = hu;
+  if (warp < heavy_warps) {
+    uint8_t* bm = s_bm[warp];
+    int* plist = s_pend[warp];
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&st->ticket_heavy, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= nheavy) break;
+      const int v = hlist[t];
+      const int np = npred[v];
+      const int64_t pb = off[v];
+      if (tr_grab && lane == 0) tr_grab[v] = globaltimer();
+      int found = 0;
+      for (int wbase = 0; !found; wbase += kHeavyWin) {
+        bmap_clear(bm, kHeavyWin);
+        __syncwarp();
+        int npend = 0;
+        int over = heavy_scan(P, pb, np, 0, color, bm, wbase, plist, npend);
+        __syncwarp();
+        // zi = GetColor candidate (first unused color of the window, 0-based),
+        // kept current as pending colors arrive: the last arrival costs a compare
+        int zi = bmap_next_zero<kHeavyWin>(bm, 0);
+        unsigned sleep_ns = 0;
+        for (;;) {
+          if (npend == 0) {
+            if (over >= np) break;
+            over = heavy_scan(P, pb, np, over, color, bm, wbase, plist, npend);
+            __syncwarp();
+            zi = bmap_next_zero<kHeavyWin>(bm, zi);
+            continue;
+          }
+          if (npend == 1 && over >= np) {  // fast path: one load per poll, then a compare-and-select
+            const int u = plist[0];
+            const int zi_next = bmap_next_zero<kHeavyWin>(bm, zi + 1);
+            int c;
+            while ((c = ld_relaxed(color + u)) == 0) {
+              if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+                found = -1;
+                break;
+              }
+              if (sleep_ns) __nanosleep(sleep_ns);
+              sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 16u;
+            }
+            if (found < 0) break;
+            zi = (c - wbase - 1 == zi) ? zi_next : zi;
+            npend = 0;
+            sleep_ns = 0;
+            continue;
+          }
+          // several preds pending: one pass drops the colored ones (never blocks)
+          int keep = 0;
+          for (int j0 = 0; j0 < npend; j0 += 32) {
+            const int j = j0 + lane;
+            int u = 0, cc = 1;
+            if (j < npend) {
+              u = plist[j];
+              cc = ld_relaxed(color + u);
+            }
+            const bool still = j < npend && cc == 0;
+            if (j < npend && cc) bmap_mark(bm, cc, wbase, kHeavyWin);
+            const unsigned bal = __ballot_sync(0xffffffffu, still);
+            __syncwarp();
+            if (still) plist[keep + __popc(bal & lt)] = u;
+            keep += __popc(bal);
+          }
+          const bool moved = keep < npend;
+          npend = keep;
+          __syncwarp();
+          if (moved) {
+            zi = bmap_next_zero<kHeavyWin>(bm, zi);
+            sleep_ns = 0;
+          } else {
+            if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+              found = -1;
+              break;
+            }
+            if (sleep_ns) __nanosleep(sleep_ns);
+            sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 16u;
           }
         }
+        __syncwarp();
+        if (found < 0) break;  // stalled (watchdog)
+        if (zi < kHeavyWin) found = wbase + zi + 1;  // GetColor (else: next window)
+        __syncwarp();
       }
+      if (found < 0) break;  // stalled: the host reports PGC_EINTERNAL
+      if (lane == 0) {
+        st_relaxed(color + v, found);
+        if (tr_done) tr_done[v] = globaltimer();
+      }
+      kmax = max(kmax, found);
     }
-    s.npend = keep;
-  };
-  for (;;) {
-    // 1. free lanes take the next tickets (one atomic per warp)
-    const unsigned want = __ballot_sync(0xffffffffu, s.v < 0 && !exhausted);
-    if (want) {
-      const int leader = __ffs(want) - 1;
-      long long t0 = 0;
-      if (lane == leader) t0 = atomicAdd(&st->ticket, (unsigned long long)__popc(want));
-      t0 = __shfl_sync(0xffffffffu, t0, leader);
-      if (s.v < 0 && !exhausted) {
-        const long long t = t0 + __popc(want & lt);
-        if (t < nb) {
-          s.v = order[NC + t];
-          s.np = npred[s.v];
-          s.pb = off[s.v];
-          s.wbase = 0;
-          s.scan = true;
-          if (tr_grab) tr_grab[s.v] = globaltimer();
-        } else {
-          exhausted = true;
+  } else {
+    const int64_t nlight = nbulk - nheavy;
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&st->ticket_light, 32);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= nlight || globaltimer() > deadline) break;
+      const int64_t pos = (int64_t)t + lane;
+      const bool valid = pos < nlight;
+      int v = 0, np = 0;
+      int64_t pb = 0;
+      unsigned long long mask = 1ull;  // used colors; bit 0 reserved (colors start at 1)
+      unsigned long long pend = 0ull;  // indices of preds still uncolored (np <= 62)
+      if (valid) {
+        v = llist[pos];
+        np = npred[v];
+        pb = off[v];
+        if (tr_grab) tr_grab[v] = globaltimer();
+      }
+      // first pass over every pred, kLightBatch loads in flight
+      for (int j0 = 0; j0 < np; j0 += kLightBatch) {
+        int u[kLightBatch], cc[kLightBatch];
+#pragma unroll
+        for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? __ldg(P + pb + j0 + k) : -1;
+#pragma unroll
+        for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+#pragma unroll
+        for (int k = 0; k < kLightBatch; ++k) {
+          if (u[k] < 0) continue;
+          if (cc[k] == 0) pend |= 1ull << (j0 + k);
+          else if (cc[k] < 64) mask |= 1ull << cc[k];
         }
       }
-    }
-    if (__ballot_sync(0xffffffffu, s.v >= 0) == 0) break;  // all lanes free and out of tickets
-    bool progress = false;
-    // 2. first pass over every pred (or a new color window)
-    if (s.v >= 0 && s.scan) {
+      // Waiting: each lane watches ONE pending pred (its lowest pending index)
+      // with a single load per poll; only when the watched pred is colored does
+      // it re-examine the remaining pending preds in one batched pass.
+      int watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
+      int watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
+      bool done = !valid;
+      unsigned sleep_ns = 32;
+      for (;;) {
+        bool progress = false;
+        if (!done && watch_u >= 0) {
+          const int cw = ld_relaxed(color + watch_u);
+          if (cw) {
+            if (cw < 64) mask |= 1ull << cw;
+            pend &= ~(1ull << watch_j);
+            progress = true;
+            // batched re-poll of the other pending preds
+            unsigned long long p = pend;
+            while (p) {
+              int js[kLightBatch], u[kLightBatch], cc[kLightBatch];
 #pragma unroll
-      for (int w = 0; w < kBulkWords; ++w) bm(w) = 0;
-      s.npend = s.np;  // every pred is "pending" until examined
-      recheck();
-      s.scan = false;
-      progress = true;
-    }
-    // 3. poll the watched pred; when it is colored, re-examine the others
-    if (s.v >= 0 && s.npend > 0) {
-      if (ld_relaxed(color + s.watch)) {
-        recheck();
-        progress = true;
-      }
-    }
-    // 4. GetColor once nothing is pending
-    if (s.v >= 0 && !s.scan && s.npend == 0) {
-      int found = 0;
+              for (int k = 0; k < kLightBatch; ++k) {
+                js[k] = p ? __ffsll((long long)p) - 1 : -1;
+                p &= p - 1;
+              }
 #pragma unroll
-      for (int w = 0; w < kBulkWords; ++w) {
-        const unsigned z = ~bm(w);
-        if (!found && z) found = s.wbase + 32 * w + __ffs(z);
+              for (int k = 0; k < kLightBatch; ++k) u[k] = js[k] >= 0 ? __ldg(P + pb + js[k]) : -1;
+#pragma unroll
+              for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 0;
+#pragma unroll
+              for (int k = 0; k < kLightBatch; ++k)
+                if (cc[k]) {
+                  if (cc[k] < 64) mask |= 1ull << cc[k];
+                  pend &= ~(1ull << js[k]);
+                }
+            }
+            watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
+            watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
+          }
+        }
+        if (!done && watch_u < 0) {  // GetColor: smallest color unused by the preds
+          const int cc = __ffsll((long long)~mask) - 1;
+          st_relaxed(color + v, cc);
+          if (tr_done) tr_done[v] = globaltimer();
+          kmax = max(kmax, cc);
+          done = true;
+          progress = true;
+        }
+        if (__ballot_sync(0xffffffffu, !done) == 0) break;
+        if (__ballot_sync(0xffffffffu, progress)) {
+          sleep_ns = 32;
+        } else {
+          if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) break;
+          __nanosleep(sleep_ns);
+          sleep_ns = min(sleep_ns * 2, light_sleep_max);
+        }
       }
-      if (found) {
-        st_relaxed(color + s.v, found);
-        if (tr_done) tr_done[s.v] = globaltimer();
-        kmax = max(kmax, found);
-        s.v = -1;
-      } else {  // all kBulkWin colors of this window used: next window
-        s.wbase += kBulkWin;
-        s.scan = true;
-      }
-      progress = true;
-    }
-    if (__ballot_sync(0xffffffffu, progress)) {
-      sleep_ns = 32;
-    } else {
-      if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) break;
-      __nanosleep(sleep_ns);
-      sleep_ns = min(sleep_ns * 2, sleep_max);
     }
   }
   kmax = warp_max(kmax);
@@ -788,7 +1035,9 @@ __global__ void __launch_bounds__(kBulkBlock) k_jp_bulk(int64_t n, const int64_t
 }
 
 __global__ void k_jp_reset(State* st) {
-  st->ticket = 0;
+  st->ticket_heavy = 0;
+  st->ticket_light = 0;
+  st->nheavy = 0;
   st->K = 0;
   st->core_n = 0;
   st->core_arcs = 0;
@@ -846,7 +1095,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
       const int NC = c.h_state->core_n;
       const long long arcs = c.h_state->core_arcs;
       int C = 0;
-      const size_t smem = ((size_t)NC * 2 + 15) & ~(size_t)15;
+      const size_t smem = kCoreFixedSmem + (((size_t)NC * 2 + 15) & ~(size_t)15);
       if (NC >= c.tune.core_min_n) {
         int want = c.tune.core_ctas > 0
                        ? c.tune.core_ctas
@@ -858,6 +1107,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
         PGC_CUDA(cudaMemsetAsync(&c.state->core_n, 0, sizeof(int), c.st));
       } else {
         c.core_ctas = C;
+        c.core_n = NC;
         const int G = c.nsm * 4;
         PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.order, c.state, c.D));
         PGC_LAUNCH(c, kGCore, "k_core_lists",
@@ -879,16 +1129,30 @@ int jp_color_run(Ctx& c, int32_t* color) {
         PGC_LAUNCH(c, kGCore, "k_jp_core",
                    PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int32_t*)c.order,
                                                (const int64_t*)c.cbase, (const int32_t*)c.cnp,
-                                               (const int32_t*)c.P, color, c.state, wd)));
+                                               (const int32_t*)c.P, color, c.state, c.trace_grab,
+                                               c.trace_done, (unsigned)c.tune.core_spin_ns, wd)));
       }
     }
-    // --- bulk ---
-    const int G = wave_grid(c, k_jp_bulk, kBulkBlock);
-    PGC_LAUNCH(c, kGJp, "k_jp_bulk",
-               k_jp_bulk<<<G, kBulkBlock, 0, c.st>>>(
-                   c.n, c.off, c.P, c.npred, c.order, c.round_key, c.seed, color, c.state,
-                   (unsigned)c.tune.jp_sleep_max, c.trace_grab, c.trace_done,
-                   (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
+    // --- bulk: stable heavy/light split of positions [core_n, n), then the dataflow ---
+    const int NC = c.core_n;
+    const int64_t nbulk = c.n - NC;
+    if (nbulk > 0) {
+      const int G = c.nsm * 8;
+      PGC_LAUNCH(c, kGJp, "k_bulk_flags",
+                 k_bulk_flags<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.state, c.U[0]));
+      if (int e = scan_ex(c, c.U[0], c.U[1], nullptr, nbulk, nbulk, &c.state->nheavy, kGJp))
+        return e;
+      PGC_LAUNCH(c, kGJp, "k_bulk_scatter",
+                 k_bulk_scatter<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.state, c.U[1], c.Rl,
+                                                     c.U[0]));
+      const int GB = wave_grid(c, k_jp_bulk, kJpBlock);
+      PGC_LAUNCH(c, kGJp, "k_jp_bulk",
+                 k_jp_bulk<<<GB, kJpBlock, 0, c.st>>>(
+                     c.off, c.P, c.npred, c.Rl, c.U[0], nbulk, color, c.state,
+                     c.tune.jp_heavy_warps, (unsigned)c.tune.jp_heavy_sleep_max,
+                     (unsigned)c.tune.jp_light_sleep_max, c.trace_grab, c.trace_done,
+                     (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
+    }
   }
   if (int e = sync_state(c)) return e;
   if (c.h_state->err == 5)

@@ -42,7 +42,8 @@ struct State {
   int core_n;                  // |core| = length of the priority prefix colored by k_jp_core
   int K;
   long long core_arcs;         // sum of |pred| over the core
-  unsigned long long ticket;   // next bulk ticket
+  int nheavy;                  // bulk vertices with |pred| > kLightPredMax
+  int ticket_heavy, ticket_light;  // next bulk tickets per class
 };
 
 // Byte offsets of every workspace region (each 256-byte aligned).
@@ -59,12 +60,15 @@ struct Tuning {
   int rounds_per_sync = 8;
   int heavy_degree = 128;   // vertices with more arcs are split into edge chunks
   int chunk_arcs = 1024;    // arcs per chunk work item
-  int jp_sleep_max = 2048;  // ns, exponential backoff cap of idle bulk JP warps
+  int jp_heavy_warps = 2;         // warps per 8-warp bulk JP block serving heavy vertices (1..7)
+  int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
+  int jp_light_sleep_max = 8192;  // ns, same for light warps
   int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
   int core_max = 65535;           // JP core: max vertices (0 disables the core engine)
   int core_min_avg = 32;          // JP core: min mean |pred| over the prefix
   int core_min_n = 256;           // JP core: smaller cores are left to the bulk kernel
   int core_ctas = 0;              // JP core: cluster size (0 = from core_arcs_per_cta)
+  int core_spin_ns = 1024;        // JP core: backoff cap (ns) of a warp still several preds away
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 4 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
@@ -105,6 +109,7 @@ struct Ctx {
   const int32_t* round_key = nullptr;  // JP first priority key (rho_ADG for JP-ADG)
   uint64_t seed = 0;                   // JP tie-break seed
   int core_ctas = 0;                   // cluster size used by the last k_jp_core (0 = none)
+  int core_n = 0;                      // core vertices colored by k_jp_core (0 = none)
   State* h_state;  // pinned host mirror
   unsigned long long* trace_grab = nullptr;  // pgc_debug_set_trace (diagnostics)
   unsigned long long* trace_done = nullptr;

@@ -127,7 +127,8 @@ def tuning():
         pgc.set_tuning(k, v)
     yield set_
     defaults = {"core_max": 65535, "core_min_avg": 32, "core_min_n": 256, "core_ctas": 0,
-                "core_arc_cap": 1 << 30, "core_arcs_per_cta": 4 << 20, "jp_sleep_max": 2048,
+                "core_arc_cap": 1 << 30, "core_arcs_per_cta": 4 << 20, "jp_heavy_warps": 2,
+                "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
                 "heavy_degree": 128, "rounds_per_sync": 8}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
@@ -202,12 +203,15 @@ def test_determinism_across_tuning(tuning):
     g = gg.rmat(14, 16, seed=2)
     pgc, off, col = dev(g)
     ref = None
-    for hd, rps, core, sleep in ((32, 1, 0, 0), (100, 3, 65535, 64), (1024, 8, 500, 8192),
-                                 (1 << 20, 8, 65535, 2048), (128, 2, 0, 100000)):
+    for hd, rps, core, hw, sleep in ((32, 1, 0, 1, 0), (100, 3, 65535, 2, 64),
+                                     (1024, 8, 500, 7, 8192), (1 << 20, 8, 65535, 4, 2048),
+                                     (128, 2, 0, 3, 100000)):
         tuning("heavy_degree", hd)
         tuning("rounds_per_sync", rps)
         tuning("core_max", core)
-        tuning("jp_sleep_max", sleep)
+        tuning("jp_heavy_warps", hw)
+        tuning("jp_heavy_sleep_max", sleep)
+        tuning("jp_light_sleep_max", sleep)
         for _ in range(2):
             r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 9)
             out = (r.cpu().numpy(), c.cpu().numpy(), T, K)

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Tuning sweep on one config: per-group device times for each knob setting.
 
-  python tools/sweep.py --config rmat24 --reps 3 sleep=512,2048 ctas=0,4,16
+  python tools/sweep.py --config rmat24 --reps 3 hw=1,2,4 ctas=0,4,16
 Results never depend on the knobs (checked here against the first setting).
 """
 import argparse
@@ -18,9 +18,9 @@ import torch  # noqa: E402
 
 import graphgen as gg  # noqa: E402
 
-KEYS = {"sleep": "jp_sleep_max", "chunk": "chunk_arcs", "heavy_deg": "heavy_degree",
+KEYS = {"hw": "jp_heavy_warps", "hsleep": "jp_heavy_sleep_max", "lsleep": "jp_light_sleep_max", "chunk": "chunk_arcs", "heavy_deg": "heavy_degree",
         "rps": "rounds_per_sync", "core": "core_max", "ctas": "core_ctas", "avg": "core_min_avg",
-        "apc": "core_arcs_per_cta"}
+        "apc": "core_arcs_per_cta", "spin": "core_spin_ns"}
 
 
 def main():

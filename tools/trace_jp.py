@@ -54,10 +54,9 @@ def main():
     tg = tg.cpu().numpy().astype(np.int64)
     td = td.cpu().numpy().astype(np.int64)
     r = rnd.cpu().numpy().astype(np.int64)
-    core = tg == 0            # colored by the cluster core engine (not traced)
-    t0 = tg[~core].min() if (~core).any() else 0
-    tg = np.where(core, 0, tg - t0)
-    td = np.where(core, 0, td - t0)
+    t0 = tg.min()
+    tg -= t0
+    td -= t0
     # oracle levels (JP DAG depth)
     _, _, lvl, J = O.jp(g, rnd.cpu().numpy(), a.seed, levels=True)
     # pred relation and ready time = max done over preds
@@ -75,6 +74,10 @@ def main():
     del src, dst, is_pred, val
     heavy = npred > 62
     has_pred = npred > 0
+    # core = the first core_vertices positions of the priority order
+    key = np.lexsort((h, r))[::-1]          # round desc, then hash desc
+    core = np.zeros(n, dtype=bool)
+    core[key[:st["core_vertices"]]] = True
     step = td - np.maximum(ready, tg)
     wait_grab = tg - ready  # >0: the vertex was grabbed after it became ready
     out = {"config": a.config, "tune": a.tune, "n": n, "J": J, "T": T, "K": K,
@@ -88,7 +91,8 @@ def main():
     marks = sorted(set([1, 10, 100, J // 4, J // 2, 3 * J // 4, J - 50, J - 10, J]))
     out["level_done_us"] = {int(L): float(lv_done[L] / 1e3) for L in marks if 0 < L <= J}
     out["ns_per_level"] = float(lv_done[J] / max(J, 1))
-    for name, m in (("heavy", heavy & has_pred & ~core), ("light", ~heavy & has_pred & ~core)):
+    for name, m in (("core", core & has_pred), ("heavy", heavy & has_pred & ~core),
+                    ("light", ~heavy & has_pred & ~core)):
         out[f"step_ns_{name}"] = pct(step[m])
         out[f"grab_after_ready_ns_{name}"] = pct(wait_grab[m])
         out[f"done_minus_grab_ns_{name}"] = pct((td - tg)[m])
@@ -106,6 +110,13 @@ def main():
         v = int(preds[np.argmax(td[preds])])
     crit = np.array(crit[::-1])
     cs = step[crit]
+    cc = core[crit]
+    out["critical_core"] = {"len": int(cc.sum()), "step_ns": pct(cs[cc]), "sum_step_ms": float(cs[cc].sum() / 1e6),
+                            "grab_after_ready_sum_ms": float(np.maximum(wait_grab[crit][cc], 0).sum() / 1e6),
+                            "span_ms": float((td[crit][cc].max() - tg[crit][cc].min()) / 1e6) if cc.any() else 0}
+    nb = ~cc
+    out["critical_bulk"] = {"len": int(nb.sum()), "step_ns": pct(cs[nb]), "sum_step_ms": float(cs[nb].sum() / 1e6),
+                            "grab_after_ready_sum_ms": float(np.maximum(wait_grab[crit][nb], 0).sum() / 1e6)}
     out["critical"] = {"len": len(crit), "step_ns": pct(cs), "heavy_frac": float(heavy[crit].mean()),
                        "rounds": np.bincount(r[crit]).tolist(),
                        "sum_step_ms": float(cs.sum() / 1e6),
