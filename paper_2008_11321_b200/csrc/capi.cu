@@ -84,6 +84,9 @@ Layout make_layout(int64_t n, int64_t nnz) {
   const size_t ncore = (size_t)(n < kCoreCap ? n : kCoreCap);
   L.cbase = take(8 * ncore);
   L.cnp = take(4 * ncore);
+  // bulk records: heavy vertices have > 62 preds, so at most nnz / 63 of them
+  L.rec_heavy_cap = (nnz / 63 < n ? nnz / 63 : n) + 1;
+  L.rec = take(16 * (size_t)(L.rec_heavy_cap + n));
   L.total = a;
   return L;
 }
@@ -141,6 +144,7 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.scan_tmp = (int32_t*)(b + c.lay.scan_tmp);
   c.cbase = (int64_t*)(b + c.lay.cbase);
   c.cnp = (int32_t*)(b + c.lay.cnp);
+  c.rec = (int4*)(b + c.lay.rec);
   if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));
   c.h_state = g_hstate;
   if (g_trace_grab && g_trace_n == g->n) {
@@ -396,7 +400,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
   struct Key { const char* name; long long lo, hi; long long* l; int* i; };
   const Key keys[] = {
       {"jp_watchdog_ms", 1, 3600000, nullptr, &g_tune.jp_watchdog_ms},
-      {"jp_heavy_warps", 1, 7, nullptr, &g_tune.jp_heavy_warps},
+      {"jp_heavy_warps", 1, 4, nullptr, &g_tune.jp_heavy_warps},
       {"jp_heavy_sleep_max", 0, 1000000, nullptr, &g_tune.jp_heavy_sleep_max},
       {"jp_light_sleep_max", 0, 1000000, nullptr, &g_tune.jp_light_sleep_max},
       {"core_max", 0, 65535, nullptr, &g_tune.core_max},

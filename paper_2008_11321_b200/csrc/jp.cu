@@ -767,43 +767,77 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int32_t* __rest
 // its class is free to take it; no worker ever blocks.
 constexpr int kLightPredMax = 62;  // light: colors 1..63 fit a u64 mask
 constexpr int kJpBlock = 256;
-constexpr int kJpWarps = kJpBlock / 32;
+constexpr int kMaxHeavyWarps = 4;  // heavy-path shared buffers exist for this many warps
 constexpr int kHeavyWin = 2048;    // colors per heavy byte-map window
 constexpr int kPendCap = 256;      // pending-pred list capacity per heavy warp (smem)
 constexpr int kLightBatch = 8;     // pred loads in flight per light lane
 
 __global__ void k_bulk_flags(int64_t n, const int32_t* __restrict__ order,
                              const int32_t* __restrict__ npred, const State* st,
-                             int32_t* __restrict__ flag) {
+                             int32_t* __restrict__ hflag, int32_t* __restrict__ lflag) {
   const int NC = st->core_n;
   for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x)
-    flag[p - NC] = npred[order[p]] > kLightPredMax ? 1 : 0;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int np = npred[order[p]];
+    hflag[p - NC] = np > kLightPredMax ? 1 : 0;
+    lflag[p - NC] = np > 0 && np <= kLightPredMax ? 1 : 0;
+  }
 }
 
+// Stable split of the bulk into heavy and light work lists.  Roots of G_rho
+// (no pred: JP Part 2's initial set) are colored 1 right
+// here (GetColor of the empty set) and listed nowhere.  Every listed vertex
+// gets a 16-byte record {v, |pred|, P slot lo, hi} so a worker fetches it with
+// one coalesced load instead of three dependent ones.  hpos / lpos are the
+// exclusive prefix counts of heavy / light flags.
 __global__ void k_bulk_scatter(int64_t n, const int32_t* __restrict__ order,
-                               const int32_t* __restrict__ npred, const State* st,
-                               const int32_t* __restrict__ hpos, int32_t* __restrict__ hlist,
-                               int32_t* __restrict__ llist) {
+                               const int32_t* __restrict__ npred,
+                               const int64_t* __restrict__ off, State* st,
+                               const int32_t* __restrict__ hpos, const int32_t* __restrict__ lpos,
+                               int4* __restrict__ hrec, int4* __restrict__ lrec, int32_t* color) {
   const int NC = st->core_n;
+  bool root = false;
   for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int v = order[p];
     const int64_t i = p - NC;
-    const int h = hpos[i];
-    if (npred[v] > kLightPredMax) hlist[h] = v;
-    else llist[i - h] = v;
+    const int np = npred[v];
+    if (np > 0) {
+      const int64_t b = off[v];
+      const int4 r = make_int4(v, np, (int)(uint32_t)b, (int)(b >> 32));
+      if (np > kLightPredMax) hrec[hpos[i]] = r;
+      else lrec[lpos[i]] = r;
+    } else {
+      st_relaxed(color + v, 1);
+      root = true;
+    }
   }
+  if (__any_sync(0xffffffffu, root) && lane_id() == 0) atomicMax(&st->K, 1);
 }
 
+__device__ __forceinline__ int64_t rec_slot(const int4& r) {
+  return (int64_t)(((uint64_t)(uint32_t)r.w << 32) | (uint32_t)r.z);
+}
+
+// Approximate priority key of u (a heuristic for WHICH pending pred to watch,
+// never for a result): the first key's 32 bits, then the top 32 hash bits.
+// Preds get colored roughly in priority order, so the pending pred of lowest
+// key is the one expected to be colored last.
+__device__ __forceinline__ unsigned long long watch_key(const int32_t* __restrict__ round,
+                                                        uint64_t seed, int u) {
+  return ((unsigned long long)((uint32_t)round[u] ^ 0x80000000u) << 32) |
+         (prio_hash(seed, (uint32_t)u) >> 32);
+}
 
 // Heavy path, one warp per vertex: examine preds [from, np) in strips of 4x32
-// (4 independent loads in flight per lane), OR colored ones into the window,
-// queue pending ones in the warp's list.  Returns the index to resume from when
-// the pending list is full, np when every pred was examined.
+// (4 independent loads in flight per lane), mark colored ones in the byte map,
+// queue pending ones (id and watch key) in the warp's list.  Returns the index
+// to resume from when the pending list is full, np when every pred was examined.
 __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t pb, int np,
-                                          int from, const int32_t* color, uint8_t* bm, int wbase,
-                                          int* plist, int& npend) {
+                                          int from, const int32_t* color,
+                                          const int32_t* __restrict__ round, uint64_t seed,
+                                          uint8_t* bm, int wbase, int* plist,
+                                          unsigned long long* pkey, int& npend) {
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
   for (int i0 = from; i0 < np; i0 += 128) {
@@ -822,27 +856,66 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
       const unsigned bal = __ballot_sync(0xffffffffu, pend);
       const int cnt = __popc(bal);
       if (npend + cnt > kPendCap) return i0 + 32 * k;  // strips before k are complete
-      if (pend) plist[npend + __popc(bal & lt)] = u[k];
+      if (pend) {
+        const int at = npend + __popc(bal & lt);
+        plist[at] = u[k];
+        pkey[at] = watch_key(round, seed, u[k]);
+      }
       npend += cnt;
     }
   }
   return np;
 }
 
-__global__ void __launch_bounds__(kJpBlock) k_jp_bulk(const int64_t* __restrict__ off,
+// Warp-wide: the pending entries with the lowest and second-lowest watch key
+// (their ids; -1 if absent).
+__device__ __forceinline__ void lowest_two(const int* plist, const unsigned long long* pkey,
+                                           int npend, int& u1, int& u2) {
+  const int lane = lane_id();
+  unsigned long long k1 = ~0ull, k2 = ~0ull;
+  int a1 = -1, a2 = -1;
+  for (int j = lane; j < npend; j += 32) {
+    const unsigned long long k = pkey[j];
+    const int u = plist[j];
+    if (k < k1) {
+      k2 = k1; a2 = a1; k1 = k; a1 = u;
+    } else if (k < k2) {
+      k2 = k; a2 = u;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ok1 = __shfl_xor_sync(0xffffffffu, k1, o);
+    const unsigned long long ok2 = __shfl_xor_sync(0xffffffffu, k2, o);
+    const int oa1 = __shfl_xor_sync(0xffffffffu, a1, o);
+    const int oa2 = __shfl_xor_sync(0xffffffffu, a2, o);
+    if (ok1 < k1) {  // other's best wins; second = min(my best, other's second)
+      if (k1 < ok2) { k2 = k1; a2 = a1; } else { k2 = ok2; a2 = oa2; }
+      k1 = ok1; a1 = oa1;
+    } else if (ok1 < k2) {
+      k2 = ok1; a2 = oa1;
+    }
+  }
+  u1 = a1;
+  u2 = a2;
+}
+
+__global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restrict__ off,
                                                      const int32_t* __restrict__ P,
                                                      const int32_t* __restrict__ npred,
-                                                     const int32_t* __restrict__ hlist,
-                                                     const int32_t* __restrict__ llist,
-                                                     int64_t nbulk, int32_t* color, State* st,
+                                                     const int4* __restrict__ hrec,
+                                                     const int4* __restrict__ lrec,
+                                                     const int32_t* __restrict__ round,
+                                                     uint64_t seed, int32_t* color, State* st,
                                                      int heavy_warps, unsigned heavy_sleep_max,
                                                      unsigned light_sleep_max,
                                                      unsigned long long* tr_grab,
                                                      unsigned long long* tr_done,
                                                      unsigned long long watchdog_ns) {
   const unsigned long long deadline = globaltimer() + watchdog_ns;
-  __shared__ __align__(16) uint8_t s_bm[kJpWarps][kHeavyWin];
-  __shared__ int s_pend[kJpWarps][kPendCap];
+  __shared__ __align__(16) uint8_t s_bm[kMaxHeavyWarps][kHeavyWin];
+  __shared__ int s_pend[kMaxHeavyWarps][kPendCap];
+  __shared__ unsigned long long s_pkey[kMaxHeavyWarps][kPendCap];
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   const int nheavy = st->nheavy;
@@ -850,39 +923,62 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_bulk(const int64_t* __restrict_
   if (warp < heavy_warps) {
     uint8_t* bm = s_bm[warp];
     int* plist = s_pend[warp];
-    for (;;) {
-      int t = 0;
+    unsigned long long* pkey = s_pkey[warp];
+    // the next ticket and its (vertex, |pred|, P slot) are fetched one vertex
+    // ahead, so their dependent loads overlap the current vertex
+    auto fetch = [&](int& t, int& v, int& np, int64_t& pb) {
+      t = 0;
       if (lane == 0) t = atomicAdd(&st->ticket_heavy, 1);
       t = __shfl_sync(0xffffffffu, t, 0);
+      if (t < nheavy) {
+        const int4 r = hrec[t];
+        v = r.x;
+        np = r.y;
+        pb = rec_slot(r);
+      }
+    };
+    int t_next, v_next = 0, np_next = 0;
+    int64_t pb_next = 0;
+    fetch(t_next, v_next, np_next, pb_next);
+    for (;;) {
+      const int t = t_next;
       if (t >= nheavy) break;
-      const int v = hlist[t];
-      const int np = npred[v];
-      const int64_t pb = off[v];
+      const int v = v_next;
+      const int np = np_next;
+      const int64_t pb = pb_next;
+      fetch(t_next, v_next, np_next, pb_next);
       if (tr_grab && lane == 0) tr_grab[v] = globaltimer();
       int found = 0;
       for (int wbase = 0; !found; wbase += kHeavyWin) {
         bmap_clear(bm, kHeavyWin);
         __syncwarp();
         int npend = 0;
-        int over = heavy_scan(P, pb, np, 0, color, bm, wbase, plist, npend);
+        int over = heavy_scan(P, pb, np, 0, color, round, seed, bm, wbase, plist, pkey, npend);
         __syncwarp();
         // zi = GetColor candidate (first unused color of the window, 0-based),
-        // kept current as pending colors arrive: the last arrival costs a compare
+        // kept current as pending colors arrive
         int zi = bmap_next_zero<kHeavyWin>(bm, 0);
         unsigned sleep_ns = 0;
         for (;;) {
           if (npend == 0) {
             if (over >= np) break;
-            over = heavy_scan(P, pb, np, over, color, bm, wbase, plist, npend);
+            over = heavy_scan(P, pb, np, over, color, round, seed, bm, wbase, plist, pkey, npend);
             __syncwarp();
             zi = bmap_next_zero<kHeavyWin>(bm, zi);
             continue;
           }
-          if (npend == 1 && over >= np) {  // fast path: one load per poll, then a compare-and-select
-            const int u = plist[0];
+#ifdef PGC_HEAVY_PASS_POLL
+          if (npend == 1 && over >= np) {
+            const int u1 = plist[0];
+#else
+          int u1, u2;
+          lowest_two(plist, pkey, npend, u1, u2);
+          if (npend == 1 && over >= np) {
+#endif
+            // tail: one load per poll on the last pred, then a compare-and-select
             const int zi_next = bmap_next_zero<kHeavyWin>(bm, zi + 1);
             int c;
-            while ((c = ld_relaxed(color + u)) == 0) {
+            while ((c = ld_relaxed(color + u1)) == 0) {
               if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
                 found = -1;
                 break;
@@ -893,39 +989,63 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_bulk(const int64_t* __restrict_
             if (found < 0) break;
             zi = (c - wbase - 1 == zi) ? zi_next : zi;
             npend = 0;
-            sleep_ns = 0;
             continue;
           }
-          // several preds pending: one pass drops the colored ones (never blocks)
+#ifndef PGC_HEAVY_PASS_POLL
+          // Several pending: watch the second-to-last expected (one load per
+          // poll, exponential backoff), then one pass drops the colored entries.
+          const int w = u2 >= 0 ? u2 : u1;
+          while (ld_relaxed(color + w) == 0) {
+            if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+              found = -1;
+              break;
+            }
+            __nanosleep(sleep_ns ? sleep_ns : 16u);
+            sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 32u;
+          }
+#endif
+          if (found < 0) break;
+#ifndef PGC_HEAVY_PASS_POLL
+          sleep_ns = 0;
+#endif
           int keep = 0;
           for (int j0 = 0; j0 < npend; j0 += 32) {
             const int j = j0 + lane;
             int u = 0, cc = 1;
+            unsigned long long kk = 0;
             if (j < npend) {
               u = plist[j];
+              kk = pkey[j];
               cc = ld_relaxed(color + u);
             }
             const bool still = j < npend && cc == 0;
             if (j < npend && cc) bmap_mark(bm, cc, wbase, kHeavyWin);
             const unsigned bal = __ballot_sync(0xffffffffu, still);
             __syncwarp();
-            if (still) plist[keep + __popc(bal & lt)] = u;
+            if (still) {
+              plist[keep + __popc(bal & lt)] = u;
+              pkey[keep + __popc(bal & lt)] = kk;
+            }
             keep += __popc(bal);
           }
+#ifdef PGC_HEAVY_PASS_POLL
           const bool moved = keep < npend;
+#endif
           npend = keep;
           __syncwarp();
+          zi = bmap_next_zero<kHeavyWin>(bm, zi);
+#ifdef PGC_HEAVY_PASS_POLL
           if (moved) {
-            zi = bmap_next_zero<kHeavyWin>(bm, zi);
             sleep_ns = 0;
           } else {
             if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
               found = -1;
               break;
             }
-            if (sleep_ns) __nanosleep(sleep_ns);
-            sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 16u;
+            __nanosleep(sleep_ns ? sleep_ns : 16u);
+            sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 32u;
           }
+#endif
         }
         __syncwarp();
         if (found < 0) break;  // stalled (watchdog)
@@ -940,93 +1060,117 @@ __global__ void __launch_bounds__(kJpBlock) k_jp_bulk(const int64_t* __restrict_
       kmax = max(kmax, found);
     }
   } else {
-    const int64_t nlight = nbulk - nheavy;
+    // Light vertices, one per lane; every lane refills independently (a lane
+    // whose vertex waits never holds up the others).  A new vertex's preds are
+    // scanned by its lane (kLightBatch loads in flight): colors go into a
+    // 64-bit used-color mask, uncolored preds into a pending bit set; the lane
+    // then watches ONE pending pred (the lowest pending index) with a single
+    // load per poll and re-examines the rest only when it is colored.
+    const int64_t nlight = st->nlight;
+    int v = -1, np = 0, watch_j = -1, watch_u = -1;
+    int64_t pb = 0;
+    unsigned long long mask = 0, pend = 0;
+    bool exhausted = false;
+    unsigned sleep_ns = 32;
     for (;;) {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&st->ticket_light, 32);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= nlight || globaltimer() > deadline) break;
-      const int64_t pos = (int64_t)t + lane;
-      const bool valid = pos < nlight;
-      int v = 0, np = 0;
-      int64_t pb = 0;
-      unsigned long long mask = 1ull;  // used colors; bit 0 reserved (colors start at 1)
-      unsigned long long pend = 0ull;  // indices of preds still uncolored (np <= 62)
-      if (valid) {
-        v = llist[pos];
-        np = npred[v];
-        pb = off[v];
-        if (tr_grab) tr_grab[v] = globaltimer();
-      }
-      // first pass over every pred, kLightBatch loads in flight
-      for (int j0 = 0; j0 < np; j0 += kLightBatch) {
-        int u[kLightBatch], cc[kLightBatch];
+      bool progress = false;
+      // 1. free lanes take the next light tickets (one atomic per warp)
+      const unsigned want = __ballot_sync(0xffffffffu, v < 0 && !exhausted);
+      if (want) {
+        const int leader = __ffs(want) - 1;
+        int t0 = 0;
+        if (lane == leader) t0 = atomicAdd(&st->ticket_light, __popc(want));
+        t0 = __shfl_sync(0xffffffffu, t0, leader);
+        if (v < 0 && !exhausted) {
+          const int64_t t = (int64_t)t0 + __popc(want & lt);
+          if (t < nlight) {
+            const int4 r = lrec[t];
+            v = r.x;
+            np = r.y;
+            pb = rec_slot(r);
+            if (tr_grab) tr_grab[v] = globaltimer();
+            // first pass over every pred
+            mask = 1ull;  // bit 0 reserved: colors start at 1
+            pend = 0ull;
+            watch_j = -1;
+            watch_u = -1;
+            for (int j0 = 0; j0 < np; j0 += kLightBatch) {
+              int u[kLightBatch], cc[kLightBatch];
 #pragma unroll
-        for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? __ldg(P + pb + j0 + k) : -1;
+              for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? __ldg(P + pb + j0 + k) : -1;
 #pragma unroll
-        for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
-#pragma unroll
-        for (int k = 0; k < kLightBatch; ++k) {
-          if (u[k] < 0) continue;
-          if (cc[k] == 0) pend |= 1ull << (j0 + k);
-          else if (cc[k] < 64) mask |= 1ull << cc[k];
-        }
-      }
-      // Waiting: each lane watches ONE pending pred (its lowest pending index)
-      // with a single load per poll; only when the watched pred is colored does
-      // it re-examine the remaining pending preds in one batched pass.
-      int watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
-      int watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
-      bool done = !valid;
-      unsigned sleep_ns = 32;
-      for (;;) {
-        bool progress = false;
-        if (!done && watch_u >= 0) {
-          const int cw = ld_relaxed(color + watch_u);
-          if (cw) {
-            if (cw < 64) mask |= 1ull << cw;
-            pend &= ~(1ull << watch_j);
-            progress = true;
-            // batched re-poll of the other pending preds
-            unsigned long long p = pend;
-            while (p) {
-              int js[kLightBatch], u[kLightBatch], cc[kLightBatch];
+              for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
 #pragma unroll
               for (int k = 0; k < kLightBatch; ++k) {
-                js[k] = p ? __ffsll((long long)p) - 1 : -1;
-                p &= p - 1;
-              }
-#pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) u[k] = js[k] >= 0 ? __ldg(P + pb + js[k]) : -1;
-#pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 0;
-#pragma unroll
-              for (int k = 0; k < kLightBatch; ++k)
-                if (cc[k]) {
-                  if (cc[k] < 64) mask |= 1ull << cc[k];
-                  pend &= ~(1ull << js[k]);
+                if (u[k] < 0) continue;
+                if (cc[k] == 0) {
+                  pend |= 1ull << (j0 + k);
+                  if (watch_j < 0) {  // watch the first pending pred
+                    watch_j = j0 + k;
+                    watch_u = u[k];
+                  }
+                } else if (cc[k] < 64) {
+                  mask |= 1ull << cc[k];
                 }
+              }
             }
-            watch_j = pend ? __ffsll((long long)pend) - 1 : -1;
-            watch_u = watch_j >= 0 ? __ldg(P + pb + watch_j) : -1;
+            progress = true;
+          } else {
+            exhausted = true;
           }
         }
-        if (!done && watch_u < 0) {  // GetColor: smallest color unused by the preds
-          const int cc = __ffsll((long long)~mask) - 1;
-          st_relaxed(color + v, cc);
-          if (tr_done) tr_done[v] = globaltimer();
-          kmax = max(kmax, cc);
-          done = true;
+      }
+      if (__ballot_sync(0xffffffffu, v >= 0) == 0) break;  // all free and out of tickets
+      // 2. poll the watched pred; when colored, re-examine the other pending preds
+      if (v >= 0 && watch_u >= 0) {
+        const int cw = ld_relaxed(color + watch_u);
+        if (cw) {
+          if (cw < 64) mask |= 1ull << cw;
+          pend &= ~(1ull << watch_j);
           progress = true;
+          unsigned long long q = pend;
+          watch_j = -1;
+          watch_u = -1;
+          while (q) {
+            int js[kLightBatch], u[kLightBatch], cc[kLightBatch];
+#pragma unroll
+            for (int k = 0; k < kLightBatch; ++k) {
+              js[k] = q ? __ffsll((long long)q) - 1 : -1;
+              q &= q - 1;
+            }
+#pragma unroll
+            for (int k = 0; k < kLightBatch; ++k) u[k] = js[k] >= 0 ? __ldg(P + pb + js[k]) : -1;
+#pragma unroll
+            for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 0;
+#pragma unroll
+            for (int k = 0; k < kLightBatch; ++k) {
+              if (u[k] < 0) continue;
+              if (cc[k]) {
+                if (cc[k] < 64) mask |= 1ull << cc[k];
+                pend &= ~(1ull << js[k]);
+              } else if (watch_j < 0) {
+                watch_j = js[k];
+                watch_u = u[k];
+              }
+            }
+          }
         }
-        if (__ballot_sync(0xffffffffu, !done) == 0) break;
-        if (__ballot_sync(0xffffffffu, progress)) {
-          sleep_ns = 32;
-        } else {
-          if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) break;
-          __nanosleep(sleep_ns);
-          sleep_ns = min(sleep_ns * 2, light_sleep_max);
-        }
+      }
+      // 3. GetColor once nothing is pending: the smallest color the preds do not use
+      if (v >= 0 && watch_u < 0) {
+        const int cc = __ffsll((long long)~mask) - 1;
+        st_relaxed(color + v, cc);
+        if (tr_done) tr_done[v] = globaltimer();
+        kmax = max(kmax, cc);
+        v = -1;
+        progress = true;
+      }
+      if (__ballot_sync(0xffffffffu, progress)) {
+        sleep_ns = 32;
+      } else {
+        if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) break;
+        __nanosleep(sleep_ns);
+        sleep_ns = min(sleep_ns * 2, light_sleep_max);
       }
     }
   }
@@ -1138,17 +1282,26 @@ int jp_color_run(Ctx& c, int32_t* color) {
     const int64_t nbulk = c.n - NC;
     if (nbulk > 0) {
       const int G = c.nsm * 8;
+      // flags: heavy -> U0, light -> U1; prefix counts: heavy -> Rl, light -> D
+      // (ADG's lists and degrees, and the core's pos[], are dead by now)
+      int32_t* hflag = c.U[0];
+      int32_t* lflag = c.U[1];
+      int32_t* hpos = c.Rl;
+      int32_t* lpos = c.D;
       PGC_LAUNCH(c, kGJp, "k_bulk_flags",
-                 k_bulk_flags<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.state, c.U[0]));
-      if (int e = scan_ex(c, c.U[0], c.U[1], nullptr, nbulk, nbulk, &c.state->nheavy, kGJp))
-        return e;
+                 k_bulk_flags<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.state, hflag, lflag));
+      if (int e = scan_ex(c, hflag, hpos, nullptr, nbulk, nbulk, &c.state->nheavy, kGJp)) return e;
+      if (int e = scan_ex(c, lflag, lpos, nullptr, nbulk, nbulk, &c.state->nlight, kGJp)) return e;
+      // records: heavy then light, in the rec region
+      int4* hrec = reinterpret_cast<int4*>(c.rec);
+      int4* lrec = hrec + c.lay.rec_heavy_cap;
       PGC_LAUNCH(c, kGJp, "k_bulk_scatter",
-                 k_bulk_scatter<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.state, c.U[1], c.Rl,
-                                                     c.U[0]));
+                 k_bulk_scatter<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.off, c.state, hpos,
+                                                     lpos, hrec, lrec, color));
       const int GB = wave_grid(c, k_jp_bulk, kJpBlock);
       PGC_LAUNCH(c, kGJp, "k_jp_bulk",
                  k_jp_bulk<<<GB, kJpBlock, 0, c.st>>>(
-                     c.off, c.P, c.npred, c.Rl, c.U[0], nbulk, color, c.state,
+                     c.off, c.P, c.npred, hrec, lrec, c.round_key, c.seed, color, c.state,
                      c.tune.jp_heavy_warps, (unsigned)c.tune.jp_heavy_sleep_max,
                      (unsigned)c.tune.jp_light_sleep_max, c.trace_grab, c.trace_done,
                      (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));

@@ -43,14 +43,15 @@ struct State {
   int K;
   long long core_arcs;         // sum of |pred| over the core
   int nheavy;                  // bulk vertices with |pred| > kLightPredMax
+  int nlight;                  // bulk vertices with 1 <= |pred| <= kLightPredMax
   int ticket_heavy, ticket_light;  // next bulk tickets per class
 };
 
 // Byte offsets of every workspace region (each 256-byte aligned).
 struct Layout {
   size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, order, hist1, base1, bcnt, bstart,
-      scan_tmp, cbase, cnp, total;
-  int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap;
+      scan_tmp, cbase, cnp, rec, total;
+  int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap, rec_heavy_cap;
 };
 
 Layout make_layout(int64_t n, int64_t nnz);
@@ -60,7 +61,7 @@ struct Tuning {
   int rounds_per_sync = 8;
   int heavy_degree = 128;   // vertices with more arcs are split into edge chunks
   int chunk_arcs = 1024;    // arcs per chunk work item
-  int jp_heavy_warps = 2;         // warps per 8-warp bulk JP block serving heavy vertices (1..7)
+  int jp_heavy_warps = 4;         // warps per 8-warp bulk JP block serving heavy vertices (1..4)
   int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
   int jp_light_sleep_max = 8192;  // ns, same for light warps
   int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
@@ -70,7 +71,7 @@ struct Tuning {
   int core_ctas = 0;              // JP core: cluster size (0 = from core_arcs_per_cta)
   int core_spin_ns = 1024;        // JP core: backoff cap (ns) of a warp still several preds away
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
-  long long core_arcs_per_cta = 4 << 20;   // JP core: pred arcs per cluster CTA
+  long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
 };
 
@@ -106,6 +107,7 @@ struct Ctx {
   int32_t* scan_tmp;
   int64_t* cbase;  // JP core: P slot of core position p
   int32_t* cnp;    // JP core: |pred| of core position p
+  int4* rec;       // JP bulk work records {v, |pred|, P slot}: heavy then light
   const int32_t* round_key = nullptr;  // JP first priority key (rho_ADG for JP-ADG)
   uint64_t seed = 0;                   // JP tie-break seed
   int core_ctas = 0;                   // cluster size used by the last k_jp_core (0 = none)

@@ -127,7 +127,7 @@ def tuning():
         pgc.set_tuning(k, v)
     yield set_
     defaults = {"core_max": 65535, "core_min_avg": 32, "core_min_n": 256, "core_ctas": 0,
-                "core_arc_cap": 1 << 30, "core_arcs_per_cta": 4 << 20, "jp_heavy_warps": 2,
+                "core_arc_cap": 1 << 30, "core_arcs_per_cta": 2 << 20, "jp_heavy_warps": 4,
                 "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
                 "heavy_degree": 128, "rounds_per_sync": 8}
     for k in touched:
@@ -204,7 +204,7 @@ def test_determinism_across_tuning(tuning):
     pgc, off, col = dev(g)
     ref = None
     for hd, rps, core, hw, sleep in ((32, 1, 0, 1, 0), (100, 3, 65535, 2, 64),
-                                     (1024, 8, 500, 7, 8192), (1 << 20, 8, 65535, 4, 2048),
+                                     (1024, 8, 500, 4, 8192), (1 << 20, 8, 65535, 4, 2048),
                                      (128, 2, 0, 3, 100000)):
         tuning("heavy_degree", hd)
         tuning("rounds_per_sync", rps)
