@@ -157,7 +157,7 @@ const char* pgc_last_error(void);
 /* Thread-local tuning knobs (results never depend on them; tests sweep them to
  * prove it).  Keys and ranges:
  *   "timing" 0/1 (per-kernel-group CUDA events), "rounds_per_sync" >= 1,
- *   "heavy_degree" >= 32 (ADG UPDATE edge-chunks rows longer than this),
+ *   "heavy_degree" >= 128 (ADG UPDATE edge-chunks rows longer than this),
  *   "chunk_arcs" >= 256, "block_threads" 64..1024 (multiple of 32),
  *   "jp_heavy_warps" 1..4 (warps per 8-warp bulk JP block serving vertices with
  *   more than 62 preds), "jp_heavy_sleep_max" / "jp_light_sleep_max" ns >= 0

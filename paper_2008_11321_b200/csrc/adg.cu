@@ -60,7 +60,7 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
                              const int32_t* __restrict__ D, int32_t* __restrict__ round,
                              uint8_t* __restrict__ rs,
                              const int32_t* __restrict__ Uin, int32_t* __restrict__ Uout,
-                             int32_t* __restrict__ Rl, int2* __restrict__ chunks,
+                             int4* __restrict__ lrec, int4* __restrict__ chunks,
                              int32_t* __restrict__ npred, State* st, int heavy_deg, int chunk,
                              int64_t chunk_cap) {
   __shared__ int sm[33];
@@ -91,12 +91,14 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
     const bool sel = valid && d <= dmax;
     bool light = false;
     int nch = 0;
+    long long o = 0, deg = 0;
     if (sel) {
       round[v] = l;
       rs[v] = (uint8_t)((l - 1) % 255 + 1);
       my_sumD += (unsigned long long)d;
       my_nR += 1;
-      const long long deg = off[v + 1] - off[v];
+      o = off[v];
+      deg = off[v + 1] - o;
       light = deg <= heavy_deg;
       if (!light) {
         nch = (int)((deg + chunk - 1) / chunk);
@@ -107,9 +109,14 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
     if (nch) {
       if (cb + (long long)nch > chunk_cap) st->err = 3;
       else
-        for (int k = 0; k < nch; ++k) chunks[cb + k] = make_int2(v, k);
+        for (int k = 0; k < nch; ++k) {
+          const long long s0 = o + (long long)k * chunk;
+          const int len = (int)min((long long)chunk, o + deg - s0);
+          chunks[2 * (cb + k)] = make_int4(v, len, (int)(uint32_t)s0, (int)(s0 >> 32));
+          chunks[2 * (cb + k) + 1] = make_int4((int)(uint32_t)o, (int)(o >> 32), 0, 0);
+        }
     }
-    block_append(light, v, Rl, &st->nLight, sm);
+    block_append_rec(light, light_rec(v, (int)deg, o), lrec, &st->nLight, sm);
     block_append(valid && !sel, v, Uout, &st->nUnext, sm);
   }
   unsigned long long t = block_sum(my_sumD, s_red);
@@ -163,37 +170,52 @@ struct Arc {
 // and walks their concatenated adjacencies (warp-level merge path: each arc
 // finds its owner by a 5-step shuffle search over the inclusive degree scan),
 // kStrips strips of 32 arcs in flight (col loads, then state gathers, then
-// classification) so each warp keeps 4 independent requests outstanding.
+// classification) so each warp keeps kStrips independent requests outstanding.
 // Pred slots: the arcs of one owner are contiguous in a strip, so an arc's
 // rank among its owner's preds is a popc of the pred ballot over the owner's
 // segment; each lane keeps its own vertex's running count in a register (no
 // shared-memory atomics).
-constexpr int kStrips = 4;
+constexpr int kStrips = 8;
 template <int MODE>
-__global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t* __restrict__ off,
-                                                      const int32_t* __restrict__ col,
-                                                      const int32_t* __restrict__ Rl,
+__global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int32_t* __restrict__ col,
+                                                      const int4* __restrict__ lrec,
                                                       int32_t* __restrict__ npred,
                                                       int32_t* __restrict__ P, State* st) {
   __shared__ unsigned long long s_red[32];
+  __shared__ int s_next;
   if (MODE != 2 && st->done) return;
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
   const int nL = st->nLight;
-  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  // each block owns a contiguous range of 32-vertex groups; its warps take
+  // groups from it dynamically (shared-memory ticket), which evens out the
+  // degree variance between groups without a contended global counter.  The
+  // next group's records are loaded one group ahead.
+  const int ngroups = (nL + 31) >> 5;
+  const int g_lo = (int)((long long)ngroups * blockIdx.x / gridDim.x);
+  const int g_hi = (int)((long long)ngroups * (blockIdx.x + 1) / gridDim.x);
+  if (threadIdx.x == 0) s_next = g_lo;
+  __syncthreads();
   unsigned long long cut = 0, preds = 0;
-  for (int b = wg * 32; b < nL; b += nwarps * 32) {
-    const int i = b + lane;
-    const bool valid = i < nL;
-    int v = 0, rv = 0, deg = 0;
-    long long o = 0;
-    if (valid) {
-      v = Rl[i];
-      o = off[v];
-      deg = (int)(off[v + 1] - o);
-      if (MODE == 2) rv = A.round[v];
-    }
+  auto take = [&](int& g, int4& r) {
+    g = 0;
+    if (lane == 0) g = atomicAdd(&s_next, 1);
+    g = __shfl_sync(0xffffffffu, g, 0);
+    const int i = g * 32 + lane;
+    r = (g < g_hi && i < nL) ? lrec[i] : make_int4(0, 0, 0, 0);
+  };
+  int g_nx;
+  int4 r_nx;
+  take(g_nx, r_nx);
+  for (;;) {
+    const int g = g_nx;
+    if (g >= g_hi) break;
+    const int4 r = r_nx;
+    take(g_nx, r_nx);
+    const bool valid = g * 32 + lane < nL;
+    const int v = r.x, deg = r.y;
+    const long long o = lo_hi(r.z, r.w);
+    const int rv = (MODE == 2 && valid) ? A.round[v] : 0;
     const uint64_t hv = (MODE != 0 && valid) ? prio_hash(A.seed, (uint32_t)v) : 0;
     int incl = deg;
 #pragma unroll
@@ -205,8 +227,7 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t
     const int excl = incl - deg;
     int cnt = 0;  // preds of this lane's vertex found so far
     for (int t0 = 0; t0 < total; t0 += 32 * kStrips) {
-      int u[kStrips], ow[kStrips], g[kStrips];
-      long long oo[kStrips];
+      int u[kStrips], ow[kStrips], gs[kStrips];
 #pragma unroll
       for (int k = 0; k < kStrips; ++k) {
         const int a = t0 + 32 * k + lane;
@@ -218,26 +239,27 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t
           if (x <= a) lo += s;
         }
         ow[k] = lo > 31 ? 31 : lo;
-        oo[k] = __shfl_sync(0xffffffffu, o, ow[k]);
+        const long long oo = __shfl_sync(0xffffffffu, o, ow[k]);
         const int oe = __shfl_sync(0xffffffffu, excl, ow[k]);
-        u[k] = a < total ? ld_stream(col + oo[k] + (a - oe)) : -1;
+        u[k] = a < total ? ld_stream(col + oo + (a - oe)) : -1;
       }
 #pragma unroll
-      for (int k = 0; k < kStrips; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
+      for (int k = 0; k < kStrips; ++k) gs[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
 #pragma unroll
       for (int k = 0; k < kStrips; ++k) {
         const int ts = t0 + 32 * k;  // first arc of this strip
         const uint64_t oh = MODE != 0 ? __shfl_sync(0xffffffffu, hv, ow[k]) : 0;
         const int orv = MODE == 2 ? __shfl_sync(0xffffffffu, rv, ow[k]) : 0;
-        const bool pred = u[k] >= 0 && A.classify(u[k], g[k], orv, oh, cut);
+        const bool pred = u[k] >= 0 && A.classify(u[k], gs[k], orv, oh, cut);
         if (MODE != 0) {
           const unsigned pb = __ballot_sync(0xffffffffu, pred);
           const int base = __shfl_sync(0xffffffffu, cnt, ow[k]);
           const int oe = __shfl_sync(0xffffffffu, excl, ow[k]);
+          const long long oo = __shfl_sync(0xffffffffu, o, ow[k]);
           const int seg0 = max(0, oe - ts);  // first lane of the owner's segment
           if (pred) {
             const int rank = __popc(pb & lt & ~((1u << seg0) - 1u));
-            st_stream(P + oo[k] + base + rank, u[k]);
+            st_stream(P + oo + base + rank, u[k]);
           }
           // own segment in this strip: lanes [lo, hi)
           const int lo = min(32, max(0, excl - ts)), hi = min(32, max(0, incl - ts));
@@ -266,43 +288,58 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int64_t
 // round trip on the critical path).
 constexpr int kSub = 512;
 template <int MODE>
-__global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int64_t* __restrict__ off,
-                                                      const int32_t* __restrict__ col,
-                                                      const int2* __restrict__ chunks,
+__global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t* __restrict__ col,
+                                                      const int4* __restrict__ chunks,
                                                       int32_t* __restrict__ npred,
-                                                      int32_t* __restrict__ P, State* st,
-                                                      int chunk) {
+                                                      int32_t* __restrict__ P, State* st) {
   __shared__ unsigned long long s_red[32];
   __shared__ int s_buf[MODE != 0 ? 8 : 1][MODE != 0 ? kSub : 1];
+  __shared__ int s_next;
   if (MODE != 2 && st->done) return;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const int nC = st->nChunks;
-  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int c_lo = (int)((long long)nC * blockIdx.x / gridDim.x);
+  const int c_hi = (int)((long long)nC * (blockIdx.x + 1) / gridDim.x);
+  if (threadIdx.x == 0) s_next = c_lo;
+  __syncthreads();
   unsigned long long cut = 0, preds = 0;
-  for (int ci = wg; ci < nC; ci += nwarps) {
-    const int2 ck = chunks[ci];
-    const int v = ck.x;
-    const long long o = off[v], end = off[v + 1];
-    const long long s = o + (long long)ck.y * chunk;
-    const long long e = min(end, s + chunk);
+  // chunk records are fetched one item ahead (lanes 0/1 load the two halves)
+  auto take = [&](int& ci, int4& r) {
+    ci = 0;
+    if (lane == 0) ci = atomicAdd(&s_next, 1);
+    ci = __shfl_sync(0xffffffffu, ci, 0);
+    r = (ci < c_hi && lane < 2) ? chunks[2 * ci + lane] : make_int4(0, 0, 0, 0);
+  };
+  int ci_nx;
+  int4 r_nx;
+  take(ci_nx, r_nx);
+  for (;;) {
+    const int ci = ci_nx;
+    if (ci >= c_hi) break;
+    const int4 r0 = r_nx;
+    take(ci_nx, r_nx);
+    const int v = __shfl_sync(0xffffffffu, r0.x, 0);
+    const int len = __shfl_sync(0xffffffffu, r0.y, 0);
+    const long long s = lo_hi(__shfl_sync(0xffffffffu, r0.z, 0), __shfl_sync(0xffffffffu, r0.w, 0));
+    const long long o = lo_hi(__shfl_sync(0xffffffffu, r0.x, 1), __shfl_sync(0xffffffffu, r0.y, 1));
+    const long long e = s + len;
     const uint64_t hv = MODE != 0 ? prio_hash(A.seed, (uint32_t)v) : 0;
     const int rv = MODE == 2 ? A.round[v] : 0;
     for (long long s0 = s; s0 < e; s0 += kSub) {
       const long long e0 = min(e, s0 + kSub);
       int cnt = 0;  // preds staged in s_buf[warp]
-      for (long long a0 = s0; a0 < e0; a0 += 128) {
-        // 4 strips of 32 arcs: 4 independent col loads, then 4 state gathers in flight
-        int u[4], g[4];
+      for (long long a0 = s0; a0 < e0; a0 += 32 * kStrips) {
+        // kStrips strips of 32 arcs: independent col loads, then state gathers in flight
+        int u[kStrips], g[kStrips];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kStrips; ++k) {
           const long long a = a0 + 32 * k + lane;
           u[k] = a < e0 ? ld_stream(col + a) : -1;
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
+        for (int k = 0; k < kStrips; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < kStrips; ++k) {
           const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut);
           if (MODE != 0) {
             const unsigned bal = __ballot_sync(0xffffffffu, pred);
@@ -365,8 +402,8 @@ __global__ void k_adg_finalize(int l, State* st, long long* per_round) {
 
 // JP Part 1 work lists for an arbitrary key (pgc_jp_color): every vertex is
 // classified, light ones into Rl, heavy ones into edge chunks.
-__global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int32_t* __restrict__ Rl,
-                              int2* __restrict__ chunks, int32_t* __restrict__ npred, State* st,
+__global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int4* __restrict__ lrec,
+                              int4* __restrict__ chunks, int32_t* __restrict__ npred, State* st,
                               int heavy_deg, int chunk, int64_t chunk_cap) {
   __shared__ int sm[33];
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -375,9 +412,11 @@ __global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int32_
     const bool valid = i < n;
     bool light = false;
     int nch = 0;
+    long long o = 0, deg = 0;
     if (valid) {
       const int v = (int)i;
-      const long long deg = off[v + 1] - off[v];
+      o = off[v];
+      deg = off[v + 1] - o;
       light = deg <= heavy_deg;
       if (!light) {
         nch = (int)((deg + chunk - 1) / chunk);
@@ -388,9 +427,14 @@ __global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int32_
     if (nch) {
       if (cb + (long long)nch > chunk_cap) st->err = 3;
       else
-        for (int k = 0; k < nch; ++k) chunks[cb + k] = make_int2((int)i, k);
+        for (int k = 0; k < nch; ++k) {
+          const long long s0 = o + (long long)k * chunk;
+          const int len = (int)min((long long)chunk, o + deg - s0);
+          chunks[2 * (cb + k)] = make_int4((int)i, len, (int)(uint32_t)s0, (int)(s0 >> 32));
+          chunks[2 * (cb + k) + 1] = make_int4((int)(uint32_t)o, (int)(o >> 32), 0, 0);
+        }
     }
-    block_append(light, (int)i, Rl, &st->nLight, sm);
+    block_append_rec(light, light_rec((int)i, (int)deg, o), lrec, &st->nLight, sm);
   }
 }
 
@@ -407,11 +451,10 @@ template <int MODE>
 static int launch_update(Ctx& c, const Arc<MODE>& A) {
   const int GL = wave_grid(c, k_update_light<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_light",
-             k_update_light<MODE><<<GL, 256, 0, c.st>>>(A, c.off, c.col, c.Rl, c.npred, c.P, c.state));
+             k_update_light<MODE><<<GL, 256, 0, c.st>>>(A, c.col, c.lrec, c.npred, c.P, c.state));
   const int GH = wave_grid(c, k_update_heavy<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_heavy",
-             k_update_heavy<MODE><<<GH, 256, 0, c.st>>>(A, c.off, c.col, c.chunks, c.npred, c.P,
-                                                       c.state, c.tune.chunk_arcs));
+             k_update_heavy<MODE><<<GH, 256, 0, c.st>>>(A, c.col, c.chunks, c.npred, c.P, c.state));
   return 0;
 }
 
@@ -430,9 +473,10 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
       const int32_t* Uin = l == 1 ? nullptr : c.U[l & 1];
       int32_t* Uout = c.U[(l + 1) & 1];
       PGC_LAUNCH(c, kGSelect, "k_adg_select",
-                 k_adg_select<<<G, B, 0, c.st>>>(l, num, den, c.off, c.D, round, c.rs, Uin, Uout, c.Rl,
-                                                 c.chunks, c.npred, c.state, c.tune.heavy_degree,
-                                                 c.tune.chunk_arcs, c.lay.chunk_cap));
+                 k_adg_select<<<G, B, 0, c.st>>>(l, num, den, c.off, c.D, round, c.rs, Uin, Uout,
+                                                 c.lrec, c.chunks, c.npred, c.state,
+                                                 c.tune.heavy_degree, c.tune.chunk_arcs,
+                                                 c.lay.chunk_cap));
       if (mode == kAdgFused) {
         if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs})) return e;
       } else {
@@ -457,7 +501,7 @@ int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color_zer
   }
   if (c.n == 0) return 0;
   PGC_LAUNCH(c, kGUpdate, "k_jp_classify",
-             k_jp_classify<<<G, 256, 0, c.st>>>(c.n, c.off, c.Rl, c.chunks, c.npred, c.state,
+             k_jp_classify<<<G, 256, 0, c.st>>>(c.n, c.off, c.lrec, c.chunks, c.npred, c.state,
                                                 c.tune.heavy_degree, c.tune.chunk_arcs,
                                                 c.lay.chunk_cap));
   return launch_update(c, Arc<2>{0, seed, round, nullptr, nullptr});

@@ -66,10 +66,11 @@ Layout make_layout(int64_t n, int64_t nnz) {
   L.U0 = take(4 * un);
   L.U1 = take(4 * un);
   L.Rl = take(4 * un);
-  // chunked vertices have degree > heavy_degree >= 32 (at most nnz/33 of them)
-  // and need ceil(deg/chunk) <= deg/kMinChunk + 1 items each
-  L.chunk_cap = nnz / kMinChunk + (nnz / 33 < n ? nnz / 33 : n) + 2;
-  L.chunks = take(sizeof(int2) * (size_t)L.chunk_cap);
+  // chunked vertices have degree > heavy_degree >= kMinHeavyDeg (at most
+  // nnz/(kMinHeavyDeg+1) of them) and need ceil(deg/chunk) <= deg/kMinChunk + 1
+  // items each; a chunk record is 2 x int4
+  L.chunk_cap = nnz / kMinChunk + (nnz / (kMinHeavyDeg + 1) < n ? nnz / (kMinHeavyDeg + 1) : n) + 2;
+  L.chunks = take(32 * (size_t)L.chunk_cap);
   L.order = take(4 * un);
   L.range_cap = n + 65536;
   L.hist1 = take(4 * (size_t)(2 * L.range_cap));
@@ -135,7 +136,7 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.U[0] = (int32_t*)(b + c.lay.U0);
   c.U[1] = (int32_t*)(b + c.lay.U1);
   c.Rl = (int32_t*)(b + c.lay.Rl);
-  c.chunks = (int2*)(b + c.lay.chunks);
+  c.chunks = (int4*)(b + c.lay.chunks);
   c.order = (int32_t*)(b + c.lay.order);
   c.hist1 = (int32_t*)(b + c.lay.hist1);
   c.base1 = (int32_t*)(b + c.lay.base1);
@@ -145,6 +146,7 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.cbase = (int64_t*)(b + c.lay.cbase);
   c.cnp = (int32_t*)(b + c.lay.cnp);
   c.rec = (int4*)(b + c.lay.rec);
+  c.lrec = c.rec;  // ADG and JP never use their records at the same time
   if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));
   c.h_state = g_hstate;
   if (g_trace_grab && g_trace_n == g->n) {
@@ -389,7 +391,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
     g_tune.rounds_per_sync = (int)value;
     return PGC_OK;
   }
-  if (!strcmp(key, "heavy_degree") && value >= 32 && value <= (1 << 30)) {
+  if (!strcmp(key, "heavy_degree") && value >= kMinHeavyDeg && value <= (1 << 30)) {
     g_tune.heavy_degree = (int)value;
     return PGC_OK;
   }

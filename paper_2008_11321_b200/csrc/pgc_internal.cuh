@@ -12,6 +12,7 @@ namespace pgc {
 
 constexpr int kWarp = 32;
 constexpr int kMinChunk = 256;        // smallest allowed arcs-per-work-item for chunked vertices
+constexpr int kMinHeavyDeg = 128;     // smallest allowed heavy_degree (sizes the chunk records)
 constexpr int kMaxRoundStats = 4096;  // per-round statistics kept in the workspace
 constexpr int kCoreCap = 65536;       // JP core: at most this many vertices (u16 positions)
 constexpr int kBucketTarget = 8;      // mean bucket occupancy target of the priority-order sort
@@ -98,7 +99,8 @@ struct Ctx {
   int32_t* P;
   int32_t* U[2];
   int32_t* Rl;
-  int2* chunks;
+  int4* lrec;      // UPDATE light work records (aliases the JP bulk record region)
+  int4* chunks;    // UPDATE edge-chunk records, 2 x int4 each
   int32_t* order;
   int32_t* hist1;
   int32_t* base1;
@@ -229,6 +231,38 @@ __device__ __forceinline__ void block_append(bool flag, int val, int32_t* out, i
   __syncthreads();
   if (flag) out[sm[nw] + sm[warp] + __popc(b & lanemask_lt())] = val;
   __syncthreads();
+}
+
+// block_append for 16-byte records (the UPDATE work lists).
+__device__ __forceinline__ void block_append_rec(bool flag, int4 val, int4* out, int* counter,
+                                                 int* sm) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned b = __ballot_sync(0xffffffffu, flag);
+  if (lane == 0) sm[warp] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      int c = sm[w];
+      sm[w] = tot;
+      tot += c;
+    }
+    sm[nw] = tot ? atomicAdd(counter, tot) : 0;
+  }
+  __syncthreads();
+  if (flag) out[sm[nw] + sm[warp] + __popc(b & lanemask_lt())] = val;
+  __syncthreads();
+}
+
+// UPDATE work records (written by the select / classify kernels, one coalesced
+// load per item in the UPDATE kernels):
+//   light vertex: {v, deg, off_lo, off_hi}
+//   edge chunk  : {v, len, start_lo, start_hi}, {base_lo, base_hi, 0, 0}
+__device__ __forceinline__ int64_t lo_hi(int lo, int hi) {
+  return (int64_t)(((uint64_t)(uint32_t)hi << 32) | (uint32_t)lo);
+}
+__device__ __forceinline__ int4 light_rec(int v, int deg, int64_t o) {
+  return make_int4(v, deg, (int)(uint32_t)o, (int)(o >> 32));
 }
 
 // Block-wide reservation: each thread asks for `cnt` slots; returns the

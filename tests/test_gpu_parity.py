@@ -203,7 +203,7 @@ def test_determinism_across_tuning(tuning):
     g = gg.rmat(14, 16, seed=2)
     pgc, off, col = dev(g)
     ref = None
-    for hd, rps, core, hw, sleep in ((32, 1, 0, 1, 0), (100, 3, 65535, 2, 64),
+    for hd, rps, core, hw, sleep in ((128, 1, 0, 1, 0), (200, 3, 65535, 2, 64),
                                      (1024, 8, 500, 4, 8192), (1 << 20, 8, 65535, 4, 2048),
                                      (128, 2, 0, 3, 100000)):
         tuning("heavy_degree", hd)
