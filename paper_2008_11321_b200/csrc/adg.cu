@@ -139,7 +139,11 @@ struct Arc {
   // (exact: rs = ((round-1) mod 255) + 1), from round[] afterwards.
   __device__ __forceinline__ int state(int u) const {
     if (l <= 255) {
+#ifdef PGC_RS_PLAIN
       const int b = rs[u];
+#else
+      const int b = __ldg(rs + u);  // read-only path: L1-cached, rs is immutable during UPDATE
+#endif
       return b == 0 ? 0 : (b == l ? 1 : 2);
     }
     const int r = round[u];

@@ -71,7 +71,6 @@ Layout make_layout(int64_t n, int64_t nnz) {
   // items each; a chunk record is 2 x int4
   L.chunk_cap = nnz / kMinChunk + (nnz / (kMinHeavyDeg + 1) < n ? nnz / (kMinHeavyDeg + 1) : n) + 2;
   L.chunks = take(32 * (size_t)L.chunk_cap);
-  L.order = take(4 * un);
   L.range_cap = n + 65536;
   L.hist1 = take(4 * (size_t)(2 * L.range_cap));
   L.base1 = take(4 * (size_t)(2 * L.range_cap + 1));
@@ -82,12 +81,10 @@ Layout make_layout(int64_t n, int64_t nnz) {
   const int64_t big = L.nb_cap > 2 * L.range_cap + 1 ? L.nb_cap : 2 * L.range_cap + 1;
   L.scan_tmp_cap = big / kScanTile + 4;
   L.scan_tmp = take(4 * (size_t)L.scan_tmp_cap);
-  const size_t ncore = (size_t)(n < kCoreCap ? n : kCoreCap);
-  L.cbase = take(8 * ncore);
-  L.cnp = take(4 * ncore);
-  // bulk records: heavy vertices have > 62 preds, so at most nnz / 63 of them
+  // JP records: n in priority order, then the bulk's heavy list (> 62 preds,
+  // so at most nnz / 63 of them) and light list (< n)
   L.rec_heavy_cap = (nnz / 63 < n ? nnz / 63 : n) + 1;
-  L.rec = take(16 * (size_t)(L.rec_heavy_cap + n));
+  L.rec = take(16 * (size_t)(L.rec_heavy_cap + 2 * n));
   L.total = a;
   return L;
 }
@@ -137,14 +134,11 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.U[1] = (int32_t*)(b + c.lay.U1);
   c.Rl = (int32_t*)(b + c.lay.Rl);
   c.chunks = (int4*)(b + c.lay.chunks);
-  c.order = (int32_t*)(b + c.lay.order);
   c.hist1 = (int32_t*)(b + c.lay.hist1);
   c.base1 = (int32_t*)(b + c.lay.base1);
   c.bcnt = (int32_t*)(b + c.lay.bcnt);
   c.bstart = (int32_t*)(b + c.lay.bstart);
   c.scan_tmp = (int32_t*)(b + c.lay.scan_tmp);
-  c.cbase = (int64_t*)(b + c.lay.cbase);
-  c.cnp = (int32_t*)(b + c.lay.cnp);
   c.rec = (int4*)(b + c.lay.rec);
   c.lrec = c.rec;  // ADG and JP never use their records at the same time
   if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));

@@ -245,16 +245,21 @@ __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, uint64_t s
   }
 }
 
+// Places every vertex's JP work record {v, |pred|, P slot lo, hi} at its
+// bucket position (the per-vertex inputs are read coalesced here, once, so the
+// JP workers fetch one 16-byte record per vertex).
 __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, uint64_t seed,
                           const State* st, const int32_t* __restrict__ hist1,
                           const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
-                          const int32_t* __restrict__ bstart, int32_t* __restrict__ order) {
+                          const int32_t* __restrict__ bstart, const int32_t* __restrict__ npred,
+                          const int64_t* __restrict__ off, int4* __restrict__ rec) {
   const int rmax = st->rmax;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
     const int pos = bstart[b] + atomicSub(&bcnt[b], 1) - 1;
-    order[pos] = (int)v;
+    const int64_t o = off[v];
+    rec[pos] = make_int4((int)v, npred[v], (int)(uint32_t)o, (int)(o >> 32));
   }
 }
 
@@ -262,9 +267,9 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, uint64_t
 // bits).  One lane per bucket (insertion sort in registers, <= 16 entries, the
 // common case at mean occupancy 4..8); larger buckets are ranked by a whole
 // warp afterwards.
-constexpr int kLaneSortMax = 16;
+constexpr int kLaneSortMax = 12;
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
-                              int32_t* __restrict__ order, uint64_t seed) {
+                              int4* __restrict__ rec, uint64_t seed) {
   const int lane = lane_id();
   const int nb = st->nbuckets;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -277,18 +282,18 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
       s = bstart[b + 1] - s0;
     }
     if (s >= 2 && s <= kLaneSortMax) {
-      int vv[kLaneSortMax];
+      int4 vv[kLaneSortMax];
       uint64_t hh[kLaneSortMax];
 #pragma unroll
       for (int i = 0; i < kLaneSortMax; ++i)
         if (i < s) {
-          vv[i] = order[s0 + i];
-          hh[i] = prio_hash(seed, (uint32_t)vv[i]);
+          vv[i] = rec[s0 + i];
+          hh[i] = prio_hash(seed, (uint32_t)vv[i].x);
         }
 #pragma unroll
       for (int i = 1; i < kLaneSortMax; ++i) {
         if (i < s) {
-          const int x = vv[i];
+          const int4 x = vv[i];
           const uint64_t hx = hh[i];
           int j = i - 1;
 #pragma unroll
@@ -304,7 +309,7 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
       }
 #pragma unroll
       for (int i = 0; i < kLaneSortMax; ++i)
-        if (i < s) order[s0 + i] = vv[i];
+        if (i < s) rec[s0 + i] = vv[i];
     }
     // rare large buckets: the whole warp ranks them, one bucket at a time
     unsigned big = __ballot_sync(0xffffffffu, s > kLaneSortMax);
@@ -314,23 +319,23 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
       const int bs0 = __shfl_sync(0xffffffffu, s0, src);
       const int bs = __shfl_sync(0xffffffffu, s, src);
       if (bs <= 32) {
-        const int v = lane < bs ? order[bs0 + lane] : 0;
-        const uint64_t h = lane < bs ? prio_hash(seed, (uint32_t)v) : 0;
+        const int4 v = lane < bs ? rec[bs0 + lane] : make_int4(0, 0, 0, 0);
+        const uint64_t h = lane < bs ? prio_hash(seed, (uint32_t)v.x) : 0;
         int rank = 0;
         for (int j = 0; j < bs; ++j) rank += __shfl_sync(0xffffffffu, h, j) > h;
         __syncwarp();
-        if (lane < bs) order[bs0 + rank] = v;
+        if (lane < bs) rec[bs0 + rank] = v;
         __syncwarp();
       } else if (lane == 0) {  // very rare: insertion sort in place
         for (int i = 1; i < bs; ++i) {
-          const int x = order[bs0 + i];
-          const uint64_t hx = prio_hash(seed, (uint32_t)x);
+          const int4 x = rec[bs0 + i];
+          const uint64_t hx = prio_hash(seed, (uint32_t)x.x);
           int j = i - 1;
-          while (j >= 0 && prio_hash(seed, (uint32_t)order[bs0 + j]) < hx) {
-            order[bs0 + j + 1] = order[bs0 + j];
+          while (j >= 0 && prio_hash(seed, (uint32_t)rec[bs0 + j].x) < hx) {
+            rec[bs0 + j + 1] = rec[bs0 + j];
             --j;
           }
-          order[bs0 + j + 1] = x;
+          rec[bs0 + j + 1] = x;
         }
       }
       __syncwarp();
@@ -382,9 +387,9 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) 
     return e;
   PGC_LAUNCH(c, kGOrder, "k_scatter",
              k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
-                                            c.bstart, c.order));
+                                            c.bstart, c.npred, c.off, c.rec));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
-             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.order, seed));
+             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.rec, seed));
   return 0;
 }
 
@@ -451,8 +456,8 @@ constexpr int kCoreFixedSmem = kCoreWarps * kCoreWin + kCoreWarps * kCorePend * 
 
 // One block: NC = the longest prefix p <= min(n, core_max) of the priority
 // order with sum(npred) >= min_avg * p and sum(npred) <= arc_cap.
-__global__ void __launch_bounds__(1024) k_core_select(int64_t n, const int32_t* __restrict__ order,
-                                                      const int32_t* __restrict__ npred, State* st,
+__global__ void __launch_bounds__(1024) k_core_select(int64_t n, const int4* __restrict__ rec,
+                                                      State* st,
                                                       int core_max, int min_avg,
                                                       long long arc_cap) {
   __shared__ long long s_w[32];
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(1024) k_core_select(int64_t n, const int32_t* 
   if (threadIdx.x == 0) s_best = 0;
   long long loc = 0;
   for (int k = 0; k < per; ++k)
-    if (t0 + k < L) loc += npred[order[t0 + k]];
+    if (t0 + k < L) loc += rec[t0 + k].y;
   long long incl = loc;
 #pragma unroll
   for (int s = 1; s < 32; s <<= 1) {
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(1024) k_core_select(int64_t n, const int32_t* 
   for (int k = 0; k < per; ++k) {
     const int p = t0 + k;
     if (p >= L) break;
-    run += npred[order[p]];  // sum over the prefix of length p + 1
+    run += rec[p].y;  // sum over the prefix of length p + 1
     if (run >= (long long)min_avg * (p + 1) && run <= arc_cap)
       best = ((unsigned long long)(p + 1) << 32) | (unsigned long long)run;
   }
@@ -501,30 +506,23 @@ __global__ void __launch_bounds__(1024) k_core_select(int64_t n, const int32_t* 
   }
 }
 
-__global__ void k_core_pos(const int32_t* __restrict__ order, const State* st,
-                           int32_t* __restrict__ pos) {
+__global__ void k_core_pos(const int4* __restrict__ rec, const State* st, int32_t* __restrict__ pos) {
   const int NC = st->core_n;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < NC; p += gridDim.x * blockDim.x)
-    pos[order[p]] = p;
+    pos[rec[p].x] = p;
 }
 
 // Warp per core vertex: rewrite its pred list in place (P slot, int32 ids ->
-// u16 core positions at the start of the same slot) and record (slot, |pred|).
-__global__ void k_core_lists(const int64_t* __restrict__ off, const int32_t* __restrict__ order,
-                             const int32_t* __restrict__ npred, const int32_t* __restrict__ pos,
-                             int32_t* P, int64_t* __restrict__ cbase, int32_t* __restrict__ cnp,
-                             const State* st) {
+// u16 core positions at the start of the same slot).
+__global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __restrict__ pos,
+                             int32_t* P, const State* st) {
   const int lane = lane_id();
   const int NC = st->core_n;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < NC; p += nw) {
-    const int v = order[p];
-    const int np = npred[v];
-    const int64_t b = off[v];
-    if (lane == 0) {
-      cbase[p] = b;
-      cnp[p] = np;
-    }
+    const int4 r = rec[p];
+    const int np = r.y;
+    const int64_t b = lo_hi(r.z, r.w);
     uint16_t* L = reinterpret_cast<uint16_t*>(P + b);
     for (int i0 = 0; i0 < np; i0 += 32) {
       const int i = i0 + lane;
@@ -586,9 +584,7 @@ __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np,
   return np;
 }
 
-__global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int32_t* __restrict__ order,
-                                                           const int64_t* __restrict__ cbase,
-                                                           const int32_t* __restrict__ cnp,
+__global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restrict__ rec,
                                                            const int32_t* __restrict__ P,
                                                            int32_t* color, State* st,
                                                            unsigned long long* tr_grab,
@@ -624,14 +620,15 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int32_t* __rest
     // chain hops inside a run stay in local shared memory
     const int p = (rank + C * (k / kCoreRun)) * kCoreRun + (k % kCoreRun);
     if (p >= NC) break;
-    const int np = cnp[p];
-    const uint16_t* L = reinterpret_cast<const uint16_t*>(P + cbase[p]);
-    const int vcore = order[p];  // loaded early: the color store must not wait on it
+    const int4 r = rec[p];
+    const int np = r.y;
+    const uint16_t* L = reinterpret_cast<const uint16_t*>(P + lo_hi(r.z, r.w));
+    const int vcore = r.x;
 #ifdef PGC_PROBE
-    const int vprobe = order[p];
+    const int vprobe = vcore;
     PROBE_STAMP(tr_done, vprobe, 0);
 #else
-    if (tr_grab && lane == 0) tr_grab[order[p]] = globaltimer();
+    if (tr_grab && lane == 0) tr_grab[vcore] = globaltimer();
 #endif
     int found = 0;
     for (int wbase = 0; !found && !stall; wbase += kCoreWin) {
@@ -772,43 +769,35 @@ constexpr int kHeavyWin = 2048;    // colors per heavy byte-map window
 constexpr int kPendCap = 256;      // pending-pred list capacity per heavy warp (smem)
 constexpr int kLightBatch = 8;     // pred loads in flight per light lane
 
-__global__ void k_bulk_flags(int64_t n, const int32_t* __restrict__ order,
-                             const int32_t* __restrict__ npred, const State* st,
+__global__ void k_bulk_flags(int64_t n, const int4* __restrict__ rec, const State* st,
                              int32_t* __restrict__ hflag, int32_t* __restrict__ lflag) {
   const int NC = st->core_n;
   for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const int np = npred[order[p]];
+    const int np = rec[p].y;
     hflag[p - NC] = np > kLightPredMax ? 1 : 0;
     lflag[p - NC] = np > 0 && np <= kLightPredMax ? 1 : 0;
   }
 }
 
-// Stable split of the bulk into heavy and light work lists.  Roots of G_rho
-// (no pred: JP Part 2's initial set) are colored 1 right
-// here (GetColor of the empty set) and listed nowhere.  Every listed vertex
-// gets a 16-byte record {v, |pred|, P slot lo, hi} so a worker fetches it with
-// one coalesced load instead of three dependent ones.  hpos / lpos are the
-// exclusive prefix counts of heavy / light flags.
-__global__ void k_bulk_scatter(int64_t n, const int32_t* __restrict__ order,
-                               const int32_t* __restrict__ npred,
-                               const int64_t* __restrict__ off, State* st,
+// Stable split of the bulk's records (priority order) into heavy and light
+// work lists: streaming reads, monotone writes.  Roots of G_rho (no pred: JP
+// Part 2's initial set) are colored 1 right here (GetColor
+// of the empty set) and listed nowhere.  hpos / lpos are the exclusive prefix
+// counts of the heavy / light flags.
+__global__ void k_bulk_scatter(int64_t n, const int4* __restrict__ rec, State* st,
                                const int32_t* __restrict__ hpos, const int32_t* __restrict__ lpos,
                                int4* __restrict__ hrec, int4* __restrict__ lrec, int32_t* color) {
   const int NC = st->core_n;
   bool root = false;
   for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const int v = order[p];
+    const int4 r = rec[p];
     const int64_t i = p - NC;
-    const int np = npred[v];
-    if (np > 0) {
-      const int64_t b = off[v];
-      const int4 r = make_int4(v, np, (int)(uint32_t)b, (int)(b >> 32));
-      if (np > kLightPredMax) hrec[hpos[i]] = r;
-      else lrec[lpos[i]] = r;
-    } else {
-      st_relaxed(color + v, 1);
+    if (r.y > kLightPredMax) hrec[hpos[i]] = r;
+    else if (r.y > 0) lrec[lpos[i]] = r;
+    else {
+      st_relaxed(color + r.x, 1);
       root = true;
     }
   }
@@ -1232,7 +1221,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
     // --- core ---
     if (c.tune.core_max > 0) {
       PGC_LAUNCH(c, kGCore, "k_core_select",
-                 k_core_select<<<1, 1024, 0, c.st>>>(c.n, c.order, c.npred, c.state,
+                 k_core_select<<<1, 1024, 0, c.st>>>(c.n, c.rec, c.state,
                                                       c.tune.core_max, c.tune.core_min_avg,
                                                       c.tune.core_arc_cap));
       if (int e = sync_state(c)) return e;
@@ -1253,10 +1242,9 @@ int jp_color_run(Ctx& c, int32_t* color) {
         c.core_ctas = C;
         c.core_n = NC;
         const int G = c.nsm * 4;
-        PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.order, c.state, c.D));
+        PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.rec, c.state, c.D));
         PGC_LAUNCH(c, kGCore, "k_core_lists",
-                   k_core_lists<<<G * 2, 256, 0, c.st>>>(c.off, c.order, c.npred, c.D, c.P,
-                                                         c.cbase, c.cnp, c.state));
+                   k_core_lists<<<G * 2, 256, 0, c.st>>>(c.rec, c.D, c.P, c.state));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(C);
         cfg.blockDim = dim3(kCoreBlock);
@@ -1271,8 +1259,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
         cfg.numAttrs = 1;
         const unsigned long long wd = (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull;
         PGC_LAUNCH(c, kGCore, "k_jp_core",
-                   PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int32_t*)c.order,
-                                               (const int64_t*)c.cbase, (const int32_t*)c.cnp,
+                   PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int4*)c.rec,
                                                (const int32_t*)c.P, color, c.state, c.trace_grab,
                                                c.trace_done, (unsigned)c.tune.core_spin_ns, wd)));
       }
@@ -1289,15 +1276,15 @@ int jp_color_run(Ctx& c, int32_t* color) {
       int32_t* hpos = c.Rl;
       int32_t* lpos = c.D;
       PGC_LAUNCH(c, kGJp, "k_bulk_flags",
-                 k_bulk_flags<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.state, hflag, lflag));
+                 k_bulk_flags<<<G, 256, 0, c.st>>>(c.n, c.rec, c.state, hflag, lflag));
       if (int e = scan_ex(c, hflag, hpos, nullptr, nbulk, nbulk, &c.state->nheavy, kGJp)) return e;
       if (int e = scan_ex(c, lflag, lpos, nullptr, nbulk, nbulk, &c.state->nlight, kGJp)) return e;
       // records: heavy then light, in the rec region
-      int4* hrec = reinterpret_cast<int4*>(c.rec);
+      int4* hrec = c.rec + c.n;
       int4* lrec = hrec + c.lay.rec_heavy_cap;
       PGC_LAUNCH(c, kGJp, "k_bulk_scatter",
-                 k_bulk_scatter<<<G, 256, 0, c.st>>>(c.n, c.order, c.npred, c.off, c.state, hpos,
-                                                     lpos, hrec, lrec, color));
+                 k_bulk_scatter<<<G, 256, 0, c.st>>>(c.n, c.rec, c.state, hpos, lpos, hrec, lrec,
+                                                     color));
       const int GB = wave_grid(c, k_jp_bulk, kJpBlock);
       PGC_LAUNCH(c, kGJp, "k_jp_bulk",
                  k_jp_bulk<<<GB, kJpBlock, 0, c.st>>>(

@@ -50,8 +50,8 @@ struct State {
 
 // Byte offsets of every workspace region (each 256-byte aligned).
 struct Layout {
-  size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, order, hist1, base1, bcnt, bstart,
-      scan_tmp, cbase, cnp, rec, total;
+  size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, hist1, base1, bcnt, bstart,
+      scan_tmp, rec, total;
   int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap, rec_heavy_cap;
 };
 
@@ -101,15 +101,13 @@ struct Ctx {
   int32_t* Rl;
   int4* lrec;      // UPDATE light work records (aliases the JP bulk record region)
   int4* chunks;    // UPDATE edge-chunk records, 2 x int4 each
-  int32_t* order;
   int32_t* hist1;
   int32_t* base1;
   int32_t* bcnt;
   int32_t* bstart;
   int32_t* scan_tmp;
-  int64_t* cbase;  // JP core: P slot of core position p
-  int32_t* cnp;    // JP core: |pred| of core position p
-  int4* rec;       // JP bulk work records {v, |pred|, P slot}: heavy then light
+  int4* rec;       // JP records {v, |pred|, P slot}: n in priority order, then the
+                   // bulk's heavy and light lists
   const int32_t* round_key = nullptr;  // JP first priority key (rho_ADG for JP-ADG)
   uint64_t seed = 0;                   // JP tie-break seed
   int core_ctas = 0;                   // cluster size used by the last k_jp_core (0 = none)
