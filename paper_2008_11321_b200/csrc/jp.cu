@@ -268,8 +268,15 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, uint64_t
 // common case at mean occupancy 4..8); larger buckets are ranked by a whole
 // warp afterwards.
 constexpr int kLaneSortMax = 12;
+// Only the buckets that start below `limit` (the region the core engine may
+// take: it needs the exact priority order) and the oversized ones are sorted.
+// The bulk is fine with an order that is exact across buckets only: a bulk
+// worker can then wait on a later ticket of its own bucket, at most
+// kMaxUnsortedBucket - 1 of them, far fewer than the workers of either class,
+// so the highest-priority uncolored vertex is always held or grabbable.
+constexpr int kMaxUnsortedBucket = 64;
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
-                              int4* __restrict__ rec, uint64_t seed) {
+                              int4* __restrict__ rec, uint64_t seed, int limit) {
   const int lane = lane_id();
   const int nb = st->nbuckets;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -280,6 +287,7 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
     if (b < nb) {
       s0 = bstart[b];
       s = bstart[b + 1] - s0;
+      if (s0 >= limit && s <= kMaxUnsortedBucket) s = 0;  // leave unsorted
     }
     if (s >= 2 && s <= kLaneSortMax) {
       int4 vv[kLaneSortMax];
@@ -389,7 +397,7 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) 
              k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
                                             c.bstart, c.npred, c.off, c.rec));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
-             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.rec, seed));
+             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.rec, seed, kCoreCap));
   return 0;
 }
 
@@ -1059,24 +1067,47 @@ __global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restri
     int v = -1, np = 0, watch_j = -1, watch_u = -1;
     int64_t pb = 0;
     unsigned long long mask = 0, pend = 0;
-    bool exhausted = false;
     unsigned sleep_ns = 32;
+    int4 nx = make_int4(0, 0, 0, 0);  // prefetched next record
+    bool have_nx = false;
+    {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(&st->ticket_light, 32);
+      const int64_t t = (int64_t)__shfl_sync(0xffffffffu, t0, 0) + lane;
+      if (t < nlight) {
+        nx = lrec[t];
+        have_nx = true;
+      }
+    }
     for (;;) {
       bool progress = false;
-      // 1. free lanes take the next light tickets (one atomic per warp)
-      const unsigned want = __ballot_sync(0xffffffffu, v < 0 && !exhausted);
+      // 1. free lanes take their prefetched record, then re-arm the prefetch
+      //    with the next light tickets (one atomic per warp): the ticket and
+      //    record loads of the NEXT vertex overlap the scan of this one
+      const bool take = v < 0 && have_nx;
+      if (take) {
+        v = nx.x;
+        np = nx.y;
+        pb = rec_slot(nx);
+        have_nx = false;
+      }
+      const unsigned want = __ballot_sync(0xffffffffu, take);
       if (want) {
         const int leader = __ffs(want) - 1;
         int t0 = 0;
         if (lane == leader) t0 = atomicAdd(&st->ticket_light, __popc(want));
         t0 = __shfl_sync(0xffffffffu, t0, leader);
-        if (v < 0 && !exhausted) {
+        if (take) {
           const int64_t t = (int64_t)t0 + __popc(want & lt);
           if (t < nlight) {
-            const int4 r = lrec[t];
-            v = r.x;
-            np = r.y;
-            pb = rec_slot(r);
+            nx = lrec[t];
+            have_nx = true;
+          }
+        }
+      }
+      {
+        if (take) {
+          {
             if (tr_grab) tr_grab[v] = globaltimer();
             // first pass over every pred
             mask = 1ull;  // bit 0 reserved: colors start at 1
@@ -1104,12 +1135,10 @@ __global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restri
               }
             }
             progress = true;
-          } else {
-            exhausted = true;
           }
         }
       }
-      if (__ballot_sync(0xffffffffu, v >= 0) == 0) break;  // all free and out of tickets
+      if (__ballot_sync(0xffffffffu, v >= 0 || have_nx) == 0) break;  // all free, out of tickets
       // 2. poll the watched pred; when colored, re-examine the other pending preds
       if (v >= 0 && watch_u >= 0) {
         const int cw = ld_relaxed(color + watch_u);
