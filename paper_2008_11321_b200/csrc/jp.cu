@@ -903,8 +903,8 @@ __global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restri
                                                      const int4* __restrict__ hrec,
                                                      const int4* __restrict__ lrec,
                                                      const int32_t* __restrict__ round,
-                                                     uint64_t seed, int32_t* color, State* st,
-                                                     int heavy_warps, unsigned heavy_sleep_max,
+                                                     uint64_t seed, int32_t* color,
+                                                     State* st, int heavy_warps, unsigned heavy_sleep_max,
                                                      unsigned light_sleep_max,
                                                      unsigned long long* tr_grab,
                                                      unsigned long long* tr_done,
@@ -1247,7 +1247,9 @@ static int pow2_floor(int x) {
 int jp_color_run(Ctx& c, int32_t* color) {
   PGC_LAUNCH(c, kGJp, "k_jp_reset", k_jp_reset<<<1, 1, 0, c.st>>>(c.state));
   if (c.n > 0) {
-    // --- core ---
+    // --- core selection and its pred-list rewrite ---
+    int C = 0;
+    size_t core_smem = 0;
     if (c.tune.core_max > 0) {
       PGC_LAUNCH(c, kGCore, "k_core_select",
                  k_core_select<<<1, 1024, 0, c.st>>>(c.n, c.rec, c.state,
@@ -1256,14 +1258,13 @@ int jp_color_run(Ctx& c, int32_t* color) {
       if (int e = sync_state(c)) return e;
       const int NC = c.h_state->core_n;
       const long long arcs = c.h_state->core_arcs;
-      int C = 0;
-      const size_t smem = kCoreFixedSmem + (((size_t)NC * 2 + 15) & ~(size_t)15);
+      core_smem = kCoreFixedSmem + (((size_t)NC * 2 + 15) & ~(size_t)15);
       if (NC >= c.tune.core_min_n) {
         int want = c.tune.core_ctas > 0
                        ? c.tune.core_ctas
                        : (int)((arcs + c.tune.core_arcs_per_cta - 1) / c.tune.core_arcs_per_cta);
         want = pow2_floor(want < 1 ? 1 : (want > 16 ? 16 : want));
-        C = core_cluster_size(want, smem);
+        C = core_cluster_size(want, core_smem);
       }
       if (C == 0) {
         PGC_CUDA(cudaMemsetAsync(&c.state->core_n, 0, sizeof(int), c.st));
@@ -1274,28 +1275,14 @@ int jp_color_run(Ctx& c, int32_t* color) {
         PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.rec, c.state, c.D));
         PGC_LAUNCH(c, kGCore, "k_core_lists",
                    k_core_lists<<<G * 2, 256, 0, c.st>>>(c.rec, c.D, c.P, c.state));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(C);
-        cfg.blockDim = dim3(kCoreBlock);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = c.st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = C;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        const unsigned long long wd = (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull;
-        PGC_LAUNCH(c, kGCore, "k_jp_core",
-                   PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int4*)c.rec,
-                                               (const int32_t*)c.P, color, c.state, c.trace_grab,
-                                               c.trace_done, (unsigned)c.tune.core_spin_ns, wd)));
       }
     }
-    // --- bulk: stable heavy/light split of positions [core_n, n), then the dataflow ---
+    // --- bulk split of positions [core_n, n) (needs only the records, so it
+    //     runs before the core kernel and the bulk starts right after it) ---
     const int NC = c.core_n;
     const int64_t nbulk = c.n - NC;
+    int4* hrec = c.rec + c.n;
+    int4* lrec = hrec + c.lay.rec_heavy_cap;
     if (nbulk > 0) {
       const int G = c.nsm * 8;
       // flags: heavy -> U0, light -> U1; prefix counts: heavy -> Rl, light -> D
@@ -1308,12 +1295,33 @@ int jp_color_run(Ctx& c, int32_t* color) {
                  k_bulk_flags<<<G, 256, 0, c.st>>>(c.n, c.rec, c.state, hflag, lflag));
       if (int e = scan_ex(c, hflag, hpos, nullptr, nbulk, nbulk, &c.state->nheavy, kGJp)) return e;
       if (int e = scan_ex(c, lflag, lpos, nullptr, nbulk, nbulk, &c.state->nlight, kGJp)) return e;
-      // records: heavy then light, in the rec region
-      int4* hrec = c.rec + c.n;
-      int4* lrec = hrec + c.lay.rec_heavy_cap;
       PGC_LAUNCH(c, kGJp, "k_bulk_scatter",
                  k_bulk_scatter<<<G, 256, 0, c.st>>>(c.n, c.rec, c.state, hpos, lpos, hrec, lrec,
                                                      color));
+    }
+    // --- core: one thread-block cluster ---
+    if (C > 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(kCoreBlock);
+      cfg.dynamicSmemBytes = core_smem;
+      cfg.stream = c.st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const unsigned long long wd = (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull;
+      PGC_LAUNCH(c, kGCore, "k_jp_core",
+                 PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int4*)c.rec,
+                                             (const int32_t*)c.P, color, c.state,
+                                             c.trace_grab, c.trace_done,
+                                             (unsigned)c.tune.core_spin_ns, wd)));
+    }
+    // --- bulk dataflow ---
+    if (nbulk > 0) {
       const int GB = wave_grid(c, k_jp_bulk, kJpBlock);
       PGC_LAUNCH(c, kGJp, "k_jp_bulk",
                  k_jp_bulk<<<GB, kJpBlock, 0, c.st>>>(

@@ -177,6 +177,15 @@ __device__ __forceinline__ int ld_relaxed(const int32_t* p) {
 __device__ __forceinline__ void st_relaxed(int32_t* p, int v) {
   asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int ld_relaxed_u16(const uint16_t* p) {
+  unsigned short v;
+  asm volatile("ld.relaxed.gpu.global.u16 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u16(uint16_t* p, int v) {
+  asm volatile("st.relaxed.gpu.global.u16 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
+
 // streaming (evict-first) accesses for data touched once: keeps the L2 for the
 // randomly gathered per-vertex state (rs, D, colors).
 __device__ __forceinline__ int ld_stream(const int32_t* p) { return __ldcs(p); }
