@@ -459,6 +459,7 @@ constexpr int kCoreWarps = kCoreBlock / 32;
 constexpr int kCoreWin = 1024;   // colors per byte-map window
 constexpr int kCorePend = 512;   // pending-pred list capacity per warp
 constexpr int kCoreRun = 32;     // consecutive core positions per CTA run
+constexpr int kCoreTail = 4;     // preds left for the collective-free tail
 // dynamic shared memory ahead of the color replica: bitmaps + pending lists
 constexpr int kCoreFixedSmem = kCoreWarps * kCoreWin + kCoreWarps * kCorePend * 2;
 
@@ -634,7 +635,7 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
     const int vcore = r.x;
 #ifdef PGC_PROBE
     const int vprobe = vcore;
-    PROBE_STAMP(tr_done, vprobe, 0);
+    PROBE_STAMP(tr_grab, vprobe, 0);
 #else
     if (tr_grab && lane == 0) tr_grab[vcore] = globaltimer();
 #endif
@@ -649,9 +650,11 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
       // kept current as pending colors arrive so that the last arrival costs
       // one compare
       int zi = bmap_next_zero<kCoreWin>(bm, 0);
-      PROBE_STAMP(tr_done, vprobe, 1);
+      PROBE_STAMP(tr_grab, vprobe, 1);
       unsigned sleep_ns = 0, polls = 0;
-      // reduce the pending set until at most the last pred is left
+      // Reduce the pending set with warp passes until at most kCoreTail preds
+      // are left (backing off while nothing arrives, so far-away waiters leave
+      // the shared-memory pipe to the warps near the front of the chain).
       for (;;) {
         if (npend == 0) {
           if (over >= np) break;
@@ -660,32 +663,8 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
           zi = bmap_next_zero<kCoreWin>(bm, zi);
           continue;
         }
-        if (npend == 1 && over >= np) break;  // the tail below takes the last one
-        // Several preds pending.  Preds get colored roughly in position order,
-        // so the second-largest pending position is the one whose coloring
-        // leaves this vertex waiting on its last pred: spin on it, then one pass
-        // drops the colored entries and (usually) hands over to the tail.
-        {
-          qmax = warp_max(qmax);
-          int q2 = -1;
-          for (int j0 = 0; j0 < npend; j0 += 32) {  // second-largest pending position
-            const int j = j0 + lane;
-            const int q = j < npend ? (int)plist[j] : -1;
-            q2 = max(q2, q < qmax ? q : -1);
-          }
-          q2 = warp_max(q2);
-          if (q2 < 0) q2 = qmax;
-          for (int k = 0; k < 64 && ld_vol_u16(s_cc + q2) == 0; ++k) {
-            if (sleep_ns) __nanosleep(sleep_ns);
-          }
-          if (ld_vol_u16(s_cc + q2) == 0)
-            sleep_ns = sleep_ns ? min(sleep_ns * 2, (unsigned)spin_ns) : (spin_ns ? 32u : 0u);
-        }
-        if ((++polls & 255u) == 0 && __shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
-          stall = true;
-          break;
-        }
-        int keep = 0, nq = -1;
+        if (npend <= kCoreTail && over >= np) break;  // the tail below takes them
+        int keep = 0;
         for (int j0 = 0; j0 < npend; j0 += 128) {
           int q[4], cc[4];
 #pragma unroll
@@ -701,50 +680,87 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
             const bool still = q[k] >= 0 && cc[k] == 0;
             if (q[k] >= 0 && cc[k]) bmap_mark(bm, cc[k], wbase, kCoreWin);
             const unsigned bal = __ballot_sync(0xffffffffu, still);
-            if (still) {
-              plist[keep + __popc(bal & lt)] = (uint16_t)q[k];
-              nq = max(nq, q[k]);
-            }
+            if (still) plist[keep + __popc(bal & lt)] = (uint16_t)q[k];
             keep += __popc(bal);
           }
         }
         const bool moved = keep < npend;
         npend = keep;
-        qmax = nq;
         __syncwarp();
+        PROBE_STAMP(tr_grab, vprobe, 3);
         if (moved) {
           zi = bmap_next_zero<kCoreWin>(bm, zi);
           sleep_ns = 0;
-        }
-      }
-      if (stall) break;
-      if (npend == 1) {
-        // Tail -- the critical path of a dependency chain.  Everything that
-        // does not need the last color is done before waiting: the candidate
-        // for "the last color takes the current candidate" is found now, so
-        // after the (warp-uniform) spin only a compare-and-select remains.
-        const int q = plist[0];
-        const int zi_next = bmap_next_zero<kCoreWin>(bm, zi + 1);
-        int c;
-        while ((c = ld_vol_u16(s_cc + q)) == 0) {
-          if ((++polls & 65535u) == 0 && globaltimer() > deadline) {
-            st->err = 5;
+        } else {
+          if ((++polls & 63u) == 0 && __shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
             stall = true;
             break;
           }
+          if (sleep_ns) __nanosleep(sleep_ns);
+          sleep_ns = sleep_ns ? min(sleep_ns * 2, (unsigned)spin_ns) : (spin_ns ? 32u : 0u);
         }
-        PROBE_STAMP(tr_grab, vprobe, 0);
-        zi = (c - wbase - 1 == zi) ? zi_next : zi;
+      }
+      if (stall) break;
+      if (npend > 0) {
+        // Tail -- the critical path of a dependency chain, free of warp
+        // collectives (each costs ~40-50 cycles on the chain).  With the used
+        // set S of the colors already seen, GetColor after the last npend <=
+        // kCoreTail colors c_k arrive is the first of the kCoreTail+1 smallest
+        // colors missing from S that no c_k takes.  Those are found now; then
+        // every lane spins on the pending preds in position order (the order
+        // they get colored in) and finishes with compares and selects.
+        int z[kCoreTail + 1];
+        z[0] = zi;
+#pragma unroll
+        for (int k = 1; k <= kCoreTail; ++k) z[k] = bmap_next_zero<kCoreWin>(bm, min(z[k - 1] + 1, kCoreWin));
+        int q[kCoreTail];
+#pragma unroll
+        for (int k = 0; k < kCoreTail; ++k) q[k] = k < npend ? (int)plist[k] : 0x7fffffff;
+#pragma unroll
+        for (int i = 1; i < kCoreTail; ++i)  // ascending positions (a sorting network)
+#pragma unroll
+          for (int k = kCoreTail - 1; k > 0; --k)
+            if (q[k] < q[k - 1]) {
+              const int t = q[k];
+              q[k] = q[k - 1];
+              q[k - 1] = t;
+            }
+        PROBE_STAMP(tr_grab, vprobe, 4);
+        int cl_[kCoreTail];
+#pragma unroll
+        for (int k = 0; k < kCoreTail; ++k) {
+          int c = 0;
+          if (k < npend) {
+            while ((c = ld_vol_u16(s_cc + q[k])) == 0) {
+              if ((++polls & 65535u) == 0 && globaltimer() > deadline) {
+                st->err = 5;
+                stall = true;
+                break;
+              }
+            }
+          }
+          cl_[k] = c - wbase - 1;  // 0-based color within the window (or out of it)
+          if (stall) break;
+        }
+        PROBE_STAMP(tr_grab, vprobe, 5);
+        int res = kCoreWin;
+#pragma unroll
+        for (int j = kCoreTail; j >= 0; --j) {
+          bool taken = false;
+#pragma unroll
+          for (int k = 0; k < kCoreTail; ++k) taken |= (k < npend) && cl_[k] == z[j];
+          if (!taken) res = z[j];
+        }
+        zi = res;
         npend = 0;
-        PROBE_STAMP(tr_grab, vprobe, 1);
       }
       if (stall) break;  // warp-uniform: every lane read the same timer in the same instruction
       if (zi < kCoreWin) found = wbase + zi + 1;  // GetColor (else: next window)
     }
-    PROBE_STAMP(tr_grab, vprobe, 2);
+    PROBE_STAMP(tr_grab, vprobe, 6);
     if (stall) break;
     if (lane < C) *(volatile uint16_t*)(remote + p) = (uint16_t)found;  // publish to every replica
-    PROBE_STAMP(tr_grab, vprobe, 3);
+    PROBE_STAMP(tr_grab, vprobe, 7);
     if (lane == 0) {
       st_relaxed(color + vcore, found);
 #ifndef PGC_PROBE
