@@ -774,6 +774,16 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
   cl.sync();  // no CTA leaves while a peer may still store into its replica
 }
 
+// Pred-list and record reads of the bulk are read once: evict-first, so the
+// randomly gathered color[] stays in L2 (PGC_JP_LDG keeps the default policy).
+__device__ __forceinline__ int jp_stream(const int32_t* p) {
+#ifdef PGC_JP_LDG
+  return __ldg(p);
+#else
+  return __ldcs(p);
+#endif
+}
+
 // ------------------------------------------------------------- bulk ---------
 // JP on the rest of the priority order (positions >= core_n) as a sync-free
 // dataflow.  The rest is split (stably, so each class stays in priority order)
@@ -791,7 +801,10 @@ constexpr int kJpBlock = 256;
 constexpr int kMaxHeavyWarps = 4;  // heavy-path shared buffers exist for this many warps
 constexpr int kHeavyWin = 2048;    // colors per heavy byte-map window
 constexpr int kPendCap = 256;      // pending-pred list capacity per heavy warp (smem)
-constexpr int kLightBatch = 8;     // pred loads in flight per light lane
+#ifndef PGC_LIGHT_BATCH
+#define PGC_LIGHT_BATCH 8
+#endif
+constexpr int kLightBatch = PGC_LIGHT_BATCH;  // pred loads in flight per light lane
 
 __global__ void k_bulk_flags(int64_t n, const int4* __restrict__ rec, const State* st,
                              int32_t* __restrict__ hflag, int32_t* __restrict__ lflag) {
@@ -858,7 +871,7 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int i = i0 + 32 * k + lane;
-      u[k] = i < np ? __ldg(P + pb + i) : -1;
+      u[k] = i < np ? jp_stream(P + pb + i) : -1;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
@@ -944,7 +957,7 @@ __global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restri
       if (lane == 0) t = atomicAdd(&st->ticket_heavy, 1);
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t < nheavy) {
-        const int4 r = hrec[t];
+        const int4 r = __ldcs(hrec + t);
         v = r.x;
         np = r.y;
         pb = rec_slot(r);
@@ -1091,7 +1104,7 @@ __global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restri
       if (lane == 0) t0 = atomicAdd(&st->ticket_light, 32);
       const int64_t t = (int64_t)__shfl_sync(0xffffffffu, t0, 0) + lane;
       if (t < nlight) {
-        nx = lrec[t];
+        nx = __ldcs(lrec + t);
         have_nx = true;
       }
     }
@@ -1116,7 +1129,7 @@ __global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restri
         if (take) {
           const int64_t t = (int64_t)t0 + __popc(want & lt);
           if (t < nlight) {
-            nx = lrec[t];
+            nx = __ldcs(lrec + t);
             have_nx = true;
           }
         }
@@ -1133,7 +1146,7 @@ __global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restri
             for (int j0 = 0; j0 < np; j0 += kLightBatch) {
               int u[kLightBatch], cc[kLightBatch];
 #pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? __ldg(P + pb + j0 + k) : -1;
+              for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? jp_stream(P + pb + j0 + k) : -1;
 #pragma unroll
               for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
 #pragma unroll
