@@ -802,7 +802,7 @@ constexpr int kMaxHeavyWarps = 4;  // heavy-path shared buffers exist for this m
 constexpr int kHeavyWin = 2048;    // colors per heavy byte-map window
 constexpr int kPendCap = 256;      // pending-pred list capacity per heavy warp (smem)
 #ifndef PGC_LIGHT_BATCH
-#define PGC_LIGHT_BATCH 8
+#define PGC_LIGHT_BATCH 4
 #endif
 constexpr int kLightBatch = PGC_LIGHT_BATCH;  // pred loads in flight per light lane
 
@@ -926,7 +926,10 @@ __device__ __forceinline__ void lowest_two(const int* plist, const unsigned long
   u2 = a2;
 }
 
-__global__ void __launch_bounds__(kJpBlock, 6) k_jp_bulk(const int64_t* __restrict__ off,
+#ifndef PGC_BULK_MINB
+#define PGC_BULK_MINB 6
+#endif
+__global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64_t* __restrict__ off,
                                                      const int32_t* __restrict__ P,
                                                      const int32_t* __restrict__ npred,
                                                      const int4* __restrict__ hrec,
