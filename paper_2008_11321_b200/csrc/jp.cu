@@ -801,6 +801,7 @@ constexpr int kJpBlock = 256;
 constexpr int kMaxHeavyWarps = 4;  // heavy-path shared buffers exist for this many warps
 constexpr int kHeavyWin = 2048;    // colors per heavy byte-map window
 constexpr int kPendCap = 256;      // pending-pred list capacity per heavy warp (smem)
+constexpr int kHeavyTail = 4;      // preds left for the collective-free heavy tail
 #ifndef PGC_LIGHT_BATCH
 #define PGC_LIGHT_BATCH 4
 #endif
@@ -996,33 +997,11 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
             zi = bmap_next_zero<kHeavyWin>(bm, zi);
             continue;
           }
-#ifdef PGC_HEAVY_PASS_POLL
-          if (npend == 1 && over >= np) {
-            const int u1 = plist[0];
-#else
-          int u1, u2;
-          lowest_two(plist, pkey, npend, u1, u2);
-          if (npend == 1 && over >= np) {
-#endif
-            // tail: one load per poll on the last pred, then a compare-and-select
-            const int zi_next = bmap_next_zero<kHeavyWin>(bm, zi + 1);
-            int c;
-            while ((c = ld_relaxed(color + u1)) == 0) {
-              if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
-                found = -1;
-                break;
-              }
-              if (sleep_ns) __nanosleep(sleep_ns);
-              sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 16u;
-            }
-            if (found < 0) break;
-            zi = (c - wbase - 1 == zi) ? zi_next : zi;
-            npend = 0;
-            continue;
-          }
-#ifndef PGC_HEAVY_PASS_POLL
+          if (npend <= kHeavyTail && over >= np) break;  // the tail below takes them
           // Several pending: watch the second-to-last expected (one load per
           // poll, exponential backoff), then one pass drops the colored entries.
+          int u1, u2;
+          lowest_two(plist, pkey, npend, u1, u2);
           const int w = u2 >= 0 ? u2 : u1;
           while (ld_relaxed(color + w) == 0) {
             if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
@@ -1032,11 +1011,8 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
             __nanosleep(sleep_ns ? sleep_ns : 16u);
             sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 32u;
           }
-#endif
           if (found < 0) break;
-#ifndef PGC_HEAVY_PASS_POLL
           sleep_ns = 0;
-#endif
           int keep = 0;
           for (int j0 = 0; j0 < npend; j0 += 32) {
             const int j = j0 + lane;
@@ -1057,27 +1033,74 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
             }
             keep += __popc(bal);
           }
-#ifdef PGC_HEAVY_PASS_POLL
-          const bool moved = keep < npend;
-#endif
           npend = keep;
           __syncwarp();
           zi = bmap_next_zero<kHeavyWin>(bm, zi);
-#ifdef PGC_HEAVY_PASS_POLL
-          if (moved) {
-            sleep_ns = 0;
-          } else {
-            if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
-              found = -1;
-              break;
-            }
-            __nanosleep(sleep_ns ? sleep_ns : 16u);
-            sleep_ns = sleep_ns ? min(sleep_ns * 2, heavy_sleep_max) : 32u;
-          }
-#endif
         }
         __syncwarp();
         if (found < 0) break;  // stalled (watchdog)
+        if (npend > 0) {
+          // Tail (the critical path of a chain), free of warp collectives: the
+          // kHeavyTail+1 smallest colors missing so far are found now; every
+          // lane then polls the <= kHeavyTail pending preds (one uniform load
+          // per poll) from the highest priority down, and GetColor is the first
+          // of those colors no arrival takes.
+          int z[kHeavyTail + 1];
+          z[0] = zi;
+#pragma unroll
+          for (int k = 1; k <= kHeavyTail; ++k)
+            z[k] = bmap_next_zero<kHeavyWin>(bm, min(z[k - 1] + 1, kHeavyWin));
+          int q[kHeavyTail];
+          unsigned long long qk[kHeavyTail];
+#pragma unroll
+          for (int k = 0; k < kHeavyTail; ++k) {
+            q[k] = k < npend ? plist[k] : -1;
+            qk[k] = k < npend ? pkey[k] : 0ull;
+          }
+#pragma unroll
+          for (int i = 1; i < kHeavyTail; ++i)  // descending priority key
+#pragma unroll
+            for (int k = kHeavyTail - 1; k > 0; --k)
+              if (qk[k] > qk[k - 1]) {
+                const unsigned long long tk = qk[k];
+                qk[k] = qk[k - 1];
+                qk[k - 1] = tk;
+                const int t = q[k];
+                q[k] = q[k - 1];
+                q[k - 1] = t;
+              }
+          int cl[kHeavyTail];
+          bool stl = false;
+#pragma unroll
+          for (int k = 0; k < kHeavyTail; ++k) {
+            int c = 0;
+            if (q[k] >= 0 && !stl) {
+              unsigned spins = 0;
+              while ((c = ld_relaxed(color + q[k])) == 0) {
+                if ((++spins & 4095u) == 0 && globaltimer() > deadline) {
+                  st->err = 5;
+                  stl = true;
+                  break;
+                }
+              }
+            }
+            cl[k] = q[k] >= 0 ? c - wbase - 1 : -1;
+          }
+          if (stl) {
+            found = -1;
+            break;
+          }
+          int res = kHeavyWin;
+#pragma unroll
+          for (int j = kHeavyTail; j >= 0; --j) {
+            bool taken = false;
+#pragma unroll
+            for (int k = 0; k < kHeavyTail; ++k) taken |= cl[k] == z[j];
+            if (!taken) res = z[j];
+          }
+          zi = res;
+          npend = 0;
+        }
         if (zi < kHeavyWin) found = wbase + zi + 1;  // GetColor (else: next window)
         __syncwarp();
       }
