@@ -34,16 +34,30 @@ __global__ void k_zero_i32_dev(int32_t* p, const int* len, int extra) {
 
 // a1: D[v] = deg(v); round[v] = 0 (v in U); optional color[v] = 0 (uncolored,
 // PAPER.md:1115).  Thread 0 initialises the round state: S_1 = nnz, |U_1| = n.
+// An isolated vertex (deg 0) is settled here: it counts in n_1 and falls into
+// R_1 (D = 0 <= Dmax_1, Q12), but it has no arc to scan and is no pred of any
+// vertex, so it gets no work record; with JP its color is GetColor of the empty
+// pred set, 1, and npred = -1 keeps it out of the priority
+// order (it can neither wait nor be waited on).
 __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ off,
                            int32_t* __restrict__ D, uint8_t* __restrict__ rs,
-                           int32_t* __restrict__ round, int32_t* __restrict__ color, State* st) {
+                           int32_t* __restrict__ round, int32_t* __restrict__ color,
+                           int32_t* __restrict__ npred, uint32_t* __restrict__ filt, State* st) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    D[v] = (int32_t)(off[v + 1] - off[v]);
+    const int32_t d = (int32_t)(off[v + 1] - off[v]);
+    D[v] = d;
     rs[v] = 0;
     round[v] = 0;
-    if (color) color[v] = 0;
+    if (color) {
+      color[v] = d == 0 ? 1 : 0;
+      if (d == 0) npred[v] = -1;
+    }
   }
+  if (filt)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * kFilterWords;
+         i += gridDim.x * blockDim.x)
+      filt[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     State s = {};
     s.S = (unsigned long long)nnz;
@@ -99,8 +113,8 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
       my_nR += 1;
       o = off[v];
       deg = off[v + 1] - o;
-      light = deg <= heavy_deg;
-      if (!light) {
+      light = deg > 0 && deg <= heavy_deg;  // isolated: settled by k_adg_init
+      if (deg > heavy_deg) {
         nch = (int)((deg + chunk - 1) / chunk);
         npred[v] = 0;
       }
@@ -112,8 +126,8 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
         for (int k = 0; k < nch; ++k) {
           const long long s0 = o + (long long)k * chunk;
           const int len = (int)min((long long)chunk, o + deg - s0);
-          chunks[2 * (cb + k)] = make_int4(v, len, (int)(uint32_t)s0, (int)(s0 >> 32));
-          chunks[2 * (cb + k) + 1] = make_int4((int)(uint32_t)o, (int)(o >> 32), 0, 0);
+          __stcs(chunks + 2 * (cb + k), make_int4(v, len, (int)(uint32_t)s0, (int)(s0 >> 32)));
+          __stcs(chunks + 2 * (cb + k) + 1, make_int4((int)(uint32_t)o, (int)(o >> 32), 0, 0));
         }
     }
     block_append_rec(light, light_rec(v, (int)deg, o), lrec, &st->nLight, sm);
@@ -136,21 +150,22 @@ struct Arc {
   const uint8_t* __restrict__ rs;
   // Round state of u.  MODE 0/1: 0 = alive (u in U), 1 = removed in this
   // round, 2 = removed earlier; read from the 1-byte rs[] while l <= 255
-  // (exact: rs = ((round-1) mod 255) + 1), from round[] afterwards.
-  __device__ __forceinline__ int state(int u) const {
-    if (l <= 255) {
-#ifdef PGC_RS_PLAIN
-      const int b = rs[u];
-#else
-      const int b = __ldg(rs + u);  // read-only path: L1-cached, rs is immutable during UPDATE
-#endif
-      return b == 0 ? 0 : (b == l ? 1 : 2);
-    }
-    const int r = round[u];
-    return r == 0 ? 0 : (r == l ? 1 : 2);
+  // (exact: rs = ((round-1) mod 255) + 1), from round[] afterwards.  MODE 2:
+  // the key round[u].  Split in two so a kernel issues all of a strip's gathers
+  // before it consumes any (raw() on a clamped address is unconditional; a
+  // gather whose use sits in the same branch would serialise on its latency).
+  __device__ __forceinline__ int raw(int u) const {
+    const int uu = u >= 0 ? u : 0;
+    if (MODE != 2 && l <= 255) return ld_u8_keep(rs + uu);  // read-only, L2 evict-last
+    return round[uu];
   }
-  // the per-arc gather: MODE 2 the key round[u], else the round state
-  __device__ __forceinline__ int gather(int u) const { return MODE == 2 ? round[u] : state(u); }
+  __device__ __forceinline__ int decode(int u, int x) const {
+    if (u < 0) return 0;
+    if (MODE == 2) return x;
+    return x == 0 ? 0 : (x == l ? 1 : 2);  // for l <= 255, rs == round of every removed u
+  }
+  __device__ __forceinline__ int state(int u) const { return decode(u, raw(u)); }
+  __device__ __forceinline__ int gather(int u) const { return state(u); }
   // true iff u in pred(v); performs UPDATE's decrement and counts cut arcs.
   // g = gather(u).
   __device__ __forceinline__ bool classify(int u, int g, int rv, uint64_t hv,
@@ -161,7 +176,7 @@ struct Arc {
     }
     const int su = g;
     if (su == 0) {                      // u in U \ R: DecrementAndFetch(D[u])
-      atomicSub(&D[u], 1);              // result unused -> RED
+      red_dec_keep(&D[u]);              // result unused -> RED
       cut += 1;
       return MODE == 1;                 // u gets a later round: higher priority
     }
@@ -180,8 +195,15 @@ struct Arc {
 // segment; each lane keeps its own vertex's running count in a register (no
 // shared-memory atomics).
 constexpr int kStrips = 8;
+#ifndef PGC_LIGHT_STRIPS
+#define PGC_LIGHT_STRIPS 8
+#endif
+#ifndef PGC_LIGHT_MINB
+#define PGC_LIGHT_MINB 1
+#endif
+constexpr int kLStrips = PGC_LIGHT_STRIPS;
 template <int MODE>
-__global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int32_t* __restrict__ col,
+__global__ void __launch_bounds__(256, PGC_LIGHT_MINB) k_update_light(Arc<MODE> A, const int32_t* __restrict__ col,
                                                       const int4* __restrict__ lrec,
                                                       int32_t* __restrict__ npred,
                                                       int32_t* __restrict__ P, State* st) {
@@ -206,7 +228,7 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int32_t
     if (lane == 0) g = atomicAdd(&s_next, 1);
     g = __shfl_sync(0xffffffffu, g, 0);
     const int i = g * 32 + lane;
-    r = (g < g_hi && i < nL) ? lrec[i] : make_int4(0, 0, 0, 0);
+    r = (g < g_hi && i < nL) ? __ldcs(lrec + i) : make_int4(0, 0, 0, 0);
   };
   int g_nx;
   int4 r_nx;
@@ -230,10 +252,10 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int32_t
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int excl = incl - deg;
     int cnt = 0;  // preds of this lane's vertex found so far
-    for (int t0 = 0; t0 < total; t0 += 32 * kStrips) {
-      int u[kStrips], ow[kStrips], gs[kStrips];
+    for (int t0 = 0; t0 < total; t0 += 32 * kLStrips) {
+      int u[kLStrips], ow[kLStrips], gs[kLStrips];
 #pragma unroll
-      for (int k = 0; k < kStrips; ++k) {
+      for (int k = 0; k < kLStrips; ++k) {
         const int a = t0 + 32 * k + lane;
         // owner = number of lanes whose inclusive prefix is <= a
         int lo = 0;
@@ -248,9 +270,11 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int32_t
         u[k] = a < total ? ld_stream(col + oo + (a - oe)) : -1;
       }
 #pragma unroll
-      for (int k = 0; k < kStrips; ++k) gs[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
+      for (int k = 0; k < kLStrips; ++k) gs[k] = A.raw(u[k]);  // all gathers in flight
 #pragma unroll
-      for (int k = 0; k < kStrips; ++k) {
+      for (int k = 0; k < kLStrips; ++k) gs[k] = A.decode(u[k], gs[k]);
+#pragma unroll
+      for (int k = 0; k < kLStrips; ++k) {
         const int ts = t0 + 32 * k;  // first arc of this strip
         const uint64_t oh = MODE != 0 ? __shfl_sync(0xffffffffu, hv, ow[k]) : 0;
         const int orv = MODE == 2 ? __shfl_sync(0xffffffffu, rv, ow[k]) : 0;
@@ -286,6 +310,12 @@ __global__ void __launch_bounds__(256) k_update_light(Arc<MODE> A, const int32_t
   }
 }
 
+constexpr uint32_t kFilterBitsFwd = kFilterBytes * 8u;
+// true iff round l runs the filtered heavy UPDATE (k_update_heavy_f)
+__device__ __forceinline__ bool filter_round(const State* st, int ratio) {
+  return ratio > 0 && st->nU * (long long)ratio <= (long long)kFilterBitsFwd;
+}
+
 // UPDATE for chunked vertices: one warp per `chunk`-arc work item.  The preds
 // found in each 512-arc sub-chunk are staged in shared memory and written as
 // one coalesced run after a single atomicAdd on npred[v] (no per-strip atomic
@@ -295,11 +325,13 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t* __restrict__ col,
                                                       const int4* __restrict__ chunks,
                                                       int32_t* __restrict__ npred,
-                                                      int32_t* __restrict__ P, State* st) {
+                                                      int32_t* __restrict__ P, State* st,
+                                                      int filter_ratio) {
   __shared__ unsigned long long s_red[32];
   __shared__ int s_buf[MODE != 0 ? 8 : 1][MODE != 0 ? kSub : 1];
   __shared__ int s_next;
   if (MODE != 2 && st->done) return;
+  if (MODE != 2 && filter_round(st, filter_ratio)) return;  // k_update_heavy_f's round
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const int nC = st->nChunks;
   const int c_lo = (int)((long long)nC * blockIdx.x / gridDim.x);
@@ -312,7 +344,7 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
     ci = 0;
     if (lane == 0) ci = atomicAdd(&s_next, 1);
     ci = __shfl_sync(0xffffffffu, ci, 0);
-    r = (ci < c_hi && lane < 2) ? chunks[2 * ci + lane] : make_int4(0, 0, 0, 0);
+    r = (ci < c_hi && lane < 2) ? __ldcs(chunks + 2 * ci + lane) : make_int4(0, 0, 0, 0);
   };
   int ci_nx;
   int4 r_nx;
@@ -341,7 +373,9 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
           u[k] = a < e0 ? ld_stream(col + a) : -1;
         }
 #pragma unroll
-        for (int k = 0; k < kStrips; ++k) g[k] = u[k] >= 0 ? A.gather(u[k]) : 0;
+        for (int k = 0; k < kStrips; ++k) g[k] = A.raw(u[k]);  // all gathers in flight
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) g[k] = A.decode(u[k], g[k]);
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) {
           const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut);
@@ -358,6 +392,141 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
         if (lane == 0) base = atomicAdd(&npred[v], cnt);
         base = __shfl_sync(0xffffffffu, base, 0);
         for (int i = lane; i < cnt; i += 32) st_stream(P + o + base + i, s_buf[warp][i]);
+        if (lane == 0) preds += (unsigned long long)cnt;
+        __syncwarp();
+      }
+    }
+  }
+  unsigned long long t = block_sum(cut, s_red);
+  if (threadIdx.x == 0 && t) atomicAdd(&st->cut, t);
+  if (MODE != 0) {
+    t = block_sum(preds, s_red);
+    if (threadIdx.x == 0 && t) atomicAdd(&st->pred_arcs, t);
+  }
+}
+
+// UPDATE for chunked vertices in the late rounds, with a membership filter.
+// Once |U_l| is small, most arcs of R_l lead to vertices removed in earlier
+// rounds (on R-MAT 24, 171 M of the 236 M arcs of rounds 4-7): their state
+// gather is a wasted L2 request, and UPDATE is bound by the L2 request rate.
+// Each CTA (one per SM, 1024 threads) first builds a one-hash Bloom filter of
+// U_l (the round's input list: alive or removed this round) in shared memory;
+// an arc whose target misses the filter is "removed earlier" for certain, and
+// only hits (members of U_l plus <= 1/kFilterRatio false positives) gather the
+// real state.  The result is identical: the filter only skips gathers whose
+// answer it already knows.  The plain kernel runs the rounds with
+// |U_l| > bits / ratio (each of the two kernels exits if the round is not its).
+constexpr int kFilterThreads = 1024;
+constexpr int kFilterSub = 256;                       // staged preds per warp
+constexpr uint32_t kFilterBits = kFilterBytes * 8u;   // 1.5 M filter bits
+constexpr size_t kFilterSmem = kFilterBytes + (kFilterThreads / 32) * kFilterSub * 4;
+static_assert(kFilterBits == kFilterBitsFwd, "filter size");
+__device__ __forceinline__ uint32_t filter_slot(int u) {
+  return __umulhi((uint32_t)u * 0x9E3779B1u, kFilterBits);
+}
+
+// Before UPDATE of round l: set the bits of U_l (the round's input list) in the
+// global filter buffer l&1 -- one RED per member, once per round, not per CTA
+// -- and clear buffer (l+1)&1 for the next round (its last reader, UPDATE of
+// round l-1, has finished).  Buffers start zeroed (k_adg_init).
+__global__ void k_filter_build(int l, const int32_t* __restrict__ Uin, uint32_t* __restrict__ filt,
+                               const State* st, int ratio) {
+  if (st->done) return;
+  uint32_t* nxt = filt + (size_t)((l + 1) & 1) * kFilterWords;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = tid; i < kFilterWords / 4; i += nt) reinterpret_cast<uint4*>(nxt)[i] = make_uint4(0, 0, 0, 0);
+  if (!filter_round(st, ratio)) return;
+  uint32_t* cur = filt + (size_t)(l & 1) * kFilterWords;
+  const long long nU = st->nU;
+  for (long long i = tid; i < nU; i += nt) {
+    const int u = Uin ? Uin[i] : (int)i;
+    const uint32_t b = filter_slot(u);
+    atomicOr(&cur[b >> 5], 1u << (b & 31));
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFilterThreads, 1)
+    k_update_heavy_f(Arc<MODE> A, const int32_t* __restrict__ col, const int4* __restrict__ chunks,
+                     const uint32_t* __restrict__ gfilt, int32_t* __restrict__ npred,
+                     int32_t* __restrict__ P, State* st, int ratio) {
+  extern __shared__ __align__(16) unsigned char f_smem[];
+  uint32_t* filt = reinterpret_cast<uint32_t*>(f_smem);
+  int* s_buf_all = reinterpret_cast<int*>(f_smem + kFilterBytes);
+  __shared__ unsigned long long s_red[32];
+  __shared__ int s_next;
+  if (st->done || !filter_round(st, ratio)) return;
+  const int nC = st->nChunks;
+  if (nC == 0) return;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  int* s_buf = s_buf_all + warp * kFilterSub;
+  {  // the round's filter (built by k_filter_build) -> shared memory
+    const uint4* src = reinterpret_cast<const uint4*>(gfilt + (size_t)(A.l & 1) * kFilterWords);
+    uint4* dst = reinterpret_cast<uint4*>(filt);
+    for (int i = threadIdx.x; i < kFilterWords / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
+  }
+  const int c_lo = (int)((long long)nC * blockIdx.x / gridDim.x);
+  const int c_hi = (int)((long long)nC * (blockIdx.x + 1) / gridDim.x);
+  if (threadIdx.x == 0) s_next = c_lo;
+  __syncthreads();
+  unsigned long long cut = 0, preds = 0;
+  auto take = [&](int& ci, int4& r) {
+    ci = 0;
+    if (lane == 0) ci = atomicAdd(&s_next, 1);
+    ci = __shfl_sync(0xffffffffu, ci, 0);
+    r = (ci < c_hi && lane < 2) ? __ldcs(chunks + 2 * ci + lane) : make_int4(0, 0, 0, 0);
+  };
+  int ci_nx;
+  int4 r_nx;
+  take(ci_nx, r_nx);
+  for (;;) {
+    const int ci = ci_nx;
+    if (ci >= c_hi) break;
+    const int4 r0 = r_nx;
+    take(ci_nx, r_nx);
+    const int v = __shfl_sync(0xffffffffu, r0.x, 0);
+    const int len = __shfl_sync(0xffffffffu, r0.y, 0);
+    const long long s = lo_hi(__shfl_sync(0xffffffffu, r0.z, 0), __shfl_sync(0xffffffffu, r0.w, 0));
+    const long long o = lo_hi(__shfl_sync(0xffffffffu, r0.x, 1), __shfl_sync(0xffffffffu, r0.y, 1));
+    const long long e = s + len;
+    const uint64_t hv = MODE != 0 ? prio_hash(A.seed, (uint32_t)v) : 0;
+    for (long long s0 = s; s0 < e; s0 += kFilterSub) {
+      const long long e0 = min(e, s0 + kFilterSub);
+      int cnt = 0;
+      for (long long a0 = s0; a0 < e0; a0 += 32 * kStrips) {
+        int u[kStrips], g[kStrips];
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) {
+          const long long a = a0 + 32 * k + lane;
+          u[k] = a < e0 ? ld_stream(col + a) : -1;
+        }
+        bool hit[kStrips];
+        uint32_t fw[kStrips];
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) fw[k] = filt[filter_slot(u[k] >= 0 ? u[k] : 0) >> 5];
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k)
+          hit[k] = u[k] >= 0 && ((fw[k] >> (filter_slot(u[k]) & 31)) & 1u);
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) g[k] = hit[k] ? A.raw(u[k]) : 0;
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) g[k] = hit[k] ? A.decode(u[k], g[k]) : 2;  // miss: earlier
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) {
+          const bool pred = u[k] >= 0 && A.classify(u[k], g[k], 0, hv, cut);
+          if (MODE != 0) {
+            const unsigned bal = __ballot_sync(0xffffffffu, pred);
+            if (pred) s_buf[cnt + __popc(bal & lanemask_lt())] = u[k];
+            cnt += __popc(bal);
+          }
+        }
+      }
+      if (MODE != 0 && cnt) {
+        __syncwarp();
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&npred[v], cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane; i < cnt; i += 32) st_stream(P + o + base + i, s_buf[i]);
         if (lane == 0) preds += (unsigned long long)cnt;
         __syncwarp();
       }
@@ -405,9 +574,12 @@ __global__ void k_adg_finalize(int l, State* st, long long* per_round) {
 }
 
 // JP Part 1 work lists for an arbitrary key (pgc_jp_color): every vertex is
-// classified, light ones into Rl, heavy ones into edge chunks.
+// classified, light ones into Rl, heavy ones into edge chunks; color[v] = 0
+// (uncolored) except isolated vertices, settled as in
+// k_adg_init (color 1, npred -1: outside the priority order).
 __global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int4* __restrict__ lrec,
-                              int4* __restrict__ chunks, int32_t* __restrict__ npred, State* st,
+                              int4* __restrict__ chunks, int32_t* __restrict__ npred,
+                              int32_t* __restrict__ color, State* st,
                               int heavy_deg, int chunk, int64_t chunk_cap) {
   __shared__ int sm[33];
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -421,11 +593,13 @@ __global__ void k_jp_classify(int64_t n, const int64_t* __restrict__ off, int4* 
       const int v = (int)i;
       o = off[v];
       deg = off[v + 1] - o;
-      light = deg <= heavy_deg;
-      if (!light) {
+      light = deg > 0 && deg <= heavy_deg;
+      if (deg > heavy_deg) {
         nch = (int)((deg + chunk - 1) / chunk);
         npred[v] = 0;
       }
+      color[v] = deg == 0 ? 1 : 0;
+      if (deg == 0) npred[v] = -1;
     }
     const int cb = block_reserve(nch, &st->nChunks, sm);
     if (nch) {
@@ -452,13 +626,29 @@ __global__ void k_state_reset_jp(State* st) {
 static int grid_for(const Ctx& c, int per_sm) { return c.nsm * per_sm; }
 
 template <int MODE>
-static int launch_update(Ctx& c, const Arc<MODE>& A) {
+static int launch_update(Ctx& c, const Arc<MODE>& A, const int32_t* Uin = nullptr) {
   const int GL = wave_grid(c, k_update_light<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_light",
              k_update_light<MODE><<<GL, 256, 0, c.st>>>(A, c.col, c.lrec, c.npred, c.P, c.state));
+  const int ratio = MODE == 2 ? 0 : c.tune.filter_ratio;
   const int GH = wave_grid(c, k_update_heavy<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_heavy",
-             k_update_heavy<MODE><<<GH, 256, 0, c.st>>>(A, c.col, c.chunks, c.npred, c.P, c.state));
+             k_update_heavy<MODE><<<GH, 256, 0, c.st>>>(A, c.col, c.chunks, c.npred, c.P, c.state,
+                                                        ratio));
+  if constexpr (MODE != 2) {
+    if (ratio > 0) {
+      static bool attr = false;  // per process: the attribute is per function
+      if (!attr) {
+        PGC_CUDA(cudaFuncSetAttribute(k_update_heavy_f<MODE>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kFilterSmem));
+        attr = true;
+      }
+      PGC_LAUNCH(c, kGUpdate, "k_update_heavy_f",
+                 k_update_heavy_f<MODE><<<c.nsm, kFilterThreads, kFilterSmem, c.st>>>(
+                     A, c.col, c.chunks, c.filt, c.npred, c.P, c.state, ratio));
+    }
+  }
   return 0;
 }
 
@@ -468,6 +658,7 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
   const int G = grid_for(c, 8);
   PGC_LAUNCH(c, kGAdgOther, "k_adg_init",
              k_adg_init<<<G, B, 0, c.st>>>(c.n, c.nnz, c.off, c.D, c.rs, round, color_zero,
+                                           c.npred, c.tune.filter_ratio > 0 ? c.filt : nullptr,
                                            c.state));
   if (c.n == 0) return sync_state(c);
   int l = 1;
@@ -481,10 +672,14 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                                  c.lrec, c.chunks, c.npred, c.state,
                                                  c.tune.heavy_degree, c.tune.chunk_arcs,
                                                  c.lay.chunk_cap));
+      if (c.tune.filter_ratio > 0)
+        PGC_LAUNCH(c, kGUpdate, "k_filter_build",
+                   k_filter_build<<<c.nsm * 2, 1024, 0, c.st>>>(l, Uin, c.filt, c.state,
+                                                                c.tune.filter_ratio));
       if (mode == kAdgFused) {
-        if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs})) return e;
+        if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs}, Uin)) return e;
       } else {
-        if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs})) return e;
+        if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs}, Uin)) return e;
       }
       PGC_LAUNCH(c, kGAdgOther, "k_adg_finalize",
                  k_adg_finalize<<<1, 32, 0, c.st>>>(l, c.state, c.per_round));
@@ -497,15 +692,13 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
   return 0;
 }
 
-int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color_zero) {
+int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color) {
   const int G = grid_for(c, 8);
   PGC_LAUNCH(c, kGAdgOther, "k_state_reset_jp", k_state_reset_jp<<<1, 1, 0, c.st>>>(c.state));
-  if (color_zero) {
-    PGC_LAUNCH(c, kGAdgOther, "k_zero_i32", k_zero_i32<<<G, 256, 0, c.st>>>(color_zero, c.n));
-  }
   if (c.n == 0) return 0;
   PGC_LAUNCH(c, kGUpdate, "k_jp_classify",
-             k_jp_classify<<<G, 256, 0, c.st>>>(c.n, c.off, c.lrec, c.chunks, c.npred, c.state,
+             k_jp_classify<<<G, 256, 0, c.st>>>(c.n, c.off, c.lrec, c.chunks, c.npred, color,
+                                                c.state,
                                                 c.tune.heavy_degree, c.tune.chunk_arcs,
                                                 c.lay.chunk_cap));
   return launch_update(c, Arc<2>{0, seed, round, nullptr, nullptr});

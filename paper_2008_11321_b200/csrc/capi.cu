@@ -85,6 +85,7 @@ Layout make_layout(int64_t n, int64_t nnz) {
   // so at most nnz / 63 of them) and light list (< n)
   L.rec_heavy_cap = (nnz / 63 < n ? nnz / 63 : n) + 1;
   L.rec = take(16 * (size_t)(L.rec_heavy_cap + 2 * n));
+  L.filt = take(2 * (size_t)kFilterBytes);
   L.total = a;
   return L;
 }
@@ -140,6 +141,7 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.bstart = (int32_t*)(b + c.lay.bstart);
   c.scan_tmp = (int32_t*)(b + c.lay.scan_tmp);
   c.rec = (int4*)(b + c.lay.rec);
+  c.filt = (uint32_t*)(b + c.lay.filt);
   c.lrec = c.rec;  // ADG and JP never use their records at the same time
   if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));
   c.h_state = g_hstate;
@@ -396,6 +398,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
   struct Key { const char* name; long long lo, hi; long long* l; int* i; };
   const Key keys[] = {
       {"jp_watchdog_ms", 1, 3600000, nullptr, &g_tune.jp_watchdog_ms},
+      {"filter_ratio", 0, 1 << 20, nullptr, &g_tune.filter_ratio},
       {"jp_heavy_warps", 1, 4, nullptr, &g_tune.jp_heavy_warps},
       {"jp_heavy_sleep_max", 0, 1000000, nullptr, &g_tune.jp_heavy_sleep_max},
       {"jp_light_sleep_max", 0, 1000000, nullptr, &g_tune.jp_light_sleep_max},

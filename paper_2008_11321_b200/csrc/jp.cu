@@ -197,25 +197,41 @@ __device__ __forceinline__ int bucket_count_for(int cnt) {
   return b;
 }
 
-// hist1[rmax - round[v]] += 1; privatised in shared memory when the key range is small.
-__global__ void k_hist1(int64_t n, const int32_t* __restrict__ round, const State* st, int range,
+// The priority order holds every vertex except the isolated ones (npred < 0,
+// settled with color 1 before JP: no pred, no succ).
+__device__ __forceinline__ bool in_order(const int32_t* __restrict__ npred, int64_t v) {
+  return npred[v] >= 0;
+}
+
+// hist1[rmax - round[v]] += 1; privatised in shared memory when the key range is
+// small.  Also counts the ordered vertices (st->n_order).
+__global__ void k_hist1(int64_t n, const int32_t* __restrict__ round,
+                        const int32_t* __restrict__ npred, State* st, int range,
                         int32_t* __restrict__ hist1) {
   extern __shared__ int sh[];
+  __shared__ int s_cnt;
   const int rmax = st->rmax;
   const bool priv = range <= 8192;
   if (priv)
     for (int i = threadIdx.x; i < range; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
+  int cnt = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
+    if (!in_order(npred, v)) continue;
     const int k = rmax - round[v];
+    ++cnt;
     if (priv) atomicAdd(&sh[k], 1);
     else atomicAdd(&hist1[k], 1);
   }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
   __syncthreads();
   if (priv)
     for (int i = threadIdx.x; i < range; i += blockDim.x)
       if (sh[i]) atomicAdd(&hist1[i], sh[i]);
+  if (threadIdx.x == 0 && s_cnt) atomicAdd(&st->n_order, s_cnt);
 }
 
 __global__ void k_bucket_sizes(int L, const int32_t* __restrict__ hist1, int32_t* __restrict__ bsz) {
@@ -235,11 +251,13 @@ __device__ __forceinline__ int bucket_of(int v, int r, uint64_t seed, int rmax,
 }
 
 __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, uint64_t seed,
+                        const int32_t* __restrict__ npred,
                         const State* st, const int32_t* __restrict__ hist1,
                         const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt) {
   const int rmax = st->rmax;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
+    if (!in_order(npred, v)) continue;
     const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
     atomicAdd(&bcnt[b], 1);
   }
@@ -256,10 +274,12 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, uint64_t
   const int rmax = st->rmax;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
+    const int np = npred[v];
+    if (np < 0) continue;  // isolated: not in the order
     const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
     const int pos = bstart[b] + atomicSub(&bcnt[b], 1) - 1;
     const int64_t o = off[v];
-    rec[pos] = make_int4((int)v, npred[v], (int)(uint32_t)o, (int)(o >> 32));
+    rec[pos] = make_int4((int)v, np, (int)(uint32_t)o, (int)(o >> 32));
   }
 }
 
@@ -358,6 +378,7 @@ __global__ void k_order_setup(State* st, int rmax_host, int use_host) {
   }
   st->nbuckets = 0;
   st->sorted = 0;
+  st->n_order = 0;
 }
 
 int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) {
@@ -382,14 +403,15 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) 
   PGC_LAUNCH(c, kGOrder, "k_zero_i32", k_zero_i32<<<G, 256, 0, c.st>>>(c.hist1, L));
   const size_t shb = L <= 8192 ? (size_t)L * sizeof(int) : 0;
   PGC_LAUNCH(c, kGOrder, "k_hist1",
-             k_hist1<<<G, 256, shb, c.st>>>(c.n, round, c.state, L, c.hist1));
+             k_hist1<<<G, 256, shb, c.st>>>(c.n, round, c.npred, c.state, L, c.hist1));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sizes",
              k_bucket_sizes<<<G, 256, 0, c.st>>>(L, c.hist1, c.base1));
   if (int e = scan_ex(c, c.base1, c.base1, nullptr, L, L, &c.state->nbuckets)) return e;
   PGC_LAUNCH(c, kGOrder, "k_zero_i32_dev",
              k_zero_i32_dev<<<G, 256, 0, c.st>>>(c.bcnt, &c.state->nbuckets, 1));
   PGC_LAUNCH(c, kGOrder, "k_hist2",
-             k_hist2<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt));
+             k_hist2<<<G, 256, 0, c.st>>>(c.n, round, seed, c.npred, c.state, c.hist1, c.base1,
+                                          c.bcnt));
   if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
                       &c.state->sorted))
     return e;
@@ -465,14 +487,15 @@ constexpr int kCoreFixedSmem = kCoreWarps * kCoreWin + kCoreWarps * kCorePend * 
 
 // One block: NC = the longest prefix p <= min(n, core_max) of the priority
 // order with sum(npred) >= min_avg * p and sum(npred) <= arc_cap.
-__global__ void __launch_bounds__(1024) k_core_select(int64_t n, const int4* __restrict__ rec,
+__global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ rec,
                                                       State* st,
                                                       int core_max, int min_avg,
                                                       long long arc_cap) {
   __shared__ long long s_w[32];
   __shared__ unsigned long long s_best;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const int L = (int)(n < (int64_t)core_max ? n : (int64_t)core_max);
+  const int no = st->n_order;
+  const int L = no < core_max ? no : core_max;
   const int per = (L + blockDim.x - 1) / blockDim.x;
   const int t0 = threadIdx.x * per;
   if (threadIdx.x == 0) s_best = 0;
@@ -1251,11 +1274,13 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
   if (lane == 0 && kmax) atomicMax(&st->K, kmax);
 }
 
-__global__ void k_jp_reset(State* st) {
+// K starts at 1 for a nonempty graph: the highest-priority vertex has no pred
+// and gets color 1 (isolated vertices and roots are colored outside the JP kernels).
+__global__ void k_jp_reset(State* st, int nonempty) {
   st->ticket_heavy = 0;
   st->ticket_light = 0;
   st->nheavy = 0;
-  st->K = 0;
+  st->K = nonempty;
   st->core_n = 0;
   st->core_arcs = 0;
 }
@@ -1300,14 +1325,15 @@ static int pow2_floor(int x) {
 }
 
 int jp_color_run(Ctx& c, int32_t* color) {
-  PGC_LAUNCH(c, kGJp, "k_jp_reset", k_jp_reset<<<1, 1, 0, c.st>>>(c.state));
+  PGC_LAUNCH(c, kGJp, "k_jp_reset", k_jp_reset<<<1, 1, 0, c.st>>>(c.state, c.n > 0 ? 1 : 0));
+  int64_t n_order = 0;
   if (c.n > 0) {
     // --- core selection and its pred-list rewrite ---
     int C = 0;
     size_t core_smem = 0;
     if (c.tune.core_max > 0) {
       PGC_LAUNCH(c, kGCore, "k_core_select",
-                 k_core_select<<<1, 1024, 0, c.st>>>(c.n, c.rec, c.state,
+                 k_core_select<<<1, 1024, 0, c.st>>>(c.rec, c.state,
                                                       c.tune.core_max, c.tune.core_min_avg,
                                                       c.tune.core_arc_cap));
       if (int e = sync_state(c)) return e;
@@ -1332,10 +1358,13 @@ int jp_color_run(Ctx& c, int32_t* color) {
                    k_core_lists<<<G * 2, 256, 0, c.st>>>(c.rec, c.D, c.P, c.state));
       }
     }
-    // --- bulk split of positions [core_n, n) (needs only the records, so it
-    //     runs before the core kernel and the bulk starts right after it) ---
+    // --- bulk split of positions [core_n, n_order) (needs only the records, so
+    //     it runs before the core kernel and the bulk starts right after it) ---
+    if (c.tune.core_max <= 0)
+      if (int e = sync_state(c)) return e;
+    n_order = c.h_state->n_order;
     const int NC = c.core_n;
-    const int64_t nbulk = c.n - NC;
+    const int64_t nbulk = n_order - NC;
     int4* hrec = c.rec + c.n;
     int4* lrec = hrec + c.lay.rec_heavy_cap;
     if (nbulk > 0) {
@@ -1347,11 +1376,11 @@ int jp_color_run(Ctx& c, int32_t* color) {
       int32_t* hpos = c.Rl;
       int32_t* lpos = c.D;
       PGC_LAUNCH(c, kGJp, "k_bulk_flags",
-                 k_bulk_flags<<<G, 256, 0, c.st>>>(c.n, c.rec, c.state, hflag, lflag));
+                 k_bulk_flags<<<G, 256, 0, c.st>>>(n_order, c.rec, c.state, hflag, lflag));
       if (int e = scan_ex(c, hflag, hpos, nullptr, nbulk, nbulk, &c.state->nheavy, kGJp)) return e;
       if (int e = scan_ex(c, lflag, lpos, nullptr, nbulk, nbulk, &c.state->nlight, kGJp)) return e;
       PGC_LAUNCH(c, kGJp, "k_bulk_scatter",
-                 k_bulk_scatter<<<G, 256, 0, c.st>>>(c.n, c.rec, c.state, hpos, lpos, hrec, lrec,
+                 k_bulk_scatter<<<G, 256, 0, c.st>>>(n_order, c.rec, c.state, hpos, lpos, hrec, lrec,
                                                      color));
     }
     // --- core: one thread-block cluster ---
@@ -1389,9 +1418,9 @@ int jp_color_run(Ctx& c, int32_t* color) {
   if (int e = sync_state(c)) return e;
   if (c.h_state->err == 5)
     return fail(4, "JP coloring stalled: no progress within %d ms (watchdog)", c.tune.jp_watchdog_ms);
-  if (c.n > 0 && c.h_state->sorted != c.n)
+  if (c.n > 0 && c.h_state->sorted != n_order)
     return fail(4, "priority order placed %d of %lld vertices", c.h_state->sorted,
-                (long long)c.n);
+                (long long)n_order);
   return 0;
 }
 

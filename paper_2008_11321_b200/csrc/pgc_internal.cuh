@@ -38,7 +38,9 @@ struct State {
   // priority-order sort
   int rmin, rmax;              // range of the first priority key
   int nbuckets;                // buckets in use
-  int sorted;                  // total placed by the scan (== n)
+  int sorted;                  // total placed by the scan (== n_order)
+  int n_order;                 // vertices in the priority order: all but the isolated ones
+  int pad1;
   // JP
   int core_n;                  // |core| = length of the priority prefix colored by k_jp_core
   int K;
@@ -51,7 +53,7 @@ struct State {
 // Byte offsets of every workspace region (each 256-byte aligned).
 struct Layout {
   size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, hist1, base1, bcnt, bstart,
-      scan_tmp, rec, total;
+      scan_tmp, rec, filt, total;
   int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap, rec_heavy_cap;
 };
 
@@ -62,6 +64,7 @@ struct Tuning {
   int rounds_per_sync = 8;
   int heavy_degree = 128;   // vertices with more arcs are split into edge chunks
   int chunk_arcs = 1024;    // arcs per chunk work item
+  int filter_ratio = 0;     // UPDATE: filtered heavy kernel once |U_l| * ratio <= filter bits (0 = off)
   int jp_heavy_warps = 4;         // warps per 8-warp bulk JP block serving heavy vertices (1..4)
   int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
   int jp_light_sleep_max = 8192;  // ns, same for light warps
@@ -99,6 +102,7 @@ struct Ctx {
   int32_t* P;
   int32_t* U[2];
   int32_t* Rl;
+  uint32_t* filt;  // 2 x kFilterWords: UPDATE membership filters of U_l (double-buffered)
   int4* lrec;      // UPDATE light work records (aliases the JP bulk record region)
   int4* chunks;    // UPDATE edge-chunk records, 2 x int4 each
   int32_t* hist1;
@@ -117,11 +121,15 @@ struct Ctx {
   unsigned long long* trace_done = nullptr;
 };
 
+// UPDATE membership filter (adg.cu): 1.5 M bits (192 KB) per buffer
+constexpr int kFilterBytes = 192 * 1024;
+constexpr int kFilterWords = kFilterBytes / 4;
+
 // ---- phases (host orchestration; return 0 or a PGC_* code) -----------------
 enum AdgMode { kAdgOnly = 0, kAdgFused = 1 };
 int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
             int32_t* color_zero);
-int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color_zero);
+int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color);
 int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known);
 int jp_color_run(Ctx& c, int32_t* color);
 int check_graph_run(Ctx& c, int64_t* bad_vertex);
@@ -191,6 +199,35 @@ __device__ __forceinline__ void st_relaxed_u16(uint16_t* p, int v) {
 __device__ __forceinline__ int ld_stream(const int32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(int32_t* p, int v) { __stcs(p, v); }
 
+// Per-vertex ADG state that UPDATE hits at random (D[] by RED, rs[] by gather)
+// is marked L2 evict-last, so the streams that pass through the L2 once (col,
+// records, P) do not push it out (PGC_NO_L2HINT builds the plain accesses for A/B).
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// D[u] -= 1 with the result unused (a RED), evict-last
+__device__ __forceinline__ void red_dec_keep(int32_t* a) {
+#ifdef PGC_NO_L2HINT
+  atomicSub(a, 1);
+#else
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(a), "r"(-1),
+               "l"(l2_keep_policy())
+               : "memory");
+#endif
+}
+// read-only byte gather (rs is immutable during UPDATE), evict-last
+__device__ __forceinline__ int ld_u8_keep(const uint8_t* a) {
+#ifdef PGC_NO_L2HINT
+  return __ldg(a);
+#else
+  unsigned short v;
+  asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(l2_keep_policy()));
+  return v;
+#endif
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -257,7 +294,7 @@ __device__ __forceinline__ void block_append_rec(bool flag, int4 val, int4* out,
     sm[nw] = tot ? atomicAdd(counter, tot) : 0;
   }
   __syncthreads();
-  if (flag) out[sm[nw] + sm[warp] + __popc(b & lanemask_lt())] = val;
+  if (flag) __stcs(out + sm[nw] + sm[warp] + __popc(b & lanemask_lt()), val);  // read once
   __syncthreads();
 }
 

@@ -31,7 +31,8 @@ def main():
     ap.add_argument("knobs", nargs="*")
     a = ap.parse_args()
     import paper_2008_11321_b200 as pgc
-    g = gg.config_graph(a.config)
+    from bench import load_graph  # /tmp-cached generator output
+    g = load_graph(a.config)
     num, den = map(int, a.eps.split("/")) if a.eps else gg.CONFIGS[a.config][1][0]
     off = torch.from_numpy(g.off).cuda()
     col = torch.from_numpy(g.col).cuda()
