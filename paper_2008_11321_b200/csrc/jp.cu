@@ -27,12 +27,12 @@ namespace pgc {
 namespace cg = cooperative_groups;
 
 // PGC_PROBE builds (tools/micro/build_probe.sh, never the product library)
-// stamp per-vertex phase times into the trace arrays ([4*v + k]) for the
-// core engine's hop breakdown (tools/micro/hop_probe.py).
+// stamp per-vertex phase times (%globaltimer) into the trace arrays ([8*v + k])
+// for the core engine hop breakdown (tools/micro/hop_probe.py, core_probe.py).
 #ifdef PGC_PROBE
 #define PROBE_STAMP(arr, v, k) \
   do {                          \
-    if ((arr) && lane == 0) (arr)[4 * (v) + (k)] = clock64(); \
+    if ((arr) && lane == 0) (arr)[8 * (v) + (k)] = globaltimer(); \
   } while (0)
 #else
 #define PROBE_STAMP(arr, v, k) \
@@ -476,7 +476,10 @@ __device__ __forceinline__ int bmap_next_zero(const uint8_t* bm, int from) {
 // 2048-color bitmap window, and publishes the color to all C replicas with
 // DSMEM stores (plus the global color[]).  A dependency hop thus costs one
 // DSMEM store + a local shared-memory poll instead of an L2 round trip.
-constexpr int kCoreBlock = 1024;
+#ifndef PGC_CORE_BLOCK
+#define PGC_CORE_BLOCK 1024
+#endif
+constexpr int kCoreBlock = PGC_CORE_BLOCK;
 constexpr int kCoreWarps = kCoreBlock / 32;
 constexpr int kCoreWin = 1024;   // colors per byte-map window
 constexpr int kCorePend = 512;   // pending-pred list capacity per warp
@@ -566,31 +569,56 @@ __global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __rest
   }
 }
 
+// 1 << d for 0 <= d < 32, else 0 (PTX clamps the shift amount)
+__device__ __forceinline__ unsigned shl1(int d) {
+  unsigned r;
+  asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(d));
+  return r;
+}
+
 __device__ __forceinline__ int ld_vol_u16(const uint16_t* p) {
   return *(volatile const uint16_t*)p;
 }
 
 
-// Examine core preds [from, np) (from even) in strips of 32 u16 pairs, 4 strips
-// (256 preds) in flight: colored ones go into the window, uncolored ones into
-// the warp's pending list; qmax tracks the largest pending core position (the
+// Examine core preds [from, np) (from even) in strips of 32 u16 pairs, 8 strips
+// (512 preds) per step, the next step's pred words loaded before this step is
+// processed (a hub's list is long: its scan must not pay one L2 latency per
+// 256 preds): colored ones go into the window, uncolored ones into the warp's
+// pending list; qmax tracks the largest pending core position (the
 // lowest-priority pending pred, i.e. the one expected to be colored last).
 // Returns where to resume when the list is full, np when every pred was examined.
+#ifndef PGC_SCAN_STRIPS
+#define PGC_SCAN_STRIPS 4
+#endif
+#ifndef PGC_SCAN_PREFETCH
+#define PGC_SCAN_PREFETCH 1
+#endif
+constexpr int kScanStrips = PGC_SCAN_STRIPS;
 __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np, int from,
                                          const uint16_t* cc, uint8_t* bm, int wbase,
                                          uint16_t* plist, int& npend, int& qmax) {
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
   const uint32_t* L2 = reinterpret_cast<const uint32_t*>(L);  // P slots are 4-byte aligned
-  for (int i0 = from; i0 < np; i0 += 256) {
-    uint32_t w[4];
+  constexpr int kStep = 64 * kScanStrips;
+  uint32_t w[kScanStrips];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = i0 + 64 * k + 2 * lane;
-      w[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
+  for (int k = 0; k < kScanStrips; ++k) {
+    const int i = from + 64 * k + 2 * lane;
+    w[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
+  }
+  for (int i0 = from; i0 < np; i0 += kStep) {
+    uint32_t wn[kScanStrips];
+    if (PGC_SCAN_PREFETCH) {
+#pragma unroll
+      for (int k = 0; k < kScanStrips; ++k) {
+        const int i = i0 + kStep + 64 * k + 2 * lane;
+        wn[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
+      }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kScanStrips; ++k) {
       const int i = i0 + 64 * k + 2 * lane;
       const int qa = i < np ? (int)(w[k] & 0xffffu) : -1;
       const int qb = i + 1 < np ? (int)(w[k] >> 16) : -1;
@@ -612,6 +640,16 @@ __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np,
       }
       npend += __popc(bb);
     }
+    if (PGC_SCAN_PREFETCH) {
+#pragma unroll
+      for (int k = 0; k < kScanStrips; ++k) w[k] = wn[k];
+    } else if (i0 + kStep < np) {
+#pragma unroll
+      for (int k = 0; k < kScanStrips; ++k) {
+        const int i = i0 + kStep + 64 * k + 2 * lane;
+        w[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
+      }
+    }
   }
   return np;
 }
@@ -621,7 +659,8 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
                                                            int32_t* color, State* st,
                                                            unsigned long long* tr_grab,
                                                            unsigned long long* tr_done,
-                                                           unsigned spin_ns,
+                                                           unsigned spin_ns, unsigned tail_ns,
+                                                           unsigned pass_ns,
                                                            unsigned long long watchdog_ns) {
   // dynamic shared memory: bitmaps | pending lists | color replica [NC] (0 = uncolored)
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -638,7 +677,12 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
   for (int i = threadIdx.x; i < NC; i += blockDim.x) s_cc[i] = 0;
   if (threadIdx.x == 0) s_ticket = 0;
   cl.sync();  // every replica is zeroed before any color is published
-  uint16_t* remote = lane < C ? cl.map_shared_rank(s_cc, lane) : nullptr;
+  // lane r < C publishes into CTA r's replica: its shared::cluster address
+  uint32_t remote = 0;
+  if (lane < C)
+    asm("mapa.shared::cluster.u32 %0, %1, %2;"
+        : "=r"(remote)
+        : "r"((uint32_t)__cvta_generic_to_shared(s_cc)), "r"(lane));
   const unsigned long long deadline = globaltimer() + watchdog_ns;
   uint8_t* bm = s_bm + warp * kCoreWin;
   uint16_t* plist = s_pend + warp * kCorePend;
@@ -714,6 +758,9 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
         if (moved) {
           zi = bmap_next_zero<kCoreWin>(bm, zi);
           sleep_ns = 0;
+          // rate-limit the passes of a warp still far from its tail: a pass
+          // per arrival would take the issue slots of the warps on the chain
+          if (pass_ns && npend > 4 * kCoreTail) __nanosleep(pass_ns);
         } else {
           if ((++polls & 63u) == 0 && __shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
             stall = true;
@@ -729,50 +776,65 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
         // collectives (each costs ~40-50 cycles on the chain).  With the used
         // set S of the colors already seen, GetColor after the last npend <=
         // kCoreTail colors c_k arrive is the first of the kCoreTail+1 smallest
-        // colors missing from S that no c_k takes.  Those are found now; then
-        // every lane spins on the pending preds in position order (the order
-        // they get colored in) and finishes with compares and selects.
+        // colors missing from S that no c_k takes.  Those are found now (as a
+        // bit mask); then the warp polls all pending preds at once and
+        // finishes with a mask and a find-first-set.
         int z[kCoreTail + 1];
         z[0] = zi;
 #pragma unroll
         for (int k = 1; k <= kCoreTail; ++k) z[k] = bmap_next_zero<kCoreWin>(bm, min(z[k - 1] + 1, kCoreWin));
+        // candidate set as a 32-bit mask relative to z[0] (exact when every
+        // candidate lies within 32 colors of z[0]; else the compare loop below)
+        unsigned F = 0u;
+#pragma unroll
+        for (int k = 0; k <= kCoreTail; ++k)
+          if (z[k] < kCoreWin && z[k] - z[0] < 32) F |= 1u << (z[k] - z[0]);
         int q[kCoreTail];
 #pragma unroll
-        for (int k = 0; k < kCoreTail; ++k) q[k] = k < npend ? (int)plist[k] : 0x7fffffff;
-#pragma unroll
-        for (int i = 1; i < kCoreTail; ++i)  // ascending positions (a sorting network)
-#pragma unroll
-          for (int k = kCoreTail - 1; k > 0; --k)
-            if (q[k] < q[k - 1]) {
-              const int t = q[k];
-              q[k] = q[k - 1];
-              q[k - 1] = t;
-            }
+        for (int k = 0; k < kCoreTail; ++k) q[k] = (int)plist[k < npend ? k : 0];
+        const int cbase = wbase + 1 + z[0];  // color -> bit index in F
         PROBE_STAMP(tr_grab, vprobe, 4);
-        int cl_[kCoreTail];
-#pragma unroll
-        for (int k = 0; k < kCoreTail; ++k) {
-          int c = 0;
-          if (k < npend) {
-            while ((c = ld_vol_u16(s_cc + q[k])) == 0) {
-              if ((++polls & 65535u) == 0 && globaltimer() > deadline) {
-                st->err = 5;
-                stall = true;
-                break;
-              }
+        // all pending preds are polled together (independent loads, one latency
+        // per poll; entries past npend repeat q[0]), the watchdog only every
+        // 512 polls: the loop is short because every waiting warp of the SM
+        // spins here and shares the issue slots with the warps on the chain
+        int c0, c1, c2, c3;
+        for (;;) {
+          bool all = false;
+          for (int it = 0; it < 512; ++it) {
+            c0 = ld_vol_u16(s_cc + q[0]);
+            c1 = ld_vol_u16(s_cc + q[1]);
+            c2 = ld_vol_u16(s_cc + q[2]);
+            c3 = ld_vol_u16(s_cc + q[3]);
+            if (c0 && c1 && c2 && c3) {
+              all = true;
+              break;
             }
           }
-          cl_[k] = c - wbase - 1;  // 0-based color within the window (or out of it)
-          if (stall) break;
+          if (all) break;
+          if (globaltimer() > deadline) {
+            st->err = 5;
+            stall = true;
+            break;
+          }
+          if (tail_ns) __nanosleep(tail_ns);
         }
         PROBE_STAMP(tr_grab, vprobe, 5);
-        int res = kCoreWin;
+        const unsigned M = shl1(c0 - cbase) | shl1(c1 - cbase) | shl1(c2 - cbase) | shl1(c3 - cbase);
+        const unsigned G = F & ~M;
+        int res;
+        if (G) {
+          res = z[0] + __ffs(G) - 1;
+        } else {  // candidates spread wider than 32 colors or past the window
+          const int cl_[kCoreTail] = {c0 - wbase - 1, c1 - wbase - 1, c2 - wbase - 1, c3 - wbase - 1};
+          res = kCoreWin;
 #pragma unroll
-        for (int j = kCoreTail; j >= 0; --j) {
-          bool taken = false;
+          for (int j = kCoreTail; j >= 0; --j) {
+            bool taken = false;
 #pragma unroll
-          for (int k = 0; k < kCoreTail; ++k) taken |= (k < npend) && cl_[k] == z[j];
-          if (!taken) res = z[j];
+            for (int k = 0; k < kCoreTail; ++k) taken |= cl_[k] == z[j];
+            if (!taken) res = z[j];
+          }
         }
         zi = res;
         npend = 0;
@@ -782,7 +844,10 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
     }
     PROBE_STAMP(tr_grab, vprobe, 6);
     if (stall) break;
-    if (lane < C) *(volatile uint16_t*)(remote + p) = (uint16_t)found;  // publish to every replica
+    if (lane < C)  // publish to every replica (DSMEM store, relaxed at cluster scope)
+      asm volatile("st.relaxed.cluster.shared::cluster.u16 [%0], %1;" ::"r"(remote + 2u * (uint32_t)p),
+                   "h"((unsigned short)found)
+                   : "memory");
     PROBE_STAMP(tr_grab, vprobe, 7);
     if (lane == 0) {
       st_relaxed(color + vcore, found);
@@ -1000,7 +1065,9 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
       const int np = np_next;
       const int64_t pb = pb_next;
       fetch(t_next, v_next, np_next, pb_next);
+#ifndef PGC_PROBE
       if (tr_grab && lane == 0) tr_grab[v] = globaltimer();
+#endif
       int found = 0;
       for (int wbase = 0; !found; wbase += kHeavyWin) {
         bmap_clear(bm, kHeavyWin);
@@ -1186,7 +1253,9 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
       {
         if (take) {
           {
+#ifndef PGC_PROBE
             if (tr_grab) tr_grab[v] = globaltimer();
+#endif
             // first pass over every pred
             mask = 1ull;  // bit 0 reserved: colors start at 1
             pend = 0ull;
@@ -1402,7 +1471,9 @@ int jp_color_run(Ctx& c, int32_t* color) {
                  PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int4*)c.rec,
                                              (const int32_t*)c.P, color, c.state,
                                              c.trace_grab, c.trace_done,
-                                             (unsigned)c.tune.core_spin_ns, wd)));
+                                             (unsigned)c.tune.core_spin_ns,
+                                             (unsigned)c.tune.core_tail_ns,
+                                             (unsigned)c.tune.core_pass_ns, wd)));
     }
     // --- bulk dataflow ---
     if (nbulk > 0) {

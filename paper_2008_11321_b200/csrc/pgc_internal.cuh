@@ -74,6 +74,8 @@ struct Tuning {
   int core_min_n = 256;           // JP core: smaller cores are left to the bulk kernel
   int core_ctas = 0;              // JP core: cluster size (0 = from core_arcs_per_cta)
   int core_spin_ns = 1024;        // JP core: backoff cap (ns) of a warp still several preds away
+  int core_tail_ns = 0;           // JP core: sleep (ns) per poll of a warp in the tail
+  int core_pass_ns = 0;           // JP core: min sleep (ns) between passes of a warp far from its tail
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;

@@ -39,7 +39,8 @@ def main():
     for kv in a.tune:
         k, val = kv.split("=")
         pgc.set_tuning(k, int(val))
-    g = gg.config_graph(a.config)
+    from bench import load_graph  # /tmp-cached generator output
+    g = load_graph(a.config)
     num, den = gg.CONFIGS[a.config][1][0] if a.config != "rmat20" else (1, 10)
     off = torch.from_numpy(g.off).cuda()
     col = torch.from_numpy(g.col).cuda()
@@ -54,9 +55,10 @@ def main():
     tg = tg.cpu().numpy().astype(np.int64)
     td = td.cpu().numpy().astype(np.int64)
     r = rnd.cpu().numpy().astype(np.int64)
-    t0 = tg.min()
-    tg -= t0
-    td -= t0
+    traced = td > 0              # isolated vertices are settled before JP (no stamps)
+    t0 = tg[traced].min()
+    tg = np.where(traced, tg - t0, 0)
+    td = np.where(traced, td - t0, 0)
     # oracle levels (JP DAG depth)
     _, _, lvl, J = O.jp(g, rnd.cpu().numpy(), a.seed, levels=True)
     # pred relation and ready time = max done over preds
@@ -111,6 +113,14 @@ def main():
     crit = np.array(crit[::-1])
     cs = step[crit]
     cc = core[crit]
+    late = wait_grab[crit] > 0   # grabbed after it was ready: its whole scan is on the path
+    out["critical_core_late_grab"] = {"n": int((cc & late).sum()),
+                                      "sum_grab_after_ready_ms": float(wait_grab[crit][cc & late].sum() / 1e6),
+                                      "sum_step_ms": float(cs[cc & late].sum() / 1e6),
+                                      "step_ns": pct(cs[cc & late])}
+    out["critical_core_early_grab"] = {"n": int((cc & ~late).sum()),
+                                       "sum_step_ms": float(cs[cc & ~late].sum() / 1e6),
+                                       "step_ns": pct(cs[cc & ~late], (10, 50, 90, 99, 100))}
     out["critical_core"] = {"len": int(cc.sum()), "step_ns": pct(cs[cc]), "sum_step_ms": float(cs[cc].sum() / 1e6),
                             "grab_after_ready_sum_ms": float(np.maximum(wait_grab[crit][cc], 0).sum() / 1e6),
                             "span_ms": float((td[crit][cc].max() - tg[crit][cc].min()) / 1e6) if cc.any() else 0}
