@@ -217,13 +217,17 @@ __global__ void k_hist1(int64_t n, const int32_t* __restrict__ round,
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   int cnt = 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (!in_order(npred, v)) continue;
-    const int k = rmax - round[v];
-    ++cnt;
-    if (priv) atomicAdd(&sh[k], 1);
-    else atomicAdd(&hist1[k], 1);
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x; v0 < n; v0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = v0 + threadIdx.x;
+    const bool in = v < n && in_order(npred, v);
+    const int k = in ? rmax - round[v] : -1;
+    cnt += in;
+    // few distinct keys: one atomic per key per warp (lanes with equal keys)
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    if (in && lane_id() == __ffs(peers) - 1) {
+      if (priv) atomicAdd(&sh[k], __popc(peers));
+      else atomicAdd(&hist1[k], __popc(peers));
+    }
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
