@@ -275,6 +275,20 @@ def run_pgc(args):
     achieved = kbytes / (kms * 1e-3) / 1e9
     traffic = ncu_traffic(kname)
     path_bytes = sum(model.values())
+    # UPDATE moves few bytes per random access: its ceiling is the measured
+    # random gather/RED rate for its exact mix (profiles/random_access_probe.json)
+    ra = None
+    try:
+        pr = json.load(open(os.path.join(PROFILES, "random_access_probe.json")))
+        arcs_per_s = nnz / (gmean["t_update_ms"] * 1e-3)
+        mix = X / nnz if nnz else 0.0
+        ra = {"arcs_per_s": arcs_per_s, "red_fraction": mix,
+              "peak_arcs_per_s": pr["gather_plus_red_42pct_arcs_per_s"],
+              "frac": arcs_per_s / pr["gather_plus_red_42pct_arcs_per_s"],
+              "note": "UPDATE = one random 1-byte state gather per arc + one RED per cross-round "
+                      "edge; peak = tools/micro/atom_probe.cu at the same RED fraction (0.42)"}
+    except Exception:
+        pass
 
     out = {
         "metric": METRIC, "value": world * m / (ms * 1e-3), "unit": "edges/s", "n_gpus": world,
@@ -291,7 +305,8 @@ def run_pgc(args):
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "bytes_per_launch": kbytes, "ms_per_launch": kms,
                      "path_bytes": path_bytes,
-                     "path_frac": path_bytes / (ms * 1e-3) / 1e9 / peak},
+                     "path_frac": path_bytes / (ms * 1e-3) / 1e9 / peak,
+                     "random_access": ra},
         "breakdown_ms": {k[2:-3]: v for k, v in gmean.items()},
         "gpu_launches": launches,
         "clocks": clk.summary(),

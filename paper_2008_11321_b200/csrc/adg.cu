@@ -46,8 +46,8 @@ __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ o
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t d = (int32_t)(off[v + 1] - off[v]);
-    D[v] = d;
-    rs[v] = 0;
+    st_i32_keep(D + v, d);
+    st_u8_keep(rs + v, 0);
     round[v] = 0;
     if (color) {
       color[v] = d == 0 ? 1 : 0;
@@ -100,7 +100,7 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
     int v = 0, d = 0;
     if (valid) {
       v = Uin ? Uin[i] : (int)i;
-      d = D[v];
+      d = ld_i32_keep(D + v);
     }
     const bool sel = valid && d <= dmax;
     bool light = false;
@@ -108,7 +108,7 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
     long long o = 0, deg = 0;
     if (sel) {
       round[v] = l;
-      rs[v] = (uint8_t)((l - 1) % 255 + 1);
+      st_u8_keep(rs + v, (l - 1) % 255 + 1);
       my_sumD += (unsigned long long)d;
       my_nR += 1;
       o = off[v];

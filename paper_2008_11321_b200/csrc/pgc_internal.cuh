@@ -219,6 +219,34 @@ __device__ __forceinline__ void red_dec_keep(int32_t* a) {
                : "memory");
 #endif
 }
+// plain int load / int and byte stores with the evict-last policy (the ADG
+// per-vertex state, so the first UPDATE finds D and rs in L2)
+__device__ __forceinline__ int ld_i32_keep(const int32_t* a) {
+#ifdef PGC_NO_L2HINT
+  return *a;
+#else
+  int v;
+  asm volatile("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(l2_keep_policy()));
+  return v;
+#endif
+}
+__device__ __forceinline__ void st_i32_keep(int32_t* a, int v) {
+#ifdef PGC_NO_L2HINT
+  *a = v;
+#else
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(l2_keep_policy())
+               : "memory");
+#endif
+}
+__device__ __forceinline__ void st_u8_keep(uint8_t* a, int v) {
+#ifdef PGC_NO_L2HINT
+  *a = (uint8_t)v;
+#else
+  asm volatile("st.global.L2::cache_hint.b8 [%0], %1, %2;" ::"l"(a), "h"((unsigned short)v),
+               "l"(l2_keep_policy())
+               : "memory");
+#endif
+}
 // read-only byte gather (rs is immutable during UPDATE), evict-last
 __device__ __forceinline__ int ld_u8_keep(const uint8_t* a) {
 #ifdef PGC_NO_L2HINT

@@ -20,7 +20,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sectors_srcunit_tex_op_red.sum", "lts__t_sectors_srcunit_tex_op_atom.sum",
         "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
         "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum",
-        "smsp__inst_executed.sum"]
+        "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "lts__t_requests.sum", "lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_tag_requests.max.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "lts__t_sectors_srcunit_tex_op_red_lookup_miss.sum"]
 
 
 def short(name):
@@ -77,9 +81,11 @@ def main():
             md.append(f"| {k} | {c} | {t / 1e6:.3f} | {100 * t / tot:.1f}% |")
         md.append(f"| **total** | {sum(v[1] for v in last.values())} | {tot / 1e6:.3f} | |\n")
         summary["launch_list_last_step"] = {k: {"ns": t, "launches": c} for k, (t, c) in last.items()}
-    rp = os.path.join(src, "prof.ncu-rep")
-    if os.path.exists(rp):
-        fl = full(rp)
+    import glob
+    fl = []
+    for rp in sorted(glob.glob(os.path.join(src, "*.ncu-rep"))):
+        fl += full(rp)
+    if fl:
         summary["full"] = fl
         md.append("## ncu --set full (selected launches)\n")
         for d in fl:

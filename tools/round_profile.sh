@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round profile (run under gpurun, one GPU): the bench line, the ncu launch list
+# of the same bench command, DRAM bytes of every UPDATE launch of one step (the
+# roofline's `traffic`), and ncu --set full of the top kernels.
+#   TAG=r1_final tools/round_profile.sh   -> gpurun_out/$TAG/
+set -u
+OUT=gpurun_out/${TAG:-prof}
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+nvidia-smi > $OUT/smi.txt 2>&1
+python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?" > $OUT/status.txt
+CMD="python bench.py --quick --steps 1 --warmup 3"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
+echo "launches rc=$?" >> $OUT/status.txt
+# one step = the second call of launch_times.py (the first is a warm-up)
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:k_update --csv --log-file $OUT/update_traffic.csv python tools/launch_times.py > $OUT/traffic.log 2>&1
+echo "traffic rc=$?" >> $OUT/status.txt
+ncu --set full --import-source on --clock-control none -k regex:k_update_light -s 8 -c 1 -o $OUT/upd_light_r1 python tools/launch_times.py > $OUT/f1.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:k_update_heavy -s 10 -c 1 -o $OUT/upd_heavy_r3 python tools/launch_times.py > $OUT/f2.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"k_jp_core|k_jp_bulk" -s 2 -c 2 -o $OUT/jp python tools/launch_times.py > $OUT/f3.log 2>&1
+echo "full rc=$?" >> $OUT/status.txt
+cat $OUT/status.txt
