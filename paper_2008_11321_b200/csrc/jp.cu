@@ -1020,7 +1020,7 @@ __device__ __forceinline__ void lowest_two(const int* plist, const unsigned long
 }
 
 #ifndef PGC_BULK_MINB
-#define PGC_BULK_MINB 6
+#define PGC_BULK_MINB 5
 #endif
 __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64_t* __restrict__ off,
                                                      const int32_t* __restrict__ P,
@@ -1265,19 +1265,29 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
             pend = 0ull;
             watch_j = -1;
             watch_u = -1;
-            for (int j0 = 0; j0 < np; j0 += kLightBatch) {
-              int u[kLightBatch], cc[kLightBatch];
+            // pred ids by aligned 16-byte loads, 8 slots per step (slots
+            // outside [pb, pb + np) belong to neighbouring lists: ignored),
+            // then their 8 color gathers in flight
+            const int64_t pe = pb + np;
+            for (int64_t s0 = pb & ~3ll; s0 < pe; s0 += 8) {
+              const int4 w0 = __ldcs(reinterpret_cast<const int4*>(P + s0));
+              const int4 w1 = s0 + 4 < pe ? __ldcs(reinterpret_cast<const int4*>(P + s0 + 4))
+                                          : make_int4(-1, -1, -1, -1);
+              int u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+              int cc[8];
 #pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) u[k] = j0 + k < np ? jp_stream(P + pb + j0 + k) : -1;
+              for (int k = 0; k < 8; ++k)
+                if (s0 + k < pb || s0 + k >= pe) u[k] = -1;
 #pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+              for (int k = 0; k < 8; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
 #pragma unroll
-              for (int k = 0; k < kLightBatch; ++k) {
+              for (int k = 0; k < 8; ++k) {
                 if (u[k] < 0) continue;
+                const int j = (int)(s0 + k - pb);
                 if (cc[k] == 0) {
-                  pend |= 1ull << (j0 + k);
+                  pend |= 1ull << j;
                   if (watch_j < 0) {  // watch the first pending pred
-                    watch_j = j0 + k;
+                    watch_j = j;
                     watch_u = u[k];
                   }
                 } else if (cc[k] < 64) {
