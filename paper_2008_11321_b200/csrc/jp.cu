@@ -942,9 +942,8 @@ __device__ __forceinline__ int64_t rec_slot(const int4& r) {
 // never for a result): the first key's 32 bits, then the top 32 hash bits.
 // Preds get colored roughly in priority order, so the pending pred of lowest
 // key is the one expected to be colored last.
-__device__ __forceinline__ unsigned long long watch_key(const int32_t* __restrict__ round,
-                                                        uint64_t seed, int u) {
-  return ((unsigned long long)((uint32_t)round[u] ^ 0x80000000u) << 32) |
+__device__ __forceinline__ unsigned long long watch_key_of(int ru, uint64_t seed, int u) {
+  return ((unsigned long long)((uint32_t)ru ^ 0x80000000u) << 32) |
          (prio_hash(seed, (uint32_t)u) >> 32);
 }
 
@@ -968,6 +967,11 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+    // first keys of the pending preds, all four strips' loads in flight
+    // before any is used (a load consumed in its own branch serialises)
+    int rk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rk[k] = __ldg(round + (u[k] >= 0 && cc[k] == 0 ? u[k] : 0));
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const bool pend = u[k] >= 0 && cc[k] == 0;
@@ -978,7 +982,7 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
       if (pend) {
         const int at = npend + __popc(bal & lt);
         plist[at] = u[k];
-        pkey[at] = watch_key(round, seed, u[k]);
+        pkey[at] = watch_key_of(rk[k], seed, u[k]);
       }
       npend += cnt;
     }
