@@ -38,6 +38,8 @@ def _load():
         lib.orc_splitmix64.argtypes = [u64]
         lib.orc_adg.restype = ctypes.c_int
         lib.orc_adg.argtypes = [i64, vp, vp, u32, u32, vp, vp, i64, vp, vp, vp]
+        lib.orc_adg_m.restype = ctypes.c_int
+        lib.orc_adg_m.argtypes = [i64, vp, vp, vp, vp]
         lib.orc_jp.restype = ctypes.c_int
         lib.orc_jp.argtypes = [i64, vp, vp, vp, u64, vp, vp, vp]
         lib.orc_degeneracy.restype = i64
@@ -84,6 +86,17 @@ def adg(g, num: int, den: int, per_round: bool = False):
         stats["S"] = ps[:T].copy()
         stats["nR"] = pr[:T].copy()
     return rnd, stats
+
+
+def adg_m(g):
+    """ADG-M rounds (median threshold).  Returns (round int32[n], stats)."""
+    off, col = _csr(g)
+    rnd = np.zeros(g.n, dtype=np.int32)
+    st = np.zeros(3, dtype=np.int64)
+    T = _load().orc_adg_m(g.n, _p(off), _p(col), _p(rnd), _p(st))
+    if T < 0:
+        raise ValueError("oracle adg_m: bad arguments")
+    return rnd, {"T": int(st[0]), "sum_active": int(st[1]), "cross_edges": int(st[2])}
 
 
 def jp(g, rnd, seed: int, levels: bool = False):

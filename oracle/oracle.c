@@ -154,6 +154,94 @@ ORC_EXPORT int orc_adg(int64_t n, const int64_t* off, const int32_t* col, uint32
 }
 
 /* ------------------------------------------------------------------------ */
+/* ADG-M -- "Degree Median Instead of Degree Average"
+ * (analysis 2553-2611).  ADG-M differs from Algorithm 1 only in that
+ *   (1) the median degree delta_m of the vertices in U replaces the mean, and
+ *   (2) R = { v in U : D[v] <= delta_m }, limited to half the size of U
+ *       (+1 if |U| is odd)                                     (2296-2301)
+ * and the paper derives delta_m from U sorted by degree with a linear-time
+ * integer sort (2286-2294).  Readings (Q19-Q21): U is sorted by
+ * (D ascending, id ascending) -- a stable integer sort of U in id order;
+ * delta_m is the D of the ceil(|U|/2)-th element of that order (the lower
+ * median); the cap keeps the first ceil(|U|/2) vertices of the order.  All of
+ * them pass the test D <= delta_m, so R_l is exactly that prefix (the (1+eps)
+ * factor of the conference text, 2277, would change nothing under the cap).
+ * UPDATE and the rest of the round are Algorithm 1's (692-696, 687-690).
+ * Returns T; stats[0] = T, stats[1] = sum_l |U_l|, stats[2] = X.            */
+static const int64_t* g_keyD;
+static int cmp_deg_id(const void* a, const void* b) {
+  int64_t u = *(const int64_t*)a, v = *(const int64_t*)b;
+  if (g_keyD[u] != g_keyD[v]) return g_keyD[u] < g_keyD[v] ? -1 : 1;
+  return u < v ? -1 : (u > v ? 1 : 0);
+}
+
+ORC_EXPORT int orc_adg_m(int64_t n, const int64_t* off, const int32_t* col, int32_t* round_out,
+                         int64_t* stats) {
+  if (n < 0) return -1;
+  int64_t* D = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  char* inU = (char*)malloc((size_t)n + 1);
+  char* inR = (char*)malloc((size_t)n + 1);
+  int64_t* U = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t sizeU = n;
+  for (int64_t v = 0; v < n; ++v) {
+    D[v] = off[v + 1] - off[v];
+    inU[v] = 1;
+    inR[v] = 0;
+    U[v] = v;
+    round_out[v] = 0;
+  }
+  int64_t l = 1, sum_active = 0, cross = 0;
+  while (sizeU > 0) {
+    sum_active += sizeU;
+    /* U in ascending (D, id) order; delta_m = D of the ceil(|U|/2)-th */
+    g_keyD = D;
+    qsort(U, (size_t)sizeU, sizeof(int64_t), cmp_deg_id);
+    const int64_t half = sizeU / 2 + (sizeU % 2);   /* half the size of U, +1 if odd */
+    const int64_t delta_m = D[U[half - 1]];
+    /* R = { v in U : D[v] <= delta_m }, limited to the first `half` of the order */
+    int64_t sizeR = 0;
+    for (int64_t i = 0; i < sizeU && sizeR < half; ++i)
+      if (D[U[i]] <= delta_m) { inR[U[i]] = 1; ++sizeR; }
+    /* UPDATE(U, R, D) (692-696) */
+    for (int64_t i = 0; i < sizeU; ++i) {
+      int64_t v = U[i];
+      if (!inR[v]) continue;
+      for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+        int64_t u = col[e];
+        if (inU[u]) {
+          D[u] -= 1;
+          if (!inR[u]) cross += 1;
+        }
+      }
+    }
+    /* U = U \ R; rho(v) = l for v in R; l += 1 (687-690) */
+    int64_t k = 0;
+    for (int64_t i = 0; i < sizeU; ++i) {
+      int64_t v = U[i];
+      if (inR[v]) {
+        inU[v] = 0;
+        inR[v] = 0;
+        round_out[v] = (int32_t)l;
+      } else {
+        U[k++] = v;
+      }
+    }
+    sizeU = k;
+    l += 1;
+  }
+  free(D);
+  free(inU);
+  free(inR);
+  free(U);
+  if (stats) {
+    stats[0] = l - 1;
+    stats[1] = sum_active;
+    stats[2] = cross;
+  }
+  return (int)(l - 1);
+}
+
+/* ------------------------------------------------------------------------ */
 /* JP priority rho = <rho_ADG, rho_R>, lexicographic (PAPER.md:1073-1078,
  * 1095-1096): u has higher priority than v iff
  *   round[u] > round[v], or round[u] == round[v] and h(u) > h(v),

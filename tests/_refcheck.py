@@ -215,3 +215,41 @@ def all_graphs(n):
     pairs = [(i, j) for i in range(n) for j in range(i + 1, n)]
     for mask in range(1 << len(pairs)):
         yield [pairs[b] for b in range(len(pairs)) if mask >> b & 1]
+
+
+# ---------------------------------------------------------------- ADG-M -----
+def adg_m_certificate(g, rnd):
+    """Characterisation of ADG-M's output (readings Q19-Q21)
+    from round[] alone: for every l, with U_l = {v : round[v] >= l} and
+    D_l(v) = |N(v) ∩ U_l|, round l removes exactly the ceil(|U_l|/2) vertices of
+    U_l that come first in ascending (D_l, id) order.  Returns None if valid."""
+    n = g.n
+    if n == 0:
+        return None if len(rnd) == 0 else "n=0 but rounds given"
+    rnd = np.asarray(rnd, dtype=np.int64)
+    if rnd.min() < 1:
+        return f"vertex {int(np.argmin(rnd))} has round < 1"
+    src = np.repeat(np.arange(n), np.diff(g.off))
+    dst = g.col.astype(np.int64)
+    for l in range(1, int(rnd.max()) + 1):
+        inU = rnd >= l
+        U = np.nonzero(inU)[0]
+        keep = inU[src] & inU[dst]
+        D = np.bincount(src[keep], minlength=n)
+        first = U[np.lexsort((U, D[U]))][: (len(U) + 1) // 2]   # key (D asc, id asc)
+        want = np.zeros(n, dtype=bool)
+        want[first] = True
+        bad = np.nonzero(want != (rnd == l))[0]
+        if len(bad):
+            return f"round {l}: vertex {int(bad[0])}"
+    return None
+
+
+def approx4_ok(g, rnd, d):
+    """Lemma (ADG-M): every vertex has at most 4d neighbours
+    ranked equal or higher."""
+    rnd = np.asarray(rnd, dtype=np.int64)
+    src = np.repeat(np.arange(g.n), np.diff(g.off))
+    dst = g.col.astype(np.int64)
+    up = np.bincount(src[rnd[dst] >= rnd[src]], minlength=g.n)
+    return bool((up <= 4 * d).all())
