@@ -130,6 +130,30 @@ int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uin
                      int32_t* num_colors, void* workspace, size_t workspace_bytes,
                      void* cuda_stream);
 
+/* ADG-M ordering only (the median variant of ADG; its
+ * analysis: O(log n) rounds, a partial 4-approximate
+ * degeneracy ordering).  Each round removes the vertices of U whose residual
+ * degree is at most the median degree of U, limited to half of |U| (+1 if |U|
+ * is odd).  Readings (Q19-Q21): U is ordered by (residual degree
+ * ascending, id ascending) -- a stable integer sort of U; the median is the
+ * degree of the ceil(|U|/2)-th vertex of that order; the cap keeps the first
+ * ceil(|U|/2) vertices.  So |U_{l+1}| = floor(|U_l| / 2) and T = floor(log2 n)
+ * + 1 exactly.  No eps, no seed.
+ *   round_out  : device int32[n], receives rho_ADG-M(v) in [1, T]
+ *   num_rounds : host int32*, receives T (0 for n = 0)
+ * Same workspace, errors and ownership as pgc_adg_order. */
+int pgc_adg_m_order(const pgc_graph* g, int32_t* round_out, int32_t* num_rounds, void* workspace,
+                    size_t workspace_bytes, void* cuda_stream);
+
+/* JP-ADG-M: ADG-M then JP with <rho_ADG-M, rho_R>
+ * (rho_R(v) = splitmix64(seed ^ v) as in pgc_color_jp_adg); at most 4d + 1
+ * colors.  JP Part 1 is fused into UPDATE as in pgc_color_jp_adg.
+ *   round_out, color_out : device int32[n]
+ *   num_rounds, num_colors : host int32* */
+int pgc_color_jp_adg_m(const pgc_graph* g, uint64_t seed, int32_t* round_out, int32_t* color_out,
+                       int32_t* num_rounds, int32_t* num_colors, void* workspace,
+                       size_t workspace_bytes, void* cuda_stream);
+
 /* JP-ADG end to end from HOST memory: copies the CSR host->device on
  * `cuda_stream`, runs pgc_color_jp_adg, copies round[] and color[] back.
  * Host buffers should be pinned (cudaHostAlloc) for full copy bandwidth.

@@ -34,9 +34,10 @@ __global__ void k_zero_i32_dev(int32_t* p, const int* len, int extra) {
 
 // a1: D[v] = deg(v); round[v] = 0 (v in U); optional color[v] = 0 (uncolored,
 // PAPER.md:1115).  Thread 0 initialises the round state: S_1 = nnz, |U_1| = n.
-// An isolated vertex (deg 0) is settled here: it counts in n_1 and falls into
-// R_1 (D = 0 <= Dmax_1, Q12), but it has no arc to scan and is no pred of any
-// vertex, so it gets no work record; with JP its color is GetColor of the empty
+// An isolated vertex (deg 0) is settled here: it counts in |U| (Q12) and gets
+// its round from the select kernel like any vertex (with ADG's mean rule that
+// is round 1: D = 0 <= Dmax_1), but it has no arc to scan and is no pred of
+// any vertex, so it gets no work record; with JP its color is GetColor of the empty
 // pred set, 1, and npred = -1 keeps it out of the priority
 // order (it can neither wait nor be waited on).
 __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ off,
@@ -70,7 +71,7 @@ __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ o
 }
 
 // a2+a3: threshold, select, compact.
-__global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
+__global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
                              const int32_t* __restrict__ D, int32_t* __restrict__ round,
                              uint8_t* __restrict__ rs,
                              const int32_t* __restrict__ Uin, int32_t* __restrict__ Uout,
@@ -91,6 +92,7 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
   }
   __syncthreads();
   const long long dmax = s_dmax;
+  const unsigned long long mkey = st->msel_key;  // ADG-M: the ceil(|U|/2)-th smallest key
   unsigned long long my_sumD = 0;
   unsigned long long my_nR = 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -102,7 +104,11 @@ __global__ void k_adg_select(int l, uint32_t num, uint32_t den, const int64_t* _
       v = Uin ? Uin[i] : (int)i;
       d = ld_i32_keep(D + v);
     }
-    const bool sel = valid && d <= dmax;
+    // ADG: D <= (1+eps) * mean (exact integer form);  ADG-M: the
+    // ceil(|U|/2) smallest keys (D, id) of U (median rule)
+    const bool sel = valid && (rule == kRuleMedian
+                                   ? ((((unsigned long long)(uint32_t)d) << 32) | (uint32_t)v) <= mkey
+                                   : d <= dmax);
     bool light = false;
     int nch = 0;
     long long o = 0, deg = 0;
@@ -540,6 +546,91 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
   }
 }
 
+// ADG-M's median (readings Q19-Q21): the ceil(|U|/2)-th
+// smallest key (D[v] << 32) | v over U by a radix select, most significant
+// digit first (digits of 11,11,11,11,11,9 bits), each pass a shared-memory
+// histogram of the keys that match the digits found so far, then one block
+// picks the digit holding the wanted rank.  Keys are distinct (the id is in
+// the low word), so R = {v in U : key <= selected key} has exactly
+// ceil(|U|/2) vertices: the first half of U in (D, id) order.
+constexpr int kMselPasses = 6;
+constexpr int kMselBins = 2048;
+__device__ __forceinline__ void msel_geom(int pass, int& shift, int& bits) {
+  bits = pass == kMselPasses - 1 ? 9 : 11;
+  shift = 64 - 11 * (pass + 1);
+  if (shift < 0) shift = 0;
+}
+__global__ void __launch_bounds__(1024) k_msel_hist(int pass, const int32_t* __restrict__ Uin,
+                                                    const int32_t* __restrict__ D,
+                                                    int32_t* __restrict__ hist, const State* st) {
+  __shared__ int sh[kMselBins];
+  if (st->done) return;
+  int shift, bits;
+  msel_geom(pass, shift, bits);
+  const unsigned long long prefix = st->msel_key;
+  for (int i = threadIdx.x; i < kMselBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const long long nU = st->nU;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nU;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int v = Uin ? Uin[i] : (int)i;
+    const unsigned long long key = (((unsigned long long)(uint32_t)ld_i32_keep(D + v)) << 32) | (uint32_t)v;
+    if (pass == 0 || (key >> (shift + bits)) == prefix)
+      atomicAdd(&sh[(int)(key >> shift) & ((1 << bits) - 1)], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMselBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+// One block of 1024 threads, two bins per thread: block scan of the histogram,
+// the digit whose inclusive count first reaches the rank, then the histogram
+// is cleared for the next pass.
+__global__ void __launch_bounds__(1024) k_msel_pick(int pass, int32_t* __restrict__ hist, State* st) {
+  __shared__ long long s_w[32];
+  __shared__ int s_digit;
+  __shared__ long long s_before;
+  if (st->done) return;
+  int shift, bits;
+  msel_geom(pass, shift, bits);
+  const long long rank = pass == 0 ? (st->nU + 1) / 2 : st->msel_rank;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const long long a = hist[2 * t], b = hist[2 * t + 1];
+  long long incl = a + b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const long long w = s_w[lane];
+    long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    s_w[lane] = wi - w;
+  }
+  __syncthreads();
+  const long long before = s_w[warp] + incl - (a + b);  // keys in bins < 2t
+  if (before < rank && rank <= before + a) {
+    s_digit = 2 * t;
+    s_before = before;
+  } else if (before + a < rank && rank <= before + a + b) {
+    s_digit = 2 * t + 1;
+    s_before = before + a;
+  }
+  __syncthreads();
+  hist[2 * t] = 0;
+  hist[2 * t + 1] = 0;
+  if (t == 0) {
+    st->msel_key = ((pass == 0 ? 0ull : st->msel_key) << bits) | (unsigned long long)s_digit;
+    st->msel_rank = rank - s_before;
+  }
+}
+
 // a2/a5: carry the cached degree sum and |U| to the next round (Q5 reading of
 // PAPER.md:2359-2361), record statistics, detect termination.
 __global__ void k_adg_finalize(int l, State* st, long long* per_round) {
@@ -653,7 +744,7 @@ static int launch_update(Ctx& c, const Arc<MODE>& A, const int32_t* Uin = nullpt
 }
 
 int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
-            int32_t* color_zero) {
+            int32_t* color_zero, int rule) {
   const int B = 256;
   const int G = grid_for(c, 8);
   PGC_LAUNCH(c, kGAdgOther, "k_adg_init",
@@ -661,14 +752,23 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                            c.npred, c.tune.filter_ratio > 0 ? c.filt : nullptr,
                                            c.state));
   if (c.n == 0) return sync_state(c);
+  int32_t* mhist = c.hist1;  // the order's histograms are free during ADG
+  if (rule == kRuleMedian)
+    PGC_LAUNCH(c, kGAdgOther, "k_zero_i32", k_zero_i32<<<4, 512, 0, c.st>>>(mhist, kMselBins));
   int l = 1;
   const int batch = c.tune.rounds_per_sync < 1 ? 1 : c.tune.rounds_per_sync;
   for (;;) {
     for (int j = 0; j < batch; ++j, ++l) {
       const int32_t* Uin = l == 1 ? nullptr : c.U[l & 1];
       int32_t* Uout = c.U[(l + 1) & 1];
+      if (rule == kRuleMedian)
+        for (int pass = 0; pass < kMselPasses; ++pass) {
+          PGC_LAUNCH(c, kGSelect, "k_msel_hist",
+                     k_msel_hist<<<c.nsm * 2, 1024, 0, c.st>>>(pass, Uin, c.D, mhist, c.state));
+          PGC_LAUNCH(c, kGSelect, "k_msel_pick", k_msel_pick<<<1, 1024, 0, c.st>>>(pass, mhist, c.state));
+        }
       PGC_LAUNCH(c, kGSelect, "k_adg_select",
-                 k_adg_select<<<G, B, 0, c.st>>>(l, num, den, c.off, c.D, round, c.rs, Uin, Uout,
+                 k_adg_select<<<G, B, 0, c.st>>>(l, rule, num, den, c.off, c.D, round, c.rs, Uin, Uout,
                                                  c.lrec, c.chunks, c.npred, c.state,
                                                  c.tune.heavy_degree, c.tune.chunk_arcs,
                                                  c.lay.chunk_cap));

@@ -311,6 +311,44 @@ int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uin
   return PGC_OK;
 }
 
+int pgc_adg_m_order(const pgc_graph* g, int32_t* round_out, int32_t* num_rounds, void* workspace,
+                    size_t workspace_bytes, void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (!num_rounds || (g->n > 0 && !round_out)) return fail(PGC_EINVAL, "output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  if (int e = adg_run(c, 1, 1, 0, round_out, kAdgOnly, nullptr, kRuleMedian)) return e;
+  *num_rounds = c.h_state->T;
+  call_end(c, c.h_state->T, 0, c.h_state->sum_active, c.h_state->cross, 0, 0);
+  return PGC_OK;
+}
+
+int pgc_color_jp_adg_m(const pgc_graph* g, uint64_t seed, int32_t* round_out, int32_t* color_out,
+                       int32_t* num_rounds, int32_t* num_colors, void* workspace,
+                       size_t workspace_bytes, void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (!num_rounds || !num_colors || (g->n > 0 && (!round_out || !color_out)))
+    return fail(PGC_EINVAL, "output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  if (int e = adg_run(c, 1, 1, seed, round_out, kAdgFused, color_out, kRuleMedian)) return e;
+  const int T = c.h_state->T;
+  const long long sum_active = c.h_state->sum_active;
+  const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
+  c.round_key = round_out;
+  c.seed = seed;
+  if (int e = jp_order_run(c, round_out, seed, true)) return e;
+  if (int e = jp_color_run(c, color_out)) return e;
+  *num_rounds = T;
+  *num_colors = c.h_state->K;
+  call_end(c, T, c.h_state->K, sum_active, cross, preds, c.core_n);
+  return PGC_OK;
+}
+
 size_t pgc_host_workspace_bytes(int64_t n, int64_t nnz) {
   if (!sizes_ok(n, nnz)) return 0;
   return a256(8 * (size_t)(n + 1)) + a256(4 * (size_t)nnz) + 2 * a256(4 * (size_t)n) +

@@ -48,6 +48,9 @@ struct State {
   int nheavy;                  // bulk vertices with |pred| > kLightPredMax
   int nlight;                  // bulk vertices with 1 <= |pred| <= kLightPredMax
   int ticket_heavy, ticket_light;  // next bulk tickets per class
+  // ADG-M radix select of the ceil(|U|/2)-th smallest key (D[v] << 32) | v
+  unsigned long long msel_key;  // key digits found so far (the full key after the last pass)
+  long long msel_rank;          // rank still to find among keys with that prefix (1-based)
 };
 
 // Byte offsets of every workspace region (each 256-byte aligned).
@@ -129,8 +132,11 @@ constexpr int kFilterWords = kFilterBytes / 4;
 
 // ---- phases (host orchestration; return 0 or a PGC_* code) -----------------
 enum AdgMode { kAdgOnly = 0, kAdgFused = 1 };
+// selection rule of a round: ADG's mean threshold (Alg. 1) or ADG-M's median
+//
+enum AdgRule { kRuleMean = 0, kRuleMedian = 1 };
 int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
-            int32_t* color_zero);
+            int32_t* color_zero, int rule = kRuleMean);
 int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color);
 int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known);
 int jp_color_run(Ctx& c, int32_t* color);

@@ -266,3 +266,58 @@ def test_timing_stats():
         assert st["kernel_launches"] > 10 and st["host_syncs"] >= 2
     finally:
         pgc.set_tuning("timing", 0)
+
+
+# ------------------------------------------------------------ ADG-M (NEXT-3) --
+def assert_parity_m(g, seed):
+    """JP-ADG-M through the C ABI against the ADG-M oracle + the JP oracle."""
+    pgc, off, col = dev(g)
+    rnd, color, T, K = pgc.color_jp_adg_m(off, col, seed)
+    torch.cuda.synchronize()
+    st = pgc.last_stats()
+    r_gpu, c_gpu = rnd.cpu().numpy(), color.cpu().numpy()
+    r_or, st_or = O.adg_m(g)
+    c_or, K_or = O.jp(g, r_or, seed)
+    assert T == st_or["T"] == (g.n.bit_length() if g.n else 0)
+    bad = np.nonzero(r_gpu != r_or)[0]
+    assert len(bad) == 0, f"ADG-M round mismatch at {bad[:10]} gpu={r_gpu[bad[:10]]} cpu={r_or[bad[:10]]}"
+    bad = np.nonzero(c_gpu != c_or)[0]
+    assert len(bad) == 0, f"color mismatch at {bad[:10]} gpu={c_gpu[bad[:10]]} cpu={c_or[bad[:10]]}"
+    assert K == K_or
+    assert st["sum_active"] == st_or["sum_active"] and st["cross_edges"] == st_or["cross_edges"]
+    # ADG-M alone gives the same rounds
+    r2, T2 = pgc.adg_m_order(off, col)
+    torch.cuda.synchronize()
+    assert T2 == T and np.array_equal(r2.cpu().numpy(), r_or)
+    return T, K
+
+
+def test_adg_m_hand_examples_and_small_graphs():
+    for c in json.load(open(os.path.join(GOLDEN, "adg_m_examples.json")))["cases"]:
+        g = gg.from_edges(c["n"], c["edges"])
+        T, K = assert_parity_m(g, 1)
+        assert T == c["T"]
+    for n in range(0, 6):
+        edges_all = list(all_graphs(n))
+        # disjoint union of every graph on n vertices (one GPU call)
+        es, base = [], 0
+        for edges in edges_all:
+            es += [(a + base, b + base) for a, b in edges]
+            base += n
+        assert_parity_m(gg.from_edges(base, es), 3)
+
+
+@pytest.mark.parametrize("name", ["er", "rmat", "grid", "clique", "edgeless"])
+def test_adg_m_random(name):
+    g = {"er": lambda: gg.er(20000, 160000, 5), "rmat": lambda: gg.rmat(15, 16, seed=2),
+         "grid": lambda: gg.grid(256, seed=4),
+         "clique": lambda: gg.from_edges(300, [(i, j) for i in range(300) for j in range(i + 1, 300)]),
+         "edgeless": lambda: gg.from_edges(1000, [])}[name]()
+    for seed in (1, 9):
+        assert_parity_m(g, seed)
+
+
+@pytest.mark.parametrize("cfg", ["rmat20", "rmat24"])
+def test_adg_m_full_size(cfg):
+    g = gg.config_graph(cfg)
+    assert_parity_m(g, 1)
