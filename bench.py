@@ -166,6 +166,23 @@ def ncu_traffic(kernel):
         return None
 
 
+# ------------------------------------------------------------- multi-GPU ----
+def reduce_max_ms(ms, dist, device):
+    """Step time of the whole job = the slowest rank (N independent replicas,
+    DESIGN.md "Multi-GPU"); identity without torch.distributed."""
+    if dist is None:
+        return ms
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(world, m, ms):
+    """Whole-job throughput: every rank colors its own copy of the graph."""
+    return world * m / (ms * 1e-3)
+
+
 # ------------------------------------------------------------------ arms ----
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -250,12 +267,8 @@ def run_pgc(args):
         torch.cuda.synchronize()
         if barrier:
             barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = reduce_max_ms(ev0.elapsed_time(ev1) / args.steps, dist, dev)
     st = pgc.last_stats()
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
 
     # ---- timed region B: same steps with per-launch CUDA events (attribution) ----
     pgc.set_tuning("timing", 1)
@@ -298,7 +311,7 @@ def run_pgc(args):
 
     out = {
         "metric": METRIC if not median else METRIC.replace("JP-ADG", "JP-ADG-M").replace("ADG+JP", "ADG-M+JP"),
-        "value": world * m / (ms * 1e-3), "unit": "edges/s", "n_gpus": world,
+        "value": job_value(world, m, ms), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": f"{args.config}-adgm" if median else f"{args.config}-eps{num}/{den}",
@@ -336,12 +349,8 @@ def run_pgc(args):
             pgc.color_jp_adg_host(h_off, h_col, num, den, args.seed, h_r, h_c)
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / args.steps
-        if dist:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        out["e2e"] = {"value": world * m / (ems * 1e-3), "unit": "edges/s",
+        ems = reduce_max_ms(e0.elapsed_time(e1) / args.steps, dist, dev)
+        out["e2e"] = {"value": job_value(world, m, ems), "unit": "edges/s",
                       "h2d_bytes_per_step": 8 * (n + 1) + 4 * nnz, "d2h_bytes_per_step": 8 * n,
                       "ms_per_step": ems}
         parity_ok = bool(torch.equal(h_r, rnd.cpu()) and torch.equal(h_c, color.cpu()))
