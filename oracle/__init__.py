@@ -38,6 +38,10 @@ def _load():
         lib.orc_splitmix64.argtypes = [u64]
         lib.orc_adg.restype = ctypes.c_int
         lib.orc_adg.argtypes = [i64, vp, vp, u32, u32, vp, vp, i64, vp, vp, vp]
+        lib.orc_adg_o.restype = ctypes.c_int
+        lib.orc_adg_o.argtypes = [i64, vp, vp, u32, u32, vp, vp, vp, vp]
+        lib.orc_jp_rho.restype = ctypes.c_int
+        lib.orc_jp_rho.argtypes = [i64, vp, vp, vp, vp]
         lib.orc_adg_m.restype = ctypes.c_int
         lib.orc_adg_m.argtypes = [i64, vp, vp, vp, vp]
         lib.orc_jp.restype = ctypes.c_int
@@ -86,6 +90,31 @@ def adg(g, num: int, den: int, per_round: bool = False):
         stats["S"] = ps[:T].copy()
         stats["nR"] = pr[:T].copy()
     return rnd, stats
+
+
+def adg_o(g, num: int, den: int):
+    """ADG-O.  Returns (round int32, rho int64, rank int64, drem int64, T)."""
+    off, col = _csr(g)
+    n = g.n
+    rnd = np.zeros(n, dtype=np.int32)
+    rho = np.zeros(n, dtype=np.int64)
+    rank = np.zeros(n, dtype=np.int64)
+    drem = np.zeros(n, dtype=np.int64)
+    T = _load().orc_adg_o(n, _p(off), _p(col), num, den, _p(rnd), _p(rho), _p(rank), _p(drem))
+    if T < 0:
+        raise ValueError("oracle adg_o: bad arguments")
+    return rnd, rho, rank, drem, int(T)
+
+
+def jp_rho(g, rho):
+    """JP colors for a total-order priority rho (int64, larger first).  Returns (color, K)."""
+    off, col = _csr(g)
+    rho = np.ascontiguousarray(rho, dtype=np.int64)
+    color = np.zeros(g.n, dtype=np.int32)
+    K = _load().orc_jp_rho(g.n, _p(off), _p(col), _p(rho), _p(color))
+    if K < 0:
+        raise ValueError("oracle jp_rho: bad arguments")
+    return color, int(K)
 
 
 def adg_m(g):

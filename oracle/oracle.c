@@ -242,6 +242,136 @@ ORC_EXPORT int orc_adg_m(int64_t n, const int64_t* off, const int32_t* col, int3
 }
 
 /* ------------------------------------------------------------------------ */
+/* ADG-O -- the listing "ADG-O, a variant of ADG with optimizations",
+ * PAPER.md:2397-2453 (sorting, 2231-2252; fused rank, 2257-2271):
+ *
+ *   D = [deg(v)];  U = V;  l = 0;  rho(v) = n for all v
+ *   while U != {}:
+ *     delta = (1/|U|) sum_{v in U} D[v]
+ *     PARTITION(U, (1+eps) delta): R = { u in U : D[u] <= (1+eps) delta }
+ *     SORT(R, D): increasing D
+ *     rho(r_i) = l + i   for r_i in R = [r_0 .. r_{|R|-1}]
+ *     U = U \ R
+ *     UPDATEandPRIORITIZE: for v in R, w in N(v) with rho(w) > rho(v):
+ *         D[w] -= 1; c += 1;  rank(v) = c
+ *     l = l + |R|
+ *
+ * The selection is Algorithm 1's (same exact integer test, Q1/Q2), so the
+ * rounds equal ADG's.  Reading Q22: SORT is stable in ascending
+ * id, i.e. R is ordered by (D ascending, id ascending).  rho is a total order
+ * (a permutation of 0..n-1), so JP needs no tie-break.  Outputs: round_out
+ * (1-based round, as Alg. 1), rho_out (int64), rank_out (int64, the number of
+ * neighbours with a higher rho = |pred(v)| for JP with rho), drem_out (D at
+ * selection time).  Returns T.                                              */
+static const int64_t* g_sortD;
+static int cmp_r_deg_id(const void* a, const void* b) {
+  int64_t u = *(const int64_t*)a, v = *(const int64_t*)b;
+  if (g_sortD[u] != g_sortD[v]) return g_sortD[u] < g_sortD[v] ? -1 : 1;
+  return u < v ? -1 : (u > v ? 1 : 0);
+}
+
+ORC_EXPORT int orc_adg_o(int64_t n, const int64_t* off, const int32_t* col, uint32_t num,
+                         uint32_t den, int32_t* round_out, int64_t* rho_out, int64_t* rank_out,
+                         int64_t* drem_out) {
+  if (n < 0 || num == 0 || den == 0) return -1;
+  int64_t* D = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  char* inU = (char*)malloc((size_t)n + 1);
+  int64_t* U = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* R = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t sizeU = n;
+  for (int64_t v = 0; v < n; ++v) {
+    D[v] = off[v + 1] - off[v];
+    inU[v] = 1;
+    U[v] = v;
+    rho_out[v] = n;        /* rho(v) = n: not yet removed */
+    round_out[v] = 0;
+  }
+  int64_t l = 0, it = 1;
+  while (sizeU > 0) {
+    uint64_t cnt = 0;
+    for (int64_t i = 0; i < sizeU; ++i) cnt += (uint64_t)D[U[i]];
+    /* PARTITION: R = { u in U : den*D[u]*|U| <= (den+num)*sum D } (exact) */
+    int64_t sizeR = 0, k = 0;
+    for (int64_t i = 0; i < sizeU; ++i) {
+      int64_t u = U[i];
+      unsigned __int128 lhs = (unsigned __int128)den * (uint64_t)D[u] * (uint64_t)sizeU;
+      unsigned __int128 rhs = ((unsigned __int128)den + num) * cnt;
+      if (lhs <= rhs) R[sizeR++] = u;
+      else U[k++] = u;
+    }
+    if (sizeR == 0) { free(D); free(inU); free(U); free(R); return -2; }
+    /* SORT(R, D): increasing D, ties by increasing id */
+    g_sortD = D;
+    qsort(R, (size_t)sizeR, sizeof(int64_t), cmp_r_deg_id);
+    for (int64_t i = 0; i < sizeR; ++i) {
+      rho_out[R[i]] = l + i;
+      round_out[R[i]] = (int32_t)it;
+      if (drem_out) drem_out[R[i]] = D[R[i]];
+      inU[R[i]] = 0;
+    }
+    sizeU = k;
+    /* UPDATEandPRIORITIZE(D, U, R, rank) */
+    for (int64_t i = 0; i < sizeR; ++i) {
+      int64_t v = R[i], c = 0;
+      for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+        int64_t w = col[e];
+        if (rho_out[w] > rho_out[v]) {
+          D[w] -= 1;
+          c += 1;
+        }
+      }
+      if (rank_out) rank_out[v] = c;
+    }
+    l += sizeR;
+    it += 1;
+  }
+  free(D);
+  free(inU);
+  free(U);
+  free(R);
+  return (int)(it - 1);
+}
+
+/* JP (Algorithm 3) for a total-order priority rho
+ * (int64, larger = higher priority), e.g. rho_ADG-O: sequential greedy in
+ * decreasing rho, GetColor (1135-1138) from the already colored preds.     */
+static const int64_t* g_rho;
+static int cmp_rho_desc(const void* a, const void* b) {
+  int64_t u = *(const int64_t*)a, v = *(const int64_t*)b;
+  return g_rho[u] > g_rho[v] ? -1 : (g_rho[u] < g_rho[v] ? 1 : 0);
+}
+
+ORC_EXPORT int orc_jp_rho(int64_t n, const int64_t* off, const int32_t* col, const int64_t* rho,
+                          int32_t* color_out) {
+  if (n < 0) return -1;
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t v = 0; v < n; ++v) order[v] = v;
+  g_rho = rho;
+  qsort(order, (size_t)n, sizeof(int64_t), cmp_rho_desc);
+  int64_t* stamp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 2));
+  for (int64_t i = 0; i < n + 2; ++i) stamp[i] = -1;
+  for (int64_t v = 0; v < n; ++v) color_out[v] = 0;
+  int32_t K = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t v = order[i], npred = 0;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+      int64_t u = col[e];
+      if (rho[u] > rho[v]) {
+        npred += 1;
+        stamp[color_out[u]] = i;
+      }
+    }
+    int64_t c = 1;
+    while (c <= npred + 1 && stamp[c] == i) ++c;
+    color_out[v] = (int32_t)c;
+    if (c > K) K = (int32_t)c;
+  }
+  free(order);
+  free(stamp);
+  return K;
+}
+
+/* ------------------------------------------------------------------------ */
 /* JP priority rho = <rho_ADG, rho_R>, lexicographic (PAPER.md:1073-1078,
  * 1095-1096): u has higher priority than v iff
  *   round[u] > round[v], or round[u] == round[v] and h(u) > h(v),

@@ -253,3 +253,40 @@ def approx4_ok(g, rnd, d):
     dst = g.col.astype(np.int64)
     up = np.bincount(src[rnd[dst] >= rnd[src]], minlength=g.n)
     return bool((up <= 4 * d).all())
+
+
+# ---------------------------------------------------------------- ADG-O -----
+def residual_at_removal(g, rnd):
+    """D_rem(v) = |N(v) ∩ U_round(v)|: the residual degree v had when its round
+    selected it (U_l = {u : round[u] >= l})."""
+    rnd = np.asarray(rnd, dtype=np.int64)
+    src = np.repeat(np.arange(g.n), np.diff(g.off))
+    dst = g.col.astype(np.int64)
+    return np.bincount(src[rnd[dst] >= rnd[src]], minlength=g.n)
+
+
+def adg_o_rho_check(g, rnd, rho):
+    """rho_ADG-O (reading Q22) is the removal order: rounds in
+    increasing order, inside a round increasing (D_rem, id); a permutation."""
+    n = g.n
+    rho = np.asarray(rho, dtype=np.int64)
+    if not np.array_equal(np.sort(rho), np.arange(n)):
+        return "rho is not a permutation of 0..n-1"
+    dr = residual_at_removal(g, rnd)
+    order = np.lexsort((np.arange(n), dr, np.asarray(rnd, dtype=np.int64)))
+    if not np.array_equal(rho[order], np.arange(n)):
+        return "rho is not the (round, D_rem, id) order"
+    return None
+
+
+def jp_certificate_rho(g, rho, color):
+    """Alg. 3's GetColor fixed point for a total-order priority rho (larger first)."""
+    adj = adjacency(g)
+    for v in range(g.n):
+        used = {int(color[u]) for u in adj[v] if rho[u] > rho[v]}
+        c = 1
+        while c in used:
+            c += 1
+        if int(color[v]) != c:
+            return f"vertex {v}: color {int(color[v])}, GetColor gives {c}"
+    return None
