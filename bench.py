@@ -49,8 +49,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline (for ncu runs)")
-    ap.add_argument("--method", choices=["jp-adg", "jp-adg-m"], default="jp-adg",
-                    help="jp-adg-m: the median variant (SURVEY.md §8(f) NEXT-3, PAPER.md:2273-2303)")
+    ap.add_argument("--method", choices=["jp-adg", "jp-adg-m", "jp-adg-o"], default="jp-adg",
+                    help="jp-adg-m: the median variant (SURVEY.md §8(f) NEXT-3, PAPER.md:2273-2303); "
+                         "jp-adg-o: ADG-O's total order (NEXT-1, PAPER.md:2397-2453)")
     return ap.parse_args()
 
 
@@ -240,10 +241,13 @@ def run_pgc(args):
     color = torch.empty(n, dtype=torch.int32, device=dev)
 
     median = args.method == "jp-adg-m"
+    sortedR = args.method == "jp-adg-o"
 
     def step():
         if median:
             return pgc.color_jp_adg_m(off, col, args.seed, round_out=rnd, color_out=color)
+        if sortedR:
+            return pgc.color_jp_adg_o(off, col, num, den, round_out=rnd, color_out=color)
         return pgc.color_jp_adg(off, col, num, den, args.seed, round_out=rnd, color_out=color)
 
     pgc.set_tuning("timing", 0)
@@ -310,11 +314,13 @@ def run_pgc(args):
         pass
 
     out = {
-        "metric": METRIC if not median else METRIC.replace("JP-ADG", "JP-ADG-M").replace("ADG+JP", "ADG-M+JP"),
+        "metric": (METRIC.replace("JP-ADG", "JP-ADG-M").replace("ADG+JP", "ADG-M+JP") if median else
+                   METRIC.replace("JP-ADG", "JP-ADG-O").replace("ADG+JP", "ADG-O+JP") if sortedR else METRIC),
         "value": job_value(world, m, ms), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.config}-adgm" if median else f"{args.config}-eps{num}/{den}",
+        "config": {"workload": f"{args.config}-adgm" if median else
+                   f"{args.config}-adgo-eps{num}/{den}" if sortedR else f"{args.config}-eps{num}/{den}",
                    "method": args.method, "n": n, "m": m, "nnz": nnz,
                    "eps": f"{num}/{den}", "seed": args.seed, "graph_seed": 1,
                    "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
@@ -334,7 +340,7 @@ def run_pgc(args):
     }
 
     # ---- end to end through the host-buffer C-ABI call ----
-    if not (args.no_e2e or args.quick or median):
+    if not (args.no_e2e or args.quick or median or sortedR):
         h_off = torch.from_numpy(g.off).pin_memory()
         h_col = torch.from_numpy(g.col).pin_memory()
         h_r = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -360,9 +366,12 @@ def run_pgc(args):
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
         import oracle as O
         t0 = time.perf_counter()
-        r_or, _ = O.adg_m(g) if median else O.adg(g, num, den)
+        if sortedR:
+            r_or, rho, _, _, _ = O.adg_o(g, num, den)
+        else:
+            r_or, _ = O.adg_m(g) if median else O.adg(g, num, den)
         t1 = time.perf_counter()
-        c_or, K_or = O.jp(g, r_or, args.seed)
+        c_or, K_or = O.jp_rho(g, rho) if sortedR else O.jp(g, r_or, args.seed)
         t2 = time.perf_counter()
         out["cpu_baseline"] = {"value": m / (t2 - t0), "unit": "edges/s", "cores": 1,
                                "kind": "oracle",

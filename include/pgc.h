@@ -154,6 +154,21 @@ int pgc_color_jp_adg_m(const pgc_graph* g, uint64_t seed, int32_t* round_out, in
                        int32_t* num_rounds, int32_t* num_colors, void* workspace,
                        size_t workspace_bytes, void* cuda_stream);
 
+/* JP-ADG-O: the ADG-O listing (explicit ordering of R,
+ * 2231-2252) then JP with its total order rho_ADG-O.  The rounds are ADG's
+ * (same eps rule); inside a round R is sorted by increasing residual degree
+ * at selection, ties by increasing id (reading Q22), and rho(v) = its position
+ * in the concatenated removal order.  JP gives the higher rho priority (no
+ * random tie-break); JP Part 1 is fused into UPDATE (UPDATEandPRIORITIZE,
+ * PAPER.md:2440-2452).
+ *   round_out, color_out : device int32[n]
+ *   num_rounds, num_colors : host int32*
+ * PGC_EINVAL also if the sum over rounds of (max residual degree at selection
+ * + 1) exceeds n + 65536 (the priority-order key range). */
+int pgc_color_jp_adg_o(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int32_t* round_out,
+                       int32_t* color_out, int32_t* num_rounds, int32_t* num_colors,
+                       void* workspace, size_t workspace_bytes, void* cuda_stream);
+
 /* JP-ADG end to end from HOST memory: copies the CSR host->device on
  * `cuda_stream`, runs pgc_color_jp_adg, copies round[] and color[] back.
  * Host buffers should be pinned (cudaHostAlloc) for full copy bandwidth.

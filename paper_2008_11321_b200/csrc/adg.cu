@@ -146,7 +146,8 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
 }
 
 // Arc classifier.  MODE 0: ADG only; 1: ADG with fused JP Part 1; 2: JP Part 1
-// for an arbitrary first key (pgc_jp_color).
+// for an arbitrary first key (pgc_jp_color); 3: ADG with fused JP Part 1 for
+// ADG-O's total order (round, D_rem, id) (UPDATEandPRIORITIZE).
 template <int MODE>
 struct Arc {
   int l;
@@ -172,6 +173,13 @@ struct Arc {
   }
   __device__ __forceinline__ int state(int u) const { return decode(u, raw(u)); }
   __device__ __forceinline__ int gather(int u) const { return state(u); }
+  // v's own second key: rho_R(v) (MODES 1, 2) or (D_rem[v], v) packed (MODE 3;
+  // D of a vertex removed this round no longer changes: only alive vertices
+  // are decremented)
+  __device__ __forceinline__ uint64_t own(int v) const {
+    if (MODE == 3) return (((uint64_t)(uint32_t)D[v]) << 32) | (uint32_t)v;
+    return prio_hash(seed, (uint32_t)v);
+  }
   // true iff u in pred(v); performs UPDATE's decrement and counts cut arcs.
   // g = gather(u).
   __device__ __forceinline__ bool classify(int u, int g, int rv, uint64_t hv,
@@ -184,9 +192,10 @@ struct Arc {
     if (su == 0) {                      // u in U \ R: DecrementAndFetch(D[u])
       red_dec_keep(&D[u]);              // result unused -> RED
       cut += 1;
-      return MODE == 1;                 // u gets a later round: higher priority
+      return MODE == 1 || MODE == 3;    // u gets a later round: higher priority
     }
     if (MODE == 1 && su == 1) return prio_hash(seed, (uint32_t)u) > hv;  // same round: hash
+    if (MODE == 3 && su == 1) return own(u) > hv;  // same round: (D_rem, id)
     return false;                       // removed earlier: lower priority
   }
 };
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(256, PGC_LIGHT_MINB) k_update_light(Arc<MODE> 
     const int v = r.x, deg = r.y;
     const long long o = lo_hi(r.z, r.w);
     const int rv = (MODE == 2 && valid) ? A.round[v] : 0;
-    const uint64_t hv = (MODE != 0 && valid) ? prio_hash(A.seed, (uint32_t)v) : 0;
+    const uint64_t hv = (MODE != 0 && valid) ? A.own(v) : 0;
     int incl = deg;
 #pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
@@ -365,7 +374,7 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
     const long long s = lo_hi(__shfl_sync(0xffffffffu, r0.z, 0), __shfl_sync(0xffffffffu, r0.w, 0));
     const long long o = lo_hi(__shfl_sync(0xffffffffu, r0.x, 1), __shfl_sync(0xffffffffu, r0.y, 1));
     const long long e = s + len;
-    const uint64_t hv = MODE != 0 ? prio_hash(A.seed, (uint32_t)v) : 0;
+    const uint64_t hv = MODE != 0 ? A.own(v) : 0;
     const int rv = MODE == 2 ? A.round[v] : 0;
     for (long long s0 = s; s0 < e; s0 += kSub) {
       const long long e0 = min(e, s0 + kSub);
@@ -495,7 +504,7 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
     const long long s = lo_hi(__shfl_sync(0xffffffffu, r0.z, 0), __shfl_sync(0xffffffffu, r0.w, 0));
     const long long o = lo_hi(__shfl_sync(0xffffffffu, r0.x, 1), __shfl_sync(0xffffffffu, r0.y, 1));
     const long long e = s + len;
-    const uint64_t hv = MODE != 0 ? prio_hash(A.seed, (uint32_t)v) : 0;
+    const uint64_t hv = MODE != 0 ? A.own(v) : 0;
     for (long long s0 = s; s0 < e; s0 += kFilterSub) {
       const long long e0 = min(e, s0 + kFilterSub);
       int cnt = 0;
@@ -778,6 +787,8 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                                                 c.tune.filter_ratio));
       if (mode == kAdgFused) {
         if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs}, Uin)) return e;
+      } else if (mode == kAdgFusedO) {
+        if (int e = launch_update(c, Arc<3>{l, seed, round, c.D, c.rs}, Uin)) return e;
       } else {
         if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs}, Uin)) return e;
       }
@@ -789,6 +800,80 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
     if (c.h_state->done) break;
     if ((int64_t)l > c.n + 2) return fail(4, "ADG did not terminate within n rounds");
   }
+  return 0;
+}
+
+// ADG-O's priority as one int32 key per vertex for the order: key1[v] =
+// goff[round[v]] + D_rem[v], goff[r] = sum over earlier rounds r' of
+// (max D_rem in r' + 1); with the id as the second key (Key2::idkey) the
+// order is (round, D_rem, id) descending = rho_ADG-O descending (Q22).
+__global__ void k_o_dmax(int64_t n, const int32_t* __restrict__ round, const int32_t* __restrict__ D,
+                         int32_t* __restrict__ dmaxr) {
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x; v0 < n; v0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = v0 + threadIdx.x;
+    const int r = v < n ? round[v] : -1;
+    const int d = v < n ? D[v] : 0;
+    const unsigned peers = __match_any_sync(0xffffffffu, r);
+    const int dm = __reduce_max_sync(peers, d);
+    if (r >= 0 && lane_id() == __ffs(peers) - 1) atomicMax(&dmaxr[r], dm);
+  }
+}
+// one block: goff[r] = exclusive prefix of (dmaxr[r] + 1) over r = 1..T
+__global__ void __launch_bounds__(1024) k_o_goff(int T, const int32_t* __restrict__ dmaxr,
+                                                 int32_t* __restrict__ goff, State* st) {
+  __shared__ long long s_w[32];
+  __shared__ long long s_carry;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) s_carry = 0;
+  __syncthreads();
+  for (int r0 = 1; r0 <= T; r0 += 1024) {
+    const int r = r0 + t;
+    const long long x = r <= T ? (long long)dmaxr[r] + 1 : 0;
+    long long incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const long long w = s_w[lane];
+      long long wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_w[lane] = wi - w;
+    }
+    __syncthreads();
+    const long long ex = s_carry + s_w[warp] + incl - x;
+    if (r <= T) goff[r] = ex > 0x7fffffffLL ? 0x7fffffff : (int)ex;
+    __syncthreads();
+    if (t == 1023) s_carry = ex + x;
+    __syncthreads();
+  }
+  if (t == 0 && s_carry > 0x7fffffffLL) st->err = 6;  // key range does not fit int32
+}
+__global__ void k_o_key(int64_t n, const int32_t* __restrict__ round, const int32_t* __restrict__ D,
+                        const int32_t* __restrict__ goff, int32_t* __restrict__ key1) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    key1[v] = goff[round[v]] + D[v];
+}
+
+int adg_o_keys(Ctx& c, const int32_t* round, int32_t* key1) {
+  const int T = c.h_state->T;
+  if (c.n == 0) return 0;
+  // the order's histogram space (2(n + 65536) ints >= 2(T + 2)) is free until jp_order_run
+  int32_t* dmaxr = c.hist1;
+  int32_t* goff = c.hist1 + T + 2;
+  const int G = grid_for(c, 8);
+  PGC_LAUNCH(c, kGOrder, "k_zero_i32", k_zero_i32<<<G, 256, 0, c.st>>>(dmaxr, (int64_t)T + 2));
+  PGC_LAUNCH(c, kGOrder, "k_o_dmax", k_o_dmax<<<G, 256, 0, c.st>>>(c.n, round, c.D, dmaxr));
+  PGC_LAUNCH(c, kGOrder, "k_o_goff", k_o_goff<<<1, 1024, 0, c.st>>>(T, dmaxr, goff, c.state));
+  PGC_LAUNCH(c, kGOrder, "k_o_key", k_o_key<<<G, 256, 0, c.st>>>(c.n, round, c.D, goff, key1));
   return 0;
 }
 

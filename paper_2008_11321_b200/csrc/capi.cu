@@ -349,6 +349,35 @@ int pgc_color_jp_adg_m(const pgc_graph* g, uint64_t seed, int32_t* round_out, in
   return PGC_OK;
 }
 
+int pgc_color_jp_adg_o(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int32_t* round_out,
+                       int32_t* color_out, int32_t* num_rounds, int32_t* num_colors,
+                       void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (eps_num == 0 || eps_den == 0) return fail(PGC_EINVAL, "eps must be num/den with num, den >= 1");
+  if (!num_rounds || !num_colors || (g->n > 0 && (!round_out || !color_out)))
+    return fail(PGC_EINVAL, "output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  if (int e = adg_run(c, eps_num, eps_den, 0, round_out, kAdgFusedO, color_out)) return e;
+  const int T = c.h_state->T;
+  const long long sum_active = c.h_state->sum_active;
+  const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
+  int32_t* key1 = c.U[0];  // ADG's lists are free after the last round
+  if (int e = adg_o_keys(c, round_out, key1)) return e;
+  if (int e = jp_order_run(c, key1, 0, false, true)) return e;
+  if (c.h_state->err == 6)
+    return fail(PGC_EINVAL, "ADG-O: sum over rounds of (max residual degree + 1) exceeds INT32_MAX");
+  c.round_key = round_out;  // the bulk's watch heuristic (never a result)
+  c.seed = 0;
+  if (int e = jp_color_run(c, color_out)) return e;
+  *num_rounds = T;
+  *num_colors = c.h_state->K;
+  call_end(c, T, c.h_state->K, sum_active, cross, preds, c.core_n);
+  return PGC_OK;
+}
+
 size_t pgc_host_workspace_bytes(int64_t n, int64_t nnz) {
   if (!sizes_ok(n, nnz)) return 0;
   return a256(8 * (size_t)(n + 1)) + a256(4 * (size_t)nnz) + 2 * a256(4 * (size_t)n) +

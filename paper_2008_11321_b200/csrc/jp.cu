@@ -243,18 +243,31 @@ __global__ void k_bucket_sizes(int L, const int32_t* __restrict__ hist1, int32_t
     bsz[i] = bucket_count_for(hist1[i]);
 }
 
-__device__ __forceinline__ int bucket_of(int v, int r, uint64_t seed, int rmax,
+// Second priority key: rho_R(v) = splitmix64(seed ^ v) (JP-ADG, JP-ADG-M,
+// pgc_jp_color), or the id itself for ADG-O's total order (Q22: inside a
+// (round, D_rem) group the larger id has the larger rho), shifted so that the
+// ids 0..n-1 span the top bits the buckets are indexed by (idkey = 64 minus
+// the bit length of n-1; 0 selects the hash).
+struct Key2 {
+  uint64_t seed;
+  int idkey;
+  __device__ __forceinline__ uint64_t operator()(uint32_t v) const {
+    return idkey ? ((uint64_t)v << idkey) : prio_hash(seed, v);
+  }
+};
+
+__device__ __forceinline__ int bucket_of(int v, int r, Key2 seed, int rmax,
                                          const int32_t* __restrict__ hist1,
                                          const int32_t* __restrict__ base1) {
   const int k = rmax - r;
   const int B = bucket_count_for(hist1[k]);
   const int lg = 31 - __clz(B);
-  const uint64_t h = prio_hash(seed, (uint32_t)v);
+  const uint64_t h = seed((uint32_t)v);
   const int hb = lg ? (int)(h >> (64 - lg)) : 0;
   return base1[k] + (B - 1 - hb);  // larger hash -> earlier bucket
 }
 
-__global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, uint64_t seed,
+__global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, Key2 seed,
                         const int32_t* __restrict__ npred,
                         const State* st, const int32_t* __restrict__ hist1,
                         const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt) {
@@ -270,7 +283,7 @@ __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, uint64_t s
 // Places every vertex's JP work record {v, |pred|, P slot lo, hi} at its
 // bucket position (the per-vertex inputs are read coalesced here, once, so the
 // JP workers fetch one 16-byte record per vertex).
-__global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, uint64_t seed,
+__global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 seed,
                           const State* st, const int32_t* __restrict__ hist1,
                           const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
                           const int32_t* __restrict__ bstart, const int32_t* __restrict__ npred,
@@ -300,7 +313,7 @@ constexpr int kLaneSortMax = 12;
 // so the highest-priority uncolored vertex is always held or grabbable.
 constexpr int kMaxUnsortedBucket = 64;
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
-                              int4* __restrict__ rec, uint64_t seed, int limit) {
+                              int4* __restrict__ rec, Key2 seed, int limit) {
   const int lane = lane_id();
   const int nb = st->nbuckets;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -320,7 +333,7 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
       for (int i = 0; i < kLaneSortMax; ++i)
         if (i < s) {
           vv[i] = rec[s0 + i];
-          hh[i] = prio_hash(seed, (uint32_t)vv[i].x);
+          hh[i] = seed((uint32_t)vv[i].x);
         }
 #pragma unroll
       for (int i = 1; i < kLaneSortMax; ++i) {
@@ -352,7 +365,7 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
       const int bs = __shfl_sync(0xffffffffu, s, src);
       if (bs <= 32) {
         const int4 v = lane < bs ? rec[bs0 + lane] : make_int4(0, 0, 0, 0);
-        const uint64_t h = lane < bs ? prio_hash(seed, (uint32_t)v.x) : 0;
+        const uint64_t h = lane < bs ? seed((uint32_t)v.x) : 0;
         int rank = 0;
         for (int j = 0; j < bs; ++j) rank += __shfl_sync(0xffffffffu, h, j) > h;
         __syncwarp();
@@ -361,9 +374,9 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
       } else if (lane == 0) {  // very rare: insertion sort in place
         for (int i = 1; i < bs; ++i) {
           const int4 x = rec[bs0 + i];
-          const uint64_t hx = prio_hash(seed, (uint32_t)x.x);
+          const uint64_t hx = seed((uint32_t)x.x);
           int j = i - 1;
-          while (j >= 0 && prio_hash(seed, (uint32_t)rec[bs0 + j].x) < hx) {
+          while (j >= 0 && seed((uint32_t)rec[bs0 + j].x) < hx) {
             rec[bs0 + j + 1] = rec[bs0 + j];
             --j;
           }
@@ -385,7 +398,14 @@ __global__ void k_order_setup(State* st, int rmax_host, int use_host) {
   st->n_order = 0;
 }
 
-int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known) {
+int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known, bool idkey) {
+  int idshift = 0;
+  if (idkey) {
+    int bits = 1;
+    while (bits < 63 && ((int64_t)1 << bits) < c.n) ++bits;  // bit length of n - 1
+    idshift = 64 - bits;
+  }
+  const Key2 seed{seed_, idshift};
   const int G = c.nsm * 8;
   if (c.n == 0) return 0;
   int rmin, rmax;

@@ -131,14 +131,16 @@ constexpr int kFilterBytes = 192 * 1024;
 constexpr int kFilterWords = kFilterBytes / 4;
 
 // ---- phases (host orchestration; return 0 or a PGC_* code) -----------------
-enum AdgMode { kAdgOnly = 0, kAdgFused = 1 };
+// kAdgFusedO: JP Part 1 for ADG-O's total order (round, D_rem, id) (Q22)
+enum AdgMode { kAdgOnly = 0, kAdgFused = 1, kAdgFusedO = 3 };
 // selection rule of a round: ADG's mean threshold (Alg. 1) or ADG-M's median
 //
 enum AdgRule { kRuleMean = 0, kRuleMedian = 1 };
 int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
             int32_t* color_zero, int rule = kRuleMean);
 int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color);
-int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known);
+int adg_o_keys(Ctx& c, const int32_t* round, int32_t* key1);
+int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known, bool idkey = false);
 int jp_color_run(Ctx& c, int32_t* color);
 int check_graph_run(Ctx& c, int64_t* bad_vertex);
 

@@ -321,3 +321,53 @@ def test_adg_m_random(name):
 def test_adg_m_full_size(cfg):
     g = gg.config_graph(cfg)
     assert_parity_m(g, 1)
+
+
+# ------------------------------------------------------------ ADG-O (NEXT-1) --
+def assert_parity_o(g, num, den):
+    """JP-ADG-O through the C ABI against the ADG-O oracle + JP for rho."""
+    pgc, off, col = dev(g)
+    rnd, color, T, K = pgc.color_jp_adg_o(off, col, num, den)
+    torch.cuda.synchronize()
+    st = pgc.last_stats()
+    r_gpu, c_gpu = rnd.cpu().numpy(), color.cpu().numpy()
+    r_or, rho, rank, drem, T_or = O.adg_o(g, num, den)
+    c_or, K_or = O.jp_rho(g, rho)
+    assert T == T_or
+    bad = np.nonzero(r_gpu != r_or)[0]
+    assert len(bad) == 0, f"round mismatch at {bad[:10]}"
+    bad = np.nonzero(c_gpu != c_or)[0]
+    assert len(bad) == 0, f"ADG-O color mismatch at {bad[:10]} gpu={c_gpu[bad[:10]]} cpu={c_or[bad[:10]]}"
+    assert K == K_or
+    assert st["pred_arcs"] == g.m   # every edge gives exactly one pred (a total order)
+    return T, K
+
+
+def test_adg_o_hand_examples_and_small_graphs():
+    for c in json.load(open(os.path.join(GOLDEN, "adg_o_examples.json")))["cases"]:
+        g = gg.from_edges(c["n"], c["edges"])
+        T, K = assert_parity_o(g, *c["eps"])
+        assert K == c["K"]
+    for n in range(0, 6):
+        es, base = [], 0
+        for edges in all_graphs(n):
+            es += [(a + base, b + base) for a, b in edges]
+            base += n
+        for num, den in [(1, 10), (1, 2)]:
+            assert_parity_o(gg.from_edges(base, es), num, den)
+
+
+@pytest.mark.parametrize("name", ["er", "rmat", "grid", "clique", "edgeless"])
+def test_adg_o_random(name):
+    g = {"er": lambda: gg.er(20000, 160000, 5), "rmat": lambda: gg.rmat(15, 16, seed=2),
+         "grid": lambda: gg.grid(256, seed=4),
+         "clique": lambda: gg.from_edges(300, [(i, j) for i in range(300) for j in range(i + 1, 300)]),
+         "edgeless": lambda: gg.from_edges(1000, [])}[name]()
+    for num, den in [(1, 100), (1, 10), (1, 2)]:
+        assert_parity_o(g, num, den)
+
+
+@pytest.mark.parametrize("cfg", ["rmat20", "rmat24"])
+def test_adg_o_full_size(cfg):
+    g = gg.config_graph(cfg)
+    assert_parity_o(g, *gg.CONFIGS[cfg][1][0])
