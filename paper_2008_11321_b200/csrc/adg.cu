@@ -182,8 +182,14 @@ struct Arc {
   }
   // true iff u in pred(v); performs UPDATE's decrement and counts cut arcs.
   // g = gather(u).
+  // MODE 3: a same-round neighbour's D_rem, loaded for a whole strip before
+  // any classify (a load consumed in its own branch would serialise)
+  __device__ __forceinline__ int same_round_d(int u, int g) const {
+    if (MODE != 3) return 0;
+    return g == 1 ? D[u] : 0;
+  }
   __device__ __forceinline__ bool classify(int u, int g, int rv, uint64_t hv,
-                                          unsigned long long& cut) const {
+                                          unsigned long long& cut, int du = 0) const {
     if (MODE == 2) {
       if (g != rv) return g > rv;
       return prio_hash(seed, (uint32_t)u) > hv;
@@ -195,7 +201,8 @@ struct Arc {
       return MODE == 1 || MODE == 3;    // u gets a later round: higher priority
     }
     if (MODE == 1 && su == 1) return prio_hash(seed, (uint32_t)u) > hv;  // same round: hash
-    if (MODE == 3 && su == 1) return own(u) > hv;  // same round: (D_rem, id)
+    if (MODE == 3 && su == 1)  // same round: (D_rem, id)
+      return ((((uint64_t)(uint32_t)du) << 32) | (uint32_t)u) > hv;
     return false;                       // removed earlier: lower priority
   }
 };
@@ -288,12 +295,15 @@ __global__ void __launch_bounds__(256, PGC_LIGHT_MINB) k_update_light(Arc<MODE> 
       for (int k = 0; k < kLStrips; ++k) gs[k] = A.raw(u[k]);  // all gathers in flight
 #pragma unroll
       for (int k = 0; k < kLStrips; ++k) gs[k] = A.decode(u[k], gs[k]);
+      int du[kLStrips];
+#pragma unroll
+      for (int k = 0; k < kLStrips; ++k) du[k] = A.same_round_d(u[k], gs[k]);
 #pragma unroll
       for (int k = 0; k < kLStrips; ++k) {
         const int ts = t0 + 32 * k;  // first arc of this strip
         const uint64_t oh = MODE != 0 ? __shfl_sync(0xffffffffu, hv, ow[k]) : 0;
         const int orv = MODE == 2 ? __shfl_sync(0xffffffffu, rv, ow[k]) : 0;
-        const bool pred = u[k] >= 0 && A.classify(u[k], gs[k], orv, oh, cut);
+        const bool pred = u[k] >= 0 && A.classify(u[k], gs[k], orv, oh, cut, du[k]);
         if (MODE != 0) {
           const unsigned pb = __ballot_sync(0xffffffffu, pred);
           const int base = __shfl_sync(0xffffffffu, cnt, ow[k]);
@@ -391,9 +401,12 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
         for (int k = 0; k < kStrips; ++k) g[k] = A.raw(u[k]);  // all gathers in flight
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) g[k] = A.decode(u[k], g[k]);
+        int du[kStrips];
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) du[k] = A.same_round_d(u[k], g[k]);
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) {
-          const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut);
+          const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut, du[k]);
           if (MODE != 0) {
             const unsigned bal = __ballot_sync(0xffffffffu, pred);
             if (pred) s_buf[warp][cnt + __popc(bal & lanemask_lt())] = u[k];
@@ -526,9 +539,12 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
         for (int k = 0; k < kStrips; ++k) g[k] = hit[k] ? A.raw(u[k]) : 0;
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) g[k] = hit[k] ? A.decode(u[k], g[k]) : 2;  // miss: earlier
+        int du[kStrips];
+#pragma unroll
+        for (int k = 0; k < kStrips; ++k) du[k] = A.same_round_d(u[k], g[k]);
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) {
-          const bool pred = u[k] >= 0 && A.classify(u[k], g[k], 0, hv, cut);
+          const bool pred = u[k] >= 0 && A.classify(u[k], g[k], 0, hv, cut, du[k]);
           if (MODE != 0) {
             const unsigned bal = __ballot_sync(0xffffffffu, pred);
             if (pred) s_buf[cnt + __popc(bal & lanemask_lt())] = u[k];
