@@ -15,6 +15,8 @@
 //                  npred[v] = |pred(v)| (= count[v] of Alg. 3).
 //   k_adg_finalize S_{l+1} = S_l - sum_{R_l} D - cut_l; |U_{l+1}| = |U_l| - |R_l|.
 #include <cstdio>
+#include <utility>
+#include <vector>
 
 #include "pgc_internal.cuh"
 
@@ -573,54 +575,71 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
 
 // ADG-M's median (readings Q19-Q21): the ceil(|U|/2)-th
 // smallest key (D[v] << 32) | v over U by a radix select, most significant
-// digit first (digits of 11,11,11,11,11,9 bits), each pass a shared-memory
-// histogram of the keys that match the digits found so far, then one block
-// picks the digit holding the wanted rank.  Keys are distinct (the id is in
-// the low word), so R = {v in U : key <= selected key} has exactly
-// ceil(|U|/2) vertices: the first half of U in (D, id) order.
-constexpr int kMselPasses = 6;
-constexpr int kMselBins = 2048;
-__device__ __forceinline__ void msel_geom(int pass, int& shift, int& bits) {
-  bits = pass == kMselPasses - 1 ? 9 : 11;
-  shift = 64 - 11 * (pass + 1);
-  if (shift < 0) shift = 0;
+// digit first.  Only bits that can be nonzero are visited: the D field's
+// bit length comes from the maximum degree, the id field's from n - 1, in
+// digits of <= 12 bits (so R-MAT 24 needs 2 + 2 passes).  A pass is ONE
+// kernel: every block histograms the keys that match the bits found so far
+// (shared memory), adds it to the global histogram, and the last block to
+// finish picks the digit holding the wanted rank and clears the histogram.
+// Keys are distinct (the id is in the low word), so R = {v in U : key <=
+// selected key} has exactly ceil(|U|/2) vertices: the first half of U in
+// (D, id) order.
+constexpr int kMselBits = 12;
+constexpr int kMselBins = 1 << kMselBits;
+__global__ void k_maxdeg(int64_t n, const int64_t* __restrict__ off, State* st) {
+  int m = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (int)(off[v + 1] - off[v]));
+  m = warp_max(m);
+  if (lane_id() == 0 && m) atomicMax(&st->maxdeg, m);
 }
-__global__ void __launch_bounds__(1024) k_msel_hist(int pass, const int32_t* __restrict__ Uin,
+__global__ void __launch_bounds__(1024) k_msel_pass(int first, int shift, int bits,
+                                                    const int32_t* __restrict__ Uin,
                                                     const int32_t* __restrict__ D,
-                                                    int32_t* __restrict__ hist, const State* st) {
+                                                    int32_t* __restrict__ hist, State* st) {
   __shared__ int sh[kMselBins];
+  __shared__ long long s_w[32];
+  __shared__ int s_last, s_digit;
+  __shared__ long long s_before;
   if (st->done) return;
-  int shift, bits;
-  msel_geom(pass, shift, bits);
-  const unsigned long long prefix = st->msel_key;
+  const unsigned long long pkey = st->msel_key, pmask = st->msel_mask;
+  const unsigned dmask = (1u << bits) - 1u;
   for (int i = threadIdx.x; i < kMselBins; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const long long nU = st->nU;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nU;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int v = Uin ? Uin[i] : (int)i;
-    const unsigned long long key = (((unsigned long long)(uint32_t)ld_i32_keep(D + v)) << 32) | (uint32_t)v;
-    if (pass == 0 || (key >> (shift + bits)) == prefix)
-      atomicAdd(&sh[(int)(key >> shift) & ((1 << bits) - 1)], 1);
+  for (long long i0 = blockIdx.x * (long long)blockDim.x; i0 < nU; i0 += (long long)gridDim.x * blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    int bin = -1;
+    if (i < nU) {
+      const int v = Uin ? Uin[i] : (int)i;
+      const unsigned long long key = (((unsigned long long)(uint32_t)ld_i32_keep(D + v)) << 32) | (uint32_t)v;
+      if ((key & pmask) == pkey) bin = (int)((unsigned)(key >> shift) & dmask);
+    }
+    // degrees concentrate on few bins: one shared atomic per distinct bin per warp
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && lane_id() == __ffs(peers) - 1) atomicAdd(&sh[bin], __popc(peers));
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kMselBins; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-// One block of 1024 threads, two bins per thread: block scan of the histogram,
-// the digit whose inclusive count first reaches the rank, then the histogram
-// is cleared for the next pass.
-__global__ void __launch_bounds__(1024) k_msel_pick(int pass, int32_t* __restrict__ hist, State* st) {
-  __shared__ long long s_w[32];
-  __shared__ int s_digit;
-  __shared__ long long s_before;
-  if (st->done) return;
-  int shift, bits;
-  msel_geom(pass, shift, bits);
-  const long long rank = pass == 0 ? (st->nU + 1) / 2 : st->msel_rank;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&st->msel_done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  // last block: block scan of the histogram (4 bins per thread), the digit
+  // whose inclusive count first reaches the rank; clear for the next pass
+  __threadfence();
+  const long long rank = first ? (nU + 1) / 2 : st->msel_rank;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const long long a = hist[2 * t], b = hist[2 * t + 1];
-  long long incl = a + b;
+  long long c4[4], tot = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    c4[k] = __ldcg(hist + 4 * t + k);
+    tot += c4[k];
+  }
+  long long incl = tot;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const long long y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -639,21 +658,30 @@ __global__ void __launch_bounds__(1024) k_msel_pick(int pass, int32_t* __restric
     s_w[lane] = wi - w;
   }
   __syncthreads();
-  const long long before = s_w[warp] + incl - (a + b);  // keys in bins < 2t
-  if (before < rank && rank <= before + a) {
-    s_digit = 2 * t;
-    s_before = before;
-  } else if (before + a < rank && rank <= before + a + b) {
-    s_digit = 2 * t + 1;
-    s_before = before + a;
+  long long before = s_w[warp] + incl - tot;  // keys in bins < 4t
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (before < rank && rank <= before + c4[k]) {
+      s_digit = 4 * t + k;
+      s_before = before;
+    }
+    before += c4[k];
   }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) hist[4 * t + k] = 0;
   __syncthreads();
-  hist[2 * t] = 0;
-  hist[2 * t + 1] = 0;
   if (t == 0) {
-    st->msel_key = ((pass == 0 ? 0ull : st->msel_key) << bits) | (unsigned long long)s_digit;
+    st->msel_key = pkey | ((unsigned long long)s_digit << shift);
+    st->msel_mask = pmask | ((unsigned long long)dmask << shift);
     st->msel_rank = rank - s_before;
+    st->msel_done = 0;
   }
+}
+// before a round's first pass: nothing determined yet
+__global__ void k_msel_reset(State* st) {
+  st->msel_key = 0;
+  st->msel_mask = 0;
+  st->msel_done = 0;
 }
 
 // a2/a5: carry the cached degree sum and |U| to the next round (Q5 reading of
@@ -778,20 +806,38 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                            c.state));
   if (c.n == 0) return sync_state(c);
   int32_t* mhist = c.hist1;  // the order's histograms are free during ADG
-  if (rule == kRuleMedian)
+  // ADG-M's radix schedule: (shift, bits) digits over the bits of (D << 32) | v
+  // that can be nonzero (D < 2^bitlen(maxdeg), v < 2^bitlen(n-1))
+  std::vector<std::pair<int, int>> digits;
+  if (rule == kRuleMedian) {
     PGC_LAUNCH(c, kGAdgOther, "k_zero_i32", k_zero_i32<<<4, 512, 0, c.st>>>(mhist, kMselBins));
+    PGC_LAUNCH(c, kGAdgOther, "k_maxdeg", k_maxdeg<<<grid_for(c, 8), 256, 0, c.st>>>(c.n, c.off, c.state));
+    if (int e = sync_state(c)) return e;
+    auto bitlen = [](long long x) { int b = 1; while (b < 62 && (1ll << b) <= x) ++b; return b; };
+    const int dbits = bitlen(c.h_state->maxdeg), ibits = bitlen(c.n - 1);
+    for (int hi = 32 + dbits; hi > 32; hi -= kMselBits) {
+      const int lo = hi - kMselBits > 32 ? hi - kMselBits : 32;
+      digits.push_back({lo, hi - lo});
+    }
+    for (int hi = ibits; hi > 0; hi -= kMselBits) {
+      const int lo = hi - kMselBits > 0 ? hi - kMselBits : 0;
+      digits.push_back({lo, hi - lo});
+    }
+  }
   int l = 1;
   const int batch = c.tune.rounds_per_sync < 1 ? 1 : c.tune.rounds_per_sync;
   for (;;) {
     for (int j = 0; j < batch; ++j, ++l) {
       const int32_t* Uin = l == 1 ? nullptr : c.U[l & 1];
       int32_t* Uout = c.U[(l + 1) & 1];
-      if (rule == kRuleMedian)
-        for (int pass = 0; pass < kMselPasses; ++pass) {
-          PGC_LAUNCH(c, kGSelect, "k_msel_hist",
-                     k_msel_hist<<<c.nsm * 2, 1024, 0, c.st>>>(pass, Uin, c.D, mhist, c.state));
-          PGC_LAUNCH(c, kGSelect, "k_msel_pick", k_msel_pick<<<1, 1024, 0, c.st>>>(pass, mhist, c.state));
-        }
+      if (rule == kRuleMedian) {
+        PGC_LAUNCH(c, kGSelect, "k_msel_reset", k_msel_reset<<<1, 1, 0, c.st>>>(c.state));
+        for (size_t p = 0; p < digits.size(); ++p)
+          PGC_LAUNCH(c, kGSelect, "k_msel_pass",
+                     k_msel_pass<<<c.nsm * 2, 1024, 0, c.st>>>(p == 0, digits[p].first,
+                                                              digits[p].second, Uin, c.D, mhist,
+                                                              c.state));
+      }
       PGC_LAUNCH(c, kGSelect, "k_adg_select",
                  k_adg_select<<<G, B, 0, c.st>>>(l, rule, num, den, c.off, c.D, round, c.rs, Uin, Uout,
                                                  c.lrec, c.chunks, c.npred, c.state,

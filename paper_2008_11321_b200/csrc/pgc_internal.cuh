@@ -49,8 +49,11 @@ struct State {
   int nlight;                  // bulk vertices with 1 <= |pred| <= kLightPredMax
   int ticket_heavy, ticket_light;  // next bulk tickets per class
   // ADG-M radix select of the ceil(|U|/2)-th smallest key (D[v] << 32) | v
-  unsigned long long msel_key;  // key digits found so far (the full key after the last pass)
-  long long msel_rank;          // rank still to find among keys with that prefix (1-based)
+  unsigned long long msel_key;   // key bits found so far (the full key after the last pass)
+  unsigned long long msel_mask;  // which key bits msel_key determines
+  long long msel_rank;           // rank still to find among keys matching msel_key (1-based)
+  int msel_done;                 // blocks finished in the current pass (last-block pick)
+  int maxdeg;                    // maximum degree (ADG-M's radix schedule)
 };
 
 // Byte offsets of every workspace region (each 256-byte aligned).
