@@ -438,18 +438,21 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
 // UPDATE for chunked vertices in the late rounds, with a membership filter.
 // Once |U_l| is small, most arcs of R_l lead to vertices removed in earlier
 // rounds (on R-MAT 24, 171 M of the 236 M arcs of rounds 4-7): their state
-// gather is a wasted L2 request, and UPDATE is bound by the L2 request rate.
-// Each CTA (one per SM, 1024 threads) first builds a one-hash Bloom filter of
-// U_l (the round's input list: alive or removed this round) in shared memory;
-// an arc whose target misses the filter is "removed earlier" for certain, and
-// only hits (members of U_l plus <= 1/kFilterRatio false positives) gather the
-// real state.  The result is identical: the filter only skips gathers whose
-// answer it already knows.  The plain kernel runs the rounds with
-// |U_l| > bits / ratio (each of the two kernels exits if the round is not its).
+// gather is a wasted random access, and UPDATE is bound by the random-access
+// rate.  Each CTA (one per SM, 1024 threads) copies a one-hash Bloom filter of
+// U_l (the round's input list: alive or removed this round; built once per
+// round by k_filter_build) into shared memory; an arc whose target misses the
+// filter is "removed earlier" for certain.  A warp first filters a 256-arc
+// step and compacts the hits (members of U_l plus <= 1/ratio false positives)
+// into shared memory, then gathers, classifies and decrements only those, 32
+// per pass: the per-arc work of a dead arc is a load, a hash and one shared
+// load.  The result is identical: the filter only skips gathers whose answer
+// it already knows.  The plain kernel runs the rounds with |U_l| > bits /
+// ratio (each of the two kernels exits if the round is not its).
 constexpr int kFilterThreads = 1024;
-constexpr int kFilterSub = 256;                       // staged preds per warp
-constexpr uint32_t kFilterBits = kFilterBytes * 8u;   // 1.5 M filter bits
-constexpr size_t kFilterSmem = kFilterBytes + (kFilterThreads / 32) * kFilterSub * 4;
+constexpr int kFilterSub = 256;                       // arcs per step; staged preds / hits per warp
+constexpr uint32_t kFilterBits = kFilterBytes * 8u;   // filter bits
+constexpr size_t kFilterSmem = kFilterBytes + 2 * (kFilterThreads / 32) * kFilterSub * 4;
 static_assert(kFilterBits == kFilterBitsFwd, "filter size");
 __device__ __forceinline__ uint32_t filter_slot(int u) {
   return __umulhi((uint32_t)u * 0x9E3779B1u, kFilterBits);
@@ -489,7 +492,9 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
   const int nC = st->nChunks;
   if (nC == 0) return;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
   int* s_buf = s_buf_all + warp * kFilterSub;
+  int* s_hit = s_buf_all + (kFilterThreads / 32 + warp) * kFilterSub;
   {  // the round's filter (built by k_filter_build) -> shared memory
     const uint4* src = reinterpret_cast<const uint4*>(gfilt + (size_t)(A.l & 1) * kFilterWords);
     uint4* dst = reinterpret_cast<uint4*>(filt);
@@ -522,34 +527,47 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
     const uint64_t hv = MODE != 0 ? A.own(v) : 0;
     for (long long s0 = s; s0 < e; s0 += kFilterSub) {
       const long long e0 = min(e, s0 + kFilterSub);
-      int cnt = 0;
-      for (long long a0 = s0; a0 < e0; a0 += 32 * kStrips) {
-        int u[kStrips], g[kStrips];
+      // 1. filter the step's arcs; compact the hits into s_hit (arc order kept)
+      int nh = 0;
+      {
+        static_assert(32 * kStrips == kFilterSub, "one filter pass per step");
+        int u[kStrips];
+        uint32_t fw[kStrips];
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) {
-          const long long a = a0 + 32 * k + lane;
+          const long long a = s0 + 32 * k + lane;
           u[k] = a < e0 ? ld_stream(col + a) : -1;
         }
-        bool hit[kStrips];
-        uint32_t fw[kStrips];
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) fw[k] = filt[filter_slot(u[k] >= 0 ? u[k] : 0) >> 5];
 #pragma unroll
-        for (int k = 0; k < kStrips; ++k)
-          hit[k] = u[k] >= 0 && ((fw[k] >> (filter_slot(u[k]) & 31)) & 1u);
-#pragma unroll
-        for (int k = 0; k < kStrips; ++k) g[k] = hit[k] ? A.raw(u[k]) : 0;
-#pragma unroll
-        for (int k = 0; k < kStrips; ++k) g[k] = hit[k] ? A.decode(u[k], g[k]) : 2;  // miss: earlier
-        int du[kStrips];
-#pragma unroll
-        for (int k = 0; k < kStrips; ++k) du[k] = A.same_round_d(u[k], g[k]);
-#pragma unroll
         for (int k = 0; k < kStrips; ++k) {
+          const bool hit = u[k] >= 0 && ((fw[k] >> (filter_slot(u[k]) & 31)) & 1u);
+          const unsigned bal = __ballot_sync(0xffffffffu, hit);
+          if (hit) s_hit[nh + __popc(bal & lt)] = u[k];
+          nh += __popc(bal);
+        }
+      }
+      __syncwarp();
+      // 2. the hits, 64 per pass (two gathers in flight per lane): the real
+      //    state, UPDATE's decrement, the pred test
+      int cnt = 0;
+      for (int j0 = 0; j0 < nh; j0 += 64) {
+        int u[2], g[2], du[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) u[k] = j0 + 32 * k + lane < nh ? s_hit[j0 + 32 * k + lane] : -1;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) g[k] = A.raw(u[k]);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) g[k] = A.decode(u[k], g[k]);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) du[k] = A.same_round_d(u[k], g[k]);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
           const bool pred = u[k] >= 0 && A.classify(u[k], g[k], 0, hv, cut, du[k]);
           if (MODE != 0) {
             const unsigned bal = __ballot_sync(0xffffffffu, pred);
-            if (pred) s_buf[cnt + __popc(bal & lanemask_lt())] = u[k];
+            if (pred) s_buf[cnt + __popc(bal & lt)] = u[k];
             cnt += __popc(bal);
           }
         }

@@ -70,7 +70,7 @@ struct Tuning {
   int rounds_per_sync = 8;
   int heavy_degree = 128;   // vertices with more arcs are split into edge chunks
   int chunk_arcs = 1024;    // arcs per chunk work item
-  int filter_ratio = 0;     // UPDATE: filtered heavy kernel once |U_l| * ratio <= filter bits (0 = off)
+  int filter_ratio = 4;     // UPDATE: filtered heavy kernel once |U_l| * ratio <= filter bits (0 = off)
   int jp_heavy_warps = 4;         // warps per 8-warp bulk JP block serving heavy vertices (1..4)
   int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
   int jp_light_sleep_max = 8192;  // ns, same for light warps
@@ -129,8 +129,8 @@ struct Ctx {
   unsigned long long* trace_done = nullptr;
 };
 
-// UPDATE membership filter (adg.cu): 1.5 M bits (192 KB) per buffer
-constexpr int kFilterBytes = 192 * 1024;
+// UPDATE membership filter (adg.cu): 1 M bits (128 KB) per buffer
+constexpr int kFilterBytes = 128 * 1024;
 constexpr int kFilterWords = kFilterBytes / 4;
 
 // ---- phases (host orchestration; return 0 or a PGC_* code) -----------------
