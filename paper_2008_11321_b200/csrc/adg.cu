@@ -73,6 +73,7 @@ __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ o
 }
 
 // a2+a3: threshold, select, compact.
+constexpr int kSelItems = 4;
 __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
                              const int32_t* __restrict__ D, int32_t* __restrict__ round,
                              uint8_t* __restrict__ rs,
@@ -97,49 +98,96 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
   const unsigned long long mkey = st->msel_key;  // ADG-M: the ceil(|U|/2)-th smallest key
   unsigned long long my_sumD = 0;
   unsigned long long my_nR = 0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long base = (long long)blockIdx.x * blockDim.x; base < count; base += stride) {
-    const long long i = base + threadIdx.x;
-    const bool valid = i < count;
-    int v = 0, d = 0;
-    if (valid) {
-      v = Uin ? Uin[i] : (int)i;
-      d = ld_i32_keep(D + v);
+  // kSelItems vertices per thread per step (coalesced: item j of thread t is
+  // base + j * blockDim + t); the three output lists (edge chunks, light
+  // records, U_{l+1}) are compacted with ONE block scan of packed counts and
+  // one atomicAdd per list per step
+  constexpr int K = kSelItems;
+  const long long step = (long long)gridDim.x * blockDim.x * K;
+  for (long long base = (long long)blockIdx.x * blockDim.x * K; base < count; base += step) {
+    int v[K], d[K], nch[K];
+    long long o[K], deg[K];
+    bool valid[K], sel[K], light[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const long long i = base + (long long)j * blockDim.x + threadIdx.x;
+      valid[j] = i < count;
+      v[j] = valid[j] ? (Uin ? Uin[i] : (int)i) : 0;
     }
-    // ADG: D <= (1+eps) * mean (exact integer form);  ADG-M: the
-    // ceil(|U|/2) smallest keys (D, id) of U (median rule)
-    const bool sel = valid && (rule == kRuleMedian
-                                   ? ((((unsigned long long)(uint32_t)d) << 32) | (uint32_t)v) <= mkey
-                                   : d <= dmax);
-    bool light = false;
-    int nch = 0;
-    long long o = 0, deg = 0;
-    if (sel) {
-      round[v] = l;
-      st_u8_keep(rs + v, (l - 1) % 255 + 1);
-      my_sumD += (unsigned long long)d;
-      my_nR += 1;
-      o = off[v];
-      deg = off[v + 1] - o;
-      light = deg > 0 && deg <= heavy_deg;  // isolated: settled by k_adg_init
-      if (deg > heavy_deg) {
-        nch = (int)((deg + chunk - 1) / chunk);
-        npred[v] = 0;
-      }
-    }
-    const int cb = block_reserve(nch, &st->nChunks, sm);
-    if (nch) {
-      if (cb + (long long)nch > chunk_cap) st->err = 3;
-      else
-        for (int k = 0; k < nch; ++k) {
-          const long long s0 = o + (long long)k * chunk;
-          const int len = (int)min((long long)chunk, o + deg - s0);
-          __stcs(chunks + 2 * (cb + k), make_int4(v, len, (int)(uint32_t)s0, (int)(s0 >> 32)));
-          __stcs(chunks + 2 * (cb + k) + 1, make_int4((int)(uint32_t)o, (int)(o >> 32), 0, 0));
+#pragma unroll
+    for (int j = 0; j < K; ++j) d[j] = valid[j] ? ld_i32_keep(D + v[j]) : 0;
+    unsigned long long packed = 0;  // chunks | light << 32 | unext << 48
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      // ADG: D <= (1+eps) * mean (exact integer form);  ADG-M: the
+      // ceil(|U|/2) smallest keys (D, id) of U (median rule)
+      sel[j] = valid[j] && (rule == kRuleMedian
+                                ? ((((unsigned long long)(uint32_t)d[j]) << 32) | (uint32_t)v[j]) <= mkey
+                                : d[j] <= dmax);
+      light[j] = false;
+      nch[j] = 0;
+      o[j] = 0;
+      deg[j] = 0;
+      if (sel[j]) {
+        round[v[j]] = l;
+        st_u8_keep(rs + v[j], (l - 1) % 255 + 1);
+        my_sumD += (unsigned long long)d[j];
+        my_nR += 1;
+        o[j] = off[v[j]];
+        deg[j] = off[v[j] + 1] - o[j];
+        light[j] = deg[j] > 0 && deg[j] <= heavy_deg;  // isolated: settled by k_adg_init
+        if (deg[j] > heavy_deg) {
+          nch[j] = (int)((deg[j] + chunk - 1) / chunk);
+          npred[v[j]] = 0;
         }
+      }
+      packed += (unsigned long long)nch[j] + ((unsigned long long)light[j] << 32) +
+                ((unsigned long long)(valid[j] && !sel[j]) << 48);
     }
-    block_append_rec(light, light_rec(v, (int)deg, o), lrec, &st->nLight, sm);
-    block_append(valid && !sel, v, Uout, &st->nUnext, sm);
+    // block exclusive scan of the packed counts
+    const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long incl = packed;
+#pragma unroll
+    for (int o_ = 1; o_ < 32; o_ <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o_);
+      if (lane >= o_) incl += y;
+    }
+    if (lane == 31) s_red[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long run = 0;
+      for (int w = 0; w < nw; ++w) {
+        const unsigned long long c = s_red[w];
+        s_red[w] = run;
+        run += c;
+      }
+      const unsigned tch = (unsigned)(run & 0xffffffffull), tl = (unsigned)((run >> 32) & 0xffff),
+                     tu = (unsigned)(run >> 48);
+      sm[0] = tch ? atomicAdd(&st->nChunks, (int)tch) : 0;
+      sm[1] = tl ? atomicAdd(&st->nLight, (int)tl) : 0;
+      sm[2] = tu ? atomicAdd(&st->nUnext, (int)tu) : 0;
+    }
+    __syncthreads();
+    const unsigned long long ex = s_red[warp] + incl - packed;
+    long long cpos = sm[0] + (long long)(ex & 0xffffffffull);
+    int lpos = sm[1] + (int)((ex >> 32) & 0xffff), upos = sm[2] + (int)(ex >> 48);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (nch[j]) {
+        if (cpos + nch[j] > chunk_cap) st->err = 3;
+        else
+          for (int k = 0; k < nch[j]; ++k) {
+            const long long s0 = o[j] + (long long)k * chunk;
+            const int len = (int)min((long long)chunk, o[j] + deg[j] - s0);
+            __stcs(chunks + 2 * (cpos + k), make_int4(v[j], len, (int)(uint32_t)s0, (int)(s0 >> 32)));
+            __stcs(chunks + 2 * (cpos + k) + 1, make_int4((int)(uint32_t)o[j], (int)(o[j] >> 32), 0, 0));
+          }
+        cpos += nch[j];
+      }
+      if (light[j]) __stcs(lrec + lpos++, light_rec(v[j], (int)deg[j], o[j]));
+      if (valid[j] && !sel[j]) Uout[upos++] = v[j];
+    }
+    __syncthreads();  // s_red / sm are reused by the next step
   }
   unsigned long long t = block_sum(my_sumD, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(&st->sumDR, t);
