@@ -909,6 +909,7 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                                  c.lrec, c.chunks, c.npred, c.state,
                                                  c.tune.heavy_degree, c.tune.chunk_arcs,
                                                  c.lay.chunk_cap));
+      if (l == 1 && c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
       if (c.tune.filter_ratio > 0)
         PGC_LAUNCH(c, kGUpdate, "k_filter_build",
                    k_filter_build<<<c.nsm * 2, 1024, 0, c.st>>>(l, Uin, c.filt, c.state,

@@ -285,10 +285,14 @@ int pgc_jp_color(const pgc_graph* g, const int32_t* round, uint64_t seed, int32_
   return PGC_OK;
 }
 
-int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uint64_t seed,
-                     int32_t* round_out, int32_t* color_out, int32_t* num_rounds,
-                     int32_t* num_colors, void* workspace, size_t workspace_bytes,
-                     void* cuda_stream) {
+// JP-ADG; the host entry point adds `col_ready` (UPDATE of round 1 waits for
+// col[], init and the first selection overlap its copy) and `side`/`h_round`
+// (round[] is final after ADG: its device->host copy overlaps JP).
+static int color_jp_adg_impl(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uint64_t seed,
+                             int32_t* round_out, int32_t* color_out, int32_t* num_rounds,
+                             int32_t* num_colors, void* workspace, size_t workspace_bytes,
+                             void* cuda_stream, cudaEvent_t col_ready, cudaStream_t side,
+                             cudaEvent_t adg_done, int32_t* h_round) {
   if (int e = check_graph_args(g)) return e;
   if (eps_num == 0 || eps_den == 0) return fail(PGC_EINVAL, "eps must be num/den with num, den >= 1");
   if (!num_rounds || !num_colors || (g->n > 0 && (!round_out || !color_out)))
@@ -296,8 +300,14 @@ int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uin
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  c.col_ready = col_ready;
   call_begin(c);
   if (int e = adg_run(c, eps_num, eps_den, seed, round_out, kAdgFused, color_out)) return e;
+  if (h_round && g->n > 0) {
+    PGC_CUDA(cudaEventRecord(adg_done, c.st));
+    PGC_CUDA(cudaStreamWaitEvent(side, adg_done, 0));
+    PGC_CUDA(cudaMemcpyAsync(h_round, round_out, 4 * (size_t)g->n, cudaMemcpyDeviceToHost, side));
+  }
   const int T = c.h_state->T;
   const long long sum_active = c.h_state->sum_active;
   const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
@@ -309,6 +319,15 @@ int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uin
   *num_colors = c.h_state->K;
   call_end(c, T, c.h_state->K, sum_active, cross, preds, c.core_n);
   return PGC_OK;
+}
+
+int pgc_color_jp_adg(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uint64_t seed,
+                     int32_t* round_out, int32_t* color_out, int32_t* num_rounds,
+                     int32_t* num_colors, void* workspace, size_t workspace_bytes,
+                     void* cuda_stream) {
+  return color_jp_adg_impl(g, eps_num, eps_den, seed, round_out, color_out, num_rounds, num_colors,
+                           workspace, workspace_bytes, cuda_stream, nullptr, nullptr, nullptr,
+                           nullptr);
 }
 
 int pgc_adg_m_order(const pgc_graph* g, int32_t* round_out, int32_t* num_rounds, void* workspace,
@@ -407,20 +426,29 @@ int pgc_color_jp_adg_host(int64_t n, int64_t nnz, const int64_t* h_row_offsets,
   int32_t* d_color = (int32_t*)b;
   b += a256(4 * (size_t)n);
   cudaStream_t st = (cudaStream_t)cuda_stream;
+  // a side stream (per thread, created once) carries col[] host->device and
+  // round[] device->host, overlapping the first ADG kernels and JP
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  if (!side) {
+    PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    for (auto& e : ev) PGC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  PGC_CUDA(cudaEventRecord(ev[0], st));  // the side stream starts after st's earlier work
+  PGC_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
   PGC_CUDA(cudaMemcpyAsync(d_off, h_row_offsets, 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, st));
   if (nnz > 0)
-    PGC_CUDA(cudaMemcpyAsync(d_col, h_col_indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice, st));
+    PGC_CUDA(cudaMemcpyAsync(d_col, h_col_indices, 4 * (size_t)nnz, cudaMemcpyHostToDevice, side));
+  PGC_CUDA(cudaEventRecord(ev[1], side));
   pgc_graph g = {n, nnz, d_off, d_col};
-  if (int e = pgc_color_jp_adg(&g, eps_num, eps_den, seed, d_round, d_color, num_rounds,
-                               num_colors, b, workspace_bytes - (size_t)(b - (char*)workspace),
-                               cuda_stream))
-    return e;
-  if (n > 0) {
-    PGC_CUDA(cudaMemcpyAsync(h_round_out, d_round, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  int rc = color_jp_adg_impl(&g, eps_num, eps_den, seed, d_round, d_color, num_rounds, num_colors,
+                             b, workspace_bytes - (size_t)(b - (char*)workspace), cuda_stream,
+                             ev[1], side, ev[2], n > 0 ? h_round_out : nullptr);
+  if (rc == PGC_OK && n > 0)
     PGC_CUDA(cudaMemcpyAsync(h_color_out, d_color, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
-  }
+  PGC_CUDA(cudaStreamSynchronize(side));  // also on error: nothing may stay in flight
   PGC_CUDA(cudaStreamSynchronize(st));
-  return PGC_OK;
+  return rc;
 }
 
 int pgc_check_graph(const pgc_graph* g, void* workspace, size_t workspace_bytes, void* cuda_stream) {

@@ -125,6 +125,7 @@ struct Ctx {
   int core_ctas = 0;                   // cluster size used by the last k_jp_core (0 = none)
   int core_n = 0;                      // core vertices colored by k_jp_core (0 = none)
   State* h_state;  // pinned host mirror
+  cudaEvent_t col_ready = nullptr;  // host entry point: col[] still in flight until this event
   unsigned long long* trace_grab = nullptr;  // pgc_debug_set_trace (diagnostics)
   unsigned long long* trace_done = nullptr;
 };
