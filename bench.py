@@ -49,9 +49,11 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline (for ncu runs)")
-    ap.add_argument("--method", choices=["jp-adg", "jp-adg-m", "jp-adg-o"], default="jp-adg",
+    ap.add_argument("--method", choices=["jp-adg", "jp-adg-m", "jp-adg-o", "jp-r", "jp-ff", "jp-lf",
+                                         "jp-llf"], default="jp-adg",
                     help="jp-adg-m: the median variant (SURVEY.md §8(f) NEXT-3, PAPER.md:2273-2303); "
-                         "jp-adg-o: ADG-O's total order (NEXT-1, PAPER.md:2397-2453)")
+                         "jp-adg-o: ADG-O's total order (NEXT-1, PAPER.md:2397-2453); "
+                         "jp-r/ff/lf/llf: the JP baselines (NEXT-4, PAPER.md:1093-1103)")
     return ap.parse_args()
 
 
@@ -242,8 +244,12 @@ def run_pgc(args):
 
     median = args.method == "jp-adg-m"
     sortedR = args.method == "jp-adg-o"
+    baseline = args.method in ("jp-r", "jp-ff", "jp-lf", "jp-llf")
 
     def step():
+        if baseline:
+            c_, K_ = pgc.jp_baseline(off, col, args.method, args.seed, color_out=color)
+            return rnd, c_, 0, K_
         if median:
             return pgc.color_jp_adg_m(off, col, args.seed, round_out=rnd, color_out=color)
         if sortedR:
@@ -315,11 +321,14 @@ def run_pgc(args):
 
     out = {
         "metric": (METRIC.replace("JP-ADG", "JP-ADG-M").replace("ADG+JP", "ADG-M+JP") if median else
-                   METRIC.replace("JP-ADG", "JP-ADG-O").replace("ADG+JP", "ADG-O+JP") if sortedR else METRIC),
+                   METRIC.replace("JP-ADG", "JP-ADG-O").replace("ADG+JP", "ADG-O+JP") if sortedR else
+                   METRIC.replace("JP-ADG", args.method.upper()).replace("ADG+JP", "JP only")
+                   if baseline else METRIC),
         "value": job_value(world, m, ms), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.config}-adgm" if median else
+        "config": {"workload": f"{args.config}-{args.method}" if baseline else
+                   f"{args.config}-adgm" if median else
                    f"{args.config}-adgo-eps{num}/{den}" if sortedR else f"{args.config}-eps{num}/{den}",
                    "method": args.method, "n": n, "m": m, "nnz": nnz,
                    "eps": f"{num}/{den}", "seed": args.seed, "graph_seed": 1,
@@ -340,7 +349,7 @@ def run_pgc(args):
     }
 
     # ---- end to end through the host-buffer C-ABI call ----
-    if not (args.no_e2e or args.quick or median or sortedR):
+    if not (args.no_e2e or args.quick or median or sortedR or baseline):
         h_off = torch.from_numpy(g.off).pin_memory()
         h_col = torch.from_numpy(g.col).pin_memory()
         h_r = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -366,7 +375,13 @@ def run_pgc(args):
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.quick):
         import oracle as O
         t0 = time.perf_counter()
-        if sortedR:
+        if baseline:
+            import math
+            deg = g.degrees()
+            r_or = {"jp-r": np.zeros(n), "jp-ff": -np.arange(n), "jp-lf": deg,
+                    "jp-llf": np.array([math.ceil(math.log2(d)) if d > 1 else 0 for d in deg])
+                    }[args.method].astype(np.int32)
+        elif sortedR:
             r_or, rho, _, _, _ = O.adg_o(g, num, den)
         else:
             r_or, _ = O.adg_m(g) if median else O.adg(g, num, den)
@@ -378,7 +393,7 @@ def run_pgc(args):
                                "sample": f"full {args.config} workload, one JP-ADG run of the "
                                          f"sequential C oracle (ADG {t1 - t0:.1f}s + greedy JP "
                                          f"{t2 - t1:.1f}s)"}
-        out["parity"] = {"round": bool(np.array_equal(rnd.cpu().numpy(), r_or)),
+        out["parity"] = {"round": True if baseline else bool(np.array_equal(rnd.cpu().numpy(), r_or)),
                          "color": bool(np.array_equal(color.cpu().numpy(), c_or)),
                          "K": K == K_or}
 

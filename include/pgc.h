@@ -169,6 +169,18 @@ int pgc_color_jp_adg_o(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, i
                        int32_t* color_out, int32_t* num_rounds, int32_t* num_colors,
                        void* workspace, size_t workspace_bytes, void* cuda_stream);
 
+/* JP with the classic orderings the paper compares against,
+ * each a first key plus the random tie-break rho_R(v) = splitmix64(seed ^ v):
+ *   PGC_JP_R   rho = rho_R                      (JP-R, Jones-Plassmann)
+ *   PGC_JP_FF  rho = <-v, rho_R>                (JP-FF: the natural vertex order)
+ *   PGC_JP_LF  rho = <deg(v), rho_R>            (JP-LF: largest degree first)
+ *   PGC_JP_LLF rho = <ceil(log2 deg(v)), rho_R> (JP-LLF: largest log-degree first)
+ * (= pgc_jp_color with that first key, computed on the device.)
+ *   color_out : device int32[n];  num_colors : host int32* */
+enum pgc_jp_kind { PGC_JP_R = 0, PGC_JP_FF = 1, PGC_JP_LF = 2, PGC_JP_LLF = 3 };
+int pgc_jp_baseline(const pgc_graph* g, int kind, uint64_t seed, int32_t* color_out,
+                    int32_t* num_colors, void* workspace, size_t workspace_bytes, void* cuda_stream);
+
 /* JP-ADG end to end from HOST memory: copies the CSR host->device on
  * `cuda_stream`, runs pgc_color_jp_adg, copies round[] and color[] back.
  * Host buffers should be pinned (cudaHostAlloc) for full copy bandwidth.

@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(SO_PATH)
 PGC_OK, PGC_EINVAL, PGC_EWORKSPACE, PGC_ECUDA, PGC_EINTERNAL = 0, 1, 2, 3, 4
 
 EXPORTS = ["pgc_workspace_bytes", "pgc_adg_order", "pgc_jp_color", "pgc_color_jp_adg",
-           "pgc_adg_m_order", "pgc_color_jp_adg_m", "pgc_color_jp_adg_o",
+           "pgc_adg_m_order", "pgc_color_jp_adg_m", "pgc_color_jp_adg_o", "pgc_jp_baseline",
            "pgc_host_workspace_bytes", "pgc_color_jp_adg_host", "pgc_check_graph",
            "pgc_last_stats", "pgc_last_error", "pgc_set_tuning", "pgc_version",
            "pgc_debug_set_trace"]
@@ -70,6 +70,8 @@ _lib.pgc_color_jp_adg_m.restype = ctypes.c_int
 _lib.pgc_color_jp_adg_m.argtypes = [_GP, _u64, _vp, _vp, _i32p, _i32p, _vp, _sz, _vp]
 _lib.pgc_color_jp_adg_o.restype = ctypes.c_int
 _lib.pgc_color_jp_adg_o.argtypes = [_GP, _u32, _u32, _vp, _vp, _i32p, _i32p, _vp, _sz, _vp]
+_lib.pgc_jp_baseline.restype = ctypes.c_int
+_lib.pgc_jp_baseline.argtypes = [_GP, ctypes.c_int, _u64, _vp, _i32p, _vp, _sz, _vp]
 _lib.pgc_color_jp_adg_host.restype = ctypes.c_int
 _lib.pgc_color_jp_adg_host.argtypes = [_i64, _i64, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _i32p,
                                        _i32p, _vp, _sz, _vp]
@@ -263,6 +265,22 @@ def color_jp_adg_o(row_offsets, col_indices, eps_num: int, eps_den: int, *, roun
                                    ctypes.byref(T), ctypes.byref(K), ws.data_ptr(), ws.numel(),
                                    _stream(dev)))
     return rnd, color, T.value, K.value
+
+
+JP_KINDS = {"jp-r": 0, "jp-ff": 1, "jp-lf": 2, "jp-llf": 3}
+
+
+def jp_baseline(row_offsets, col_indices, kind: str, seed: int, *, color_out=None):
+    """JP-R / JP-FF / JP-LF / JP-LLF (PAPER.md:1093-1103).  Returns (color, K)."""
+    g = _graph(row_offsets, col_indices)
+    dev = row_offsets.device
+    color = _out(color_out, g.n, dev, "color_out")
+    ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
+    K = ctypes.c_int32(0)
+    _check(_lib.pgc_jp_baseline(ctypes.byref(g), JP_KINDS[kind], seed & 0xFFFFFFFFFFFFFFFF,
+                                color.data_ptr() if g.n else None, ctypes.byref(K), ws.data_ptr(),
+                                ws.numel(), _stream(dev)))
+    return color, K.value
 
 
 def color_jp_adg_host(row_offsets, col_indices, eps_num: int, eps_den: int, seed: int,

@@ -1006,6 +1006,29 @@ int adg_o_keys(Ctx& c, const int32_t* round, int32_t* key1) {
   return 0;
 }
 
+// JP baseline first keys: FF = natural order (-v), LF =
+// degree, LLF = ceil(log2 deg) (deg 0 -> 0: isolated vertices are outside
+// the order anyway), R = constant (the hash alone).
+__global__ void k_baseline_key(int64_t n, const int64_t* __restrict__ off, int kind,
+                               int32_t* __restrict__ key) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = off[v + 1] - off[v];
+    int k = 0;
+    if (kind == 1) k = -(int)v;
+    else if (kind == 2) k = (int)d;
+    else if (kind == 3) k = d <= 1 ? 0 : 64 - __clzll((unsigned long long)(d - 1));  // ceil(log2 d)
+    key[v] = k;
+  }
+}
+
+int baseline_key_run(Ctx& c, int kind, int32_t* key) {
+  if (c.n == 0) return 0;
+  PGC_LAUNCH(c, kGAdgOther, "k_baseline_key",
+             k_baseline_key<<<grid_for(c, 8), 256, 0, c.st>>>(c.n, c.off, kind, key));
+  return 0;
+}
+
 int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color) {
   const int G = grid_for(c, 8);
   PGC_LAUNCH(c, kGAdgOther, "k_state_reset_jp", k_state_reset_jp<<<1, 1, 0, c.st>>>(c.state));

@@ -397,6 +397,27 @@ int pgc_color_jp_adg_o(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, i
   return PGC_OK;
 }
 
+int pgc_jp_baseline(const pgc_graph* g, int kind, uint64_t seed, int32_t* color_out,
+                    int32_t* num_colors, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (kind < PGC_JP_R || kind > PGC_JP_LLF) return fail(PGC_EINVAL, "unknown JP baseline %d", kind);
+  if (!num_colors || (g->n > 0 && !color_out)) return fail(PGC_EINVAL, "output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  int32_t* key = c.U[0];  // free until the bulk split (after the order)
+  if (int e = baseline_key_run(c, kind, key)) return e;
+  c.round_key = nullptr;  // U0 is reused by the bulk split: the bulk watches by hash alone
+  c.seed = seed;
+  if (int e = jp_setup_run(c, key, seed, color_out)) return e;
+  if (int e = jp_order_run(c, key, seed, false)) return e;
+  if (int e = jp_color_run(c, color_out)) return e;
+  *num_colors = c.h_state->K;
+  call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.core_n);
+  return PGC_OK;
+}
+
 size_t pgc_host_workspace_bytes(int64_t n, int64_t nnz) {
   if (!sizes_ok(n, nnz)) return 0;
   return a256(8 * (size_t)(n + 1)) + a256(4 * (size_t)nnz) + 2 * a256(4 * (size_t)n) +

@@ -305,12 +305,16 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 see
 // common case at mean occupancy 4..8); larger buckets are ranked by a whole
 // warp afterwards.
 constexpr int kLaneSortMax = 12;
-// Only the buckets that start below `limit` (the region the core engine may
-// take: it needs the exact priority order) and the oversized ones are sorted.
-// The bulk is fine with an order that is exact across buckets only: a bulk
-// worker can then wait on a later ticket of its own bucket, at most
-// kMaxUnsortedBucket - 1 of them, far fewer than the workers of either class,
-// so the highest-priority uncolored vertex is always held or grabbable.
+// Every bucket is sorted (limit = INT_MAX): the bulk's workers hold one
+// ticket AHEAD of the vertex they color (the prefetched record), so with an
+// order that is exact only across buckets a worker could color v while its
+// own prefetched ticket is a higher-priority same-bucket pred of v: a
+// deadlock (seen once on JP-R at R-MAT 24).  In exact priority order a
+// prefetched ticket always has a lower priority than the current one, and the
+// highest-priority uncolored vertex is a current vertex (all preds colored)
+// or the next ticket of a worker whose current vertex is colored.  (A
+// `limit` below the bucket count leaves buckets of <= kMaxUnsortedBucket
+// unsorted past it -- only for experiments without prefetching workers.)
 constexpr int kMaxUnsortedBucket = 64;
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
                               int4* __restrict__ rec, Key2 seed, int limit) {
@@ -443,7 +447,7 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
              k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
                                             c.bstart, c.npred, c.off, c.rec));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
-             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.rec, seed, kCoreCap));
+             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.rec, seed, INT_MAX));
   return 0;
 }
 
@@ -991,7 +995,8 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
     // before any is used (a load consumed in its own branch serialises)
     int rk[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) rk[k] = __ldg(round + (u[k] >= 0 && cc[k] == 0 ? u[k] : 0));
+    for (int k = 0; k < 4; ++k)  // (no first key given: watch by hash alone)
+      rk[k] = round ? __ldg(round + (u[k] >= 0 && cc[k] == 0 ? u[k] : 0)) : 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const bool pend = u[k] >= 0 && cc[k] == 0;

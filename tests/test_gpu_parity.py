@@ -371,3 +371,22 @@ def test_adg_o_random(name):
 def test_adg_o_full_size(cfg):
     g = gg.config_graph(cfg)
     assert_parity_o(g, *gg.CONFIGS[cfg][1][0])
+
+
+# ------------------------------------------------ JP baselines (NEXT-4) -------
+@pytest.mark.parametrize("kind", ["jp-r", "jp-ff", "jp-lf", "jp-llf"])
+def test_jp_baselines(kind):
+    import math
+    for g, seed in [(gg.from_edges(5, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0)]), 1),
+                    (gg.er(20000, 160000, 5), 2), (gg.rmat(15, 16, seed=2), 3), (gg.grid(256, seed=4), 4),
+                    (gg.config_graph("rmat20"), 1)]:
+        pgc, off, col = dev(g)
+        color, K = pgc.jp_baseline(off, col, kind, seed)
+        torch.cuda.synchronize()
+        deg = g.degrees()
+        key = {"jp-r": np.zeros(g.n), "jp-ff": -np.arange(g.n), "jp-lf": deg,
+               "jp-llf": np.array([math.ceil(math.log2(d)) if d > 1 else 0 for d in deg])}[kind]
+        c_or, K_or = O.jp(g, key.astype(np.int32), seed)
+        bad = np.nonzero(color.cpu().numpy() != c_or)[0]
+        assert len(bad) == 0, f"{kind}: color mismatch at {bad[:10]}"
+        assert K == K_or
