@@ -74,8 +74,8 @@ Layout make_layout(int64_t n, int64_t nnz) {
   L.range_cap = n + 65536;
   L.hist1 = take(4 * (size_t)(2 * L.range_cap));
   L.base1 = take(4 * (size_t)(2 * L.range_cap + 1));
-  // sum over keys of pow2ceil(ceil(cnt/8)) <= n/4 + 2 * (nonempty keys) <= n/4 + 2n
-  L.nb_cap = n / 4 + 2 * n + 2;
+  // sum over keys of pow2ceil(ceil(cnt/T)) <= 2n/T + 2 * (nonempty keys) <= 2n/T + 2n
+  L.nb_cap = 2 * n / kBucketTarget + 2 * n + 2;
   L.bcnt = take(4 * (size_t)(L.nb_cap + 1));
   L.bstart = take(4 * (size_t)(L.nb_cap + 1));
   const int64_t big = L.nb_cap > 2 * L.range_cap + 1 ? L.nb_cap : 2 * L.range_cap + 1;

@@ -15,7 +15,10 @@ constexpr int kMinChunk = 256;        // smallest allowed arcs-per-work-item for
 constexpr int kMinHeavyDeg = 128;     // smallest allowed heavy_degree (sizes the chunk records)
 constexpr int kMaxRoundStats = 4096;  // per-round statistics kept in the workspace
 constexpr int kCoreCap = 65536;       // JP core: at most this many vertices (u16 positions)
-constexpr int kBucketTarget = 8;      // mean bucket occupancy target of the priority-order sort
+#ifndef PGC_BUCKET_TARGET
+#define PGC_BUCKET_TARGET 8
+#endif
+constexpr int kBucketTarget = PGC_BUCKET_TARGET;  // mean bucket occupancy target of the priority-order sort
 constexpr int kScanTile = 4096;       // elements per block in the device-wide scan
 
 // Device-resident scalars of one call.  Lives at the head of the workspace.
