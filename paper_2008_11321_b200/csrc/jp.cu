@@ -975,6 +975,10 @@ __device__ __forceinline__ unsigned long long watch_key_of(int ru, uint64_t seed
 // (4 independent loads in flight per lane), mark colored ones in the byte map,
 // queue pending ones (id and watch key) in the warp's list.  Returns the index
 // to resume from when the pending list is full, np when every pred was examined.
+#ifndef PGC_HEAVY_STRIPS
+#define PGC_HEAVY_STRIPS 4
+#endif
+constexpr int kHS = PGC_HEAVY_STRIPS;  // strips of 32 preds in flight per heavy-scan step
 __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t pb, int np,
                                           int from, const int32_t* color,
                                           const int32_t* __restrict__ round, uint64_t seed,
@@ -982,23 +986,23 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
                                           unsigned long long* pkey, int& npend) {
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
-  for (int i0 = from; i0 < np; i0 += 128) {
-    int u[4], cc[4];
+  for (int i0 = from; i0 < np; i0 += 32 * kHS) {
+    int u[kHS], cc[kHS];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kHS; ++k) {
       const int i = i0 + 32 * k + lane;
       u[k] = i < np ? jp_stream(P + pb + i) : -1;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+    for (int k = 0; k < kHS; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
     // first keys of the pending preds, all four strips' loads in flight
     // before any is used (a load consumed in its own branch serialises)
-    int rk[4];
+    int rk[kHS];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)  // (no first key given: watch by hash alone)
+    for (int k = 0; k < kHS; ++k)  // (no first key given: watch by hash alone)
       rk[k] = round ? __ldg(round + (u[k] >= 0 && cc[k] == 0 ? u[k] : 0)) : 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < kHS; ++k) {
       const bool pend = u[k] >= 0 && cc[k] == 0;
       if (u[k] >= 0 && cc[k]) bmap_mark(bm, cc[k], wbase, kHeavyWin);
       const unsigned bal = __ballot_sync(0xffffffffu, pend);
