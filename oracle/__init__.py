@@ -42,6 +42,8 @@ def _load():
         lib.orc_adg_o.argtypes = [i64, vp, vp, u32, u32, vp, vp, vp, vp]
         lib.orc_jp_rho.restype = ctypes.c_int
         lib.orc_jp_rho.argtypes = [i64, vp, vp, vp, vp]
+        lib.orc_dec_adg_itr.restype = ctypes.c_int
+        lib.orc_dec_adg_itr.argtypes = [i64, vp, vp, vp, ctypes.c_int32, u64, vp, vp]
         lib.orc_adg_m.restype = ctypes.c_int
         lib.orc_adg_m.argtypes = [i64, vp, vp, vp, vp]
         lib.orc_jp.restype = ctypes.c_int
@@ -115,6 +117,20 @@ def jp_rho(g, rho):
     if K < 0:
         raise ValueError("oracle jp_rho: bad arguments")
     return color, int(K)
+
+
+def dec_adg_itr(g, rnd, seed: int):
+    """DEC-ADG-ITR colors for ADG rounds rnd.  Returns (color, K, passes)."""
+    off, col = _csr(g)
+    rnd = np.ascontiguousarray(rnd, dtype=np.int32)
+    color = np.zeros(g.n, dtype=np.int32)
+    passes = ctypes.c_int64(0)
+    T = int(rnd.max()) if g.n else 0
+    K = _load().orc_dec_adg_itr(g.n, _p(off), _p(col), _p(rnd), T, seed & 0xFFFFFFFFFFFFFFFF,
+                                _p(color), ctypes.addressof(passes))
+    if K < 0:
+        raise ValueError("oracle dec_adg_itr: bad arguments")
+    return color, int(K), int(passes.value)
 
 
 def adg_m(g):

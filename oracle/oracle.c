@@ -372,6 +372,98 @@ ORC_EXPORT int orc_jp_rho(int64_t n, const int64_t* off, const int32_t* col, con
 }
 
 /* ------------------------------------------------------------------------ */
+/* DEC-ADG-ITR: DEC-ADG (Algorithm "DEC-ADG",
+ * PAPER.md:1346-1369) with SIM-COL changed in its Part 1:
+ * "colors are not picked randomly, but we choose the smallest color not in
+ * B_v".
+ *
+ *   C = 0; rho = ADG(G)                      (partitions R(l) = {v : rho(v) = l})
+ *   for l = T down to 1:                     (the densest partition first)
+ *     B_v = colors of v's neighbours in the colored partitions Q (1366-1368)
+ *     SIM-COL-ITR(G(l), B):  U = R(l)
+ *       while U != {}:
+ *         Part 1: for v in U: C[v] = min({1, 2, ...} \ B_v)
+ *         Part 2: for v in U: if some u in N_U(v) has C[u] == C[v]: C[v] = 0
+ *         Part 3: for v in U, u in N_U(v): if C[u] > 0: B_v = B_v u {C[u]}
+ *         U = U \ {v in U : C[v] > 0}
+ *
+ * Reading Q23: with Part 1 deterministic, two adjacent vertices
+ * with equal B would pick the same color forever (SIM-COL's random choice is
+ * what breaks that tie), so Part 2 resets v only for a same-colored active
+ * neighbour u of HIGHER priority, h(u) > h(v) with h(x) = splitmix64(seed ^ x)
+ * (the tie-break of JP-ADG; ITR resolves conflicts the same way, one endpoint
+ * keeping its color).  The highest-priority vertex of U always keeps its color,
+ * so every pass fixes at least one vertex.  Reading Q24: ADG runs with the
+ * caller's eps (the eps/12 of DEC-ADG's listing is a proof device, 1391-1393).
+ * B_v is exactly the set of colors of v's fixed neighbours, so Part 1 is the
+ * mex over the neighbours colored so far (earlier partitions and earlier
+ * passes).  Returns K; passes_out (optional) receives the total number of
+ * SIM-COL passes over all partitions.                                         */
+ORC_EXPORT int orc_dec_adg_itr(int64_t n, const int64_t* off, const int32_t* col,
+                               const int32_t* round, int32_t T, uint64_t seed,
+                               int32_t* color_out, int64_t* passes_out) {
+  if (n < 0) return -1;
+  int32_t* tent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+  char* active = (char*)malloc((size_t)n + 1);
+  int64_t* U = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* W = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* stamp = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 2));
+  for (int64_t i = 0; i < n + 2; ++i) stamp[i] = -1;
+  for (int64_t v = 0; v < n; ++v) { color_out[v] = 0; active[v] = 0; }
+  int32_t K = 0;
+  int64_t passes = 0, tick = 0;
+  for (int32_t l = T; l >= 1; --l) {
+    int64_t sizeU = 0;
+    for (int64_t v = 0; v < n; ++v)
+      if (round[v] == l) { U[sizeU++] = v; active[v] = 1; }
+    while (sizeU > 0) {
+      passes += 1;
+      /* Part 1: C[v] = smallest color not in B_v (the fixed neighbours' colors) */
+      for (int64_t i = 0; i < sizeU; ++i) {
+        int64_t v = U[i];
+        tick += 1;
+        for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+          int64_t u = col[e];
+          if (color_out[u] > 0 && color_out[u] <= n + 1) stamp[color_out[u]] = tick;
+        }
+        int32_t c = 1;
+        while (stamp[c] == tick) ++c;
+        tent[v] = c;
+      }
+      /* Part 2: reset on a same-colored active neighbour of higher priority (Q23) */
+      int64_t k = 0, nw = 0;
+      for (int64_t i = 0; i < sizeU; ++i) {
+        int64_t v = U[i];
+        int keep = 1;
+        const uint64_t hv = orc_splitmix64(seed ^ (uint64_t)v);
+        for (int64_t e = off[v]; e < off[v + 1] && keep; ++e) {
+          int64_t u = col[e];
+          if (active[u] && tent[u] == tent[v] && orc_splitmix64(seed ^ (uint64_t)u) > hv) keep = 0;
+        }
+        if (keep) W[nw++] = v;   /* C[v] stays: v is colored */
+        else U[k++] = v;         /* C[v] = 0: v stays in U */
+      }
+      /* Part 3 and U = U \ {colored}: the colored ones leave U; their colors
+       * reach the neighbours' B_v through Part 1's mex over colored neighbours */
+      for (int64_t i = 0; i < nw; ++i) {
+        const int64_t v = W[i];
+        color_out[v] = tent[v];
+        active[v] = 0;
+        if (tent[v] > K) K = tent[v];
+      }
+      sizeU = k;
+    }
+  }
+  free(tent);
+  free(active);
+  free(U);
+  free(W);
+  free(stamp);
+  if (passes_out) *passes_out = passes;
+  return K;
+}
+
+/* ------------------------------------------------------------------------ */
 /* JP priority rho = <rho_ADG, rho_R>, lexicographic (PAPER.md:1073-1078,
  * 1095-1096): u has higher priority than v iff
  *   round[u] > round[v], or round[u] == round[v] and h(u) > h(v),
