@@ -50,10 +50,11 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline (for ncu runs)")
     ap.add_argument("--method", choices=["jp-adg", "jp-adg-m", "jp-adg-o", "jp-r", "jp-ff", "jp-lf",
-                                         "jp-llf"], default="jp-adg",
+                                         "jp-llf", "dec-adg-itr"], default="jp-adg",
                     help="jp-adg-m: the median variant (SURVEY.md §8(f) NEXT-3, PAPER.md:2273-2303); "
                          "jp-adg-o: ADG-O's total order (NEXT-1, PAPER.md:2397-2453); "
-                         "jp-r/ff/lf/llf: the JP baselines (NEXT-4, PAPER.md:1093-1103)")
+                         "jp-r/ff/lf/llf: the JP baselines (NEXT-4, PAPER.md:1093-1103); "
+                         "dec-adg-itr: DEC-ADG-ITR (NEXT-2, PAPER.md:1957-1972)")
     return ap.parse_args()
 
 
@@ -245,8 +246,11 @@ def run_pgc(args):
     median = args.method == "jp-adg-m"
     sortedR = args.method == "jp-adg-o"
     baseline = args.method in ("jp-r", "jp-ff", "jp-lf", "jp-llf")
+    decitr = args.method == "dec-adg-itr"
 
     def step():
+        if decitr:
+            return pgc.color_dec_adg_itr(off, col, num, den, args.seed, round_out=rnd, color_out=color)
         if baseline:
             c_, K_ = pgc.jp_baseline(off, col, args.method, args.seed, color_out=color)
             return rnd, c_, 0, K_
@@ -323,11 +327,13 @@ def run_pgc(args):
         "metric": (METRIC.replace("JP-ADG", "JP-ADG-M").replace("ADG+JP", "ADG-M+JP") if median else
                    METRIC.replace("JP-ADG", "JP-ADG-O").replace("ADG+JP", "ADG-O+JP") if sortedR else
                    METRIC.replace("JP-ADG", args.method.upper()).replace("ADG+JP", "JP only")
-                   if baseline else METRIC),
+                   if baseline else
+                   METRIC.replace("JP-ADG", "DEC-ADG-ITR").replace("ADG+JP", "ADG+SIM-COL-ITR")
+                   if decitr else METRIC),
         "value": job_value(world, m, ms), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.config}-{args.method}" if baseline else
+        "config": {"workload": f"{args.config}-{args.method}" if (baseline or decitr) else
                    f"{args.config}-adgm" if median else
                    f"{args.config}-adgo-eps{num}/{den}" if sortedR else f"{args.config}-eps{num}/{den}",
                    "method": args.method, "n": n, "m": m, "nnz": nnz,
@@ -349,7 +355,7 @@ def run_pgc(args):
     }
 
     # ---- end to end through the host-buffer C-ABI call ----
-    if not (args.no_e2e or args.quick or median or sortedR or baseline):
+    if not (args.no_e2e or args.quick or median or sortedR or baseline or decitr):
         h_off = torch.from_numpy(g.off).pin_memory()
         h_col = torch.from_numpy(g.col).pin_memory()
         h_r = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -386,7 +392,10 @@ def run_pgc(args):
         else:
             r_or, _ = O.adg_m(g) if median else O.adg(g, num, den)
         t1 = time.perf_counter()
-        c_or, K_or = O.jp_rho(g, rho) if sortedR else O.jp(g, r_or, args.seed)
+        if decitr:
+            c_or, K_or, _ = O.dec_adg_itr(g, r_or, args.seed)
+        else:
+            c_or, K_or = O.jp_rho(g, rho) if sortedR else O.jp(g, r_or, args.seed)
         t2 = time.perf_counter()
         out["cpu_baseline"] = {"value": m / (t2 - t0), "unit": "edges/s", "cores": 1,
                                "kind": "oracle",

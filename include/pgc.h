@@ -89,7 +89,7 @@ typedef struct pgc_stats {
   int32_t kernel_launches; /* CUDA kernels this call launched                             */
   int32_t host_syncs;      /* stream synchronisations this call performed                 */
   int32_t core_ctas;       /* JP: thread-block cluster size of the core engine (0 = none) */
-  int32_t pad0;
+  int32_t sim_col_passes;  /* DEC-ADG-ITR: SIM-COL passes over all partitions (else 0)    */
   /* Device time per kernel group, from CUDA events on the call's stream; all -1
    * unless pgc_set_tuning("timing", 1).  Groups: ADG select (a2/a3), ADG UPDATE
    * with fused JP Part 1 (a4/a7), other ADG kernels (init, finalize), the
@@ -180,6 +180,20 @@ int pgc_color_jp_adg_o(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, i
 enum pgc_jp_kind { PGC_JP_R = 0, PGC_JP_FF = 1, PGC_JP_LF = 2, PGC_JP_LLF = 3 };
 int pgc_jp_baseline(const pgc_graph* g, int kind, uint64_t seed, int32_t* color_out,
                     int32_t* num_colors, void* workspace, size_t workspace_bytes, void* cuda_stream);
+
+/* DEC-ADG-ITR: ADG's rounds as partitions R(T), ..., R(1),
+ * colored in that order by SIM-COL with ITR's Part 1: each
+ * uncolored vertex of the partition takes the smallest color no colored
+ * neighbour uses; a vertex keeps it unless an uncolored same-partition
+ * neighbour took the same color and has a larger splitmix64(seed ^ v) (the
+ * conflict rule, reading Q23); repeat until the partition is colored.  At most
+ * floor(2(1+eps)d) + 1 colors (the bound of JP-ADG).
+ *   round_out, color_out : device int32[n]
+ *   num_rounds, num_colors : host int32*;  pgc_last_stats().sim_col_passes */
+int pgc_color_dec_adg_itr(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uint64_t seed,
+                          int32_t* round_out, int32_t* color_out, int32_t* num_rounds,
+                          int32_t* num_colors, void* workspace, size_t workspace_bytes,
+                          void* cuda_stream);
 
 /* JP-ADG end to end from HOST memory: copies the CSR host->device on
  * `cuda_stream`, runs pgc_color_jp_adg, copies round[] and color[] back.

@@ -28,6 +28,7 @@ PGC_OK, PGC_EINVAL, PGC_EWORKSPACE, PGC_ECUDA, PGC_EINTERNAL = 0, 1, 2, 3, 4
 
 EXPORTS = ["pgc_workspace_bytes", "pgc_adg_order", "pgc_jp_color", "pgc_color_jp_adg",
            "pgc_adg_m_order", "pgc_color_jp_adg_m", "pgc_color_jp_adg_o", "pgc_jp_baseline",
+           "pgc_color_dec_adg_itr",
            "pgc_host_workspace_bytes", "pgc_color_jp_adg_host", "pgc_check_graph",
            "pgc_last_stats", "pgc_last_error", "pgc_set_tuning", "pgc_version",
            "pgc_debug_set_trace"]
@@ -43,7 +44,7 @@ class Stats(ctypes.Structure):
                 ("sum_active", ctypes.c_int64), ("cross_edges", ctypes.c_int64),
                 ("pred_arcs", ctypes.c_int64), ("core_vertices", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int32), ("host_syncs", ctypes.c_int32),
-                ("core_ctas", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("core_ctas", ctypes.c_int32), ("sim_col_passes", ctypes.c_int32),
                 ("t_select_ms", ctypes.c_float), ("t_update_ms", ctypes.c_float),
                 ("t_adg_other_ms", ctypes.c_float), ("t_order_ms", ctypes.c_float),
                 ("t_core_ms", ctypes.c_float), ("t_jp_ms", ctypes.c_float),
@@ -72,6 +73,8 @@ _lib.pgc_color_jp_adg_o.restype = ctypes.c_int
 _lib.pgc_color_jp_adg_o.argtypes = [_GP, _u32, _u32, _vp, _vp, _i32p, _i32p, _vp, _sz, _vp]
 _lib.pgc_jp_baseline.restype = ctypes.c_int
 _lib.pgc_jp_baseline.argtypes = [_GP, ctypes.c_int, _u64, _vp, _i32p, _vp, _sz, _vp]
+_lib.pgc_color_dec_adg_itr.restype = ctypes.c_int
+_lib.pgc_color_dec_adg_itr.argtypes = [_GP, _u32, _u32, _u64, _vp, _vp, _i32p, _i32p, _vp, _sz, _vp]
 _lib.pgc_color_jp_adg_host.restype = ctypes.c_int
 _lib.pgc_color_jp_adg_host.argtypes = [_i64, _i64, _vp, _vp, _u32, _u32, _u64, _vp, _vp, _i32p,
                                        _i32p, _vp, _sz, _vp]
@@ -281,6 +284,22 @@ def jp_baseline(row_offsets, col_indices, kind: str, seed: int, *, color_out=Non
                                 color.data_ptr() if g.n else None, ctypes.byref(K), ws.data_ptr(),
                                 ws.numel(), _stream(dev)))
     return color, K.value
+
+
+def color_dec_adg_itr(row_offsets, col_indices, eps_num: int, eps_den: int, seed: int, *,
+                      round_out=None, color_out=None):
+    """DEC-ADG-ITR (PAPER.md:1957-1972).  Returns (round, color, T, K)."""
+    g = _graph(row_offsets, col_indices)
+    dev = row_offsets.device
+    rnd = _out(round_out, g.n, dev, "round_out")
+    color = _out(color_out, g.n, dev, "color_out")
+    ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
+    T, K = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(_lib.pgc_color_dec_adg_itr(ctypes.byref(g), eps_num, eps_den, seed & 0xFFFFFFFFFFFFFFFF,
+                                      rnd.data_ptr() if g.n else None,
+                                      color.data_ptr() if g.n else None, ctypes.byref(T),
+                                      ctypes.byref(K), ws.data_ptr(), ws.numel(), _stream(dev)))
+    return rnd, color, T.value, K.value
 
 
 def color_jp_adg_host(row_offsets, col_indices, eps_num: int, eps_den: int, seed: int,

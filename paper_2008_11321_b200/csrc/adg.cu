@@ -54,7 +54,7 @@ __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ o
     round[v] = 0;
     if (color) {
       color[v] = d == 0 ? 1 : 0;
-      if (d == 0) npred[v] = -1;
+      npred[v] = d == 0 ? -1 : 0;  // (the fused UPDATE overwrites it with |pred(v)|)
     }
   }
   if (filt)

@@ -218,6 +218,7 @@ static void call_end(Ctx& c, int rounds, int colors, long long sum_active,
   g_stats.core_ctas = c.core_ctas;
   g_stats.kernel_launches = c.launches;
   g_stats.host_syncs = c.syncs;
+  g_stats.sim_col_passes = 0;
   float t[kNumGroups] = {-1.f, -1.f, -1.f, -1.f, -1.f, -1.f};
   float total = -1.f;
   if (g_log.on) {
@@ -415,6 +416,38 @@ int pgc_jp_baseline(const pgc_graph* g, int kind, uint64_t seed, int32_t* color_
   if (int e = jp_color_run(c, color_out)) return e;
   *num_colors = c.h_state->K;
   call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.core_n);
+  return PGC_OK;
+}
+
+int pgc_color_dec_adg_itr(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, uint64_t seed,
+                          int32_t* round_out, int32_t* color_out, int32_t* num_rounds,
+                          int32_t* num_colors, void* workspace, size_t workspace_bytes,
+                          void* cuda_stream) {
+  if (int e = check_graph_args(g)) return e;
+  if (eps_num == 0 || eps_den == 0) return fail(PGC_EINVAL, "eps must be num/den with num, den >= 1");
+  if (!num_rounds || !num_colors || (g->n > 0 && (!round_out || !color_out)))
+    return fail(PGC_EINVAL, "output pointer is NULL");
+  if (int e = check_ws(g, workspace, workspace_bytes)) return e;
+  Ctx c;
+  if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
+  call_begin(c);
+  if (int e = adg_run(c, eps_num, eps_den, seed, round_out, kAdgOnly, color_out)) return e;
+  const int T = c.h_state->T;
+  const long long sum_active = c.h_state->sum_active;
+  const unsigned long long cross = c.h_state->cross;
+  // the partitions R(T), ..., R(1) as ranges of the priority order
+  if (int e = jp_order_run(c, round_out, seed, true)) return e;
+  PGC_CUDA(cudaMemsetAsync(&c.state->K, 0, sizeof(int), c.st));
+  if (g->n > 0) {  // nonempty graph: K >= 1 (isolated vertices already hold color 1)
+    const int one = 1;
+    PGC_CUDA(cudaMemcpyAsync(&c.state->K, &one, sizeof(int), cudaMemcpyHostToDevice, c.st));
+  }
+  long long passes = 0;
+  if (int e = dec_itr_run(c, round_out, seed, color_out, &passes)) return e;
+  *num_rounds = T;
+  *num_colors = c.h_state->K;
+  call_end(c, T, c.h_state->K, sum_active, cross, 0, 0);
+  g_stats.sim_col_passes = (int32_t)(passes > 0x7fffffff ? 0x7fffffff : passes);
   return PGC_OK;
 }
 

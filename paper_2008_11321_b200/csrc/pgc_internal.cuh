@@ -148,6 +148,7 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
 int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color);
 int adg_o_keys(Ctx& c, const int32_t* round, int32_t* key1);
 int baseline_key_run(Ctx& c, int kind, int32_t* key);
+int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, long long* passes);
 int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known, bool idkey = false);
 int jp_color_run(Ctx& c, int32_t* color);
 int check_graph_run(Ctx& c, int64_t* bad_vertex);

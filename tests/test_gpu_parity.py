@@ -390,3 +390,43 @@ def test_jp_baselines(kind):
         bad = np.nonzero(color.cpu().numpy() != c_or)[0]
         assert len(bad) == 0, f"{kind}: color mismatch at {bad[:10]}"
         assert K == K_or
+
+
+# ------------------------------------------------ DEC-ADG-ITR (NEXT-2) --------
+def assert_parity_dec(g, num, den, seed):
+    pgc, off, col = dev(g)
+    rnd, color, T, K = pgc.color_dec_adg_itr(off, col, num, den, seed)
+    torch.cuda.synchronize()
+    st = pgc.last_stats()
+    r_or, st_or = O.adg(g, num, den)
+    c_or, K_or, passes = O.dec_adg_itr(g, r_or, seed)
+    assert T == st_or["T"] and np.array_equal(rnd.cpu().numpy(), r_or)
+    bad = np.nonzero(color.cpu().numpy() != c_or)[0]
+    assert len(bad) == 0, f"DEC-ADG-ITR color mismatch at {bad[:10]} gpu={color.cpu().numpy()[bad[:10]]} cpu={c_or[bad[:10]]}"
+    assert K == K_or
+    return T, K
+
+
+def test_dec_adg_itr_small_graphs():
+    for n in range(0, 6):
+        es, base = [], 0
+        for edges in all_graphs(n):
+            es += [(a + base, b + base) for a, b in edges]
+            base += n
+        for num, den in [(1, 10), (1, 2)]:
+            for seed in (1, 2):
+                assert_parity_dec(gg.from_edges(base, es), num, den, seed)
+    n = 40
+    assert_parity_dec(gg.from_edges(n, [(i, j) for i in range(n) for j in range(i + 1, n)]), 1, 10, 3)
+
+
+@pytest.mark.parametrize("name", ["er", "rmat", "grid", "edgeless"])
+def test_dec_adg_itr_random(name):
+    g = {"er": lambda: gg.er(20000, 160000, 5), "rmat": lambda: gg.rmat(15, 16, seed=2),
+         "grid": lambda: gg.grid(256, seed=4), "edgeless": lambda: gg.from_edges(1000, [])}[name]()
+    for num, den in [(1, 100), (1, 10), (1, 2)]:
+        assert_parity_dec(g, num, den, 7)
+
+
+def test_dec_adg_itr_rmat20():
+    assert_parity_dec(gg.config_graph("rmat20"), 1, 10, 1)
