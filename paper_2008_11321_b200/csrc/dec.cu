@@ -29,12 +29,89 @@ constexpr int kItrWin = 1024;  // colors per byte-map window (Part 1)
 constexpr int kItrBlock = 256;
 constexpr int kItrBatch = 16;  // passes between host synchronisations
 
-// Part 1
+// Partition start (warp per vertex of R(l)): one scan of the full adjacency.
+// B_v so far = the colors of v's neighbours in the colored partitions Q; it
+// is summarised by base[v] = mex(B_v) and the 64-bit mask freem[v] of the
+// colors base..base+63 NOT in B_v.  The neighbours inside R(l) are listed in
+// v's own CSR slot of P (count icnt[v]): every pass only touches those.
+__global__ void __launch_bounds__(kItrBlock) k_itr_prep(int l, const int64_t* __restrict__ off,
+                                                        const int32_t* __restrict__ col,
+                                                        const int32_t* __restrict__ round,
+                                                        const int32_t* color,
+                                                        const int32_t* __restrict__ A,
+                                                        const int* __restrict__ nA,
+                                                        int32_t* __restrict__ P,
+                                                        int32_t* __restrict__ icnt,
+                                                        int32_t* __restrict__ base,
+                                                        unsigned long long* __restrict__ freem) {
+  __shared__ __align__(16) uint8_t s_bm[kItrBlock / 32][kItrWin];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  uint8_t* bm = s_bm[warp];
+  const int na = *nA;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nw) {
+    const int v = A[i];
+    const int64_t b = off[v], e = off[v + 1];
+    int bs = 0;
+    unsigned long long fm = 0;
+    for (int wbase = 0;; wbase += kItrWin) {
+      for (int j = lane; j < kItrWin / 16; j += 32) reinterpret_cast<uint4*>(bm)[j] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      int cnt = 0;
+      for (int64_t a0 = b; a0 < e; a0 += 32) {
+        const int64_t a = a0 + lane;
+        const int u = a < e ? __ldg(col + a) : -1;
+        const int c = u >= 0 ? color[u] : 0;
+        const int k = c - wbase - 1;
+        if (c > 0 && k >= 0 && k < kItrWin) bm[k] = 1;
+        if (wbase == 0) {  // intra-partition neighbours, listed once
+          const bool in = u >= 0 && round[u] == l;
+          const unsigned bal = __ballot_sync(0xffffffffu, in);
+          if (in) P[b + cnt + __popc(bal & lt)] = u;
+          cnt += __popc(bal);
+        }
+      }
+      if (wbase == 0 && lane == 0) icnt[v] = cnt;
+      __syncwarp();
+      int z = -1;
+      for (int b0 = 0; b0 < kItrWin && z < 0; b0 += 32) {
+        const unsigned m = __ballot_sync(0xffffffffu, bm[b0 + lane] == 0);
+        if (m) z = b0 + __ffs(m) - 1;
+      }
+      if (z >= 0) {  // mex found in this window; the free mask of the next 64 colors
+        bs = wbase + z + 1;
+        const int k0 = z + lane, k1 = z + 32 + lane;
+        // (colors past the window count as taken: a pass whose candidates run
+        // out rescans and refreshes the summary)
+        const unsigned lo = __ballot_sync(0xffffffffu, k0 < kItrWin && bm[k0] == 0);
+        const unsigned hi = __ballot_sync(0xffffffffu, k1 < kItrWin && bm[k1] == 0);
+        fm = ((unsigned long long)hi << 32) | lo;
+        break;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      base[v] = bs;
+      freem[v] = fm;
+    }
+  }
+}
+
+// Part 1: tent[v] = the smallest color free in B_v and not taken by an
+// intra-partition neighbour colored in an earlier pass: from the cached 64
+// candidates, else (all taken -- a dense partition) a rescan of the whole
+// adjacency that also refreshes base/freem from every colored neighbour, so
+// the next 64 passes of v are cheap again.
 __global__ void __launch_bounds__(kItrBlock) k_itr_tent(const int64_t* __restrict__ off,
                                                         const int32_t* __restrict__ col,
                                                         const int32_t* color,
                                                         const int32_t* __restrict__ A,
                                                         const int* __restrict__ nA,
+                                                        const int32_t* __restrict__ P,
+                                                        const int32_t* __restrict__ icnt,
+                                                        int32_t* __restrict__ base,
+                                                        unsigned long long* __restrict__ freem,
                                                         int32_t* __restrict__ tent) {
   __shared__ __align__(16) uint8_t s_bm[kItrBlock / 32][kItrWin];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -43,37 +120,66 @@ __global__ void __launch_bounds__(kItrBlock) k_itr_tent(const int64_t* __restric
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nw) {
     const int v = A[i];
-    const int64_t b = off[v], e = off[v + 1];
+    const int64_t b = off[v];
+    const int ni = icnt[v], bs = base[v];
+    unsigned long long taken = 0;
+    for (int j0 = 0; j0 < ni; j0 += 32) {
+      const int j = j0 + lane;
+      const int c = j < ni ? color[__ldg(P + b + j)] : 0;
+      const int d = c - bs;
+      if (c > 0 && d >= 0 && d < 64) taken |= 1ull << d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) taken |= __shfl_xor_sync(0xffffffffu, taken, o);
+    const unsigned long long g = freem[v] & ~taken;
     int found = 0;
-    for (int wbase = 0; !found; wbase += kItrWin) {
-      for (int j = lane; j < kItrWin / 16; j += 32) reinterpret_cast<uint4*>(bm)[j] = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      for (int64_t a0 = b; a0 < e; a0 += 32) {
-        const int64_t a = a0 + lane;
-        const int u = a < e ? __ldg(col + a) : -1;
-        const int c = u >= 0 ? color[u] : 0;
-        const int k = c - wbase - 1;
-        if (c > 0 && k >= 0 && k < kItrWin) bm[k] = 1;
+    if (g) {
+      found = bs + __ffsll((long long)g) - 1;
+    } else {  // rescan everything and refresh the summary
+      const int64_t e = off[v + 1];
+      unsigned long long fm = 0;
+      for (int wbase = 0; !found; wbase += kItrWin) {
+        for (int j = lane; j < kItrWin / 16; j += 32) reinterpret_cast<uint4*>(bm)[j] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+        for (int64_t a0 = b; a0 < e; a0 += 32) {
+          const int64_t a = a0 + lane;
+          const int u = a < e ? __ldg(col + a) : -1;
+          const int c = u >= 0 ? color[u] : 0;
+          const int k = c - wbase - 1;
+          if (c > 0 && k >= 0 && k < kItrWin) bm[k] = 1;
+        }
+        __syncwarp();
+        int z = -1;
+        for (int b0 = 0; b0 < kItrWin && z < 0; b0 += 32) {
+          const unsigned m = __ballot_sync(0xffffffffu, bm[b0 + lane] == 0);
+          if (m) z = b0 + __ffs(m) - 1;
+        }
+        if (z >= 0) {
+          found = wbase + z + 1;
+          const int k0 = z + lane, k1 = z + 32 + lane;
+          const unsigned lo = __ballot_sync(0xffffffffu, k0 < kItrWin && bm[k0] == 0);
+          const unsigned hi = __ballot_sync(0xffffffffu, k1 < kItrWin && bm[k1] == 0);
+          fm = ((unsigned long long)hi << 32) | lo;
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      for (int b0 = 0; b0 < kItrWin && !found; b0 += 32) {
-        const unsigned m = __ballot_sync(0xffffffffu, bm[b0 + lane] == 0);
-        if (m) found = wbase + b0 + __ffs(m);
+      if (lane == 0) {
+        base[v] = found;
+        freem[v] = fm;
       }
-      __syncwarp();
     }
     if (lane == 0) tent[v] = found;
   }
 }
 
-// Part 2
-__global__ void __launch_bounds__(kItrBlock) k_itr_conflict(int l, uint64_t seed,
+// Part 2: only the intra-partition neighbours can be active
+__global__ void __launch_bounds__(kItrBlock) k_itr_conflict(uint64_t seed,
                                                             const int64_t* __restrict__ off,
-                                                            const int32_t* __restrict__ col,
-                                                            const int32_t* __restrict__ round,
                                                             const int32_t* color,
                                                             const int32_t* __restrict__ A,
                                                             const int* __restrict__ nA,
+                                                            const int32_t* __restrict__ P,
+                                                            const int32_t* __restrict__ icnt,
                                                             const int32_t* __restrict__ tent,
                                                             uint8_t* __restrict__ won) {
   const int lane = threadIdx.x & 31;
@@ -83,14 +189,15 @@ __global__ void __launch_bounds__(kItrBlock) k_itr_conflict(int l, uint64_t seed
     const int v = A[i];
     const int tv = tent[v];
     const uint64_t hv = prio_hash(seed, (uint32_t)v);
-    const int64_t b = off[v], e = off[v + 1];
+    const int64_t b = off[v];
+    const int ni = icnt[v];
     bool lose = false;
-    for (int64_t a0 = b; a0 < e && !lose; a0 += 32) {
-      const int64_t a = a0 + lane;
+    for (int j0 = 0; j0 < ni && !lose; j0 += 32) {
+      const int j = j0 + lane;
       bool x = false;
-      if (a < e) {
-        const int u = __ldg(col + a);
-        if (round[u] == l && color[u] == 0 && tent[u] == tv) x = prio_hash(seed, (uint32_t)u) > hv;
+      if (j < ni) {
+        const int u = __ldg(P + b + j);
+        if (color[u] == 0 && tent[u] == tv) x = prio_hash(seed, (uint32_t)u) > hv;
       }
       lose = __any_sync(0xffffffffu, x);
     }
@@ -152,26 +259,35 @@ int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, lon
   std::vector<int> cnt(T + 1, 0);
   PGC_CUDA(cudaMemcpyAsync(cnt.data(), c.hist1, sizeof(int) * (size_t)T, cudaMemcpyDeviceToHost, c.st));
   PGC_CUDA(cudaStreamSynchronize(c.st));
+  // scratch (ADG's and the order's arrays are free now)
   int32_t* A[2] = {c.U[0], c.U[1]};
-  int* nA = reinterpret_cast<int*>(c.Rl);  // two counters (ADG's lists are free)
+  int* nA = c.hist1;                 // two list counters
   int32_t* tent = c.D;
   uint8_t* won = c.rs;
+  int32_t* icnt = c.npred;
+  int32_t* base = c.Rl;
+  unsigned long long* freem = reinterpret_cast<unsigned long long*>(c.bcnt);  // >= 2n + 2 ints
+  int32_t* intra = c.P;               // intra-partition neighbours, in each vertex's CSR slot
   const int G = c.nsm * 8;
-  int base = 0;
+  int pbase = 0;
   for (int l = T; l >= 1; --l) {
     const int cl = cnt[T - l];
     if (cl == 0) continue;
     int cur = 0;
     PGC_LAUNCH(c, kGJp, "k_itr_init",
-               k_itr_init<<<G, 256, 0, c.st>>>(c.rec, base, cl, A[0], nA, nA + 1));
-    base += cl;
+               k_itr_init<<<G, 256, 0, c.st>>>(c.rec, pbase, cl, A[0], nA, nA + 1));
+    pbase += cl;
+    PGC_LAUNCH(c, kGJp, "k_itr_prep",
+               k_itr_prep<<<G, kItrBlock, 0, c.st>>>(l, c.off, c.col, round, color, A[0], nA, intra,
+                                                      icnt, base, freem));
     for (;;) {
       for (int j = 0; j < kItrBatch; ++j) {
         PGC_LAUNCH(c, kGJp, "k_itr_tent",
-                   k_itr_tent<<<G, kItrBlock, 0, c.st>>>(c.off, c.col, color, A[cur], nA + cur, tent));
+                   k_itr_tent<<<G, kItrBlock, 0, c.st>>>(c.off, c.col, color, A[cur], nA + cur,
+                                                          intra, icnt, base, freem, tent));
         PGC_LAUNCH(c, kGJp, "k_itr_conflict",
-                   k_itr_conflict<<<G, kItrBlock, 0, c.st>>>(l, seed, c.off, c.col, round, color,
-                                                              A[cur], nA + cur, tent, won));
+                   k_itr_conflict<<<G, kItrBlock, 0, c.st>>>(seed, c.off, color, A[cur], nA + cur,
+                                                              intra, icnt, tent, won));
         PGC_LAUNCH(c, kGJp, "k_itr_apply",
                    k_itr_apply<<<G, kItrBlock, 0, c.st>>>(A[cur], nA + cur, tent, won, color,
                                                            A[cur ^ 1], nA + (cur ^ 1), c.state));
