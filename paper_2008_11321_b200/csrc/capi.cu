@@ -558,6 +558,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"core_spin_ns", 0, 100000, nullptr, &g_tune.core_spin_ns},
       {"core_tail_ns", 0, 100000, nullptr, &g_tune.core_tail_ns},
       {"core_pass_ns", 0, 100000, nullptr, &g_tune.core_pass_ns},
+      {"itr_blocks_per_sm", 0, 64, nullptr, &g_tune.itr_blocks_per_sm},
       {"core_arc_cap", 0, 1ll << 40, &g_tune.core_arc_cap, nullptr},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };

@@ -5,19 +5,27 @@
 // tentative color up only to a same-colored active neighbour of larger
 // h = splitmix64(seed ^ v)).
 //
-// One SIM-COL pass over the active list A of partition l = three kernels:
-//   k_itr_tent     Part 1: tent[v] = mex of the colors of v's colored
-//                  neighbours (warp per vertex, shared-memory byte map window)
-//   k_itr_conflict Part 2: won[v] = no active neighbour u (round[u] == l,
-//                  color[u] == 0) has tent[u] == tent[v] and h(u) > h(v)
-//   k_itr_apply    Part 3 + U = U \ {colored}: color[v] = tent[v] for the
-//                  winners (their colors reach the neighbours' B through the
-//                  next Part 1), the others are compacted into the next list.
-// The winners' colors are written only in k_itr_apply, so "active" in Part 2
-// is the state at the start of the pass, as in the listing.  Passes run in
-// batches between host synchronisations; a pass on an empty list exits at
-// once.  The partitions are contiguous ranges of the priority order
-// (jp_order_run sorts by round).
+// One persistent cooperative kernel per partition (no launch per pass):
+//   prep           B_v so far (the colors of v's neighbours in the colored
+//                  partitions) summarised as base = mex(B_v) and a 64-bit mask
+//                  of the free colors base..base+63; v's neighbours inside
+//                  R(l) listed in its CSR slot of P (every pass reads only those)
+//   loop over SIM-COL passes while the active list A is not empty:
+//     Part 1       tent[v] = the smallest cached candidate not taken by an
+//                  intra-partition neighbour colored in an earlier pass (all 64
+//                  taken -- a dense partition -- : rescan, refresh the summary)
+//     Part 2       won[v] = no active intra-partition neighbour u (color[u] ==
+//                  0) has tent[u] == tent[v] and h(u) > h(v)
+//     Part 3       color[v] = tent[v] for the winners (their colors reach the
+//                  neighbours' B through the next Part 1), the others are
+//                  compacted into the next list (U = U \ {colored})
+//   with a grid barrier between the parts, so "active" in Part 2 is the state
+//   at the start of the pass, as in the listing.  Data written by other blocks
+//   is read with ld.cg (L1 is not coherent inside one kernel).
+// The partitions are contiguous ranges of the priority order (jp_order_run
+// sorts by round).
+#include <cooperative_groups.h>
+
 #include <cstdio>
 #include <vector>
 
@@ -25,230 +33,199 @@
 
 namespace pgc {
 
-constexpr int kItrWin = 1024;  // colors per byte-map window (Part 1)
-constexpr int kItrBlock = 256;
-constexpr int kItrBatch = 16;  // passes between host synchronisations
+namespace cg = cooperative_groups;
 
-// Partition start (warp per vertex of R(l)): one scan of the full adjacency.
-// B_v so far = the colors of v's neighbours in the colored partitions Q; it
-// is summarised by base[v] = mex(B_v) and the 64-bit mask freem[v] of the
-// colors base..base+63 NOT in B_v.  The neighbours inside R(l) are listed in
-// v's own CSR slot of P (count icnt[v]): every pass only touches those.
-__global__ void __launch_bounds__(kItrBlock) k_itr_prep(int l, const int64_t* __restrict__ off,
-                                                        const int32_t* __restrict__ col,
-                                                        const int32_t* __restrict__ round,
-                                                        const int32_t* color,
-                                                        const int32_t* __restrict__ A,
-                                                        const int* __restrict__ nA,
-                                                        int32_t* __restrict__ P,
-                                                        int32_t* __restrict__ icnt,
-                                                        int32_t* __restrict__ base,
-                                                        unsigned long long* __restrict__ freem) {
+constexpr int kItrWin = 1024;  // colors per byte-map window
+constexpr int kItrBlock = 256;
+
+__device__ __forceinline__ int ldcg(const int32_t* p) { return __ldcg(p); }
+
+// mex over the colors of ALL colored neighbours of v (a warp, byte-map windows);
+// also the free mask of the 64 colors from the mex on (bits past the window: taken)
+__device__ __forceinline__ int itr_full_mex(const int64_t* __restrict__ off,
+                                            const int32_t* __restrict__ col, const int32_t* color,
+                                            int v, uint8_t* bm, unsigned long long& fm) {
+  const int lane = lane_id();
+  const int64_t b = off[v], e = off[v + 1];
+  int found = 0;
+  fm = 0;
+  for (int wbase = 0; !found; wbase += kItrWin) {
+    for (int j = lane; j < kItrWin / 16; j += 32) reinterpret_cast<uint4*>(bm)[j] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    // 8 strips of 32 arcs per step, all loads in flight (a hub's list is long)
+    for (int64_t a0 = b; a0 < e; a0 += 256) {
+      int u[8], c[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t x = a0 + 32 * k + lane;
+        u[k] = x < e ? __ldg(col + x) : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = u[k] >= 0 ? ldcg(color + u[k]) : 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int q = c[k] - wbase - 1;
+        if (c[k] > 0 && q >= 0 && q < kItrWin) bm[q] = 1;
+      }
+    }
+    __syncwarp();
+    int z = -1;
+    for (int b0 = 0; b0 < kItrWin && z < 0; b0 += 32) {
+      const unsigned m = __ballot_sync(0xffffffffu, bm[b0 + lane] == 0);
+      if (m) z = b0 + __ffs(m) - 1;
+    }
+    if (z >= 0) {
+      found = wbase + z + 1;
+      const int k0 = z + lane, k1 = z + 32 + lane;
+      const unsigned lo = __ballot_sync(0xffffffffu, k0 < kItrWin && bm[k0] == 0);
+      const unsigned hi = __ballot_sync(0xffffffffu, k1 < kItrWin && bm[k1] == 0);
+      fm = ((unsigned long long)hi << 32) | lo;
+    }
+    __syncwarp();
+  }
+  return found;
+}
+
+struct ItrArgs {
+  int l;
+  uint64_t seed;
+  const int64_t* off;
+  const int32_t* col;
+  const int32_t* round;
+  int32_t* color;
+  const int4* rec;
+  int pbase, cl;          // the partition: rec[pbase, pbase + cl)
+  int32_t* A[2];          // active lists
+  int* nA;                // their counters [2]
+  int32_t* P;             // intra-partition neighbour lists (CSR slots)
+  int32_t* icnt;
+  int32_t* base;
+  unsigned long long* freem;
+  int32_t* tent;
+  uint8_t* won;
+  State* st;
+  long long* passes;      // device counter
+};
+
+__global__ void __launch_bounds__(kItrBlock) k_itr_partition(ItrArgs a) {
   __shared__ __align__(16) uint8_t s_bm[kItrBlock / 32][kItrWin];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int sm[kItrBlock / 32 + 1];
+  cg::grid_group grid = cg::this_grid();
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   uint8_t* bm = s_bm[warp];
-  const int na = *nA;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nw) {
-    const int v = A[i];
-    const int64_t b = off[v], e = off[v + 1];
-    int bs = 0;
-    unsigned long long fm = 0;
-    for (int wbase = 0;; wbase += kItrWin) {
-      for (int j = lane; j < kItrWin / 16; j += 32) reinterpret_cast<uint4*>(bm)[j] = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      int cnt = 0;
-      for (int64_t a0 = b; a0 < e; a0 += 32) {
-        const int64_t a = a0 + lane;
-        const int u = a < e ? __ldg(col + a) : -1;
-        const int c = u >= 0 ? color[u] : 0;
-        const int k = c - wbase - 1;
-        if (c > 0 && k >= 0 && k < kItrWin) bm[k] = 1;
-        if (wbase == 0) {  // intra-partition neighbours, listed once
-          const bool in = u >= 0 && round[u] == l;
-          const unsigned bal = __ballot_sync(0xffffffffu, in);
-          if (in) P[b + cnt + __popc(bal & lt)] = u;
-          cnt += __popc(bal);
-        }
-      }
-      if (wbase == 0 && lane == 0) icnt[v] = cnt;
-      __syncwarp();
-      int z = -1;
-      for (int b0 = 0; b0 < kItrWin && z < 0; b0 += 32) {
-        const unsigned m = __ballot_sync(0xffffffffu, bm[b0 + lane] == 0);
-        if (m) z = b0 + __ffs(m) - 1;
-      }
-      if (z >= 0) {  // mex found in this window; the free mask of the next 64 colors
-        bs = wbase + z + 1;
-        const int k0 = z + lane, k1 = z + 32 + lane;
-        // (colors past the window count as taken: a pass whose candidates run
-        // out rescans and refreshes the summary)
-        const unsigned lo = __ballot_sync(0xffffffffu, k0 < kItrWin && bm[k0] == 0);
-        const unsigned hi = __ballot_sync(0xffffffffu, k1 < kItrWin && bm[k1] == 0);
-        fm = ((unsigned long long)hi << 32) | lo;
-        break;
-      }
-      __syncwarp();
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  const int gw = tid >> 5, nwarps = nt >> 5;
+  // the partition -> active list 0
+  for (int i = tid; i < a.cl; i += nt) a.A[0][i] = a.rec[a.pbase + i].x;
+  if (tid == 0) {
+    a.nA[0] = a.cl;
+    a.nA[1] = 0;
+  }
+  grid.sync();
+  // prep: summary of B_v and the intra-partition lists
+  for (int i = gw; i < a.cl; i += nwarps) {
+    const int v = ldcg(a.A[0] + i);
+    const int64_t b = a.off[v], e = a.off[v + 1];
+    int cnt = 0;
+    for (int64_t a0 = b; a0 < e; a0 += 32) {
+      const int64_t x = a0 + lane;
+      const int u = x < e ? __ldg(a.col + x) : -1;
+      const bool in = u >= 0 && a.round[u] == a.l;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      if (in) a.P[b + cnt + __popc(bal & lt)] = u;
+      cnt += __popc(bal);
     }
+    unsigned long long fm;
+    const int bs = itr_full_mex(a.off, a.col, a.color, v, bm, fm);
     if (lane == 0) {
-      base[v] = bs;
-      freem[v] = fm;
+      a.icnt[v] = cnt;
+      a.base[v] = bs;
+      a.freem[v] = fm;
     }
   }
-}
-
-// Part 1: tent[v] = the smallest color free in B_v and not taken by an
-// intra-partition neighbour colored in an earlier pass: from the cached 64
-// candidates, else (all taken -- a dense partition) a rescan of the whole
-// adjacency that also refreshes base/freem from every colored neighbour, so
-// the next 64 passes of v are cheap again.
-__global__ void __launch_bounds__(kItrBlock) k_itr_tent(const int64_t* __restrict__ off,
-                                                        const int32_t* __restrict__ col,
-                                                        const int32_t* color,
-                                                        const int32_t* __restrict__ A,
-                                                        const int* __restrict__ nA,
-                                                        const int32_t* __restrict__ P,
-                                                        const int32_t* __restrict__ icnt,
-                                                        int32_t* __restrict__ base,
-                                                        unsigned long long* __restrict__ freem,
-                                                        int32_t* __restrict__ tent) {
-  __shared__ __align__(16) uint8_t s_bm[kItrBlock / 32][kItrWin];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint8_t* bm = s_bm[warp];
-  const int na = *nA;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nw) {
-    const int v = A[i];
-    const int64_t b = off[v];
-    const int ni = icnt[v], bs = base[v];
-    unsigned long long taken = 0;
-    for (int j0 = 0; j0 < ni; j0 += 32) {
-      const int j = j0 + lane;
-      const int c = j < ni ? color[__ldg(P + b + j)] : 0;
-      const int d = c - bs;
-      if (c > 0 && d >= 0 && d < 64) taken |= 1ull << d;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) taken |= __shfl_xor_sync(0xffffffffu, taken, o);
-    const unsigned long long g = freem[v] & ~taken;
-    int found = 0;
-    if (g) {
-      found = bs + __ffsll((long long)g) - 1;
-    } else {  // rescan everything and refresh the summary
-      const int64_t e = off[v + 1];
-      unsigned long long fm = 0;
-      for (int wbase = 0; !found; wbase += kItrWin) {
-        for (int j = lane; j < kItrWin / 16; j += 32) reinterpret_cast<uint4*>(bm)[j] = make_uint4(0, 0, 0, 0);
-        __syncwarp();
-        for (int64_t a0 = b; a0 < e; a0 += 32) {
-          const int64_t a = a0 + lane;
-          const int u = a < e ? __ldg(col + a) : -1;
-          const int c = u >= 0 ? color[u] : 0;
-          const int k = c - wbase - 1;
-          if (c > 0 && k >= 0 && k < kItrWin) bm[k] = 1;
-        }
-        __syncwarp();
-        int z = -1;
-        for (int b0 = 0; b0 < kItrWin && z < 0; b0 += 32) {
-          const unsigned m = __ballot_sync(0xffffffffu, bm[b0 + lane] == 0);
-          if (m) z = b0 + __ffs(m) - 1;
-        }
-        if (z >= 0) {
-          found = wbase + z + 1;
-          const int k0 = z + lane, k1 = z + 32 + lane;
-          const unsigned lo = __ballot_sync(0xffffffffu, k0 < kItrWin && bm[k0] == 0);
-          const unsigned hi = __ballot_sync(0xffffffffu, k1 < kItrWin && bm[k1] == 0);
-          fm = ((unsigned long long)hi << 32) | lo;
-        }
-        __syncwarp();
-      }
-      if (lane == 0) {
-        base[v] = found;
-        freem[v] = fm;
-      }
-    }
-    if (lane == 0) tent[v] = found;
-  }
-}
-
-// Part 2: only the intra-partition neighbours can be active
-__global__ void __launch_bounds__(kItrBlock) k_itr_conflict(uint64_t seed,
-                                                            const int64_t* __restrict__ off,
-                                                            const int32_t* color,
-                                                            const int32_t* __restrict__ A,
-                                                            const int* __restrict__ nA,
-                                                            const int32_t* __restrict__ P,
-                                                            const int32_t* __restrict__ icnt,
-                                                            const int32_t* __restrict__ tent,
-                                                            uint8_t* __restrict__ won) {
-  const int lane = threadIdx.x & 31;
-  const int na = *nA;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nw) {
-    const int v = A[i];
-    const int tv = tent[v];
-    const uint64_t hv = prio_hash(seed, (uint32_t)v);
-    const int64_t b = off[v];
-    const int ni = icnt[v];
-    bool lose = false;
-    for (int j0 = 0; j0 < ni && !lose; j0 += 32) {
-      const int j = j0 + lane;
-      bool x = false;
-      if (j < ni) {
-        const int u = __ldg(P + b + j);
-        if (color[u] == 0 && tent[u] == tv) x = prio_hash(seed, (uint32_t)u) > hv;
-      }
-      lose = __any_sync(0xffffffffu, x);
-    }
-    if (lane == 0) won[v] = lose ? 0 : 1;
-  }
-}
-
-// Part 3 and U = U \ {colored}: block-level compaction of the losers
-__global__ void __launch_bounds__(kItrBlock) k_itr_apply(const int32_t* __restrict__ A,
-                                                         const int* __restrict__ nA,
-                                                         const int32_t* __restrict__ tent,
-                                                         const uint8_t* __restrict__ won,
-                                                         int32_t* color, int32_t* __restrict__ Anext,
-                                                         int* nAnext, State* st) {
-  __shared__ int sm[kItrBlock / 32 + 1];
-  const int na = *nA;
+  grid.sync();
+  int cur = 0;
   int kmax = 0;
-  for (int base = blockIdx.x * blockDim.x; base < na; base += gridDim.x * blockDim.x) {
-    const int i = base + threadIdx.x;
-    int v = 0;
-    bool stay = false;
-    if (i < na) {
-      v = A[i];
-      if (won[v]) {
-        color[v] = tent[v];
-        kmax = max(kmax, tent[v]);
-      } else {
-        stay = true;
+  for (;;) {
+    const int na = ldcg(a.nA + cur);
+    if (na == 0) break;
+    const int32_t* A = a.A[cur];
+    // Part 1
+    for (int i = gw; i < na; i += nwarps) {
+      const int v = ldcg(A + i);
+      const int64_t b = a.off[v];
+      const int ni = ldcg(a.icnt + v), bs = ldcg(a.base + v);
+      unsigned long long taken = 0;
+      for (int j0 = 0; j0 < ni; j0 += 32) {
+        const int j = j0 + lane;
+        const int c = j < ni ? ldcg(a.color + ldcg(a.P + b + j)) : 0;
+        const int d = c - bs;
+        if (c > 0 && d >= 0 && d < 64) taken |= 1ull << d;
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) taken |= __shfl_xor_sync(0xffffffffu, taken, o);
+      const unsigned long long g = __ldcg(a.freem + v) & ~taken;
+      int found;
+      if (g) {
+        found = bs + __ffsll((long long)g) - 1;
+      } else {  // the cached candidates are used up: rescan, refresh the summary
+        unsigned long long fm;
+        found = itr_full_mex(a.off, a.col, a.color, v, bm, fm);
+        if (lane == 0) {
+          a.base[v] = found;
+          a.freem[v] = fm;
+        }
+      }
+      if (lane == 0) a.tent[v] = found;
     }
-    block_append(stay, v, Anext, nAnext, sm);
+    grid.sync();
+    // Part 2
+    for (int i = gw; i < na; i += nwarps) {
+      const int v = ldcg(A + i);
+      const int tv = ldcg(a.tent + v);
+      const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
+      const int64_t b = a.off[v];
+      const int ni = ldcg(a.icnt + v);
+      bool lose = false;
+      for (int j0 = 0; j0 < ni && !lose; j0 += 32) {
+        const int j = j0 + lane;
+        bool x = false;
+        if (j < ni) {
+          const int u = ldcg(a.P + b + j);
+          if (ldcg(a.color + u) == 0 && ldcg(a.tent + u) == tv) x = prio_hash(a.seed, (uint32_t)u) > hv;
+        }
+        lose = __any_sync(0xffffffffu, x);
+      }
+      if (lane == 0) a.won[v] = lose ? 0 : 1;
+    }
+    grid.sync();
+    // Part 3 and U = U \ {colored}
+    int32_t* An = a.A[cur ^ 1];
+    int* nn = a.nA + (cur ^ 1);
+    for (int bb = blockIdx.x * blockDim.x; bb < na; bb += nt) {
+      const int i = bb + threadIdx.x;
+      int v = 0;
+      bool stay = false;
+      if (i < na) {
+        v = ldcg(A + i);
+        if (__ldcg(a.won + v)) {
+          const int t = ldcg(a.tent + v);
+          a.color[v] = t;
+          kmax = max(kmax, t);
+        } else {
+          stay = true;
+        }
+      }
+      block_append(stay, v, An, nn, sm);
+    }
+    if (tid == 0) ++*a.passes;
+    grid.sync();
+    if (tid == 0) a.nA[cur] = 0;  // the next pass's output counter (read two barriers later)
+    cur ^= 1;
   }
   kmax = warp_max(kmax);
-  if (lane_id() == 0 && kmax) atomicMax(&st->K, kmax);
-}
-
-// the partition's vertices (a range of the priority order) -> active list
-__global__ void k_itr_init(const int4* __restrict__ rec, int base, int cnt, int32_t* __restrict__ A,
-                           int* nA, int* nAnext) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
-    A[i] = rec[base + i].x;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *nA = cnt;
-    *nAnext = 0;
-  }
-}
-// after a pass: the consumed list's counter becomes the next output counter;
-// the remaining count is published for the host (State::sorted is free now)
-__global__ void k_itr_swap(int* consumed, const int* remaining, State* st) {
-  *consumed = 0;
-  st->sorted = *remaining;
+  if (lane == 0 && kmax) atomicMax(&a.st->K, kmax);
 }
 
 int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, long long* passes) {
@@ -259,49 +236,48 @@ int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, lon
   std::vector<int> cnt(T + 1, 0);
   PGC_CUDA(cudaMemcpyAsync(cnt.data(), c.hist1, sizeof(int) * (size_t)T, cudaMemcpyDeviceToHost, c.st));
   PGC_CUDA(cudaStreamSynchronize(c.st));
-  // scratch (ADG's and the order's arrays are free now)
-  int32_t* A[2] = {c.U[0], c.U[1]};
-  int* nA = c.hist1;                 // two list counters
-  int32_t* tent = c.D;
-  uint8_t* won = c.rs;
-  int32_t* icnt = c.npred;
-  int32_t* base = c.Rl;
-  unsigned long long* freem = reinterpret_cast<unsigned long long*>(c.bcnt);  // >= 2n + 2 ints
-  int32_t* intra = c.P;               // intra-partition neighbours, in each vertex's CSR slot
-  const int G = c.nsm * 8;
+  // scratch: ADG's and the order's arrays are free now
+  ItrArgs a = {};
+  a.seed = seed;
+  a.off = c.off;
+  a.col = c.col;
+  a.round = round;
+  a.color = color;
+  a.rec = c.rec;
+  a.A[0] = c.U[0];
+  a.A[1] = c.U[1];
+  a.nA = c.hist1;  // two counters, then the pass counter (8-byte aligned)
+  a.passes = reinterpret_cast<long long*>(c.hist1 + 2);
+  a.P = c.P;
+  a.icnt = c.npred;
+  a.base = c.Rl;
+  a.freem = reinterpret_cast<unsigned long long*>(c.bcnt);  // >= 2n + 2 ints
+  a.tent = c.D;
+  a.won = c.rs;
+  a.st = c.state;
+  PGC_CUDA(cudaMemsetAsync(a.passes, 0, sizeof(long long), c.st));
+  // one wave: every block resident (a grid barrier needs them all)
+  int occ = 0;
+  PGC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_itr_partition, kItrBlock, 0));
+  occ = occ < 1 ? 1 : occ;
+  const int bps = c.tune.itr_blocks_per_sm > 0 && c.tune.itr_blocks_per_sm < occ ? c.tune.itr_blocks_per_sm : occ;
+  const int G = c.nsm * bps;
   int pbase = 0;
   for (int l = T; l >= 1; --l) {
     const int cl = cnt[T - l];
     if (cl == 0) continue;
-    int cur = 0;
-    PGC_LAUNCH(c, kGJp, "k_itr_init",
-               k_itr_init<<<G, 256, 0, c.st>>>(c.rec, pbase, cl, A[0], nA, nA + 1));
+    a.l = l;
+    a.pbase = pbase;
+    a.cl = cl;
     pbase += cl;
-    PGC_LAUNCH(c, kGJp, "k_itr_prep",
-               k_itr_prep<<<G, kItrBlock, 0, c.st>>>(l, c.off, c.col, round, color, A[0], nA, intra,
-                                                      icnt, base, freem));
-    for (;;) {
-      for (int j = 0; j < kItrBatch; ++j) {
-        PGC_LAUNCH(c, kGJp, "k_itr_tent",
-                   k_itr_tent<<<G, kItrBlock, 0, c.st>>>(c.off, c.col, color, A[cur], nA + cur,
-                                                          intra, icnt, base, freem, tent));
-        PGC_LAUNCH(c, kGJp, "k_itr_conflict",
-                   k_itr_conflict<<<G, kItrBlock, 0, c.st>>>(seed, c.off, color, A[cur], nA + cur,
-                                                              intra, icnt, tent, won));
-        PGC_LAUNCH(c, kGJp, "k_itr_apply",
-                   k_itr_apply<<<G, kItrBlock, 0, c.st>>>(A[cur], nA + cur, tent, won, color,
-                                                           A[cur ^ 1], nA + (cur ^ 1), c.state));
-        // A[cur^1] / nA[cur^1] hold the next active list
-        PGC_LAUNCH(c, kGJp, "k_itr_swap",
-                   k_itr_swap<<<1, 1, 0, c.st>>>(nA + cur, nA + (cur ^ 1), c.state));
-        cur ^= 1;
-        ++*passes;
-      }
-      if (int e = sync_state(c)) return e;
-      if (c.h_state->sorted == 0) break;
-    }
+    void* args[] = {&a};
+    PGC_LAUNCH(c, kGJp, "k_itr_partition",
+               PGC_CUDA(cudaLaunchCooperativeKernel((const void*)k_itr_partition, dim3(G),
+                                                    dim3(kItrBlock), args, 0, c.st)));
   }
-  return sync_state(c);
+  if (int e = sync_state(c)) return e;
+  PGC_CUDA(cudaMemcpy(passes, a.passes, sizeof(long long), cudaMemcpyDeviceToHost));
+  return 0;
 }
 
 }  // namespace pgc
