@@ -872,7 +872,15 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
     }
     PROBE_STAMP(tr_grab, vprobe, 6);
     if (stall) break;
-    if (lane < C)  // publish to every replica (DSMEM store, relaxed at cluster scope)
+    // publish to every replica: DSMEM stores (relaxed, cluster scope) to the
+    // peers, a plain shared store to the own replica (the chain's hops inside
+    // a run of kCoreRun positions are local)
+#ifndef PGC_LOCAL_PUBLISH
+#define PGC_LOCAL_PUBLISH 1
+#endif
+    if (PGC_LOCAL_PUBLISH && lane == rank)
+      *(volatile uint16_t*)(s_cc + p) = (uint16_t)found;
+    else if (lane < C)
       asm volatile("st.relaxed.cluster.shared::cluster.u16 [%0], %1;" ::"r"(remote + 2u * (uint32_t)p),
                    "h"((unsigned short)found)
                    : "memory");
