@@ -512,7 +512,10 @@ constexpr int kCoreWarps = kCoreBlock / 32;
 constexpr int kCoreWin = 1024;   // colors per byte-map window
 constexpr int kCorePend = 512;   // pending-pred list capacity per warp
 constexpr int kCoreRun = 32;     // consecutive core positions per CTA run
-constexpr int kCoreTail = 4;     // preds left for the collective-free tail
+#ifndef PGC_CORE_TAIL
+#define PGC_CORE_TAIL 4
+#endif
+constexpr int kCoreTail = PGC_CORE_TAIL;  // preds left for the collective-free tail
 // dynamic shared memory ahead of the color replica: bitmaps + pending lists
 constexpr int kCoreFixedSmem = kCoreWarps * kCoreWin + kCoreWarps * kCorePend * 2;
 
@@ -826,15 +829,17 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
         // per poll; entries past npend repeat q[0]), the watchdog only every
         // 512 polls: the loop is short because every waiting warp of the SM
         // spins here and shares the issue slots with the warps on the chain
-        int c0, c1, c2, c3;
+        int cc[kCoreTail];
         for (;;) {
           bool all = false;
           for (int it = 0; it < 512; ++it) {
-            c0 = ld_vol_u16(s_cc + q[0]);
-            c1 = ld_vol_u16(s_cc + q[1]);
-            c2 = ld_vol_u16(s_cc + q[2]);
-            c3 = ld_vol_u16(s_cc + q[3]);
-            if (c0 && c1 && c2 && c3) {
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < kCoreTail; ++k) {
+              cc[k] = ld_vol_u16(s_cc + q[k]);
+              ok &= cc[k] != 0;
+            }
+            if (ok) {
               all = true;
               break;
             }
@@ -848,19 +853,20 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
           if (tail_ns) __nanosleep(tail_ns);
         }
         PROBE_STAMP(tr_grab, vprobe, 5);
-        const unsigned M = shl1(c0 - cbase) | shl1(c1 - cbase) | shl1(c2 - cbase) | shl1(c3 - cbase);
+        unsigned M = 0u;
+#pragma unroll
+        for (int k = 0; k < kCoreTail; ++k) M |= shl1(cc[k] - cbase);
         const unsigned G = F & ~M;
         int res;
         if (G) {
           res = z[0] + __ffs(G) - 1;
         } else {  // candidates spread wider than 32 colors or past the window
-          const int cl_[kCoreTail] = {c0 - wbase - 1, c1 - wbase - 1, c2 - wbase - 1, c3 - wbase - 1};
           res = kCoreWin;
 #pragma unroll
           for (int j = kCoreTail; j >= 0; --j) {
             bool taken = false;
 #pragma unroll
-            for (int k = 0; k < kCoreTail; ++k) taken |= cl_[k] == z[j];
+            for (int k = 0; k < kCoreTail; ++k) taken |= cc[k] - wbase - 1 == z[j];
             if (!taken) res = z[j];
           }
         }

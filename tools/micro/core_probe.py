@@ -90,3 +90,10 @@ out["slow_scan_after_ready"] = int((slow & (A[crit, 1] > rd)).sum())
 out["slow_lastpass_after_ready"] = int((slow & (A[crit, 3] > rd)).sum())
 out["fast_step_p50"] = float(np.median(step[~slow])) if (~slow).any() else 0
 print(json.dumps(out, indent=1))
+# slow hops in detail: when were they grabbed, how long did their first scan take
+sl = crit[slow]
+npred_core = np.bincount(src, minlength=n)
+det = {"grab-ready_us": pct((A[sl, 0] - ready[sl]) / 1e3), "scan_us": pct((A[sl, 1] - A[sl, 0]) / 1e3),
+       "np": pct(npred_core[sl]), "fast_np": pct(npred_core[crit[~slow]]),
+       "fast_scan_us": pct((A[crit[~slow], 1] - A[crit[~slow], 0]) / 1e3)}
+print(json.dumps(det))
