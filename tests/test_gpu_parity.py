@@ -430,3 +430,15 @@ def test_dec_adg_itr_random(name):
 
 def test_dec_adg_itr_rmat20():
     assert_parity_dec(gg.config_graph("rmat20"), 1, 10, 1)
+
+
+# ------------------------------------- next rows on the other full-size configs --
+@pytest.mark.parametrize("cfg", ["cl", "grid"])
+def test_next_rows_full_size(cfg):
+    """ADG-O, ADG-M and DEC-ADG-ITR at full size on the heavy-hub Chung-Lu graph
+    and the low-degree grid (many ADG rounds)."""
+    g = gg.config_graph(cfg)
+    eps = gg.CONFIGS[cfg][1]
+    assert_parity_o(g, *eps[0])
+    assert_parity_m(g, 5)
+    assert_parity_dec(g, *eps[-1], 3)
