@@ -40,13 +40,15 @@ constexpr int kItrBlock = 256;
 
 __device__ __forceinline__ int ldcg(const int32_t* p) { return __ldcg(p); }
 
-// mex over the colors of ALL colored neighbours of v (a warp, byte-map windows);
-// also the free mask of the 64 colors from the mex on (bits past the window: taken)
-__device__ __forceinline__ int itr_full_mex(const int64_t* __restrict__ off,
-                                            const int32_t* __restrict__ col, const int32_t* color,
-                                            int v, uint8_t* bm, unsigned long long& fm) {
+// mex over the colors of the colored vertices in two lists (a warp, byte-map
+// windows); also the free mask of the 64 colors from the mex on (bits past the
+// window: taken).  The lists are v's neighbours in R(l) and in the colored
+// partitions: every neighbour that can be colored while R(l) is.
+__device__ __forceinline__ int itr_full_mex(const int32_t* la, int na_, const int32_t* lb, int nb_,
+                                            const int32_t* color, uint8_t* bm,
+                                            unsigned long long& fm) {
   const int lane = lane_id();
-  const int64_t b = off[v], e = off[v + 1];
+  const int64_t b = 0, e = (int64_t)na_ + nb_;
   int found = 0;
   fm = 0;
   for (int wbase = 0; !found; wbase += kItrWin) {
@@ -58,7 +60,7 @@ __device__ __forceinline__ int itr_full_mex(const int64_t* __restrict__ off,
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int64_t x = a0 + 32 * k + lane;
-        u[k] = x < e ? __ldg(col + x) : -1;
+        u[k] = x < e ? ldcg(x < na_ ? la + x : lb + (x - na_)) : -1;
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) c[k] = u[k] >= 0 ? ldcg(color + u[k]) : 0;
@@ -98,7 +100,8 @@ struct ItrArgs {
   int32_t* A[2];          // active lists
   int* nA;                // their counters [2]
   int32_t* P;             // intra-partition neighbour lists (CSR slots)
-  int32_t* icnt;
+  int32_t* icnt;          // intra-partition neighbours (first in the slot)
+  int32_t* ucnt;          // neighbours in the colored partitions (at the back of the slot)
   int32_t* base;
   unsigned long long* freem;
   int32_t* tent;
@@ -107,44 +110,69 @@ struct ItrArgs {
   long long* passes;      // device counter
 };
 
-__global__ void __launch_bounds__(kItrBlock) k_itr_partition(ItrArgs a) {
+// Partition start (a plain launch over the whole GPU): the active list, the
+// neighbour lists of the slots and the B_v summaries.
+__global__ void __launch_bounds__(kItrBlock) k_itr_prep(ItrArgs a) {
   __shared__ __align__(16) uint8_t s_bm[kItrBlock / 32][kItrWin];
-  __shared__ int sm[kItrBlock / 32 + 1];
-  cg::grid_group grid = cg::this_grid();
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   uint8_t* bm = s_bm[warp];
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   const int gw = tid >> 5, nwarps = nt >> 5;
-  // the partition -> active list 0
-  for (int i = tid; i < a.cl; i += nt) a.A[0][i] = a.rec[a.pbase + i].x;
   if (tid == 0) {
     a.nA[0] = a.cl;
     a.nA[1] = 0;
   }
-  grid.sync();
-  // prep: summary of B_v and the intra-partition lists
   for (int i = gw; i < a.cl; i += nwarps) {
-    const int v = ldcg(a.A[0] + i);
+    const int v = a.rec[a.pbase + i].x;
+    if (lane == 0) a.A[0][i] = v;
     const int64_t b = a.off[v], e = a.off[v + 1];
-    int cnt = 0;
-    for (int64_t a0 = b; a0 < e; a0 += 32) {
-      const int64_t x = a0 + lane;
-      const int u = x < e ? __ldg(a.col + x) : -1;
-      const bool in = u >= 0 && a.round[u] == a.l;
-      const unsigned bal = __ballot_sync(0xffffffffu, in);
-      if (in) a.P[b + cnt + __popc(bal & lt)] = u;
-      cnt += __popc(bal);
+    // the slot: intra-partition neighbours from its front, those in colored
+    // partitions from its back (8 strips of loads in flight: hubs are long);
+    // then the latter are moved up behind the former
+    int cnt = 0, upb = 0;
+    for (int64_t a0 = b; a0 < e; a0 += 256) {
+      int u[8], r[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t x = a0 + 32 * k + lane;
+        u[k] = x < e ? __ldg(a.col + x) : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r[k] = u[k] >= 0 ? __ldg(a.round + u[k]) : -1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool in = r[k] == a.l, hi = r[k] > a.l;
+        const unsigned bi = __ballot_sync(0xffffffffu, in), bh = __ballot_sync(0xffffffffu, hi);
+        if (in) a.P[b + cnt + __popc(bi & lt)] = u[k];
+        if (hi) a.P[e - 1 - upb - __popc(bh & lt)] = u[k];
+        cnt += __popc(bi);
+        upb += __popc(bh);
+      }
     }
+    __syncwarp();
     unsigned long long fm;
-    const int bs = itr_full_mex(a.off, a.col, a.color, v, bm, fm);
+    const int bs = itr_full_mex(a.P + b, cnt, a.P + e - upb, upb, a.color, bm, fm);
     if (lane == 0) {
       a.icnt[v] = cnt;
+      a.ucnt[v] = upb;
       a.base[v] = bs;
       a.freem[v] = fm;
     }
   }
-  grid.sync();
+}
+
+// The SIM-COL passes of one partition: a cooperative launch sized to the
+// partition (a grid barrier among few blocks is cheap for the small, dense
+// partitions that need many passes).
+__global__ void __launch_bounds__(kItrBlock) k_itr_partition(ItrArgs a) {
+  __shared__ __align__(16) uint8_t s_bm[kItrBlock / 32][kItrWin];
+  __shared__ int sm[kItrBlock / 32 + 1];
+  cg::grid_group grid = cg::this_grid();
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  uint8_t* bm = s_bm[warp];
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  const int gw = tid >> 5, nwarps = nt >> 5;
   int cur = 0;
   int kmax = 0;
   for (;;) {
@@ -171,7 +199,8 @@ __global__ void __launch_bounds__(kItrBlock) k_itr_partition(ItrArgs a) {
         found = bs + __ffsll((long long)g) - 1;
       } else {  // the cached candidates are used up: rescan, refresh the summary
         unsigned long long fm;
-        found = itr_full_mex(a.off, a.col, a.color, v, bm, fm);
+        const int nup = ldcg(a.ucnt + v);
+        found = itr_full_mex(a.P + b, ni, a.P + a.off[v + 1] - nup, nup, a.color, bm, fm);
         if (lane == 0) {
           a.base[v] = found;
           a.freem[v] = fm;
@@ -250,6 +279,7 @@ int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, lon
   a.passes = reinterpret_cast<long long*>(c.hist1 + 2);
   a.P = c.P;
   a.icnt = c.npred;
+  a.ucnt = reinterpret_cast<int32_t*>(c.rec + c.n);  // the bulk's record lists are unused here
   a.base = c.Rl;
   a.freem = reinterpret_cast<unsigned long long*>(c.bcnt);  // >= 2n + 2 ints
   a.tent = c.D;
@@ -270,9 +300,13 @@ int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, lon
     a.pbase = pbase;
     a.cl = cl;
     pbase += cl;
+    PGC_LAUNCH(c, kGJp, "k_itr_prep", k_itr_prep<<<G, kItrBlock, 0, c.st>>>(a));
+    // passes: about one warp per 4 active vertices of the partition's start
+    const int want = (cl + 4 * (kItrBlock / 32) - 1) / (4 * (kItrBlock / 32));
+    const int GP = want < G ? (want < 1 ? 1 : want) : G;
     void* args[] = {&a};
     PGC_LAUNCH(c, kGJp, "k_itr_partition",
-               PGC_CUDA(cudaLaunchCooperativeKernel((const void*)k_itr_partition, dim3(G),
+               PGC_CUDA(cudaLaunchCooperativeKernel((const void*)k_itr_partition, dim3(GP),
                                                     dim3(kItrBlock), args, 0, c.st)));
   }
   if (int e = sync_state(c)) return e;
