@@ -442,3 +442,33 @@ def test_next_rows_full_size(cfg):
     assert_parity_o(g, *eps[0])
     assert_parity_m(g, 5)
     assert_parity_dec(g, *eps[-1], 3)
+
+
+# ------------------------------------------------ repeat / stress -------------
+def test_repeat_runs_are_identical_and_never_stall():
+    """The dataflow kernels are schedule-dependent inside; the results must not
+    be.  Repeats of every entry point on one graph, with a short watchdog (a
+    stall would surface as PGC_EINTERNAL, not a hang)."""
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    g = gg.rmat(17, 16, seed=9)
+    _, off, col = dev(g)
+    pgc.set_tuning("jp_watchdog_ms", 5000)
+    try:
+        ref = None
+        for rep in range(12):
+            out = []
+            r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 4)
+            out += [r.cpu().numpy(), c.cpu().numpy()]
+            r, c, T, K = pgc.color_jp_adg_o(off, col, 1, 10)
+            out += [c.cpu().numpy()]
+            for kind in ("jp-r", "jp-lf"):
+                c, K = pgc.jp_baseline(off, col, kind, 4)
+                out += [c.cpu().numpy()]
+            r, c, T, K = pgc.color_dec_adg_itr(off, col, 1, 10, 4)
+            out += [c.cpu().numpy()]
+            if ref is None:
+                ref = out
+            else:
+                assert all(np.array_equal(x, y) for x, y in zip(out, ref)), f"repeat {rep} differs"
+    finally:
+        pgc.set_tuning("jp_watchdog_ms", 20000)
