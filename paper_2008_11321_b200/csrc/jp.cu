@@ -935,7 +935,11 @@ constexpr int kHeavyTail = 4;      // preds left for the collective-free heavy t
 #ifndef PGC_LIGHT_BATCH
 #define PGC_LIGHT_BATCH 4
 #endif
-constexpr int kLightBatch = PGC_LIGHT_BATCH;  // pred loads in flight per light lane
+constexpr int kLightBatch = PGC_LIGHT_BATCH;  // pred loads in flight per light lane (re-exam)
+#ifndef PGC_LIGHT_VEC
+#define PGC_LIGHT_VEC 2
+#endif
+constexpr int kLV = PGC_LIGHT_VEC;  // 16-byte pred-id loads per first-pass step of a light lane
 
 __global__ void k_bulk_flags(int64_t n, const int4* __restrict__ rec, const State* st,
                              int32_t* __restrict__ hflag, int32_t* __restrict__ lflag) {
@@ -1316,19 +1320,25 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
             // outside [pb, pb + np) belong to neighbouring lists: ignored),
             // then their 8 color gathers in flight
             const int64_t pe = pb + np;
-            for (int64_t s0 = pb & ~3ll; s0 < pe; s0 += 8) {
-              const int4 w0 = __ldcs(reinterpret_cast<const int4*>(P + s0));
-              const int4 w1 = s0 + 4 < pe ? __ldcs(reinterpret_cast<const int4*>(P + s0 + 4))
-                                          : make_int4(-1, -1, -1, -1);
-              int u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-              int cc[8];
+            for (int64_t s0 = pb & ~3ll; s0 < pe; s0 += 4 * kLV) {
+              int u[4 * kLV], cc[4 * kLV];
 #pragma unroll
-              for (int k = 0; k < 8; ++k)
+              for (int q = 0; q < kLV; ++q) {
+                const int4 w = (q == 0 || s0 + 4 * q < pe)
+                                   ? __ldcs(reinterpret_cast<const int4*>(P + s0 + 4 * q))
+                                   : make_int4(-1, -1, -1, -1);
+                u[4 * q] = w.x;
+                u[4 * q + 1] = w.y;
+                u[4 * q + 2] = w.z;
+                u[4 * q + 3] = w.w;
+              }
+#pragma unroll
+              for (int k = 0; k < 4 * kLV; ++k)
                 if (s0 + k < pb || s0 + k >= pe) u[k] = -1;
 #pragma unroll
-              for (int k = 0; k < 8; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+              for (int k = 0; k < 4 * kLV; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
+              for (int k = 0; k < 4 * kLV; ++k) {
                 if (u[k] < 0) continue;
                 const int j = (int)(s0 + k - pb);
                 if (cc[k] == 0) {
