@@ -1004,21 +1004,36 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
                                           unsigned long long* pkey, int& npend) {
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
+  int un[kHS];  // the next step's pred ids, loaded one step ahead
+#pragma unroll
+  for (int k = 0; k < kHS; ++k) {
+    const int i = from + 32 * k + lane;
+    un[k] = i < np ? jp_stream(P + pb + i) : -1;
+  }
   for (int i0 = from; i0 < np; i0 += 32 * kHS) {
     int u[kHS], cc[kHS];
 #pragma unroll
+    for (int k = 0; k < kHS; ++k) u[k] = un[k];
+#pragma unroll
     for (int k = 0; k < kHS; ++k) {
-      const int i = i0 + 32 * k + lane;
-      u[k] = i < np ? jp_stream(P + pb + i) : -1;
+      const int i = i0 + 32 * kHS + 32 * k + lane;
+      un[k] = i < np ? jp_stream(P + pb + i) : -1;
     }
 #pragma unroll
     for (int k = 0; k < kHS; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
-    // first keys of the pending preds, all four strips' loads in flight
-    // before any is used (a load consumed in its own branch serialises)
+    // first keys of the pending preds (only when some are pending: a ready
+    // vertex pays no extra latency), all strips' loads in flight before any
+    // is used (a load consumed in its own branch serialises)
+    bool anyp = false;
+#pragma unroll
+    for (int k = 0; k < kHS; ++k) anyp |= u[k] >= 0 && cc[k] == 0;
     int rk[kHS];
 #pragma unroll
-    for (int k = 0; k < kHS; ++k)  // (no first key given: watch by hash alone)
-      rk[k] = round ? __ldg(round + (u[k] >= 0 && cc[k] == 0 ? u[k] : 0)) : 0;
+    for (int k = 0; k < kHS; ++k) rk[k] = 0;
+    if (round && __any_sync(0xffffffffu, anyp)) {
+#pragma unroll
+      for (int k = 0; k < kHS; ++k) rk[k] = __ldg(round + (u[k] >= 0 && cc[k] == 0 ? u[k] : 0));
+    }
 #pragma unroll
     for (int k = 0; k < kHS; ++k) {
       const bool pend = u[k] >= 0 && cc[k] == 0;
