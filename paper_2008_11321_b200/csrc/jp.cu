@@ -940,6 +940,10 @@ constexpr int kLightBatch = PGC_LIGHT_BATCH;  // pred loads in flight per light 
 #define PGC_LIGHT_VEC 2
 #endif
 constexpr int kLV = PGC_LIGHT_VEC;  // 16-byte pred-id loads per first-pass step of a light lane
+#ifndef PGC_LIGHT_STEPS
+#define PGC_LIGHT_STEPS 2
+#endif
+constexpr int kLightSteps = PGC_LIGHT_STEPS;  // first-pass steps per lane per loop iteration
 
 __global__ void k_bulk_flags(int64_t n, const int4* __restrict__ rec, const State* st,
                              int32_t* __restrict__ hflag, int32_t* __restrict__ lflag) {
@@ -1280,7 +1284,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
     // load per poll and re-examines the rest only when it is colored.
     const int64_t nlight = st->nlight;
     int v = -1, np = 0, watch_j = -1, watch_u = -1;
-    int64_t pb = 0;
+    int64_t pb = 0, pe = 0, scan = 0;  // scan: next P slot of the first pass (pe: done)
     unsigned long long mask = 0, pend = 0;
     unsigned sleep_ns = 32;
     int4 nx = make_int4(0, 0, 0, 0);  // prefetched next record
@@ -1320,60 +1324,61 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
           }
         }
       }
-      {
-        if (take) {
-          {
+      if (take) {
 #ifndef PGC_PROBE
-            if (tr_grab) tr_grab[v] = globaltimer();
+        if (tr_grab) tr_grab[v] = globaltimer();
 #endif
-            // first pass over every pred
-            mask = 1ull;  // bit 0 reserved: colors start at 1
-            pend = 0ull;
-            watch_j = -1;
-            watch_u = -1;
-            // pred ids by aligned 16-byte loads, 8 slots per step (slots
-            // outside [pb, pb + np) belong to neighbouring lists: ignored),
-            // then their 8 color gathers in flight
-            const int64_t pe = pb + np;
-            for (int64_t s0 = pb & ~3ll; s0 < pe; s0 += 4 * kLV) {
-              int u[4 * kLV], cc[4 * kLV];
+        mask = 1ull;  // bit 0 reserved: colors start at 1
+        pend = 0ull;
+        watch_j = -1;
+        watch_u = -1;
+        pe = pb + np;
+        scan = pb & ~3ll;
+      }
+      // first pass over the preds, at most kLightSteps steps per iteration (the
+      // warp's lanes run in lockstep: one long list must not hold up the
+      // lanes that could finish and refill).  Pred ids by aligned 16-byte loads,
+      // 4 * kLV slots per step (slots outside [pb, pe) belong to neighbouring
+      // lists: ignored), then their color gathers in flight.
+      for (int step = 0; step < kLightSteps && v >= 0 && scan < pe; ++step) {
+        const int64_t s0 = scan;
+        int u[4 * kLV], cc[4 * kLV];
 #pragma unroll
-              for (int q = 0; q < kLV; ++q) {
-                const int4 w = (q == 0 || s0 + 4 * q < pe)
-                                   ? __ldcs(reinterpret_cast<const int4*>(P + s0 + 4 * q))
-                                   : make_int4(-1, -1, -1, -1);
-                u[4 * q] = w.x;
-                u[4 * q + 1] = w.y;
-                u[4 * q + 2] = w.z;
-                u[4 * q + 3] = w.w;
-              }
+        for (int q = 0; q < kLV; ++q) {
+          const int4 w = (q == 0 || s0 + 4 * q < pe)
+                             ? __ldcs(reinterpret_cast<const int4*>(P + s0 + 4 * q))
+                             : make_int4(-1, -1, -1, -1);
+          u[4 * q] = w.x;
+          u[4 * q + 1] = w.y;
+          u[4 * q + 2] = w.z;
+          u[4 * q + 3] = w.w;
+        }
 #pragma unroll
-              for (int k = 0; k < 4 * kLV; ++k)
-                if (s0 + k < pb || s0 + k >= pe) u[k] = -1;
+        for (int k = 0; k < 4 * kLV; ++k)
+          if (s0 + k < pb || s0 + k >= pe) u[k] = -1;
 #pragma unroll
-              for (int k = 0; k < 4 * kLV; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+        for (int k = 0; k < 4 * kLV; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
 #pragma unroll
-              for (int k = 0; k < 4 * kLV; ++k) {
-                if (u[k] < 0) continue;
-                const int j = (int)(s0 + k - pb);
-                if (cc[k] == 0) {
-                  pend |= 1ull << j;
-                  if (watch_j < 0) {  // watch the first pending pred
-                    watch_j = j;
-                    watch_u = u[k];
-                  }
-                } else if (cc[k] < 64) {
-                  mask |= 1ull << cc[k];
-                }
-              }
+        for (int k = 0; k < 4 * kLV; ++k) {
+          if (u[k] < 0) continue;
+          const int j = (int)(s0 + k - pb);
+          if (cc[k] == 0) {
+            pend |= 1ull << j;
+            if (watch_j < 0) {  // watch the first pending pred
+              watch_j = j;
+              watch_u = u[k];
             }
-            progress = true;
+          } else if (cc[k] < 64) {
+            mask |= 1ull << cc[k];
           }
         }
+        scan = s0 + 4 * kLV;
+        progress = true;
       }
+      const bool scanned = v >= 0 && scan >= pe;
       if (__ballot_sync(0xffffffffu, v >= 0 || have_nx) == 0) break;  // all free, out of tickets
       // 2. poll the watched pred; when colored, re-examine the other pending preds
-      if (v >= 0 && watch_u >= 0) {
+      if (scanned && watch_u >= 0) {
         const int cw = ld_relaxed(color + watch_u);
         if (cw) {
           if (cw < 64) mask |= 1ull << cw;
@@ -1408,7 +1413,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         }
       }
       // 3. GetColor once nothing is pending: the smallest color the preds do not use
-      if (v >= 0 && watch_u < 0) {
+      if (scanned && watch_u < 0) {
         const int cc = __ffsll((long long)~mask) - 1;
         st_relaxed(color + v, cc);
         if (tr_done) tr_done[v] = globaltimer();
