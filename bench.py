@@ -40,7 +40,7 @@ PROFILES = os.path.join(ROOT, "profiles")
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["pgc", "reference"], default="pgc")
     ap.add_argument("--config", default="rmat24", choices=sorted(gg.CONFIGS))
@@ -123,8 +123,20 @@ class ClockSampler:
 
     def __enter__(self):
         if self.ok:
+            # warm NVML up first (its first calls can take tens of ms), so the
+            # samples cover the timed region that follows
+            try:
+                self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 1.0:
+                time.sleep(0.001)
+            self.samples.clear()   # keep only samples taken inside the region
+            self.reasons.clear()
         return self
 
     def __exit__(self, *a):
