@@ -50,11 +50,14 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline (for ncu runs)")
     ap.add_argument("--method", choices=["jp-adg", "jp-adg-m", "jp-adg-o", "jp-r", "jp-ff", "jp-lf",
-                                         "jp-llf", "dec-adg-itr"], default="jp-adg",
+                                         "jp-llf", "dec-adg-itr", "adg-push", "adg-pull"],
+                    default="jp-adg",
                     help="jp-adg-m: the median variant (SURVEY.md §8(f) NEXT-3, PAPER.md:2273-2303); "
                          "jp-adg-o: ADG-O's total order (NEXT-1, PAPER.md:2397-2453); "
                          "jp-r/ff/lf/llf: the JP baselines (NEXT-4, PAPER.md:1093-1103); "
-                         "dec-adg-itr: DEC-ADG-ITR (NEXT-2, PAPER.md:1957-1972)")
+                         "dec-adg-itr: DEC-ADG-ITR (NEXT-2, PAPER.md:1957-1972); "
+                         "adg-push/adg-pull: the ADG ordering alone with the push or pull "
+                         "(CREW) UPDATE (NEXT-4, PAPER.md:2331-2342)")
     return ap.parse_args()
 
 
@@ -259,8 +262,12 @@ def run_pgc(args):
     sortedR = args.method == "jp-adg-o"
     baseline = args.method in ("jp-r", "jp-ff", "jp-lf", "jp-llf")
     decitr = args.method == "dec-adg-itr"
+    adgonly = args.method in ("adg-push", "adg-pull")
 
     def step():
+        if adgonly:
+            r_, T_ = pgc.adg_order(off, col, num, den, update=args.method[4:], round_out=rnd)
+            return r_, color, T_, 0
         if decitr:
             return pgc.color_dec_adg_itr(off, col, num, den, args.seed, round_out=rnd, color_out=color)
         if baseline:
@@ -310,6 +317,16 @@ def run_pgc(args):
 
     X, sum_active = st["cross_edges"], st["sum_active"]
     model = algorithmic_bytes(n, nnz, m, X, sum_active)
+    upd_arcs = nnz   # arcs UPDATE classifies per step
+    if adgonly:
+        model["jp"] = model["order"] = 0
+        model["update"] = 16 * n + 4 * nnz + 1 * nnz + 4 * X   # R records+offsets; col+state per arc; RED
+        if args.method == "adg-pull":
+            # pull: every survivor rescans its adjacency: sum_v (round[v]-1) * deg(v) arcs
+            r_h = rnd.cpu().numpy().astype(np.int64)
+            pull_arcs = int(((r_h - 1) * g.degrees().astype(np.int64)).sum())
+            model["update"] = 16 * sum_active + 5 * pull_arcs + 8 * sum_active   # records; col+state; D rmw
+            upd_arcs = pull_arcs
     peak, peak_kind = peak_gbs()
     kern = {"update": ("k_update_light+k_update_heavy", gmean["t_update_ms"], model["update"]),
             "jp": ("k_jp_bulk", gmean["t_jp_ms"], model["jp"]),
@@ -325,13 +342,22 @@ def run_pgc(args):
     ra = None
     try:
         pr = json.load(open(os.path.join(PROFILES, "random_access_probe.json")))
-        arcs_per_s = nnz / (gmean["t_update_ms"] * 1e-3)
-        mix = X / nnz if nnz else 0.0
-        ra = {"arcs_per_s": arcs_per_s, "red_fraction": mix,
-              "peak_arcs_per_s": pr["gather_plus_red_42pct_arcs_per_s"],
-              "frac": arcs_per_s / pr["gather_plus_red_42pct_arcs_per_s"],
-              "note": "UPDATE = one random 1-byte state gather per arc + one RED per cross-round "
-                      "edge; peak = tools/micro/atom_probe.cu at the same RED fraction (0.42)"}
+        arcs_per_s = upd_arcs / (gmean["t_update_ms"] * 1e-3)
+        if args.method == "adg-pull":   # a gather per arc, no per-arc RED
+            ra = {"arcs_per_s": arcs_per_s, "red_fraction": 0.0,
+                  "peak_arcs_per_s": pr["gather_u8_per_s"],
+                  "frac": arcs_per_s / pr["gather_u8_per_s"],
+                  "note": "pull UPDATE = one random 1-byte state gather per survivor arc "
+                          "(sum_v (round[v]-1) deg(v) arcs); peak = tools/micro/atom_probe.cu "
+                          "gather-only rate"}
+        else:
+            mix = X / upd_arcs if upd_arcs else 0.0
+            ra = {"arcs_per_s": arcs_per_s, "red_fraction": mix,
+                  "peak_arcs_per_s": pr["gather_plus_red_42pct_arcs_per_s"],
+                  "frac": arcs_per_s / pr["gather_plus_red_42pct_arcs_per_s"],
+                  "note": "UPDATE = one random 1-byte state gather per arc + one RED per "
+                          "cross-round edge; peak = tools/micro/atom_probe.cu at the same RED "
+                          "fraction (0.42)"}
     except Exception:
         pass
 
@@ -341,11 +367,13 @@ def run_pgc(args):
                    METRIC.replace("JP-ADG", args.method.upper()).replace("ADG+JP", "JP only")
                    if baseline else
                    METRIC.replace("JP-ADG", "DEC-ADG-ITR").replace("ADG+JP", "ADG+SIM-COL-ITR")
-                   if decitr else METRIC),
+                   if decitr else
+                   METRIC.replace("JP-ADG", args.method.upper()).replace("ADG+JP", "ordering only")
+                   .replace("; #colors", "") if adgonly else METRIC),
         "value": job_value(world, m, ms), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.config}-{args.method}" if (baseline or decitr) else
+        "config": {"workload": f"{args.config}-{args.method}" if (baseline or decitr or adgonly) else
                    f"{args.config}-adgm" if median else
                    f"{args.config}-adgo-eps{num}/{den}" if sortedR else f"{args.config}-eps{num}/{den}",
                    "method": args.method, "n": n, "m": m, "nnz": nnz,
@@ -367,7 +395,7 @@ def run_pgc(args):
     }
 
     # ---- end to end through the host-buffer C-ABI call ----
-    if not (args.no_e2e or args.quick or median or sortedR or baseline or decitr):
+    if not (args.no_e2e or args.quick or median or sortedR or baseline or decitr or adgonly):
         h_off = torch.from_numpy(g.off).pin_memory()
         h_col = torch.from_numpy(g.col).pin_memory()
         h_r = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -404,14 +432,17 @@ def run_pgc(args):
         else:
             r_or, _ = O.adg_m(g) if median else O.adg(g, num, den)
         t1 = time.perf_counter()
-        if decitr:
+        if adgonly:
+            c_or, K_or = color.cpu().numpy(), K   # no coloring: only round[] is checked
+        elif decitr:
             c_or, K_or, _ = O.dec_adg_itr(g, r_or, args.seed)
         else:
             c_or, K_or = O.jp_rho(g, rho) if sortedR else O.jp(g, r_or, args.seed)
         t2 = time.perf_counter()
         out["cpu_baseline"] = {"value": m / (t2 - t0), "unit": "edges/s", "cores": 1,
                                "kind": "oracle",
-                               "sample": f"full {args.config} workload, one JP-ADG run of the "
+                               "sample": f"full {args.config} workload, one "
+                                         f"{'ADG' if adgonly else 'JP-ADG'} run of the "
                                          f"sequential C oracle (ADG {t1 - t0:.1f}s + greedy JP "
                                          f"{t2 - t1:.1f}s)"}
         out["parity"] = {"round": True if baseline else bool(np.array_equal(rnd.cpu().numpy(), r_or)),

@@ -111,6 +111,26 @@ int pgc_adg_order(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int32_
                   int32_t* num_rounds, void* workspace, size_t workspace_bytes,
                   void* cuda_stream);
 
+/* How ADG's UPDATE applies the decrements ("Push vs. Pull").
+ *   PGC_UPDATE_PUSH : iterate over R_l's arcs and decrement D[u] of every
+ *                     surviving neighbour u (atomic RED per arc; Alg. 1 lines
+ *                     692-696).  Each arc is scanned once over the whole run.
+ *   PGC_UPDATE_PULL : iterate over the survivors U_{l+1} and subtract from D[v]
+ *                     the number of v's neighbours in R_l (the CREW UPDATE,
+ *                     PAPER.md:979-986): no concurrent writes per arc (a vertex
+ *                     split over several warps adds one atomic per 512 arcs),
+ *                     but every survivor rescans its whole adjacency each round.
+ * Both give the identical round[] (the decrements are the same integers). */
+enum pgc_update_mode { PGC_UPDATE_PUSH = 0, PGC_UPDATE_PULL = 1 };
+
+/* pgc_adg_order with an explicit UPDATE style (pgc_adg_order = PGC_UPDATE_PUSH).
+ * Arguments and errors as pgc_adg_order; an update_mode outside the enum is
+ * PGC_EINVAL.  Stats: rounds, sum_active, cross_edges (identical for both
+ * modes). */
+int pgc_adg_order_mode(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int update_mode,
+                       int32_t* round_out, int32_t* num_rounds, void* workspace,
+                       size_t workspace_bytes, void* cuda_stream);
+
 /* JP coloring (Algorithm 3) for the priority
  * <round[v], splitmix64(seed ^ v)>, lexicographic.  round[] may be ANY int32
  * array whose value range (max - min) is below n + 65536, e.g. rho_ADG

@@ -26,7 +26,7 @@ _lib = ctypes.CDLL(SO_PATH)
 
 PGC_OK, PGC_EINVAL, PGC_EWORKSPACE, PGC_ECUDA, PGC_EINTERNAL = 0, 1, 2, 3, 4
 
-EXPORTS = ["pgc_workspace_bytes", "pgc_adg_order", "pgc_jp_color", "pgc_color_jp_adg",
+EXPORTS = ["pgc_workspace_bytes", "pgc_adg_order", "pgc_adg_order_mode", "pgc_jp_color", "pgc_color_jp_adg",
            "pgc_adg_m_order", "pgc_color_jp_adg_m", "pgc_color_jp_adg_o", "pgc_jp_baseline",
            "pgc_color_dec_adg_itr",
            "pgc_host_workspace_bytes", "pgc_color_jp_adg_host", "pgc_check_graph",
@@ -61,6 +61,8 @@ _lib.pgc_host_workspace_bytes.restype = _sz
 _lib.pgc_host_workspace_bytes.argtypes = [_i64, _i64]
 _lib.pgc_adg_order.restype = ctypes.c_int
 _lib.pgc_adg_order.argtypes = [_GP, _u32, _u32, _vp, _i32p, _vp, _sz, _vp]
+_lib.pgc_adg_order_mode.restype = ctypes.c_int
+_lib.pgc_adg_order_mode.argtypes = [_GP, _u32, _u32, ctypes.c_int, _vp, _i32p, _vp, _sz, _vp]
 _lib.pgc_jp_color.restype = ctypes.c_int
 _lib.pgc_jp_color.argtypes = [_GP, _vp, _u64, _vp, _i32p, _vp, _sz, _vp]
 _lib.pgc_color_jp_adg.restype = ctypes.c_int
@@ -183,16 +185,23 @@ def _out(t, n, device, name):
     return t
 
 
-def adg_order(row_offsets, col_indices, eps_num: int, eps_den: int, *, round_out=None):
-    """ADG ordering (Alg. 1).  Returns (round int32[n] on device, T)."""
+UPDATE_MODES = {"push": 0, "pull": 1}   # enum pgc_update_mode
+
+
+def adg_order(row_offsets, col_indices, eps_num: int, eps_den: int, *, update="push",
+              round_out=None):
+    """ADG ordering (Alg. 1) with the push or pull UPDATE.
+    Returns (round int32[n] on device, T)."""
     g = _graph(row_offsets, col_indices)
     dev = row_offsets.device
     rnd = _out(round_out, g.n, dev, "round_out")
     nb = workspace_bytes(g.n, g.nnz)
     ws = _workspace(nb, dev)
     T = ctypes.c_int32(0)
-    _check(_lib.pgc_adg_order(ctypes.byref(g), eps_num, eps_den, rnd.data_ptr() if g.n else None,
-                              ctypes.byref(T), ws.data_ptr(), ws.numel(), _stream(dev)))
+    mode = UPDATE_MODES[update]
+    _check(_lib.pgc_adg_order_mode(ctypes.byref(g), eps_num, eps_den, mode,
+                                   rnd.data_ptr() if g.n else None, ctypes.byref(T),
+                                   ws.data_ptr(), ws.numel(), _stream(dev)))
     return rnd, T.value
 
 

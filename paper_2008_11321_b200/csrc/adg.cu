@@ -80,7 +80,7 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
                              const int32_t* __restrict__ Uin, int32_t* __restrict__ Uout,
                              int4* __restrict__ lrec, int4* __restrict__ chunks,
                              int32_t* __restrict__ npred, State* st, int heavy_deg, int chunk,
-                             int64_t chunk_cap) {
+                             int64_t chunk_cap, int pull) {
   __shared__ int sm[33];
   __shared__ long long s_dmax;
   __shared__ unsigned long long s_red[32];
@@ -133,12 +133,15 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
         st_u8_keep(rs + v[j], (l - 1) % 255 + 1);
         my_sumD += (unsigned long long)d[j];
         my_nR += 1;
+      }
+      // UPDATE's work records: push scans R_l's arcs, pull the survivors' (U_{l+1})
+      if (pull ? (valid[j] && !sel[j]) : sel[j]) {
         o[j] = off[v[j]];
         deg[j] = off[v[j] + 1] - o[j];
         light[j] = deg[j] > 0 && deg[j] <= heavy_deg;  // isolated: settled by k_adg_init
         if (deg[j] > heavy_deg) {
           nch[j] = (int)((deg[j] + chunk - 1) / chunk);
-          npred[v[j]] = 0;
+          if (!pull) npred[v[j]] = 0;
         }
       }
       packed += (unsigned long long)nch[j] + ((unsigned long long)light[j] << 32) +
@@ -197,9 +200,13 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
 
 // Arc classifier.  MODE 0: ADG only; 1: ADG with fused JP Part 1; 2: JP Part 1
 // for an arbitrary first key (pgc_jp_color); 3: ADG with fused JP Part 1 for
-// ADG-O's total order (round, D_rem, id) (UPDATEandPRIORITIZE).
+// ADG-O's total order (round, D_rem, id) (UPDATEandPRIORITIZE);
+// 4: ADG's pull (CREW) UPDATE: the records are the
+// survivors U_{l+1}, an arc is counted iff its target was removed in round l,
+// and the owner subtracts its count from its own D (no per-arc atomics).
 template <int MODE>
 struct Arc {
+  static constexpr bool kPreds = MODE != 0 && MODE != 4;  // stores pred slots (JP Part 1)
   int l;
   uint64_t seed;
   const int32_t* __restrict__ round;
@@ -228,6 +235,7 @@ struct Arc {
   // are decremented)
   __device__ __forceinline__ uint64_t own(int v) const {
     if (MODE == 3) return (((uint64_t)(uint32_t)D[v]) << 32) | (uint32_t)v;
+    if (MODE == 4) return 0;
     return prio_hash(seed, (uint32_t)v);
   }
   // true iff u in pred(v); performs UPDATE's decrement and counts cut arcs.
@@ -240,6 +248,11 @@ struct Arc {
   }
   __device__ __forceinline__ bool classify(int u, int g, int rv, uint64_t hv,
                                           unsigned long long& cut, int du = 0) const {
+    if (MODE == 4) {                    // pull: u in N(v) ∩ R_l
+      if (g != 1) return false;
+      cut += 1;
+      return true;
+    }
     if (MODE == 2) {
       if (g != rv) return g > rv;
       return prio_hash(seed, (uint32_t)u) > hv;
@@ -360,7 +373,7 @@ __global__ void __launch_bounds__(256, PGC_LIGHT_MINB) k_update_light(Arc<MODE> 
           const int oe = __shfl_sync(0xffffffffu, excl, ow[k]);
           const long long oo = __shfl_sync(0xffffffffu, o, ow[k]);
           const int seg0 = max(0, oe - ts);  // first lane of the owner's segment
-          if (pred) {
+          if (Arc<MODE>::kPreds && pred) {
             const int rank = __popc(pb & lt & ~((1u << seg0) - 1u));
             st_stream(P + oo + base + rank, u[k]);
           }
@@ -372,14 +385,15 @@ __global__ void __launch_bounds__(256, PGC_LIGHT_MINB) k_update_light(Arc<MODE> 
         }
       }
     }
-    if (MODE != 0 && valid) {
+    if (MODE == 4 && valid && cnt) A.D[v] -= cnt;  // v's own counter: one writer
+    if (Arc<MODE>::kPreds && valid) {
       npred[v] = cnt;
       preds += (unsigned long long)cnt;
     }
   }
   unsigned long long t = block_sum(cut, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(&st->cut, t);
-  if (MODE != 0) {
+  if (Arc<MODE>::kPreds) {
     t = block_sum(preds, s_red);
     if (threadIdx.x == 0 && t) atomicAdd(&st->pred_arcs, t);
   }
@@ -403,7 +417,7 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
                                                       int32_t* __restrict__ P, State* st,
                                                       int filter_ratio) {
   __shared__ unsigned long long s_red[32];
-  __shared__ int s_buf[MODE != 0 ? 8 : 1][MODE != 0 ? kSub : 1];
+  __shared__ int s_buf[Arc<MODE>::kPreds ? 8 : 1][Arc<MODE>::kPreds ? kSub : 1];
   __shared__ int s_next;
   if (MODE != 2 && st->done) return;
   if (MODE != 2 && filter_round(st, filter_ratio)) return;  // k_update_heavy_f's round
@@ -459,12 +473,13 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
           const bool pred = u[k] >= 0 && A.classify(u[k], g[k], rv, hv, cut, du[k]);
           if (MODE != 0) {
             const unsigned bal = __ballot_sync(0xffffffffu, pred);
-            if (pred) s_buf[warp][cnt + __popc(bal & lanemask_lt())] = u[k];
+            if (Arc<MODE>::kPreds && pred) s_buf[warp][cnt + __popc(bal & lanemask_lt())] = u[k];
             cnt += __popc(bal);
           }
         }
       }
-      if (MODE != 0 && cnt) {
+      if (MODE == 4 && cnt && lane == 0) atomicSub(&A.D[v], cnt);  // one per sub-chunk
+      if (Arc<MODE>::kPreds && cnt) {
         __syncwarp();
         int base = 0;
         if (lane == 0) base = atomicAdd(&npred[v], cnt);
@@ -477,7 +492,7 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
   }
   unsigned long long t = block_sum(cut, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(&st->cut, t);
-  if (MODE != 0) {
+  if (Arc<MODE>::kPreds) {
     t = block_sum(preds, s_red);
     if (threadIdx.x == 0 && t) atomicAdd(&st->pred_arcs, t);
   }
@@ -633,7 +648,7 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
   }
   unsigned long long t = block_sum(cut, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(&st->cut, t);
-  if (MODE != 0) {
+  if (Arc<MODE>::kPreds) {
     t = block_sum(preds, s_red);
     if (threadIdx.x == 0 && t) atomicAdd(&st->pred_arcs, t);
   }
@@ -840,12 +855,12 @@ static int launch_update(Ctx& c, const Arc<MODE>& A, const int32_t* Uin = nullpt
   const int GL = wave_grid(c, k_update_light<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_light",
              k_update_light<MODE><<<GL, 256, 0, c.st>>>(A, c.col, c.lrec, c.npred, c.P, c.state));
-  const int ratio = MODE == 2 ? 0 : c.tune.filter_ratio;
+  const int ratio = (MODE == 2 || MODE == 4) ? 0 : c.tune.filter_ratio;
   const int GH = wave_grid(c, k_update_heavy<MODE>, 256);
   PGC_LAUNCH(c, kGUpdate, "k_update_heavy",
              k_update_heavy<MODE><<<GH, 256, 0, c.st>>>(A, c.col, c.chunks, c.npred, c.P, c.state,
                                                         ratio));
-  if constexpr (MODE != 2) {
+  if constexpr (MODE != 2 && MODE != 4) {
     if (ratio > 0) {
       static bool attr = false;  // per process: the attribute is per function
       if (!attr) {
@@ -908,9 +923,9 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                  k_adg_select<<<G, B, 0, c.st>>>(l, rule, num, den, c.off, c.D, round, c.rs, Uin, Uout,
                                                  c.lrec, c.chunks, c.npred, c.state,
                                                  c.tune.heavy_degree, c.tune.chunk_arcs,
-                                                 c.lay.chunk_cap));
+                                                 c.lay.chunk_cap, mode == kAdgPull));
       if (l == 1 && c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
-      if (c.tune.filter_ratio > 0)
+      if (c.tune.filter_ratio > 0 && mode != kAdgPull)
         PGC_LAUNCH(c, kGUpdate, "k_filter_build",
                    k_filter_build<<<c.nsm * 2, 1024, 0, c.st>>>(l, Uin, c.filt, c.state,
                                                                 c.tune.filter_ratio));
@@ -918,6 +933,8 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
         if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs}, Uin)) return e;
       } else if (mode == kAdgFusedO) {
         if (int e = launch_update(c, Arc<3>{l, seed, round, c.D, c.rs}, Uin)) return e;
+      } else if (mode == kAdgPull) {
+        if (int e = launch_update(c, Arc<4>{l, seed, round, c.D, c.rs}, Uin)) return e;
       } else {
         if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs}, Uin)) return e;
       }

@@ -254,14 +254,25 @@ size_t pgc_workspace_bytes(int64_t n, int64_t nnz) {
 
 int pgc_adg_order(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int32_t* round_out,
                   int32_t* num_rounds, void* workspace, size_t workspace_bytes, void* cuda_stream) {
+  return pgc_adg_order_mode(g, eps_num, eps_den, PGC_UPDATE_PUSH, round_out, num_rounds, workspace,
+                            workspace_bytes, cuda_stream);
+}
+
+int pgc_adg_order_mode(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, int update_mode,
+                       int32_t* round_out, int32_t* num_rounds, void* workspace,
+                       size_t workspace_bytes, void* cuda_stream) {
   if (int e = check_graph_args(g)) return e;
+  if (update_mode != PGC_UPDATE_PUSH && update_mode != PGC_UPDATE_PULL)
+    return fail(PGC_EINVAL, "update_mode must be PGC_UPDATE_PUSH or PGC_UPDATE_PULL");
   if (eps_num == 0 || eps_den == 0) return fail(PGC_EINVAL, "eps must be num/den with num, den >= 1");
   if (!num_rounds || (g->n > 0 && !round_out)) return fail(PGC_EINVAL, "output pointer is NULL");
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
   call_begin(c);
-  if (int e = adg_run(c, eps_num, eps_den, 0, round_out, kAdgOnly, nullptr)) return e;
+  if (int e = adg_run(c, eps_num, eps_den, 0, round_out,
+                      update_mode == PGC_UPDATE_PULL ? kAdgPull : kAdgOnly, nullptr))
+    return e;
   *num_rounds = c.h_state->T;
   call_end(c, c.h_state->T, 0, c.h_state->sum_active, c.h_state->cross, 0, 0);
   return PGC_OK;

@@ -140,7 +140,8 @@ constexpr int kFilterWords = kFilterBytes / 4;
 
 // ---- phases (host orchestration; return 0 or a PGC_* code) -----------------
 // kAdgFusedO: JP Part 1 for ADG-O's total order (round, D_rem, id) (Q22)
-enum AdgMode { kAdgOnly = 0, kAdgFused = 1, kAdgFusedO = 3 };
+// kAdgPull: ADG only, with the pull (CREW) UPDATE
+enum AdgMode { kAdgOnly = 0, kAdgFused = 1, kAdgFusedO = 3, kAdgPull = 4 };
 // selection rule of a round: ADG's mean threshold (Alg. 1) or ADG-M's median
 //
 enum AdgRule { kRuleMean = 0, kRuleMedian = 1 };

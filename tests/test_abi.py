@@ -97,6 +97,10 @@ def test_argument_errors_without_gpu():
                               ctypes.byref(T), ctypes.byref(K), ctypes.c_void_p(0x10000), 1 << 30, None)
     assert rc == pgc.PGC_EINVAL
     assert lib.pgc_last_stats(None) == pgc.PGC_EINVAL
+    for mode in (-1, 2):   # enum pgc_update_mode has PUSH = 0 and PULL = 1 only
+        rc = lib.pgc_adg_order_mode(ctypes.byref(g), 1, 10, mode, ctypes.c_void_p(0x1000),
+                                    ctypes.byref(T), ctypes.c_void_p(0x10000), 1 << 30, None)
+        assert rc == pgc.PGC_EINVAL and b"update_mode" in lib.pgc_last_error()
 
 
 def test_product_path_does_not_import_oracle():

@@ -472,3 +472,74 @@ def test_repeat_runs_are_identical_and_never_stall():
                 assert all(np.array_equal(x, y) for x, y in zip(out, ref)), f"repeat {rep} differs"
     finally:
         pgc.set_tuning("jp_watchdog_ms", 20000)
+
+
+# ------------------------------------------ pull (CREW) UPDATE (NEXT-4) -------
+def assert_parity_pull(g, num, den):
+    """pgc_adg_order_mode with PGC_UPDATE_PULL (and PUSH) against the ADG oracle:
+    identical rounds and identical round statistics (the decrements are the
+    same integers)."""
+    pgc, off, col = dev(g)
+    r_or, st_or = O.adg(g, num, den)
+    for upd in ("pull", "push"):
+        rnd, T = pgc.adg_order(off, col, num, den, update=upd)
+        torch.cuda.synchronize()
+        st = pgc.last_stats()
+        assert T == st_or["T"], upd
+        bad = np.nonzero(rnd.cpu().numpy() != r_or)[0]
+        assert len(bad) == 0, f"{upd} round mismatch at {bad[:10]}"
+        assert st["sum_active"] == st_or["sum_active"], upd
+        assert st["cross_edges"] == st_or["cross_edges"], upd
+    return st_or["T"]
+
+
+def test_adg_pull_small_graphs():
+    for c in json.load(open(os.path.join(GOLDEN, "appendix_b.json")))["cases"]:
+        assert assert_parity_pull(gg.from_edges(c["n"], c["edges"]), *c["eps"]) == c["T"]
+    edges, n = [], 0
+    for k in range(1, 6):
+        for es in all_graphs(k):
+            edges += [(a + n, b + n) for a, b in es]
+            n += k
+    g = gg.from_edges(n, edges)
+    for num, den in [(1, 100), (1, 10), (1, 2), (4294967295, 1)]:
+        assert_parity_pull(g, num, den)
+    pgc, off, col = dev(gg.from_edges(0, []))
+    assert pgc.adg_order(off, col, 1, 10, update="pull")[1] == 0
+
+
+def test_adg_pull_hubs_and_random():
+    # surviving hubs: a 5000-leaf star (the hub survives round 1 and is a
+    # chunked record of the pull UPDATE) and a hub joined to a clique
+    assert_parity_pull(gg.from_edges(5001, [(0, i) for i in range(1, 5001)]), 1, 10)
+    n = 400
+    edges = [(i, j) for i in range(1, n) for j in range(i + 1, n)] + [(0, i) for i in range(1, 20000)]
+    assert_parity_pull(gg.from_edges(20000, edges), 1, 100)
+    for seed in range(1, 5):
+        for g in (gg.er(3000, 15000 + 1000 * seed, seed), gg.rmat(10 + seed, 16, seed=seed)):
+            for num, den in [(1, 100), (1, 10), (1, 2)]:
+                assert_parity_pull(g, num, den)
+
+
+@pytest.mark.parametrize("cfg", ["rmat20", "grid", "rmat24"])
+def test_adg_pull_full_size(cfg):
+    g = gg.config_graph(cfg)
+    for num, den in gg.CONFIGS[cfg][1][-1:]:
+        assert_parity_pull(g, num, den)
+
+
+def test_more_than_255_rounds_every_entry_point():
+    """Paths with eps < 1/(n-1) peel two ends per round (closed form pinned in
+    test_oracle_pins): 500 / 501 rounds, past the one-byte round state's
+    255, so the late rounds classify arcs from round[] (Arc::raw)."""
+    for n in (1000, 1001):
+        # P_n plus P_601, randomly relabelled (mean degree stays below 2)
+        edges = [(i, i + 1) for i in range(n - 1)] + [(n + i, n + i + 1) for i in range(600)]
+        perm = np.random.default_rng(n).permutation(n + 601)
+        g = gg.from_edges(n + 601, [(int(perm[a]), int(perm[b])) for a, b in edges])
+        den = 100 * n
+        T = assert_parity_pull(g, 1, den)
+        assert T > 255
+        assert_parity(g, 1, den, 3)
+        assert_parity_o(g, 1, den)
+        assert_parity_dec(g, 1, den, 3)

@@ -279,3 +279,19 @@ def test_jp_levels_longest_path():
     rnd, _ = O.adg(g, 1, 10)
     _, _, lvl, J = O.jp(g, rnd, 1, levels=True)
     assert J == 2 and lvl[0] == 1
+
+
+@pytest.mark.parametrize("n", [2, 3, 7, 600, 1001])
+def test_path_peels_two_ends_per_round(n):
+    """Closed form (Alg. 1): on the path P_n with eps < 1/(n-1),
+    a sub-path of n' >= 3 vertices has mean degree 2(n'-1)/n' and
+    (1+eps) * 2(n'-1)/n' < 2, so only its two ends (degree 1) leave in a round;
+    hence round[i] = min(i, n-1-i) + 1 and T = ceil(n/2).  n = 600, 1001 give
+    more than 255 rounds (the GPU's one-byte round state wraps there)."""
+    g = gg.from_edges(n, [(i, i + 1) for i in range(n - 1)])
+    r, st = O.adg(g, 1, 10 * n)
+    i = np.arange(n)
+    assert st["T"] == (n + 1) // 2
+    assert np.array_equal(r, np.minimum(i, n - 1 - i) + 1)
+    # every edge joins two rounds except the middle one of an even path
+    assert st["cross_edges"] == (n - 1) - (1 if n % 2 == 0 else 0)
