@@ -267,16 +267,28 @@ __device__ __forceinline__ int bucket_of(int v, int r, Key2 seed, int rmax,
   return base1[k] + (B - 1 - hb);  // larger hash -> earlier bucket
 }
 
+#ifndef PGC_ORD_ITEMS
+#define PGC_ORD_ITEMS 4
+#endif
+constexpr int kOrdItems = PGC_ORD_ITEMS;
 __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, Key2 seed,
                         const int32_t* __restrict__ npred,
                         const State* st, const int32_t* __restrict__ hist1,
                         const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt) {
   const int rmax = st->rmax;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (!in_order(npred, v)) continue;
-    const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
-    atomicAdd(&bcnt[b], 1);
+  // kOrdItems vertices per thread per step, all loads before any use
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += stride * kOrdItems) {
+    int np[kOrdItems], r[kOrdItems];
+#pragma unroll
+    for (int j = 0; j < kOrdItems; ++j) {
+      const int64_t v = v0 + j * stride;
+      np[j] = v < n ? __ldcs(npred + v) : -1;
+      r[j] = v < n ? __ldcs(round + v) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kOrdItems; ++j)
+      if (np[j] >= 0) atomicAdd(&bcnt[bucket_of((int)(v0 + j * stride), r[j], seed, rmax, hist1, base1)], 1);
   }
 }
 
@@ -288,6 +300,8 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 see
                           const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
                           const int32_t* __restrict__ bstart, const int32_t* __restrict__ npred,
                           const int64_t* __restrict__ off, int4* __restrict__ rec) {
+  // (bound by the random 16-byte record stores into a 141 MB array: more
+  // vertices per thread in flight measured no faster)
   const int rmax = st->rmax;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
@@ -590,11 +604,25 @@ __global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __rest
     const int np = r.y;
     const int64_t b = lo_hi(r.z, r.w);
     uint16_t* L = reinterpret_cast<uint16_t*>(P + b);
-    for (int i0 = 0; i0 < np; i0 += 32) {
-      const int i = i0 + lane;
-      const int y = i < np ? pos[P[b + i]] : 0;
-      __syncwarp();  // every lane has read its int32 entry before any u16 lands
-      if (i < np) L[i] = (uint16_t)y;
+    // kListStrips strips of 32 entries per step: loads, then gathers, in flight
+    // together; the u16 writes of a step land on int32 entries the step (or an
+    // earlier one) has already read
+    constexpr int kListStrips = 8;
+    for (int i0 = 0; i0 < np; i0 += 32 * kListStrips) {
+      int x[kListStrips], y[kListStrips];
+#pragma unroll
+      for (int k = 0; k < kListStrips; ++k) {
+        const int i = i0 + 32 * k + lane;
+        x[k] = i < np ? P[b + i] : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < kListStrips; ++k) y[k] = x[k] >= 0 ? pos[x[k]] : 0;
+      __syncwarp();  // every lane has read its int32 entries before any u16 lands
+#pragma unroll
+      for (int k = 0; k < kListStrips; ++k) {
+        const int i = i0 + 32 * k + lane;
+        if (i < np) L[i] = (uint16_t)y[k];
+      }
       __syncwarp();
     }
   }
