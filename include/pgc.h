@@ -252,7 +252,10 @@ const char* pgc_last_error(void);
  *   "core_min_avg" (min mean |pred| of the core prefix), "core_min_n",
  *   "core_ctas" 0..16 (cluster size; 0 = automatic), "core_spin_ns" (backoff cap
  *   of a core warp several preds away from ready), "core_arc_cap",
- *   "core_arcs_per_cta".
+ *   "core_arcs_per_cta", "itr_blocks_per_sm" 0..64 (DEC-ADG-ITR pass kernel;
+ *   0 = occupancy), "jp_split_overlap" 0/1 (JP: the bulk's work-list split runs
+ *   on a second stream while the core kernel, one cluster of <= 16 SMs, runs;
+ *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns".
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

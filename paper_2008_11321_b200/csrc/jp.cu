@@ -1546,8 +1546,11 @@ int jp_color_run(Ctx& c, int32_t* color) {
                    k_core_lists<<<G * 2, 256, 0, c.st>>>(c.rec, c.D, c.P, c.state));
       }
     }
-    // --- bulk split of positions [core_n, n_order) (needs only the records, so
-    //     it runs before the core kernel and the bulk starts right after it) ---
+    // --- bulk split of positions [core_n, n_order) (needs only the records)
+    //     and the core kernel: the core is one cluster of <= 16 SMs, so the
+    //     split runs beside it on a second stream (it writes only the bulk's
+    //     lists, the bulk's colors and its own counters; the core's pos[]
+    //     in D is dead once k_core_lists has run) ---
     if (c.tune.core_max <= 0)
       if (int e = sync_state(c)) return e;
     n_order = c.h_state->n_order;
@@ -1555,7 +1558,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
     const int64_t nbulk = n_order - NC;
     int4* hrec = c.rec + c.n;
     int4* lrec = hrec + c.lay.rec_heavy_cap;
-    if (nbulk > 0) {
+    auto split = [&]() -> int {
       const int G = c.nsm * 8;
       // flags: heavy -> U0, light -> U1; prefix counts: heavy -> Rl, light -> D
       // (ADG's lists and degrees, and the core's pos[], are dead by now)
@@ -1570,9 +1573,9 @@ int jp_color_run(Ctx& c, int32_t* color) {
       PGC_LAUNCH(c, kGJp, "k_bulk_scatter",
                  k_bulk_scatter<<<G, 256, 0, c.st>>>(n_order, c.rec, c.state, hpos, lpos, hrec, lrec,
                                                      color));
-    }
-    // --- core: one thread-block cluster ---
-    if (C > 0) {
+      return 0;
+    };
+    auto core = [&]() -> int {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(C);
       cfg.blockDim = dim3(kCoreBlock);
@@ -1593,6 +1596,35 @@ int jp_color_run(Ctx& c, int32_t* color) {
                                              (unsigned)c.tune.core_spin_ns,
                                              (unsigned)c.tune.core_tail_ns,
                                              (unsigned)c.tune.core_pass_ns, wd)));
+      return 0;
+    };
+    if (C > 0 && nbulk > 0 && c.tune.jp_split_overlap) {
+      // fork: the core first (it is launched first and finds its SMs free), the
+      // split on the side stream; join before the bulk
+      static thread_local cudaStream_t side = nullptr;
+      static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+      if (!side) {
+        PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        for (auto& e : ev) PGC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      PGC_CUDA(cudaEventRecord(ev[0], c.st));
+      if (int e = core()) return e;
+      PGC_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
+      const cudaStream_t main = c.st;
+      c.st = side;
+      const int e = split();
+      c.st = main;
+      if (e) {
+        cudaStreamSynchronize(side);  // nothing may stay in flight on the error path
+        return e;
+      }
+      PGC_CUDA(cudaEventRecord(ev[1], side));
+      PGC_CUDA(cudaStreamWaitEvent(c.st, ev[1], 0));
+    } else {
+      if (nbulk > 0)
+        if (int e = split()) return e;
+      if (C > 0)
+        if (int e = core()) return e;
     }
     // --- bulk dataflow ---
     if (nbulk > 0) {

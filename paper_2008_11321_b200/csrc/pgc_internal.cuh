@@ -86,6 +86,7 @@ struct Tuning {
   int core_tail_ns = 0;           // JP core: sleep (ns) per poll of a warp in the tail
   int core_pass_ns = 0;           // JP core: min sleep (ns) between passes of a warp far from its tail
   int itr_blocks_per_sm = 0;      // DEC-ADG-ITR: blocks per SM of the cooperative kernel (0 = occupancy)
+  int jp_split_overlap = 1;       // JP: run the bulk split on a side stream beside the core kernel
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
