@@ -255,6 +255,8 @@ const char* pgc_last_error(void);
  *   "core_arcs_per_cta", "itr_blocks_per_sm" 0..64 (DEC-ADG-ITR pass kernel;
  *   0 = occupancy), "jp_split_overlap" 0/1 (JP: the bulk's work-list split runs
  *   on a second stream while the core kernel, one cluster of <= 16 SMs, runs;
+ *   default 1), "update_atom" 0/1 (ADG round 1 classifies each arc by the old
+ *   value of ONE atomic decrement instead of a state gather plus a RED;
  *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns".
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);

@@ -75,12 +75,12 @@ __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ o
 // a2+a3: threshold, select, compact.
 constexpr int kSelItems = 4;
 __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
-                             const int32_t* __restrict__ D, int32_t* __restrict__ round,
+                             int32_t* __restrict__ D, int32_t* __restrict__ round,
                              uint8_t* __restrict__ rs,
                              const int32_t* __restrict__ Uin, int32_t* __restrict__ Uout,
                              int4* __restrict__ lrec, int4* __restrict__ chunks,
                              int32_t* __restrict__ npred, State* st, int heavy_deg, int chunk,
-                             int64_t chunk_cap, int pull) {
+                             int64_t chunk_cap, int pull, int mark_removed) {
   __shared__ int sm[33];
   __shared__ long long s_dmax;
   __shared__ unsigned long long s_red[32];
@@ -131,6 +131,7 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
       if (sel[j]) {
         round[v[j]] = l;
         st_u8_keep(rs + v[j], (l - 1) % 255 + 1);
+        if (mark_removed) st_i32_keep(D + v[j], -1);  // round 1's atomic UPDATE (Arc::atom)
         my_sumD += (unsigned long long)d[j];
         my_nR += 1;
       }
@@ -212,6 +213,13 @@ struct Arc {
   const int32_t* __restrict__ round;
   int32_t* __restrict__ D;
   const uint8_t* __restrict__ rs;
+  // Round 1 of MODES 0/1 (knob update_atom): ONE atomic per arc instead of a
+  // state gather plus a RED.  k_adg_select has set D = -1 on R_1, so the
+  // DecrementAndFetch's old value classifies the target (>= 0: alive, < 0:
+  // removed this round; no vertex was removed earlier); the decrement of a
+  // removed vertex is harmless (its D is never read again in these modes and
+  // stays negative: at most deg < 2^31 decrements).
+  int atom = 0;
   // Round state of u.  MODE 0/1: 0 = alive (u in U), 1 = removed in this
   // round, 2 = removed earlier; read from the 1-byte rs[] while l <= 255
   // (exact: rs = ((round-1) mod 255) + 1), from round[] afterwards.  MODE 2:
@@ -219,6 +227,7 @@ struct Arc {
   // before it consumes any (raw() on a clamped address is unconditional; a
   // gather whose use sits in the same branch would serialise on its latency).
   __device__ __forceinline__ int raw(int u) const {
+    if ((MODE == 0 || MODE == 1) && atom) return u >= 0 ? atomicAdd(&D[u], -1) : 0;
     const int uu = u >= 0 ? u : 0;
     if (MODE != 2 && l <= 255) return ld_u8_keep(rs + uu);  // read-only, L2 evict-last
     return round[uu];
@@ -226,6 +235,7 @@ struct Arc {
   __device__ __forceinline__ int decode(int u, int x) const {
     if (u < 0) return 0;
     if (MODE == 2) return x;
+    if ((MODE == 0 || MODE == 1) && atom) return x < 0 ? 1 : 0;
     return x == 0 ? 0 : (x == l ? 1 : 2);  // for l <= 255, rs == round of every removed u
   }
   __device__ __forceinline__ int state(int u) const { return decode(u, raw(u)); }
@@ -259,7 +269,8 @@ struct Arc {
     }
     const int su = g;
     if (su == 0) {                      // u in U \ R: DecrementAndFetch(D[u])
-      red_dec_keep(&D[u]);              // result unused -> RED
+      if (!((MODE == 0 || MODE == 1) && atom))
+        red_dec_keep(&D[u]);            // result unused -> RED (the atom path has decremented)
       cut += 1;
       return MODE == 1 || MODE == 3;    // u gets a later round: higher priority
     }
@@ -911,6 +922,7 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
     for (int j = 0; j < batch; ++j, ++l) {
       const int32_t* Uin = l == 1 ? nullptr : c.U[l & 1];
       int32_t* Uout = c.U[(l + 1) & 1];
+      const int atom = l == 1 && c.tune.update_atom && (mode == kAdgOnly || mode == kAdgFused);
       if (rule == kRuleMedian) {
         PGC_LAUNCH(c, kGSelect, "k_msel_reset", k_msel_reset<<<1, 1, 0, c.st>>>(c.state));
         for (size_t p = 0; p < digits.size(); ++p)
@@ -923,20 +935,20 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                  k_adg_select<<<G, B, 0, c.st>>>(l, rule, num, den, c.off, c.D, round, c.rs, Uin, Uout,
                                                  c.lrec, c.chunks, c.npred, c.state,
                                                  c.tune.heavy_degree, c.tune.chunk_arcs,
-                                                 c.lay.chunk_cap, mode == kAdgPull));
+                                                 c.lay.chunk_cap, mode == kAdgPull, atom));
       if (l == 1 && c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
       if (c.tune.filter_ratio > 0 && mode != kAdgPull)
         PGC_LAUNCH(c, kGUpdate, "k_filter_build",
                    k_filter_build<<<c.nsm * 2, 1024, 0, c.st>>>(l, Uin, c.filt, c.state,
                                                                 c.tune.filter_ratio));
       if (mode == kAdgFused) {
-        if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs}, Uin)) return e;
+        if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs, atom}, Uin)) return e;
       } else if (mode == kAdgFusedO) {
         if (int e = launch_update(c, Arc<3>{l, seed, round, c.D, c.rs}, Uin)) return e;
       } else if (mode == kAdgPull) {
         if (int e = launch_update(c, Arc<4>{l, seed, round, c.D, c.rs}, Uin)) return e;
       } else {
-        if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs}, Uin)) return e;
+        if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs, atom}, Uin)) return e;
       }
       PGC_LAUNCH(c, kGAdgOther, "k_adg_finalize",
                  k_adg_finalize<<<1, 32, 0, c.st>>>(l, c.state, c.per_round));
