@@ -292,46 +292,45 @@ __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, Key2 seed,
   }
 }
 
-// Places every vertex's JP work record {v, |pred|, P slot lo, hi} at its
-// bucket position (the per-vertex inputs are read coalesced here, once, so the
-// JP workers fetch one 16-byte record per vertex).
+// Places every ordered vertex's id at a slot of its bucket (4-byte stores into
+// an n-int array that stays in L2; the 16-byte records are written by
+// k_bucket_sort, bucket by bucket, after the sort).
 __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 seed,
                           const State* st, const int32_t* __restrict__ hist1,
                           const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
                           const int32_t* __restrict__ bstart, const int32_t* __restrict__ npred,
-                          const int64_t* __restrict__ off, int4* __restrict__ rec) {
-  // (bound by the random 16-byte record stores into a 141 MB array: more
-  // vertices per thread in flight measured no faster)
+                          int32_t* __restrict__ ord) {
   const int rmax = st->rmax;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int np = npred[v];
-    if (np < 0) continue;  // isolated: not in the order
+    if (!in_order(npred, v)) continue;  // isolated: not in the order
     const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
-    const int pos = bstart[b] + atomicSub(&bcnt[b], 1) - 1;
-    const int64_t o = off[v];
-    rec[pos] = make_int4((int)v, np, (int)(uint32_t)o, (int)(o >> 32));
+    ord[bstart[b] + atomicSub(&bcnt[b], 1) - 1] = (int)v;
   }
 }
 
 // Sort every bucket by h descending (bucket = same round, same top hash
-// bits).  One lane per bucket (insertion sort in registers, <= 16 entries, the
+// bits) and write its JP work records {v, |pred|, P slot lo, hi} in that
+// order.  One lane per bucket (insertion sort in registers, <= 12 entries, the
 // common case at mean occupancy 4..8); larger buckets are ranked by a whole
-// warp afterwards.
+// warp.  Every bucket is sorted: the bulk's workers hold one ticket AHEAD of
+// the vertex they color (the prefetched record), so with an order that is
+// exact only across buckets a worker could color v while its own prefetched
+// ticket is a higher-priority same-bucket pred of v: a deadlock (seen once on
+// JP-R at R-MAT 24).  In exact priority order a prefetched ticket always has a
+// lower priority than the current one, and the highest-priority uncolored
+// vertex is a current vertex (all preds colored) or the next ticket of a
+// worker whose current vertex is colored.
 constexpr int kLaneSortMax = 12;
-// Every bucket is sorted (limit = INT_MAX): the bulk's workers hold one
-// ticket AHEAD of the vertex they color (the prefetched record), so with an
-// order that is exact only across buckets a worker could color v while its
-// own prefetched ticket is a higher-priority same-bucket pred of v: a
-// deadlock (seen once on JP-R at R-MAT 24).  In exact priority order a
-// prefetched ticket always has a lower priority than the current one, and the
-// highest-priority uncolored vertex is a current vertex (all preds colored)
-// or the next ticket of a worker whose current vertex is colored.  (A
-// `limit` below the bucket count leaves buckets of <= kMaxUnsortedBucket
-// unsorted past it -- only for experiments without prefetching workers.)
-constexpr int kMaxUnsortedBucket = 64;
+__device__ __forceinline__ int4 work_rec(int v, const int32_t* __restrict__ npred,
+                                         const int64_t* __restrict__ off) {
+  const int64_t o = off[v];
+  return make_int4(v, npred[v], (int)(uint32_t)o, (int)(o >> 32));
+}
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
-                              int4* __restrict__ rec, Key2 seed, int limit) {
+                              int32_t* __restrict__ ord, const int32_t* __restrict__ npred,
+                              const int64_t* __restrict__ off, int4* __restrict__ rec,
+                              Key2 seed) {
   const int lane = lane_id();
   const int nb = st->nbuckets;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -342,21 +341,20 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
     if (b < nb) {
       s0 = bstart[b];
       s = bstart[b + 1] - s0;
-      if (s0 >= limit && s <= kMaxUnsortedBucket) s = 0;  // leave unsorted
     }
-    if (s >= 2 && s <= kLaneSortMax) {
-      int4 vv[kLaneSortMax];
+    if (s >= 1 && s <= kLaneSortMax) {
+      int vv[kLaneSortMax];
       uint64_t hh[kLaneSortMax];
 #pragma unroll
       for (int i = 0; i < kLaneSortMax; ++i)
         if (i < s) {
-          vv[i] = rec[s0 + i];
-          hh[i] = seed((uint32_t)vv[i].x);
+          vv[i] = ord[s0 + i];
+          hh[i] = seed((uint32_t)vv[i]);
         }
 #pragma unroll
       for (int i = 1; i < kLaneSortMax; ++i) {
         if (i < s) {
-          const int4 x = vv[i];
+          const int x = vv[i];
           const uint64_t hx = hh[i];
           int j = i - 1;
 #pragma unroll
@@ -370,9 +368,13 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
           }
         }
       }
+      int4 r[kLaneSortMax];
+#pragma unroll
+      for (int i = 0; i < kLaneSortMax; ++i)  // all gathers in flight
+        if (i < s) r[i] = work_rec(vv[i], npred, off);
 #pragma unroll
       for (int i = 0; i < kLaneSortMax; ++i)
-        if (i < s) rec[s0 + i] = vv[i];
+        if (i < s) rec[s0 + i] = r[i];
     }
     // rare large buckets: the whole warp ranks them, one bucket at a time
     unsigned big = __ballot_sync(0xffffffffu, s > kLaneSortMax);
@@ -382,24 +384,25 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
       const int bs0 = __shfl_sync(0xffffffffu, s0, src);
       const int bs = __shfl_sync(0xffffffffu, s, src);
       if (bs <= 32) {
-        const int4 v = lane < bs ? rec[bs0 + lane] : make_int4(0, 0, 0, 0);
-        const uint64_t h = lane < bs ? seed((uint32_t)v.x) : 0;
+        const int v = lane < bs ? ord[bs0 + lane] : 0;
+        const uint64_t h = lane < bs ? seed((uint32_t)v) : 0;
         int rank = 0;
         for (int j = 0; j < bs; ++j) rank += __shfl_sync(0xffffffffu, h, j) > h;
-        __syncwarp();
-        if (lane < bs) rec[bs0 + rank] = v;
-        __syncwarp();
-      } else if (lane == 0) {  // very rare: insertion sort in place
-        for (int i = 1; i < bs; ++i) {
-          const int4 x = rec[bs0 + i];
-          const uint64_t hx = seed((uint32_t)x.x);
-          int j = i - 1;
-          while (j >= 0 && seed((uint32_t)rec[bs0 + j].x) < hx) {
-            rec[bs0 + j + 1] = rec[bs0 + j];
-            --j;
+        if (lane < bs) rec[bs0 + rank] = work_rec(v, npred, off);
+      } else {
+        if (lane == 0)  // very rare: insertion sort of the ids in place
+          for (int i = 1; i < bs; ++i) {
+            const int x = ord[bs0 + i];
+            const uint64_t hx = seed((uint32_t)x);
+            int j = i - 1;
+            while (j >= 0 && seed((uint32_t)ord[bs0 + j]) < hx) {
+              ord[bs0 + j + 1] = ord[bs0 + j];
+              --j;
+            }
+            ord[bs0 + j + 1] = x;
           }
-          rec[bs0 + j + 1] = x;
-        }
+        __syncwarp();
+        for (int i = lane; i < bs; i += 32) rec[bs0 + i] = work_rec(ord[bs0 + i], npred, off);
       }
       __syncwarp();
     }
@@ -459,9 +462,10 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
     return e;
   PGC_LAUNCH(c, kGOrder, "k_scatter",
              k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
-                                            c.bstart, c.npred, c.off, c.rec));
+                                            c.bstart, c.npred, c.U[1]));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
-             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.rec, seed, INT_MAX));
+             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.U[1], c.npred, c.off, c.rec,
+                                                seed));
   return 0;
 }
 
