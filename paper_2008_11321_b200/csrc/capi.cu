@@ -290,7 +290,7 @@ int pgc_jp_color(const pgc_graph* g, const int32_t* round, uint64_t seed, int32_
   c.round_key = round;
   c.seed = seed;
   if (int e = jp_setup_run(c, round, seed, color_out)) return e;
-  if (int e = jp_order_run(c, round, seed, false)) return e;
+  if (int e = jp_order_run(c, round, seed, false, false, true)) return e;
   if (int e = jp_color_run(c, color_out)) return e;
   *num_colors = c.h_state->K;
   call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.core_n);
@@ -325,7 +325,7 @@ static int color_jp_adg_impl(const pgc_graph* g, uint32_t eps_num, uint32_t eps_
   const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
   c.round_key = round_out;
   c.seed = seed;
-  if (int e = jp_order_run(c, round_out, seed, true)) return e;
+  if (int e = jp_order_run(c, round_out, seed, true, false, true)) return e;
   if (int e = jp_color_run(c, color_out)) return e;
   *num_rounds = T;
   *num_colors = c.h_state->K;
@@ -372,7 +372,7 @@ int pgc_color_jp_adg_m(const pgc_graph* g, uint64_t seed, int32_t* round_out, in
   const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
   c.round_key = round_out;
   c.seed = seed;
-  if (int e = jp_order_run(c, round_out, seed, true)) return e;
+  if (int e = jp_order_run(c, round_out, seed, true, false, true)) return e;
   if (int e = jp_color_run(c, color_out)) return e;
   *num_rounds = T;
   *num_colors = c.h_state->K;
@@ -397,7 +397,7 @@ int pgc_color_jp_adg_o(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, i
   const unsigned long long cross = c.h_state->cross, preds = c.h_state->pred_arcs;
   int32_t* key1 = c.U[0];  // ADG's lists are free after the last round
   if (int e = adg_o_keys(c, round_out, key1)) return e;
-  if (int e = jp_order_run(c, key1, 0, false, true)) return e;
+  if (int e = jp_order_run(c, key1, 0, false, true, true)) return e;
   if (c.h_state->err == 6)
     return fail(PGC_EINVAL, "ADG-O: sum over rounds of (max residual degree + 1) exceeds INT32_MAX");
   c.round_key = round_out;  // the bulk's watch heuristic (never a result)
@@ -423,7 +423,7 @@ int pgc_jp_baseline(const pgc_graph* g, int kind, uint64_t seed, int32_t* color_
   c.round_key = nullptr;  // U0 is reused by the bulk split: the bulk watches by hash alone
   c.seed = seed;
   if (int e = jp_setup_run(c, key, seed, color_out)) return e;
-  if (int e = jp_order_run(c, key, seed, false)) return e;
+  if (int e = jp_order_run(c, key, seed, false, false, true)) return e;
   if (int e = jp_color_run(c, color_out)) return e;
   *num_colors = c.h_state->K;
   call_end(c, 0, c.h_state->K, 0, 0, c.h_state->pred_arcs, c.core_n);

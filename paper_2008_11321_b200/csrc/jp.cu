@@ -299,12 +299,16 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 see
                           const State* st, const int32_t* __restrict__ hist1,
                           const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
                           const int32_t* __restrict__ bstart, const int32_t* __restrict__ npred,
-                          int32_t* __restrict__ ord) {
+                          int32_t* __restrict__ ord, int part) {
   const int rmax = st->rmax;
+  const int ktop = st->ord_ktop;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     if (!in_order(npred, v)) continue;  // isolated: not in the order
-    const int b = bucket_of((int)v, round[v], seed, rmax, hist1, base1);
+    const int r = round[v];
+    // part 0: the top keys only, 1: the rest, -1: all
+    if (part >= 0 && ((rmax - r <= ktop) != (part == 0))) continue;
+    const int b = bucket_of((int)v, r, seed, rmax, hist1, base1);
     ord[bstart[b] + atomicSub(&bcnt[b], 1) - 1] = (int)v;
   }
 }
@@ -330,12 +334,14 @@ __device__ __forceinline__ int4 work_rec(int v, const int32_t* __restrict__ npre
 __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstart,
                               int32_t* __restrict__ ord, const int32_t* __restrict__ npred,
                               const int64_t* __restrict__ off, int4* __restrict__ rec,
-                              Key2 seed) {
+                              Key2 seed, int part) {
   const int lane = lane_id();
-  const int nb = st->nbuckets;
+  // part 0: buckets [0, ord_btop), 1: [ord_btop, nb), -1: all
+  const int nb = part == 0 ? st->ord_btop : st->nbuckets;
+  const int bfirst = part == 1 ? st->ord_btop : 0;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nthreads = gridDim.x * blockDim.x;
-  for (int b0 = tid - lane; b0 < nb; b0 += nthreads) {
+  for (int b0 = bfirst + tid - lane; b0 < nb; b0 += nthreads) {
     const int b = b0 + lane;
     int s0 = 0, s = 0;
     if (b < nb) {
@@ -419,7 +425,48 @@ __global__ void k_order_setup(State* st, int rmax_host, int use_host) {
   st->n_order = 0;
 }
 
-int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known, bool idkey) {
+// Split point of a deferred order: the smallest key index ktop whose keys
+// 0..ktop (the top rounds) hold >= target ordered vertices (every key if
+// none), and the first bucket past them.  One block, chunked scan of hist1.
+__global__ void __launch_bounds__(1024) k_order_top(State* st, const int32_t* __restrict__ hist1,
+                                                   const int32_t* __restrict__ base1, int L,
+                                                   int target) {
+  __shared__ int s_w[32];
+  __shared__ int s_k;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_k = L - 1;
+  long long run = 0;
+  for (int k0 = 0; k0 < L; k0 += blockDim.x) {
+    const int k = k0 + threadIdx.x;
+    const int x = k < L ? hist1[k] : 0;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    int wex = 0, tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < warp) wex += s_w[w];
+      tot += s_w[w];
+    }
+    if (k < L && run + wex + incl >= target && run + wex + incl - x < target) s_k = k;
+    __syncthreads();
+    run += tot;
+    if (run >= target) break;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int k = s_k;
+    st->ord_ktop = k;
+    st->ord_btop = k + 1 < L ? base1[k + 1] : st->nbuckets;
+  }
+}
+
+int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known, bool idkey,
+                 bool defer) {
   int idshift = 0;
   if (idkey) {
     int bits = 1;
@@ -460,12 +507,36 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
   if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
                       &c.state->sorted))
     return e;
+  // deferred: the top rounds now (the core's prefix), the rest beside the core
+  defer = defer && c.tune.jp_split_overlap && c.tune.core_max > 0;
+  const int part = defer ? 0 : -1;
+  if (defer)
+    PGC_LAUNCH(c, kGOrder, "k_order_top",
+               k_order_top<<<1, 1024, 0, c.st>>>(c.state, c.hist1, c.base1, L, c.tune.core_max));
   PGC_LAUNCH(c, kGOrder, "k_scatter",
              k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
-                                            c.bstart, c.npred, c.U[1]));
+                                            c.bstart, c.npred, c.U[1], part));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
              k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.U[1], c.npred, c.off, c.rec,
-                                                seed));
+                                                seed, part));
+  c.ord_pending = defer;
+  c.ord_round = round;
+  c.ord_seed = seed_;
+  c.ord_idshift = idshift;
+  return 0;
+}
+
+// The bottom part of a deferred order (on c.st, which may be a side stream).
+static int jp_order_bottom(Ctx& c) {
+  const Key2 seed{c.ord_seed, c.ord_idshift};
+  const int G = c.nsm * 8;
+  PGC_LAUNCH(c, kGOrder, "k_scatter",
+             k_scatter<<<G, 256, 0, c.st>>>(c.n, c.ord_round, seed, c.state, c.hist1, c.base1,
+                                            c.bcnt, c.bstart, c.npred, c.U[1], 1));
+  PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
+             k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.U[1], c.npred, c.off, c.rec,
+                                                seed, 1));
+  c.ord_pending = false;
   return 0;
 }
 
@@ -1563,6 +1634,9 @@ int jp_color_run(Ctx& c, int32_t* color) {
     int4* hrec = c.rec + c.n;
     int4* lrec = hrec + c.lay.rec_heavy_cap;
     auto split = [&]() -> int {
+      if (c.ord_pending)  // the rest of the priority order first (same stream)
+        if (int e = jp_order_bottom(c)) return e;
+      if (nbulk <= 0) return 0;
       const int G = c.nsm * 8;
       // flags: heavy -> U0, light -> U1; prefix counts: heavy -> Rl, light -> D
       // (ADG's lists and degrees, and the core's pos[], are dead by now)
@@ -1625,8 +1699,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
       PGC_CUDA(cudaEventRecord(ev[1], side));
       PGC_CUDA(cudaStreamWaitEvent(c.st, ev[1], 0));
     } else {
-      if (nbulk > 0)
-        if (int e = split()) return e;
+      if (int e = split()) return e;
       if (C > 0)
         if (int e = core()) return e;
     }

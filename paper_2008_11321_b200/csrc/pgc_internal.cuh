@@ -43,6 +43,8 @@ struct State {
   int nbuckets;                // buckets in use
   int sorted;                  // total placed by the scan (== n_order)
   int n_order;                 // vertices in the priority order: all but the isolated ones
+  int ord_ktop;                // split order: keys 0..ord_ktop (the top rounds) placed first
+  int ord_btop;                // ... their buckets are 0..ord_btop-1
   int pad1;
   // JP
   int core_n;                  // |core| = length of the priority prefix colored by k_jp_core
@@ -130,6 +132,11 @@ struct Ctx {
   uint64_t seed = 0;                   // JP tie-break seed
   int core_ctas = 0;                   // cluster size used by the last k_jp_core (0 = none)
   int core_n = 0;                      // core vertices colored by k_jp_core (0 = none)
+  // split order (jp_order_run with defer): the bottom part still to place
+  bool ord_pending = false;
+  const int32_t* ord_round = nullptr;
+  uint64_t ord_seed = 0;
+  int ord_idshift = 0;
   State* h_state;  // pinned host mirror
   cudaEvent_t col_ready = nullptr;  // host entry point: col[] still in flight until this event
   unsigned long long* trace_grab = nullptr;  // pgc_debug_set_trace (diagnostics)
@@ -153,7 +160,10 @@ int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color);
 int adg_o_keys(Ctx& c, const int32_t* round, int32_t* key1);
 int baseline_key_run(Ctx& c, int kind, int32_t* key);
 int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, long long* passes);
-int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known, bool idkey = false);
+// defer: place only the top rounds' records (enough for the JP core's prefix)
+// and leave the rest to jp_color_run, which places them beside the core kernel
+int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known, bool idkey = false,
+                 bool defer = false);
 int jp_color_run(Ctx& c, int32_t* color);
 int check_graph_run(Ctx& c, int64_t* bad_vertex);
 
