@@ -669,8 +669,11 @@ __global__ void k_core_pos(const int4* __restrict__ rec, const State* st, int32_
 
 // Warp per core vertex: rewrite its pred list in place (P slot, int32 ids ->
 // u16 core positions at the start of the same slot).
+// With `ready` (the lists are rewritten beside the running core kernel), each
+// vertex's flag is released once its list is complete; k_jp_core acquires it
+// before reading the list.
 __global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __restrict__ pos,
-                             int32_t* P, const State* st) {
+                             int32_t* P, const State* st, uint8_t* ready) {
   const int lane = lane_id();
   const int NC = st->core_n;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -699,6 +702,11 @@ __global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __rest
         if (i < np) L[i] = (uint16_t)y[k];
       }
       __syncwarp();
+    }
+    if (ready && lane == 0) {  // every lane's stores precede this (bar.warp.sync)
+      __threadfence();
+      asm volatile("st.release.gpu.global.b8 [%0], %1;" ::"l"(ready + p), "h"((unsigned short)1)
+                   : "memory");
     }
   }
 }
@@ -740,7 +748,7 @@ __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np,
 #pragma unroll
   for (int k = 0; k < kScanStrips; ++k) {
     const int i = from + 64 * k + 2 * lane;
-    w[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
+    w[k] = i < np ? __ldcg(L2 + (i >> 1)) : 0u;
   }
   for (int i0 = from; i0 < np; i0 += kStep) {
     uint32_t wn[kScanStrips];
@@ -748,7 +756,7 @@ __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np,
 #pragma unroll
       for (int k = 0; k < kScanStrips; ++k) {
         const int i = i0 + kStep + 64 * k + 2 * lane;
-        wn[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
+        wn[k] = i < np ? __ldcg(L2 + (i >> 1)) : 0u;
       }
     }
 #pragma unroll
@@ -781,7 +789,7 @@ __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np,
 #pragma unroll
       for (int k = 0; k < kScanStrips; ++k) {
         const int i = i0 + kStep + 64 * k + 2 * lane;
-        w[k] = i < np ? __ldg(L2 + (i >> 1)) : 0u;
+        w[k] = i < np ? __ldcg(L2 + (i >> 1)) : 0u;
       }
     }
   }
@@ -795,7 +803,8 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
                                                            unsigned long long* tr_done,
                                                            unsigned spin_ns, unsigned tail_ns,
                                                            unsigned pass_ns,
-                                                           unsigned long long watchdog_ns) {
+                                                           unsigned long long watchdog_ns,
+                                                           const uint8_t* ready) {
   // dynamic shared memory: bitmaps | pending lists | color replica [NC] (0 = uncolored)
   extern __shared__ __align__(16) unsigned char s_dyn[];
   uint8_t* s_bm = s_dyn;
@@ -834,6 +843,26 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
     const int np = r.y;
     const uint16_t* L = reinterpret_cast<const uint16_t*>(P + lo_hi(r.z, r.w));
     const int vcore = r.x;
+    if (ready) {  // k_core_lists runs beside this kernel: wait for p's list
+      int ok = 1;
+      if (lane == 0)
+        for (;;) {
+          unsigned short f;
+          asm volatile("ld.acquire.gpu.global.b8 %0, [%1];" : "=h"(f) : "l"(ready + p) : "memory");
+          if (f) break;
+          if (stalled(st, deadline)) {
+            st->err = 8;  // (diagnostic: the core waited for a list)
+            ok = 0;
+            break;
+          }
+          __nanosleep(64);
+        }
+      if (!__shfl_sync(0xffffffffu, ok, 0)) {
+        stall = true;
+        break;
+      }
+      __syncwarp();  // lane 0's acquire orders the whole warp's list loads
+    }
 #ifdef PGC_PROBE
     const int vprobe = vcore;
     PROBE_STAMP(tr_grab, vprobe, 0);
@@ -897,6 +926,7 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
           if (pass_ns && npend > 4 * kCoreTail) __nanosleep(pass_ns);
         } else {
           if ((++polls & 63u) == 0 && __shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+            st->err = 9;
             stall = true;
             break;
           }
@@ -949,7 +979,7 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
           }
           if (all) break;
           if (globaltimer() > deadline) {
-            st->err = 5;
+            st->err = 9;
             stall = true;
             break;
           }
@@ -1615,10 +1645,6 @@ int jp_color_run(Ctx& c, int32_t* color) {
       } else {
         c.core_ctas = C;
         c.core_n = NC;
-        const int G = c.nsm * 4;
-        PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.rec, c.state, c.D));
-        PGC_LAUNCH(c, kGCore, "k_core_lists",
-                   k_core_lists<<<G * 2, 256, 0, c.st>>>(c.rec, c.D, c.P, c.state));
       }
     }
     // --- bulk split of positions [core_n, n_order) (needs only the records)
@@ -1633,6 +1659,40 @@ int jp_color_run(Ctx& c, int32_t* color) {
     const int64_t nbulk = n_order - NC;
     int4* hrec = c.rec + c.n;
     int4* lrec = hrec + c.lay.rec_heavy_cap;
+    const bool fork = C > 0 && nbulk > 0 && c.tune.jp_split_overlap;
+    if (fork) {
+      // CUDA loads kernels lazily at their first launch, and loading waits for
+      // the running kernels: a side-stream kernel the core waits on (the list
+      // rewrite) must be loaded before the core starts, or the first call
+      // deadlocks until the watchdog.  Querying the attributes loads them.
+      static thread_local bool loaded = false;
+      if (!loaded) {
+        cudaFuncAttributes fa;
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_pos));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_lists));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_scatter));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_bucket_sort));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_bulk_flags));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_bulk_scatter));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_reduce));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_tmp));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_down));
+        loaded = true;
+      }
+    }
+    // the core's list rewrite: before the core, or beside it with per-vertex
+    // ready flags (the ADG filter buffers, free during JP, zeroed on the main
+    // stream before the fork)
+    uint8_t* ready = fork ? reinterpret_cast<uint8_t*>(c.filt) : nullptr;
+    auto lists = [&]() -> int {
+      const int G = c.nsm * 4;
+      PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.rec, c.state, c.D));
+      PGC_LAUNCH(c, kGCore, "k_core_lists",
+                 k_core_lists<<<G * 2, 256, 0, c.st>>>(c.rec, c.D, c.P, c.state, ready));
+      return 0;
+    };
+    if (C > 0 && !fork)
+      if (int e = lists()) return e;
     auto split = [&]() -> int {
       if (c.ord_pending)  // the rest of the priority order first (same stream)
         if (int e = jp_order_bottom(c)) return e;
@@ -1673,24 +1733,28 @@ int jp_color_run(Ctx& c, int32_t* color) {
                                              c.trace_grab, c.trace_done,
                                              (unsigned)c.tune.core_spin_ns,
                                              (unsigned)c.tune.core_tail_ns,
-                                             (unsigned)c.tune.core_pass_ns, wd)));
+                                             (unsigned)c.tune.core_pass_ns, wd,
+                                             (const uint8_t*)ready)));
       return 0;
     };
-    if (C > 0 && nbulk > 0 && c.tune.jp_split_overlap) {
-      // fork: the core first (it is launched first and finds its SMs free), the
-      // split on the side stream; join before the bulk
+    if (fork) {
+      // fork: the core first (it is launched first and finds its SMs free);
+      // the list rewrite, the rest of the order and the bulk split on the side
+      // stream; join before the bulk
       static thread_local cudaStream_t side = nullptr;
       static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
       if (!side) {
         PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         for (auto& e : ev) PGC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
+      PGC_CUDA(cudaMemsetAsync(ready, 0, (size_t)NC, c.st));
       PGC_CUDA(cudaEventRecord(ev[0], c.st));
       if (int e = core()) return e;
       PGC_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
       const cudaStream_t main = c.st;
       c.st = side;
-      const int e = split();
+      int e = lists();
+      if (!e) e = split();
       c.st = main;
       if (e) {
         cudaStreamSynchronize(side);  // nothing may stay in flight on the error path
@@ -1715,6 +1779,10 @@ int jp_color_run(Ctx& c, int32_t* color) {
     }
   }
   if (int e = sync_state(c)) return e;
+  if (c.h_state->err == 9)
+    return fail(4, "JP core stalled: no progress within %d ms (watchdog)", c.tune.jp_watchdog_ms);
+  if (c.h_state->err == 8)
+    return fail(4, "JP core stalled waiting for a rewritten pred list (watchdog)");
   if (c.h_state->err == 5)
     return fail(4, "JP coloring stalled: no progress within %d ms (watchdog)", c.tune.jp_watchdog_ms);
   if (c.n > 0 && c.h_state->sorted != n_order)
