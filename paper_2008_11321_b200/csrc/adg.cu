@@ -97,7 +97,7 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
   const long long dmax = s_dmax;
   const unsigned long long mkey = st->msel_key;  // ADG-M: the ceil(|U|/2)-th smallest key
   unsigned long long my_sumD = 0;
-  unsigned long long my_nR = 0;
+  unsigned long long my_nR = 0, my_nOrd = 0;
   // kSelItems vertices per thread per step (coalesced: item j of thread t is
   // base + j * blockDim + t); the three output lists (edge chunks, light
   // records, U_{l+1}) are compacted with ONE block scan of packed counts and
@@ -147,6 +147,7 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
       }
       packed += (unsigned long long)nch[j] + ((unsigned long long)light[j] << 32) +
                 ((unsigned long long)(valid[j] && !sel[j]) << 48);
+      my_nOrd += (!pull && (light[j] || nch[j] > 0)) ? 1 : 0;  // removed, not isolated
     }
     // block exclusive scan of the packed counts
     const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -197,6 +198,8 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
   if (threadIdx.x == 0 && t) atomicAdd(&st->sumDR, t);
   t = block_sum(my_nR, s_red);
   if (threadIdx.x == 0 && t) atomicAdd(&st->nR, (int)t);
+  t = block_sum(my_nOrd, s_red);
+  if (threadIdx.x == 0 && t) atomicAdd(&st->nOrdR, (int)t);
 }
 
 // Arc classifier.  MODE 0: ADG only; 1: ADG with fused JP Part 1; 2: JP Part 1
@@ -778,7 +781,10 @@ __global__ void k_msel_reset(State* st) {
 
 // a2/a5: carry the cached degree sum and |U| to the next round (Q5 reading of
 // PAPER.md:2359-2361), record statistics, detect termination.
-__global__ void k_adg_finalize(int l, State* st, long long* per_round) {
+// ord_cnt[l-1] = the non-isolated vertices of R_l (capacity cap): the
+// priority order's round histogram, so the order needs no counting pass
+__global__ void k_adg_finalize(int l, State* st, long long* per_round, int32_t* ord_cnt,
+                               int64_t cap) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (st->done) return;
   const int nR = st->nR;
@@ -794,6 +800,8 @@ __global__ void k_adg_finalize(int l, State* st, long long* per_round) {
   }
   st->sum_active += st->nU;
   st->cross += st->cut;
+  if (l - 1 < cap) ord_cnt[l - 1] = st->nOrdR;
+  st->nOrdR = 0;
   const long long nU1 = st->nU - nR;
   if (st->nUnext != nU1) st->err = 2;
   st->S = st->S - st->sumDR - st->cut;
@@ -951,7 +959,8 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
         if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs, atom}, Uin)) return e;
       }
       PGC_LAUNCH(c, kGAdgOther, "k_adg_finalize",
-                 k_adg_finalize<<<1, 32, 0, c.st>>>(l, c.state, c.per_round));
+                 k_adg_finalize<<<1, 32, 0, c.st>>>(l, c.state, c.per_round,
+                                                    c.hist1 + c.lay.range_cap, c.lay.range_cap));
     }
     if (int e = sync_state(c)) return e;
     if (c.h_state->err) return fail(4, "ADG internal invariant failed (code %d)", c.h_state->err);

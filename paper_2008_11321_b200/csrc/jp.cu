@@ -238,6 +238,27 @@ __global__ void k_hist1(int64_t n, const int32_t* __restrict__ round,
   if (threadIdx.x == 0 && s_cnt) atomicAdd(&st->n_order, s_cnt);
 }
 
+// hist1[k] = cnt[T-1-k] (key k = rmax - round = T - round), n_order = sum:
+// the ADG selection counted every round's ordered (non-isolated) vertices.
+__global__ void __launch_bounds__(1024) k_hist1_rounds(int T, const int32_t* __restrict__ cnt,
+                                                       int32_t* __restrict__ hist1, State* st) {
+  __shared__ int s_w[32];
+  int sum = 0;
+  for (int k = threadIdx.x; k < T; k += blockDim.x) {
+    const int x = cnt[T - 1 - k];
+    hist1[k] = x;
+    sum += x;
+  }
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  if (lane_id() == 0) s_w[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+    st->n_order = t;
+  }
+}
+
 __global__ void k_bucket_sizes(int L, const int32_t* __restrict__ hist1, int32_t* __restrict__ bsz) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
     bsz[i] = bucket_count_for(hist1[i]);
@@ -274,8 +295,10 @@ constexpr int kOrdItems = PGC_ORD_ITEMS;
 __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, Key2 seed,
                         const int32_t* __restrict__ npred,
                         const State* st, const int32_t* __restrict__ hist1,
-                        const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt) {
+                        const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
+                        int part) {
   const int rmax = st->rmax;
+  const int ktop = st->ord_ktop;
   // kOrdItems vertices per thread per step, all loads before any use
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += stride * kOrdItems) {
@@ -288,7 +311,9 @@ __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, Key2 seed,
     }
 #pragma unroll
     for (int j = 0; j < kOrdItems; ++j)
-      if (np[j] >= 0) atomicAdd(&bcnt[bucket_of((int)(v0 + j * stride), r[j], seed, rmax, hist1, base1)], 1);
+      // part 0: the top keys only, 1: the rest, -1: all
+      if (np[j] >= 0 && (part < 0 || ((rmax - r[j] <= ktop) == (part == 0))))
+        atomicAdd(&bcnt[bucket_of((int)(v0 + j * stride), r[j], seed, rmax, hist1, base1)], 1);
   }
 }
 
@@ -302,6 +327,9 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 see
                           int32_t* __restrict__ ord, int part) {
   const int rmax = st->rmax;
   const int ktop = st->ord_ktop;
+  // the bottom part's buckets were counted and scanned on their own: its
+  // positions start after the top part's
+  const int base = part == 1 ? st->ord_ptop : 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     if (!in_order(npred, v)) continue;  // isolated: not in the order
@@ -309,7 +337,7 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 see
     // part 0: the top keys only, 1: the rest, -1: all
     if (part >= 0 && ((rmax - r <= ktop) != (part == 0))) continue;
     const int b = bucket_of((int)v, r, seed, rmax, hist1, base1);
-    ord[bstart[b] + atomicSub(&bcnt[b], 1) - 1] = (int)v;
+    ord[base + bstart[b] + atomicSub(&bcnt[b], 1) - 1] = (int)v;
   }
 }
 
@@ -339,6 +367,7 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
   // part 0: buckets [0, ord_btop), 1: [ord_btop, nb), -1: all
   const int nb = part == 0 ? st->ord_btop : st->nbuckets;
   const int bfirst = part == 1 ? st->ord_btop : 0;
+  const int base = part == 1 ? st->ord_ptop : 0;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nthreads = gridDim.x * blockDim.x;
   for (int b0 = bfirst + tid - lane; b0 < nb; b0 += nthreads) {
@@ -347,6 +376,7 @@ __global__ void k_bucket_sort(const State* st, const int32_t* __restrict__ bstar
     if (b < nb) {
       s0 = bstart[b];
       s = bstart[b + 1] - s0;
+      s0 += base;
     }
     if (s >= 1 && s <= kLaneSortMax) {
       int vv[kLaneSortMax];
@@ -422,6 +452,7 @@ __global__ void k_order_setup(State* st, int rmax_host, int use_host) {
   }
   st->nbuckets = 0;
   st->sorted = 0;
+  st->sorted_bot = 0;
   st->n_order = 0;
 }
 
@@ -433,8 +464,12 @@ __global__ void __launch_bounds__(1024) k_order_top(State* st, const int32_t* __
                                                    int target) {
   __shared__ int s_w[32];
   __shared__ int s_k;
+  __shared__ long long s_p;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_k = L - 1;
+  if (threadIdx.x == 0) {
+    s_k = L - 1;
+    s_p = -1;
+  }
   long long run = 0;
   for (int k0 = 0; k0 < L; k0 += blockDim.x) {
     const int k = k0 + threadIdx.x;
@@ -452,7 +487,10 @@ __global__ void __launch_bounds__(1024) k_order_top(State* st, const int32_t* __
       if (w < warp) wex += s_w[w];
       tot += s_w[w];
     }
-    if (k < L && run + wex + incl >= target && run + wex + incl - x < target) s_k = k;
+    if (k < L && run + wex + incl >= target && run + wex + incl - x < target) {
+      s_k = k;
+      s_p = run + wex + incl;
+    }
     __syncthreads();
     run += tot;
     if (run >= target) break;
@@ -462,6 +500,7 @@ __global__ void __launch_bounds__(1024) k_order_top(State* st, const int32_t* __
     const int k = s_k;
     st->ord_ktop = k;
     st->ord_btop = k + 1 < L ? base1[k + 1] : st->nbuckets;
+    st->ord_ptop = s_p >= 0 ? (int)s_p : st->n_order;
   }
 }
 
@@ -492,27 +531,34 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
   if (range < 1 || range > c.lay.range_cap)
     return fail(1, "round[] value range %lld exceeds n + 65536", (long long)range);
   const int L = (int)range;
-  PGC_LAUNCH(c, kGOrder, "k_zero_i32", k_zero_i32<<<G, 256, 0, c.st>>>(c.hist1, L));
-  const size_t shb = L <= 8192 ? (size_t)L * sizeof(int) : 0;
-  PGC_LAUNCH(c, kGOrder, "k_hist1",
-             k_hist1<<<G, 256, shb, c.st>>>(c.n, round, c.npred, c.state, L, c.hist1));
+  if (range_known && L <= c.lay.range_cap) {
+    // ADG rounds: the histogram was counted by the selection (k_adg_finalize)
+    PGC_LAUNCH(c, kGOrder, "k_hist1_rounds",
+               k_hist1_rounds<<<1, 1024, 0, c.st>>>(L, c.hist1 + c.lay.range_cap, c.hist1,
+                                                    c.state));
+  } else {
+    PGC_LAUNCH(c, kGOrder, "k_zero_i32", k_zero_i32<<<G, 256, 0, c.st>>>(c.hist1, L));
+    const size_t shb = L <= 8192 ? (size_t)L * sizeof(int) : 0;
+    PGC_LAUNCH(c, kGOrder, "k_hist1",
+               k_hist1<<<G, 256, shb, c.st>>>(c.n, round, c.npred, c.state, L, c.hist1));
+  }
   PGC_LAUNCH(c, kGOrder, "k_bucket_sizes",
              k_bucket_sizes<<<G, 256, 0, c.st>>>(L, c.hist1, c.base1));
   if (int e = scan_ex(c, c.base1, c.base1, nullptr, L, L, &c.state->nbuckets)) return e;
-  PGC_LAUNCH(c, kGOrder, "k_zero_i32_dev",
-             k_zero_i32_dev<<<G, 256, 0, c.st>>>(c.bcnt, &c.state->nbuckets, 1));
-  PGC_LAUNCH(c, kGOrder, "k_hist2",
-             k_hist2<<<G, 256, 0, c.st>>>(c.n, round, seed, c.npred, c.state, c.hist1, c.base1,
-                                          c.bcnt));
-  if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
-                      &c.state->sorted))
-    return e;
   // deferred: the top rounds now (the core's prefix), the rest beside the core
   defer = defer && c.tune.jp_split_overlap && c.tune.core_max > 0;
   const int part = defer ? 0 : -1;
   if (defer)
     PGC_LAUNCH(c, kGOrder, "k_order_top",
                k_order_top<<<1, 1024, 0, c.st>>>(c.state, c.hist1, c.base1, L, c.tune.core_max));
+  PGC_LAUNCH(c, kGOrder, "k_zero_i32_dev",
+             k_zero_i32_dev<<<G, 256, 0, c.st>>>(c.bcnt, &c.state->nbuckets, 1));
+  PGC_LAUNCH(c, kGOrder, "k_hist2",
+             k_hist2<<<G, 256, 0, c.st>>>(c.n, round, seed, c.npred, c.state, c.hist1, c.base1,
+                                          c.bcnt, part));
+  if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
+                      &c.state->sorted))
+    return e;
   PGC_LAUNCH(c, kGOrder, "k_scatter",
              k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
                                             c.bstart, c.npred, c.U[1], part));
@@ -520,6 +566,7 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
              k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.U[1], c.npred, c.off, c.rec,
                                                 seed, part));
   c.ord_pending = defer;
+  c.ord_deferred = defer;
   c.ord_round = round;
   c.ord_seed = seed_;
   c.ord_idshift = idshift;
@@ -530,6 +577,13 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
 static int jp_order_bottom(Ctx& c) {
   const Key2 seed{c.ord_seed, c.ord_idshift};
   const int G = c.nsm * 8;
+  // the top part's bucket counts are spent (0): count and scan the rest alone
+  PGC_LAUNCH(c, kGOrder, "k_hist2",
+             k_hist2<<<G, 256, 0, c.st>>>(c.n, c.ord_round, seed, c.npred, c.state, c.hist1,
+                                          c.base1, c.bcnt, 1));
+  if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
+                      &c.state->sorted_bot))
+    return e;
   PGC_LAUNCH(c, kGOrder, "k_scatter",
              k_scatter<<<G, 256, 0, c.st>>>(c.n, c.ord_round, seed, c.state, c.hist1, c.base1,
                                             c.bcnt, c.bstart, c.npred, c.U[1], 1));
@@ -614,44 +668,68 @@ __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ r
                                                       State* st,
                                                       int core_max, int min_avg,
                                                       long long arc_cap) {
+  // warp w scans the contiguous chunk [wb, we) of the prefix, lanes reading
+  // consecutive records, kCsU strips in flight: pass 1 sums the chunk, a
+  // block scan of the warp sums gives each chunk's base, pass 2 evaluates
+  // every prefix length
+  constexpr int kCsU = 8;
   __shared__ long long s_w[32];
   __shared__ unsigned long long s_best;
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int no = st->n_order;
   const int L = no < core_max ? no : core_max;
-  const int per = (L + blockDim.x - 1) / blockDim.x;
-  const int t0 = threadIdx.x * per;
+  const int cw = ((L + nw - 1) / nw + 31) & ~31;
+  const int wb = min(L, warp * cw), we = min(L, wb + cw);
   if (threadIdx.x == 0) s_best = 0;
   long long loc = 0;
-  for (int k = 0; k < per; ++k)
-    if (t0 + k < L) loc += rec[t0 + k].y;
-  long long incl = loc;
+  for (int j0 = wb; j0 < we; j0 += 32 * kCsU) {
+    int x[kCsU];
 #pragma unroll
-  for (int s = 1; s < 32; s <<= 1) {
-    long long y = __shfl_up_sync(0xffffffffu, incl, s);
-    if (lane >= s) incl += y;
+    for (int u = 0; u < kCsU; ++u) {
+      const int p = j0 + 32 * u + lane;
+      x[u] = p < we ? rec[p].y : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kCsU; ++u) loc += x[u];
   }
-  if (lane == 31) s_w[warp] = incl;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+  if (lane == 0) s_w[warp] = loc;
   __syncthreads();
   if (warp == 0) {
-    long long w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+    const long long w = lane < nw ? s_w[lane] : 0;
     long long wi = w;
 #pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-      long long y = __shfl_up_sync(0xffffffffu, wi, s);
-      if (lane >= s) wi += y;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
     }
-    s_w[lane] = wi - w;
+    if (lane < nw) s_w[lane] = wi - w;
   }
   __syncthreads();
-  long long run = s_w[warp] + incl - loc;
+  long long run = s_w[warp];  // sum over the positions before this chunk
   unsigned long long best = 0;
-  for (int k = 0; k < per; ++k) {
-    const int p = t0 + k;
-    if (p >= L) break;
-    run += rec[p].y;  // sum over the prefix of length p + 1
-    if (run >= (long long)min_avg * (p + 1) && run <= arc_cap)
-      best = ((unsigned long long)(p + 1) << 32) | (unsigned long long)run;
+  for (int j0 = wb; j0 < we; j0 += 32 * kCsU) {
+    int x[kCsU];
+#pragma unroll
+    for (int u = 0; u < kCsU; ++u) {
+      const int p = j0 + 32 * u + lane;
+      x[u] = p < we ? rec[p].y : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kCsU; ++u) {
+      long long incl = x[u];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int p = j0 + 32 * u + lane;
+      const long long pre = run + incl;  // sum over the prefix of length p + 1
+      if (p < we && pre >= (long long)min_avg * (p + 1) && pre <= arc_cap)
+        best = ((unsigned long long)(p + 1) << 32) | (unsigned long long)pre;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
   }
   atomicMax(&s_best, best);
   __syncthreads();
@@ -1670,6 +1748,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
         cudaFuncAttributes fa;
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_pos));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_lists));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_hist2));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scatter));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_bucket_sort));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_bulk_flags));
@@ -1785,9 +1864,10 @@ int jp_color_run(Ctx& c, int32_t* color) {
     return fail(4, "JP core stalled waiting for a rewritten pred list (watchdog)");
   if (c.h_state->err == 5)
     return fail(4, "JP coloring stalled: no progress within %d ms (watchdog)", c.tune.jp_watchdog_ms);
-  if (c.n > 0 && c.h_state->sorted != n_order)
-    return fail(4, "priority order placed %d of %lld vertices", c.h_state->sorted,
-                (long long)n_order);
+  const long long placed =
+      (long long)c.h_state->sorted + (c.ord_deferred ? c.h_state->sorted_bot : 0);
+  if (c.n > 0 && placed != n_order)
+    return fail(4, "priority order placed %lld of %lld vertices", placed, (long long)n_order);
   return 0;
 }
 

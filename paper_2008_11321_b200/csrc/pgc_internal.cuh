@@ -34,6 +34,8 @@ struct State {
   unsigned long long sumDR;    // sum of D over R_l
   unsigned long long cut;      // arcs from R_l into U_{l+1}
   int nR, nLight, nUnext, nChunks;
+  int nOrdR;                   // non-isolated vertices of R_l (the priority order's round histogram)
+  int pad2;
   // totals
   long long sum_active;        // sum_l |U_l|
   unsigned long long cross;    // X
@@ -45,7 +47,8 @@ struct State {
   int n_order;                 // vertices in the priority order: all but the isolated ones
   int ord_ktop;                // split order: keys 0..ord_ktop (the top rounds) placed first
   int ord_btop;                // ... their buckets are 0..ord_btop-1
-  int pad1;
+  int ord_ptop;                // ... and positions 0..ord_ptop-1
+  int sorted_bot;              // split order: placed by the bottom part
   // JP
   int core_n;                  // |core| = length of the priority prefix colored by k_jp_core
   int K;
@@ -134,6 +137,7 @@ struct Ctx {
   int core_n = 0;                      // core vertices colored by k_jp_core (0 = none)
   // split order (jp_order_run with defer): the bottom part still to place
   bool ord_pending = false;
+  bool ord_deferred = false;
   const int32_t* ord_round = nullptr;
   uint64_t ord_seed = 0;
   int ord_idshift = 0;
