@@ -745,47 +745,63 @@ __global__ void k_core_pos(const int4* __restrict__ rec, const State* st, int32_
     pos[rec[p].x] = p;
 }
 
-// Warp per core vertex: rewrite its pred list in place (P slot, int32 ids ->
-// u16 core positions at the start of the same slot).
-// With `ready` (the lists are rewritten beside the running core kernel), each
-// vertex's flag is released once its list is complete; k_jp_core acquires it
-// before reading the list.
+// One warp rewrites core vertex p's pred list in place (P slot, int32 ids ->
+// u16 core positions at the start of the same slot): kListStrips strips of 32
+// entries per step (loads, then gathers, in flight together); the u16 writes
+// of a step land on int32 entries the step (or an earlier one) has read.
+__device__ __forceinline__ void core_list_rewrite(const int4& r, const int32_t* __restrict__ pos,
+                                                  int32_t* P) {
+  const int lane = lane_id();
+  const int np = r.y;
+  const int64_t b = lo_hi(r.z, r.w);
+  uint16_t* L = reinterpret_cast<uint16_t*>(P + b);
+  constexpr int kListStrips = 8;
+  for (int i0 = 0; i0 < np; i0 += 32 * kListStrips) {
+    int x[kListStrips], y[kListStrips];
+#pragma unroll
+    for (int k = 0; k < kListStrips; ++k) {
+      const int i = i0 + 32 * k + lane;
+      x[k] = i < np ? __ldcg(P + b + i) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < kListStrips; ++k) y[k] = x[k] >= 0 ? pos[x[k]] : 0;
+    __syncwarp();  // every lane has read its int32 entries before any u16 lands
+#pragma unroll
+    for (int k = 0; k < kListStrips; ++k) {
+      const int i = i0 + 32 * k + lane;
+      if (i < np) L[i] = (uint16_t)y[k];
+    }
+    __syncwarp();
+  }
+}
+
+// Per-vertex list states while the rewrite runs beside the core kernel:
+// 0 = untouched, 1 = claimed (being rewritten), 2 = done.  Whoever claims a
+// list (atomicCAS 0 -> 1) rewrites it and releases 2; the core claims the
+// lists k_core_lists has not reached when it has waited too long -- so the
+// core also finishes when the two kernels do not run concurrently (a
+// profiler, CUDA_LAUNCH_BLOCKING).
+constexpr int kListTodo = 0, kListBusy = 1, kListDone = 2;
+__device__ __forceinline__ void list_release(int32_t* ready, int p) {
+  // every lane's stores precede this (bar.warp.sync in core_list_rewrite)
+  __threadfence();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + p), "r"(kListDone) : "memory");
+}
+
+// Warp per core vertex; with `ready`, each list is claimed first (see above).
 __global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __restrict__ pos,
-                             int32_t* P, const State* st, uint8_t* ready) {
+                             int32_t* P, const State* st, int32_t* ready) {
   const int lane = lane_id();
   const int NC = st->core_n;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < NC; p += nw) {
-    const int4 r = rec[p];
-    const int np = r.y;
-    const int64_t b = lo_hi(r.z, r.w);
-    uint16_t* L = reinterpret_cast<uint16_t*>(P + b);
-    // kListStrips strips of 32 entries per step: loads, then gathers, in flight
-    // together; the u16 writes of a step land on int32 entries the step (or an
-    // earlier one) has already read
-    constexpr int kListStrips = 8;
-    for (int i0 = 0; i0 < np; i0 += 32 * kListStrips) {
-      int x[kListStrips], y[kListStrips];
-#pragma unroll
-      for (int k = 0; k < kListStrips; ++k) {
-        const int i = i0 + 32 * k + lane;
-        x[k] = i < np ? P[b + i] : -1;
-      }
-#pragma unroll
-      for (int k = 0; k < kListStrips; ++k) y[k] = x[k] >= 0 ? pos[x[k]] : 0;
-      __syncwarp();  // every lane has read its int32 entries before any u16 lands
-#pragma unroll
-      for (int k = 0; k < kListStrips; ++k) {
-        const int i = i0 + 32 * k + lane;
-        if (i < np) L[i] = (uint16_t)y[k];
-      }
-      __syncwarp();
+    if (ready) {
+      int claimed = 0;
+      if (lane == 0) claimed = atomicCAS(ready + p, kListTodo, kListBusy) == kListTodo;
+      if (!__shfl_sync(0xffffffffu, claimed, 0)) continue;  // the core took it
     }
-    if (ready && lane == 0) {  // every lane's stores precede this (bar.warp.sync)
-      __threadfence();
-      asm volatile("st.release.gpu.global.b8 [%0], %1;" ::"l"(ready + p), "h"((unsigned short)1)
-                   : "memory");
-    }
+    core_list_rewrite(rec[p], pos, P);
+    if (ready && lane == 0) list_release(ready, p);
   }
 }
 
@@ -875,20 +891,22 @@ __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np,
 }
 
 __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restrict__ rec,
-                                                           const int32_t* __restrict__ P,
+                                                           int32_t* P,  // pred lists (u16 core positions; rewritten here if claimed)
                                                            int32_t* color, State* st,
                                                            unsigned long long* tr_grab,
                                                            unsigned long long* tr_done,
                                                            unsigned spin_ns, unsigned tail_ns,
                                                            unsigned pass_ns,
                                                            unsigned long long watchdog_ns,
-                                                           const uint8_t* ready) {
+                                                           int32_t* ready,
+                                                           const int32_t* __restrict__ pos) {
   // dynamic shared memory: bitmaps | pending lists | color replica [NC] (0 = uncolored)
   extern __shared__ __align__(16) unsigned char s_dyn[];
   uint8_t* s_bm = s_dyn;
   uint16_t* s_pend = reinterpret_cast<uint16_t*>(s_dyn + kCoreFixedSmem - kCoreWarps * kCorePend * 2);
   uint16_t* s_cc = reinterpret_cast<uint16_t*>(s_dyn + kCoreFixedSmem);
   __shared__ int s_ticket;
+  __shared__ int s_selfserve;  // a list wait timed out: claim lists without waiting
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
@@ -896,7 +914,10 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   for (int i = threadIdx.x; i < NC; i += blockDim.x) s_cc[i] = 0;
-  if (threadIdx.x == 0) s_ticket = 0;
+  if (threadIdx.x == 0) {
+    s_ticket = 0;
+    s_selfserve = 0;
+  }
   cl.sync();  // every replica is zeroed before any color is published
   // lane r < C publishes into CTA r's replica: its shared::cluster address
   uint32_t remote = 0;
@@ -921,25 +942,39 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
     const int np = r.y;
     const uint16_t* L = reinterpret_cast<const uint16_t*>(P + lo_hi(r.z, r.w));
     const int vcore = r.x;
-    if (ready) {  // k_core_lists runs beside this kernel: wait for p's list
-      int ok = 1;
-      if (lane == 0)
+    if (ready) {  // k_core_lists runs beside this kernel: p's list must be done
+      int act = 0;  // 0: done, 1: rewrite it here, 2: watchdog
+      if (lane == 0) {
+        const unsigned long long t_give = globaltimer() + 20000;  // 20 us
         for (;;) {
-          unsigned short f;
-          asm volatile("ld.acquire.gpu.global.b8 %0, [%1];" : "=h"(f) : "l"(ready + p) : "memory");
-          if (f) break;
+          int f;
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(ready + p) : "memory");
+          if (f == kListDone) break;
+          if (f == kListTodo && (*(volatile int*)&s_selfserve || globaltimer() > t_give)) {
+            if (atomicCAS(ready + p, kListTodo, kListBusy) == kListTodo) {
+              *(volatile int*)&s_selfserve = 1;
+              act = 1;
+              break;
+            }
+          }
           if (stalled(st, deadline)) {
             st->err = 8;  // (diagnostic: the core waited for a list)
-            ok = 0;
+            act = 2;
             break;
           }
           __nanosleep(64);
         }
-      if (!__shfl_sync(0xffffffffu, ok, 0)) {
+      }
+      act = __shfl_sync(0xffffffffu, act, 0);
+      if (act == 2) {
         stall = true;
         break;
       }
-      __syncwarp();  // lane 0's acquire orders the whole warp's list loads
+      if (act == 1) {
+        core_list_rewrite(r, pos, P);
+        if (lane == 0) list_release(ready, p);
+      }
+      __syncwarp();  // lane 0's acquire (or the warp's own rewrite) orders the list loads
     }
 #ifdef PGC_PROBE
     const int vprobe = vcore;
@@ -1762,12 +1797,16 @@ int jp_color_run(Ctx& c, int32_t* color) {
     // the core's list rewrite: before the core, or beside it with per-vertex
     // ready flags (the ADG filter buffers, free during JP, zeroed on the main
     // stream before the fork)
-    uint8_t* ready = fork ? reinterpret_cast<uint8_t*>(c.filt) : nullptr;
+    int32_t* ready = fork ? reinterpret_cast<int32_t*>(c.filt) : nullptr;
+    // pos[] before the fork (the core may rewrite lists itself), in the upper
+    // half of the round-histogram space: the bulk split reuses D beside the core
+    int32_t* pos = c.hist1 + c.lay.range_cap;
+    if (C > 0)
+      PGC_LAUNCH(c, kGCore, "k_core_pos",
+                 k_core_pos<<<c.nsm * 4, 256, 0, c.st>>>(c.rec, c.state, pos));
     auto lists = [&]() -> int {
-      const int G = c.nsm * 4;
-      PGC_LAUNCH(c, kGCore, "k_core_pos", k_core_pos<<<G, 256, 0, c.st>>>(c.rec, c.state, c.D));
       PGC_LAUNCH(c, kGCore, "k_core_lists",
-                 k_core_lists<<<G * 2, 256, 0, c.st>>>(c.rec, c.D, c.P, c.state, ready));
+                 k_core_lists<<<c.nsm * 8, 256, 0, c.st>>>(c.rec, pos, c.P, c.state, ready));
       return 0;
     };
     if (C > 0 && !fork)
@@ -1807,13 +1846,13 @@ int jp_color_run(Ctx& c, int32_t* color) {
       cfg.numAttrs = 1;
       const unsigned long long wd = (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull;
       PGC_LAUNCH(c, kGCore, "k_jp_core",
-                 PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int4*)c.rec,
-                                             (const int32_t*)c.P, color, c.state,
+                 PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int4*)c.rec, c.P, color,
+                                             c.state,
                                              c.trace_grab, c.trace_done,
                                              (unsigned)c.tune.core_spin_ns,
                                              (unsigned)c.tune.core_tail_ns,
-                                             (unsigned)c.tune.core_pass_ns, wd,
-                                             (const uint8_t*)ready)));
+                                             (unsigned)c.tune.core_pass_ns, wd, ready,
+                                             (const int32_t*)pos)));
       return 0;
     };
     if (fork) {
@@ -1826,7 +1865,8 @@ int jp_color_run(Ctx& c, int32_t* color) {
         PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         for (auto& e : ev) PGC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
-      PGC_CUDA(cudaMemsetAsync(ready, 0, (size_t)NC, c.st));
+      static_assert(65535 * 4 <= 2 * kFilterBytes, "list states fit the filter buffers");
+      PGC_CUDA(cudaMemsetAsync(ready, 0, 4 * (size_t)NC, c.st));
       PGC_CUDA(cudaEventRecord(ev[0], c.st));
       if (int e = core()) return e;
       PGC_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
