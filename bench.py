@@ -49,6 +49,10 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="skip e2e, cpu baseline (for ncu runs)")
+    ap.add_argument("--serial-schedule", action="store_true",
+                    help="one stream (tuning jp_split_overlap=0): for ncu launch lists, which "
+                         "serialise kernels anyway (the overlapped schedule would make the core "
+                         "rewrite its lists itself there)")
     ap.add_argument("--method", choices=["jp-adg", "jp-adg-m", "jp-adg-o", "jp-r", "jp-ff", "jp-lf",
                                          "jp-llf", "dec-adg-itr", "adg-push", "adg-pull"],
                     default="jp-adg",
@@ -280,6 +284,8 @@ def run_pgc(args):
         return pgc.color_jp_adg(off, col, num, den, args.seed, round_out=rnd, color_out=color)
 
     pgc.set_tuning("timing", 0)
+    if args.serial_schedule:
+        pgc.set_tuning("jp_split_overlap", 0)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

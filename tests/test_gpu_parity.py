@@ -129,7 +129,7 @@ def tuning():
     defaults = {"core_max": 65535, "core_min_avg": 32, "core_min_n": 256, "core_ctas": 0,
                 "core_arc_cap": 1 << 30, "core_arcs_per_cta": 2 << 20, "jp_heavy_warps": 4,
                 "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
-                "heavy_degree": 128, "rounds_per_sync": 8}
+                "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
 
@@ -203,9 +203,12 @@ def test_determinism_across_tuning(tuning):
     g = gg.rmat(14, 16, seed=2)
     pgc, off, col = dev(g)
     ref = None
-    for hd, rps, core, hw, sleep in ((128, 1, 0, 1, 0), (200, 3, 65535, 2, 64),
-                                     (1024, 8, 500, 4, 8192), (1 << 20, 8, 65535, 4, 2048),
-                                     (128, 2, 0, 3, 100000)):
+    for hd, rps, core, hw, sleep, ovl, atom in ((128, 1, 0, 1, 0, 1, 1), (200, 3, 65535, 2, 64, 0, 0),
+                                                (1024, 8, 500, 4, 8192, 1, 0),
+                                                (1 << 20, 8, 65535, 4, 2048, 1, 1),
+                                                (128, 2, 0, 3, 100000, 0, 1)):
+        tuning("jp_split_overlap", ovl)
+        tuning("update_atom", atom)
         tuning("heavy_degree", hd)
         tuning("rounds_per_sync", rps)
         tuning("core_max", core)
@@ -543,3 +546,29 @@ def test_more_than_255_rounds_every_entry_point():
         assert_parity(g, 1, den, 3)
         assert_parity_o(g, 1, den)
         assert_parity_dec(g, 1, den, 3)
+
+
+def test_serialised_kernels_do_not_deadlock():
+    """With every launch serialised (CUDA_LAUNCH_BLOCKING=1, as under a
+    profiler) the core kernel cannot wait for the list rewrite running beside
+    it: it must claim and rewrite the lists itself (claim protocol in jp.cu).
+    A fresh process also exercises the first-call path (kernels loaded before
+    the fork)."""
+    import subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, 'tests')\n"
+        "import numpy as np, torch\n"
+        "import graphgen as gg, oracle as O, paper_2008_11321_b200 as pgc\n"
+        "pgc.set_tuning('jp_watchdog_ms', 5000)\n"
+        "g = gg.rmat(15, 16, seed=6)\n"
+        "off = torch.from_numpy(g.off).cuda(); col = torch.from_numpy(g.col).cuda()\n"
+        "r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 5)\n"
+        "assert pgc.last_stats()['core_vertices'] > 0\n"
+        "r_or, _ = O.adg(g, 1, 10); c_or, K_or = O.jp(g, r_or, 5)\n"
+        "assert np.array_equal(r.cpu().numpy(), r_or) and np.array_equal(c.cpu().numpy(), c_or)\n"
+        "print('ok')\n")
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

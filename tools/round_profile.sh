@@ -9,7 +9,8 @@ mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 nvidia-smi > $OUT/smi.txt 2>&1
 python bench.py > $OUT/bench.log 2>&1; echo "bench rc=$?" > $OUT/status.txt
-CMD="python bench.py --quick --steps 1 --warmup 3"
+# ncu serialises kernels: profile the one-stream schedule (same kernels, see bench.py)
+CMD="python bench.py --quick --serial-schedule --steps 1 --warmup 3"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 echo "launches rc=$?" >> $OUT/status.txt
 # one step = the second call of launch_times.py (the first is a warm-up)
@@ -18,6 +19,6 @@ ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum 
 echo "traffic rc=$?" >> $OUT/status.txt
 ncu --set full --import-source on --clock-control none -k regex:k_update_light -s 8 -c 1 -o $OUT/upd_light_r1 python tools/launch_times.py > $OUT/f1.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_update_heavy -s 10 -c 1 -o $OUT/upd_heavy_r3 python tools/launch_times.py > $OUT/f2.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"k_jp_core|k_jp_bulk" -s 2 -c 2 -o $OUT/jp python tools/launch_times.py > $OUT/f3.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"k_jp_core|k_jp_bulk" -s 2 -c 2 -o $OUT/jp python tools/launch_times.py jp_split_overlap=0 > $OUT/f3.log 2>&1
 echo "full rc=$?" >> $OUT/status.txt
 cat $OUT/status.txt
