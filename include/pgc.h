@@ -257,7 +257,8 @@ const char* pgc_last_error(void);
  *   on a second stream while the core kernel, one cluster of <= 16 SMs, runs;
  *   default 1), "update_atom" 0/1 (ADG round 1 classifies each arc by the old
  *   value of ONE atomic decrement instead of a state gather plus a RED;
- *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns".
+ *   default 1), "fuse_init" 0/1 (ADG's first selection also initialises the
+ *   per-vertex state; default 1), "filter_ratio", "core_tail_ns", "core_pass_ns".
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

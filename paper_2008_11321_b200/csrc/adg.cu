@@ -72,6 +72,18 @@ __global__ void k_adg_init(int64_t n, int64_t nnz, const int64_t* __restrict__ o
   }
 }
 
+// The state part of k_adg_init alone: with the mean rule, round 1's
+// selection initialises the per-vertex arrays itself (first = 1).
+__global__ void k_adg_state_init(int64_t n, int64_t nnz, State* st) {
+  State s = {};
+  s.S = (unsigned long long)nnz;
+  s.nU = n;
+  s.done = (n == 0);
+  s.rmin = 1;
+  s.rmax = 0;
+  *st = s;
+}
+
 // a2+a3: threshold, select, compact.
 constexpr int kSelItems = 4;
 __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
@@ -80,7 +92,8 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
                              const int32_t* __restrict__ Uin, int32_t* __restrict__ Uout,
                              int4* __restrict__ lrec, int4* __restrict__ chunks,
                              int32_t* __restrict__ npred, State* st, int heavy_deg, int chunk,
-                             int64_t chunk_cap, int pull, int mark_removed) {
+                             int64_t chunk_cap, int pull, int mark_removed, int first,
+                             int32_t* __restrict__ color, uint32_t* __restrict__ filt) {
   __shared__ int sm[33];
   __shared__ long long s_dmax;
   __shared__ unsigned long long s_red[32];
@@ -95,7 +108,11 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
   }
   __syncthreads();
   const long long dmax = s_dmax;
-  const unsigned long long mkey = st->msel_key;  // ADG-M: the ceil(|U|/2)-th smallest key
+  const unsigned long long mkey = st->msel_key;
+  if (first && filt)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * kFilterWords;
+         i += gridDim.x * blockDim.x)
+      filt[i] = 0;  // ADG-M: the ceil(|U|/2)-th smallest key
   unsigned long long my_sumD = 0;
   unsigned long long my_nR = 0, my_nOrd = 0;
   // kSelItems vertices per thread per step (coalesced: item j of thread t is
@@ -114,8 +131,19 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
       valid[j] = i < count;
       v[j] = valid[j] ? (Uin ? Uin[i] : (int)i) : 0;
     }
+    long long o0[K] = {}, e0[K] = {};
+    if (first) {  // round 1 fused with init: D[v] = deg(v) from the offsets
 #pragma unroll
-    for (int j = 0; j < K; ++j) d[j] = valid[j] ? ld_i32_keep(D + v[j]) : 0;
+      for (int j = 0; j < K; ++j) {
+        o0[j] = valid[j] ? off[v[j]] : 0;
+        e0[j] = valid[j] ? off[v[j] + 1] : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) d[j] = (int)(e0[j] - o0[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < K; ++j) d[j] = valid[j] ? ld_i32_keep(D + v[j]) : 0;
+    }
     unsigned long long packed = 0;  // chunks | light << 32 | unext << 48
 #pragma unroll
     for (int j = 0; j < K; ++j) {
@@ -128,17 +156,27 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
       nch[j] = 0;
       o[j] = 0;
       deg[j] = 0;
-      if (sel[j]) {
+      if (first && valid[j]) {  // k_adg_init's per-vertex state (a1), then round 1's
+        st_i32_keep(D + v[j], sel[j] && mark_removed ? -1 : d[j]);
+        st_u8_keep(rs + v[j], sel[j] ? 1 : 0);
+        round[v[j]] = sel[j] ? l : 0;
+        if (color) {
+          color[v[j]] = d[j] == 0 ? 1 : 0;
+          npred[v[j]] = d[j] == 0 ? -1 : 0;
+        }
+      } else if (sel[j]) {
         round[v[j]] = l;
         st_u8_keep(rs + v[j], (l - 1) % 255 + 1);
         if (mark_removed) st_i32_keep(D + v[j], -1);  // round 1's atomic UPDATE (Arc::atom)
+      }
+      if (sel[j]) {
         my_sumD += (unsigned long long)d[j];
         my_nR += 1;
       }
       // UPDATE's work records: push scans R_l's arcs, pull the survivors' (U_{l+1})
       if (pull ? (valid[j] && !sel[j]) : sel[j]) {
-        o[j] = off[v[j]];
-        deg[j] = off[v[j] + 1] - o[j];
+        o[j] = first ? o0[j] : off[v[j]];
+        deg[j] = first ? e0[j] - o0[j] : off[v[j] + 1] - o[j];
         light[j] = deg[j] > 0 && deg[j] <= heavy_deg;  // isolated: settled by k_adg_init
         if (deg[j] > heavy_deg) {
           nch[j] = (int)((deg[j] + chunk - 1) / chunk);
@@ -900,10 +938,16 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
             int32_t* color_zero, int rule) {
   const int B = 256;
   const int G = grid_for(c, 8);
-  PGC_LAUNCH(c, kGAdgOther, "k_adg_init",
-             k_adg_init<<<G, B, 0, c.st>>>(c.n, c.nnz, c.off, c.D, c.rs, round, color_zero,
-                                           c.npred, c.tune.filter_ratio > 0 ? c.filt : nullptr,
-                                           c.state));
+  // mean rule: round 1's selection does init's per-vertex work (one pass less)
+  const bool fuse_init = rule == kRuleMean && c.tune.fuse_init;
+  if (fuse_init)
+    PGC_LAUNCH(c, kGAdgOther, "k_adg_state_init",
+               k_adg_state_init<<<1, 1, 0, c.st>>>(c.n, c.nnz, c.state));
+  else
+    PGC_LAUNCH(c, kGAdgOther, "k_adg_init",
+               k_adg_init<<<G, B, 0, c.st>>>(c.n, c.nnz, c.off, c.D, c.rs, round, color_zero,
+                                             c.npred, c.tune.filter_ratio > 0 ? c.filt : nullptr,
+                                             c.state));
   if (c.n == 0) return sync_state(c);
   int32_t* mhist = c.hist1;  // the order's histograms are free during ADG
   // ADG-M's radix schedule: (shift, bits) digits over the bits of (D << 32) | v
@@ -943,7 +987,9 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                  k_adg_select<<<G, B, 0, c.st>>>(l, rule, num, den, c.off, c.D, round, c.rs, Uin, Uout,
                                                  c.lrec, c.chunks, c.npred, c.state,
                                                  c.tune.heavy_degree, c.tune.chunk_arcs,
-                                                 c.lay.chunk_cap, mode == kAdgPull, atom));
+                                                 c.lay.chunk_cap, mode == kAdgPull, atom,
+                                                 fuse_init && l == 1, color_zero,
+                                                 c.tune.filter_ratio > 0 ? c.filt : nullptr));
       if (l == 1 && c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
       if (c.tune.filter_ratio > 0 && mode != kAdgPull)
         PGC_LAUNCH(c, kGUpdate, "k_filter_build",

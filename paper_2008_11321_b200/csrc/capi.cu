@@ -572,6 +572,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"itr_blocks_per_sm", 0, 64, nullptr, &g_tune.itr_blocks_per_sm},
       {"jp_split_overlap", 0, 1, nullptr, &g_tune.jp_split_overlap},
       {"update_atom", 0, 1, nullptr, &g_tune.update_atom},
+      {"fuse_init", 0, 1, nullptr, &g_tune.fuse_init},
       {"core_arc_cap", 0, 1ll << 40, &g_tune.core_arc_cap, nullptr},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };

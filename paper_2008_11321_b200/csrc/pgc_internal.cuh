@@ -92,6 +92,7 @@ struct Tuning {
   int core_pass_ns = 0;           // JP core: min sleep (ns) between passes of a warp far from its tail
   int itr_blocks_per_sm = 0;      // DEC-ADG-ITR: blocks per SM of the cooperative kernel (0 = occupancy)
   int jp_split_overlap = 1;       // JP: run the bulk split on a side stream beside the core kernel
+  int fuse_init = 1;              // ADG: round 1's selection also initialises D, rs, round, color
   int update_atom = 1;            // ADG round 1: one atomic per arc instead of gather + RED (Arc::atom)
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
