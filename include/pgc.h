@@ -258,7 +258,9 @@ const char* pgc_last_error(void);
  *   default 1), "update_atom" 0/1 (ADG round 1 classifies each arc by the old
  *   value of ONE atomic decrement instead of a state gather plus a RED;
  *   default 1), "fuse_init" 0/1 (ADG's first selection also initialises the
- *   per-vertex state; default 1), "filter_ratio", "core_tail_ns", "core_pass_ns".
+ *   per-vertex state; default 1), "top_list" 0/1 (JP-ADG: ADG keeps the top
+ *   rounds' vertex list so the split order's top part skips a pass over n;
+ *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns".
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

@@ -84,6 +84,21 @@ __global__ void k_adg_state_init(int64_t n, int64_t nnz, State* st) {
   *st = s;
 }
 
+// After round l's selection: in the round where |U| drops below target
+// (|U_l| >= target > |U_{l+1}|), keep a copy of U_l -- the smallest U holding
+// every vertex of the top rounds the JP core's prefix is drawn from (with the
+// mean rule U_l, l >= 2, holds no isolated vertex) -- so the priority order's
+// top part need not pass over all n vertices.  U_1 (every vertex) is not kept.
+__global__ void k_top_save(int l, const int32_t* __restrict__ Uin, State* st,
+                           int32_t* __restrict__ save, int target) {
+  if (st->done || l < 2) return;
+  const long long cnt = st->nU;
+  if (cnt < target || st->nUnext >= target) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->top_n = (int)cnt;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    save[i] = Uin[i];
+}
+
 // a2+a3: threshold, select, compact.
 constexpr int kSelItems = 4;
 __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
@@ -940,6 +955,10 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
   const int G = grid_for(c, 8);
   // mean rule: round 1's selection does init's per-vertex work (one pass less)
   const bool fuse_init = rule == kRuleMean && c.tune.fuse_init;
+  // JP-ADG: keep the top rounds' vertex list for the split priority order
+  const bool save_top = mode == kAdgFused && rule == kRuleMean && c.tune.jp_split_overlap &&
+                        c.tune.core_max > 0 && c.tune.top_list;
+  c.top_list = save_top;
   if (fuse_init)
     PGC_LAUNCH(c, kGAdgOther, "k_adg_state_init",
                k_adg_state_init<<<1, 1, 0, c.st>>>(c.n, c.nnz, c.state));
@@ -990,6 +1009,9 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                                  c.lay.chunk_cap, mode == kAdgPull, atom,
                                                  fuse_init && l == 1, color_zero,
                                                  c.tune.filter_ratio > 0 ? c.filt : nullptr));
+      if (save_top)
+        PGC_LAUNCH(c, kGAdgOther, "k_top_save",
+                   k_top_save<<<c.nsm * 4, 256, 0, c.st>>>(l, Uin, c.state, c.Rl, c.tune.core_max));
       if (l == 1 && c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
       if (c.tune.filter_ratio > 0 && mode != kAdgPull)
         PGC_LAUNCH(c, kGUpdate, "k_filter_build",

@@ -573,6 +573,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"jp_split_overlap", 0, 1, nullptr, &g_tune.jp_split_overlap},
       {"update_atom", 0, 1, nullptr, &g_tune.update_atom},
       {"fuse_init", 0, 1, nullptr, &g_tune.fuse_init},
+      {"top_list", 0, 1, nullptr, &g_tune.top_list},
       {"core_arc_cap", 0, 1ll << 40, &g_tune.core_arc_cap, nullptr},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };

@@ -296,24 +296,32 @@ __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, Key2 seed,
                         const int32_t* __restrict__ npred,
                         const State* st, const int32_t* __restrict__ hist1,
                         const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
-                        int part) {
+                        int part, const int32_t* __restrict__ list) {
   const int rmax = st->rmax;
   const int ktop = st->ord_ktop;
+  // `list` (part 0): a superset of the top rounds saved by ADG (k_top_save)
+  const bool use_list = list && st->top_n > 0;
+  const int64_t cnt = use_list ? st->top_n : n;
   // kOrdItems vertices per thread per step, all loads before any use
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < n; v0 += stride * kOrdItems) {
-    int np[kOrdItems], r[kOrdItems];
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < cnt; i0 += stride * kOrdItems) {
+    int vv[kOrdItems], np[kOrdItems], r[kOrdItems];
 #pragma unroll
     for (int j = 0; j < kOrdItems; ++j) {
-      const int64_t v = v0 + j * stride;
-      np[j] = v < n ? __ldcs(npred + v) : -1;
-      r[j] = v < n ? __ldcs(round + v) : 0;
+      const int64_t i = i0 + j * stride;
+      vv[j] = i < cnt ? (use_list ? list[i] : (int)i) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kOrdItems; ++j) {
+      const bool ok = i0 + j * stride < cnt;
+      np[j] = ok ? (use_list ? npred[vv[j]] : __ldcs(npred + vv[j])) : -1;
+      r[j] = ok ? (use_list ? round[vv[j]] : __ldcs(round + vv[j])) : 0;
     }
 #pragma unroll
     for (int j = 0; j < kOrdItems; ++j)
       // part 0: the top keys only, 1: the rest, -1: all
       if (np[j] >= 0 && (part < 0 || ((rmax - r[j] <= ktop) == (part == 0))))
-        atomicAdd(&bcnt[bucket_of((int)(v0 + j * stride), r[j], seed, rmax, hist1, base1)], 1);
+        atomicAdd(&bcnt[bucket_of(vv[j], r[j], seed, rmax, hist1, base1)], 1);
   }
 }
 
@@ -324,14 +332,18 @@ __global__ void k_scatter(int64_t n, const int32_t* __restrict__ round, Key2 see
                           const State* st, const int32_t* __restrict__ hist1,
                           const int32_t* __restrict__ base1, int32_t* __restrict__ bcnt,
                           const int32_t* __restrict__ bstart, const int32_t* __restrict__ npred,
-                          int32_t* __restrict__ ord, int part) {
+                          int32_t* __restrict__ ord, int part,
+                          const int32_t* __restrict__ list) {
   const int rmax = st->rmax;
   const int ktop = st->ord_ktop;
   // the bottom part's buckets were counted and scanned on their own: its
   // positions start after the top part's
   const int base = part == 1 ? st->ord_ptop : 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
+  const bool use_list = list && st->top_n > 0;
+  const int64_t cnt = use_list ? st->top_n : n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = use_list ? list[i] : i;
     if (!in_order(npred, v)) continue;  // isolated: not in the order
     const int r = round[v];
     // part 0: the top keys only, 1: the rest, -1: all
@@ -548,6 +560,8 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
   // deferred: the top rounds now (the core's prefix), the rest beside the core
   defer = defer && c.tune.jp_split_overlap && c.tune.core_max > 0;
   const int part = defer ? 0 : -1;
+  // ADG's saved top-round list (superset of the top part) replaces the pass over n
+  const int32_t* top_list = defer && range_known && c.top_list ? c.Rl : nullptr;
   if (defer)
     PGC_LAUNCH(c, kGOrder, "k_order_top",
                k_order_top<<<1, 1024, 0, c.st>>>(c.state, c.hist1, c.base1, L, c.tune.core_max));
@@ -555,13 +569,13 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
              k_zero_i32_dev<<<G, 256, 0, c.st>>>(c.bcnt, &c.state->nbuckets, 1));
   PGC_LAUNCH(c, kGOrder, "k_hist2",
              k_hist2<<<G, 256, 0, c.st>>>(c.n, round, seed, c.npred, c.state, c.hist1, c.base1,
-                                          c.bcnt, part));
+                                          c.bcnt, part, top_list));
   if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
                       &c.state->sorted))
     return e;
   PGC_LAUNCH(c, kGOrder, "k_scatter",
              k_scatter<<<G, 256, 0, c.st>>>(c.n, round, seed, c.state, c.hist1, c.base1, c.bcnt,
-                                            c.bstart, c.npred, c.U[1], part));
+                                            c.bstart, c.npred, c.U[1], part, top_list));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
              k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.U[1], c.npred, c.off, c.rec,
                                                 seed, part));
@@ -580,13 +594,13 @@ static int jp_order_bottom(Ctx& c) {
   // the top part's bucket counts are spent (0): count and scan the rest alone
   PGC_LAUNCH(c, kGOrder, "k_hist2",
              k_hist2<<<G, 256, 0, c.st>>>(c.n, c.ord_round, seed, c.npred, c.state, c.hist1,
-                                          c.base1, c.bcnt, 1));
+                                          c.base1, c.bcnt, 1, nullptr));
   if (int e = scan_ex(c, c.bcnt, c.bstart, &c.state->nbuckets, -1, c.lay.nb_cap,
                       &c.state->sorted_bot))
     return e;
   PGC_LAUNCH(c, kGOrder, "k_scatter",
              k_scatter<<<G, 256, 0, c.st>>>(c.n, c.ord_round, seed, c.state, c.hist1, c.base1,
-                                            c.bcnt, c.bstart, c.npred, c.U[1], 1));
+                                            c.bcnt, c.bstart, c.npred, c.U[1], 1, nullptr));
   PGC_LAUNCH(c, kGOrder, "k_bucket_sort",
              k_bucket_sort<<<G, 256, 0, c.st>>>(c.state, c.bstart, c.U[1], c.npred, c.off, c.rec,
                                                 seed, 1));

@@ -35,7 +35,7 @@ struct State {
   unsigned long long cut;      // arcs from R_l into U_{l+1}
   int nR, nLight, nUnext, nChunks;
   int nOrdR;                   // non-isolated vertices of R_l (the priority order's round histogram)
-  int pad2;
+  int top_n;                   // length of the saved top-round list (k_top_save; 0 = none)
   // totals
   long long sum_active;        // sum_l |U_l|
   unsigned long long cross;    // X
@@ -92,6 +92,7 @@ struct Tuning {
   int core_pass_ns = 0;           // JP core: min sleep (ns) between passes of a warp far from its tail
   int itr_blocks_per_sm = 0;      // DEC-ADG-ITR: blocks per SM of the cooperative kernel (0 = occupancy)
   int jp_split_overlap = 1;       // JP: run the bulk split on a side stream beside the core kernel
+  int top_list = 1;               // JP-ADG: ADG saves the top rounds' list for the split order
   int fuse_init = 1;              // ADG: round 1's selection also initialises D, rs, round, color
   int update_atom = 1;            // ADG round 1: one atomic per arc instead of gather + RED (Arc::atom)
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
@@ -139,6 +140,7 @@ struct Ctx {
   // split order (jp_order_run with defer): the bottom part still to place
   bool ord_pending = false;
   bool ord_deferred = false;
+  bool top_list = false;  // ADG saved U_l (the last with |U_l| >= core_max) in Rl
   const int32_t* ord_round = nullptr;
   uint64_t ord_seed = 0;
   int ord_idshift = 0;

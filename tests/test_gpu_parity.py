@@ -129,7 +129,7 @@ def tuning():
     defaults = {"core_max": 65535, "core_min_avg": 32, "core_min_n": 256, "core_ctas": 0,
                 "core_arc_cap": 1 << 30, "core_arcs_per_cta": 2 << 20, "jp_heavy_warps": 4,
                 "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
-                "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1}
+                "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1, "top_list": 1}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
 
@@ -210,6 +210,7 @@ def test_determinism_across_tuning(tuning):
         tuning("jp_split_overlap", ovl)
         tuning("update_atom", atom)
         tuning("fuse_init", atom ^ ovl ^ 1)
+        tuning("top_list", hw & 1)
         tuning("heavy_degree", hd)
         tuning("rounds_per_sync", rps)
         tuning("core_max", core)
