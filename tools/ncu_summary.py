@@ -40,7 +40,7 @@ def launches(path):
     for r in rows[hi + 1:]:
         name = short(r[ki])
         t = float(r[vi].replace(",", ""))
-        if name == "k_adg_init":
+        if name in ("k_adg_init", "k_adg_state_init"):
             steps.append(collections.OrderedDict())
         if steps:
             steps[-1].setdefault(name, [0.0, 0])
