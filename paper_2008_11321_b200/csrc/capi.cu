@@ -493,11 +493,17 @@ int pgc_color_jp_adg_host(int64_t n, int64_t nnz, const int64_t* h_row_offsets,
   cudaStream_t st = (cudaStream_t)cuda_stream;
   // a side stream (per thread, created once) carries col[] host->device and
   // round[] device->host, overlapping the first ADG kernels and JP
-  static thread_local cudaStream_t side = nullptr;
-  static thread_local cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // (per thread and device: streams and events belong to one device)
+  static thread_local cudaStream_t sides[64] = {};
+  static thread_local cudaEvent_t evs[64][3] = {};
+  int dev = 0;
+  PGC_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(PGC_EINTERNAL, "device ordinal %d out of range", dev);
+  cudaStream_t& side = sides[dev];
+  cudaEvent_t* ev = evs[dev];
   if (!side) {
     PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    for (auto& e : ev) PGC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int i = 0; i < 3; ++i) PGC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
   }
   PGC_CUDA(cudaEventRecord(ev[0], st));  // the side stream starts after st's earlier work
   PGC_CUDA(cudaStreamWaitEvent(side, ev[0], 0));

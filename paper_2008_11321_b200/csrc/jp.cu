@@ -1792,8 +1792,10 @@ int jp_color_run(Ctx& c, int32_t* color) {
       // the running kernels: a side-stream kernel the core waits on (the list
       // rewrite) must be loaded before the core starts, or the first call
       // deadlocks until the watchdog.  Querying the attributes loads them.
-      static thread_local bool loaded = false;
-      if (!loaded) {
+      static thread_local bool loaded[64] = {};  // per device: modules are per context
+      int dev = 0;
+      PGC_CUDA(cudaGetDevice(&dev));
+      if (dev < 0 || dev >= 64 || !loaded[dev]) {
         cudaFuncAttributes fa;
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_pos));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_lists));
@@ -1805,7 +1807,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_reduce));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_tmp));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_down));
-        loaded = true;
+        if (dev >= 0 && dev < 64) loaded[dev] = true;
       }
     }
     // the core's list rewrite: before the core, or beside it with per-vertex
@@ -1873,11 +1875,17 @@ int jp_color_run(Ctx& c, int32_t* color) {
       // fork: the core first (it is launched first and finds its SMs free);
       // the list rewrite, the rest of the order and the bulk split on the side
       // stream; join before the bulk
-      static thread_local cudaStream_t side = nullptr;
-      static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+      // per thread and device (streams and events belong to one device)
+      static thread_local cudaStream_t sides[64] = {};
+      static thread_local cudaEvent_t evs[64][2] = {};
+      int dev = 0;
+      PGC_CUDA(cudaGetDevice(&dev));
+      if (dev < 0 || dev >= 64) return fail(4, "device ordinal %d out of range", dev);
+      cudaStream_t& side = sides[dev];
+      cudaEvent_t* ev = evs[dev];
       if (!side) {
         PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-        for (auto& e : ev) PGC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (int i = 0; i < 2; ++i) PGC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
       }
       static_assert(65535 * 4 <= 2 * kFilterBytes, "list states fit the filter buffers");
       PGC_CUDA(cudaMemsetAsync(ready, 0, 4 * (size_t)NC, c.st));
