@@ -1549,6 +1549,12 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
     unsigned sleep_ns = 32;
     int4 nx = make_int4(0, 0, 0, 0);  // prefetched next record
     bool have_nx = false;
+    // the warp's ticket queue [q_t, q_t + q_n): light tickets are taken 32 at a
+    // time (one atomic on the shared counter per 32 vertices, not per refill)
+    // and handed to the lanes in order, so every ticket the warp holds but has
+    // not started is of lower priority than the ones it has started (the
+    // deadlock-freedom argument of the prefetch, k_bucket_sort)
+    int q_t = 0, q_n = 0;
     {
       int t0 = 0;
       if (lane == 0) t0 = atomicAdd(&st->ticket_light, 32);
@@ -1572,16 +1578,27 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
       }
       const unsigned want = __ballot_sync(0xffffffffu, take);
       if (want) {
-        const int leader = __ffs(want) - 1;
-        int t0 = 0;
-        if (lane == leader) t0 = atomicAdd(&st->ticket_light, __popc(want));
-        t0 = __shfl_sync(0xffffffffu, t0, leader);
+        const int need = __popc(want);
+        int fresh = 0;
+        if (need > q_n) {  // the queue runs dry: a fresh block of 32 tickets
+          const int leader = __ffs(want) - 1;
+          if (lane == leader) fresh = atomicAdd(&st->ticket_light, 32);
+          fresh = __shfl_sync(0xffffffffu, fresh, leader);
+        }
         if (take) {
-          const int64_t t = (int64_t)t0 + __popc(want & lt);
+          const int rank = __popc(want & lt);
+          const int64_t t = rank < q_n ? (int64_t)q_t + rank : (int64_t)fresh + (rank - q_n);
           if (t < nlight) {
             nx = __ldcs(lrec + t);
             have_nx = true;
           }
+        }
+        if (need > q_n) {
+          q_t = fresh + (need - q_n);
+          q_n = 32 - (need - q_n);
+        } else {
+          q_t += need;
+          q_n -= need;
         }
       }
       if (take) {
