@@ -1203,6 +1203,9 @@ constexpr int kLV = PGC_LIGHT_VEC;  // 16-byte pred-id loads per first-pass step
 #ifndef PGC_LIGHT_STEPS
 #define PGC_LIGHT_STEPS 2
 #endif
+#ifndef PGC_LIGHT_Q
+#define PGC_LIGHT_Q 32
+#endif
 constexpr int kLightSteps = PGC_LIGHT_STEPS;  // first-pass steps per lane per loop iteration
 
 __global__ void k_bulk_flags(int64_t n, const int4* __restrict__ rec, const State* st,
@@ -1554,6 +1557,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
     // and handed to the lanes in order, so every ticket the warp holds but has
     // not started is of lower priority than the ones it has started (the
     // deadlock-freedom argument of the prefetch, k_bucket_sort)
+    constexpr int kLightQ = PGC_LIGHT_Q;  // tickets per refill of the queue (>= 32)
     int q_t = 0, q_n = 0;
     {
       int t0 = 0;
@@ -1582,7 +1586,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         int fresh = 0;
         if (need > q_n) {  // the queue runs dry: a fresh block of 32 tickets
           const int leader = __ffs(want) - 1;
-          if (lane == leader) fresh = atomicAdd(&st->ticket_light, 32);
+          if (lane == leader) fresh = atomicAdd(&st->ticket_light, kLightQ);
           fresh = __shfl_sync(0xffffffffu, fresh, leader);
         }
         if (take) {
@@ -1595,7 +1599,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         }
         if (need > q_n) {
           q_t = fresh + (need - q_n);
-          q_n = 32 - (need - q_n);
+          q_n = kLightQ - (need - q_n);
         } else {
           q_t += need;
           q_n -= need;
