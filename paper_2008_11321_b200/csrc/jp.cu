@@ -668,6 +668,7 @@ constexpr int kCoreBlock = PGC_CORE_BLOCK;
 constexpr int kCoreWarps = kCoreBlock / 32;
 constexpr int kCoreWin = 1024;   // colors per byte-map window
 constexpr int kCorePend = 512;   // pending-pred list capacity per warp
+constexpr int kCoreVertsPerCta = 4096;  // cluster sizing: core vertices per CTA
 constexpr int kCoreRun = 32;     // consecutive core positions per CTA run
 #ifndef PGC_CORE_TAIL
 #define PGC_CORE_TAIL 4
@@ -1782,9 +1783,14 @@ int jp_color_run(Ctx& c, int32_t* color) {
       const long long arcs = c.h_state->core_arcs;
       core_smem = kCoreFixedSmem + (((size_t)NC * 2 + 15) & ~(size_t)15);
       if (NC >= c.tune.core_min_n) {
-        int want = c.tune.core_ctas > 0
-                       ? c.tune.core_ctas
-                       : (int)((arcs + c.tune.core_arcs_per_cta - 1) / c.tune.core_arcs_per_cta);
+        // CTAs for the arcs AND for the chain: each CTA keeps 32 vertices in
+        // flight, and a long prefix needs many in flight even when its lists
+        // are short (R-MAT 20: 65 535 core vertices, 22 M arcs -- 4 CTAs by
+        // arcs, 1.86 ms; 16 CTAs, 1.00 ms)
+        const long long by_arcs = (arcs + c.tune.core_arcs_per_cta - 1) / c.tune.core_arcs_per_cta;
+        const long long by_verts = (NC + kCoreVertsPerCta - 1) / kCoreVertsPerCta;
+        int want = c.tune.core_ctas > 0 ? c.tune.core_ctas
+                                        : (int)(by_arcs > by_verts ? by_arcs : by_verts);
         want = pow2_floor(want < 1 ? 1 : (want > 16 ? 16 : want));
         C = core_cluster_size(want, core_smem);
       }
