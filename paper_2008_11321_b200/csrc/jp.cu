@@ -668,7 +668,7 @@ constexpr int kCoreBlock = PGC_CORE_BLOCK;
 constexpr int kCoreWarps = kCoreBlock / 32;
 constexpr int kCoreWin = 1024;   // colors per byte-map window
 constexpr int kCorePend = 512;   // pending-pred list capacity per warp
-constexpr int kCoreVertsPerCta = 4096;  // cluster sizing: core vertices per CTA
+constexpr int kCoreVertsPerCta = 1024;  // cluster sizing: core vertices per CTA
 constexpr int kCoreRun = 32;     // consecutive core positions per CTA run
 #ifndef PGC_CORE_TAIL
 #define PGC_CORE_TAIL 4
