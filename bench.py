@@ -160,15 +160,31 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ model ---
-def algorithmic_bytes(n, nnz, m, X, sum_active):
-    """Bytes each kernel group must move (each logical access once, at its size,
-    no sector inflation, no cache credit).  DESIGN.md "Roofline model"."""
+def survey_bytes(n, nnz, m, X, sum_active):
+    """Algorithmic bytes of SURVEY.md §8(d) (per-touch model: each logical
+    access once at its size, no sector inflation, no cache credit), with JP
+    Part 1 fused into UPDATE at zero extra bytes:
+      init 20n | ADG scans 12 sum_l n_l | per removed vertex 16n |
+      ADG arcs 8 nnz + 8X | JP per vertex 20n | JP arcs 8 nnz + 12m
+    B_alg = 44m + 8X + 12 sum_l n_l + 56n (nnz = 2m)."""
+    t = {"init": 20 * n, "adg_scans": 12 * sum_active, "adg_vertex": 16 * n,
+         "adg_arcs": 8 * nnz + 8 * X, "jp_vertex": 20 * n, "jp_arcs": 8 * nnz + 12 * m}
+    t["update"] = t["adg_arcs"] + t["adg_vertex"]       # row a4 (+ its per-vertex term)
+    t["path"] = 44 * m + 8 * X + 12 * sum_active + 56 * n
+    assert t["path"] == sum(t[k] for k in ("init", "adg_scans", "adg_vertex", "adg_arcs",
+                                           "jp_vertex", "jp_arcs"))
+    return t
+
+
+def builder_bytes(n, nnz, m, X, sum_active):
+    """The builder's own per-group model (round 1), kept for context only: it
+    also charges this design's pred-list stores (4m) and record traffic."""
     return {
-        "init": 8 * n + 12 * n,                                  # read off; write D, round, color
-        "select": 12 * sum_active + 20 * n,                      # U list + D + list write; round + offsets of R
-        "update": 24 * n + 8 * nnz + 8 * X + 4 * m,              # R entry+offsets+npred; col+round per arc; RED; pred write
-        "order": 56 * n,                                         # key/npred reads x3, atomics x2, order write/read/write
-        "jp": 20 * n + 8 * m,                                    # order, npred, off, color store; pred id + pred color
+        "init": 8 * n + 12 * n,
+        "select": 12 * sum_active + 20 * n,
+        "update": 24 * n + 8 * nnz + 8 * X + 4 * m,
+        "order": 56 * n,
+        "jp": 20 * n + 8 * m,
     }
 
 
@@ -179,14 +195,45 @@ def peak_gbs():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu summary, if any."""
-    p = os.path.join(PROFILES, "ncu_traffic.json")
+def measured_traffic(workload):
+    """DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) of one
+    step's UPDATE launches on THIS workload, from profiles/traffic.json
+    (written by tools/traffic.py from an ncu pass over the same path and
+    workload); None when that workload was never captured."""
     try:
-        d = json.load(open(p))
-        return d.get(kernel)
+        d = json.load(open(os.path.join(PROFILES, "traffic.json")))
+        e = d.get(workload)
+        return (e["update_dram_bytes_per_step"], e["source"]) if e else (None, None)
     except Exception:
-        return None
+        return None, None
+
+
+def host_info():
+    model, mhz = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name") and model is None:
+                model = line.split(":", 1)[1].strip()
+            if line.startswith("cpu MHz") and mhz is None:
+                mhz = float(line.split(":", 1)[1])
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "cpu_mhz": mhz}
+
+
+def step_stats(times_ms):
+    """median, min, mean and the 95% CI of the mean (t quantile; the paper's
+    reporting, PAPER.md:2992-2996)."""
+    k = len(times_ms)
+    mean = statistics.mean(times_ms)
+    sd = statistics.stdev(times_ms) if k > 1 else 0.0
+    tq = {1: 12.71, 2: 4.30, 3: 3.18, 4: 2.78, 5: 2.57, 6: 2.45, 7: 2.36, 8: 2.31, 9: 2.26,
+          10: 2.23, 15: 2.13, 20: 2.09, 30: 2.04}
+    df = max(1, k - 1)
+    q = tq.get(df) or tq[min(tq, key=lambda d: abs(d - df))]
+    half = q * sd / (k ** 0.5) if k > 1 else 0.0
+    return {"median_ms": statistics.median(times_ms), "min_ms": min(times_ms), "mean_ms": mean,
+            "ci95_ms": [mean - half, mean + half], "steps": k}
 
 
 # ------------------------------------------------------------- multi-GPU ----
@@ -292,21 +339,24 @@ def run_pgc(args):
     stream = torch.cuda.current_stream(dev)
 
     # ---- timed region A: the headline (no per-launch events) ----
+    # an event between consecutive steps gives per-step times (each call blocks
+    # until its stream is idle, so the events add nothing to a step)
     launches = 0
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local_rank) as clk:
         if barrier:
             barrier()
         torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             _, _, T, K = step()
             launches += pgc.last_stats()["kernel_launches"]
-        ev1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize()
         if barrier:
             barrier()
-    ms = reduce_max_ms(ev0.elapsed_time(ev1) / args.steps, dist, dev)
+    ms = reduce_max_ms(evs[0].elapsed_time(evs[-1]) / args.steps, dist, dev)
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     st = pgc.last_stats()
 
     # ---- timed region B: same steps with per-launch CUDA events (attribution) ----
@@ -321,49 +371,52 @@ def run_pgc(args):
     pgc.set_tuning("timing", 0)
     gmean = {k: statistics.mean(v) for k, v in groups.items()}
 
+    # ---- J (JP levels): one more, untimed call with the levels pass on ----
+    J = None
+    if not (adgonly or decitr):
+        pgc.set_tuning("levels", 1)
+        step()
+        J = pgc.last_stats()["jp_levels"]
+        pgc.set_tuning("levels", 0)
+
     X, sum_active = st["cross_edges"], st["sum_active"]
-    model = algorithmic_bytes(n, nnz, m, X, sum_active)
+    sv = survey_bytes(n, nnz, m, X, sum_active)
+    model = builder_bytes(n, nnz, m, X, sum_active)
     upd_arcs = nnz   # arcs UPDATE classifies per step
+    upd_bytes = sv["update"]
+    path_bytes = sv["path"]
+    path_model = "SURVEY 8(d): B_alg = 44m + 8X + 12 sum_l n_l + 56n"
     if adgonly:
-        model["jp"] = model["order"] = 0
-        model["update"] = 16 * n + 4 * nnz + 1 * nnz + 4 * X   # R records+offsets; col+state per arc; RED
+        # ADG alone: init, scans, per-vertex and arcs terms of 8(d) (no JP rows)
+        path_bytes = sv["init"] + sv["adg_scans"] + sv["adg_vertex"] + sv["adg_arcs"]
+        path_model = "SURVEY 8(d) ADG rows: 20n + 12 sum_l n_l + 16n + 8 nnz + 8X"
         if args.method == "adg-pull":
-            # pull: every survivor rescans its adjacency: sum_v (round[v]-1) * deg(v) arcs
+            # pull: every survivor rescans its adjacency: sum_v (round[v]-1) * deg(v) arcs,
+            # a col read + a state gather each, one D update per survivor per round
             r_h = rnd.cpu().numpy().astype(np.int64)
             pull_arcs = int(((r_h - 1) * g.degrees().astype(np.int64)).sum())
-            model["update"] = 16 * sum_active + 5 * pull_arcs + 8 * sum_active   # records; col+state; D rmw
+            upd_bytes = 8 * pull_arcs + 8 * sum_active
+            path_bytes = sv["init"] + sv["adg_scans"] + sv["adg_vertex"] + upd_bytes
             upd_arcs = pull_arcs
     peak, peak_kind = peak_gbs()
-    kern = {"update": ("k_update_light+k_update_heavy", gmean["t_update_ms"], model["update"]),
-            "jp": ("k_jp_bulk", gmean["t_jp_ms"], model["jp"]),
-            "select": ("k_adg_select", gmean["t_select_ms"], model["select"]),
-            "order": ("order (bucket sort)", gmean["t_order_ms"], model["order"])}
-    dom = max(kern, key=lambda k: kern[k][1])
-    kname, kms, kbytes = kern[dom]
-    achieved = kbytes / (kms * 1e-3) / 1e9
-    traffic = ncu_traffic(kname)
-    path_bytes = sum(model.values())
-    # UPDATE moves few bytes per random access: its ceiling is the measured
-    # random gather/RED rate for its exact mix (profiles/random_access_probe.json)
+    t_upd = gmean["t_update_ms"]
+    achieved = upd_bytes / (t_upd * 1e-3) / 1e9
+    workload = (f"{args.config}-{args.method}" if (baseline or decitr or adgonly) else
+                f"{args.config}-adgm" if median else
+                f"{args.config}-adgo-eps{num}/{den}" if sortedR else f"{args.config}-eps{num}/{den}")
+    traffic, traffic_src = measured_traffic(workload)
+    # the builder's uniform-target probe of the gather+RED mix (context, not a ceiling:
+    # UPDATE beats it because hub targets hit in L2)
     ra = None
     try:
         pr = json.load(open(os.path.join(PROFILES, "random_access_probe.json")))
-        arcs_per_s = upd_arcs / (gmean["t_update_ms"] * 1e-3)
-        if args.method == "adg-pull":   # a gather per arc, no per-arc RED
-            ra = {"arcs_per_s": arcs_per_s, "red_fraction": 0.0,
-                  "peak_arcs_per_s": pr["gather_u8_per_s"],
-                  "frac": arcs_per_s / pr["gather_u8_per_s"],
-                  "note": "pull UPDATE = one random 1-byte state gather per survivor arc "
-                          "(sum_v (round[v]-1) deg(v) arcs); peak = tools/micro/atom_probe.cu "
-                          "gather-only rate"}
-        else:
-            mix = X / upd_arcs if upd_arcs else 0.0
-            ra = {"arcs_per_s": arcs_per_s, "red_fraction": mix,
-                  "peak_arcs_per_s": pr["gather_plus_red_42pct_arcs_per_s"],
-                  "frac": arcs_per_s / pr["gather_plus_red_42pct_arcs_per_s"],
-                  "note": "UPDATE = one random 1-byte state gather per arc + one RED per "
-                          "cross-round edge; peak = tools/micro/atom_probe.cu at the same RED "
-                          "fraction (0.42)"}
+        arcs_per_s = upd_arcs / (t_upd * 1e-3)
+        key = "gather_u8_per_s" if args.method == "adg-pull" else "gather_plus_red_42pct_arcs_per_s"
+        ra = {"arcs_per_s": arcs_per_s, "red_fraction": 0.0 if args.method == "adg-pull" else
+              (X / upd_arcs if upd_arcs else 0.0),
+              "uniform_probe_arcs_per_s": pr[key], "ratio_to_uniform_probe": arcs_per_s / pr[key],
+              "note": "tools/micro/atom_probe.cu: uniformly random targets on a 16.7 M-vertex "
+                      "state; NOT a ceiling for skewed (R-MAT) targets"}
     except Exception:
         pass
 
@@ -379,21 +432,35 @@ def run_pgc(args):
         "value": job_value(world, m, ms), "unit": "edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": f"{args.config}-{args.method}" if (baseline or decitr or adgonly) else
-                   f"{args.config}-adgm" if median else
-                   f"{args.config}-adgo-eps{num}/{den}" if sortedR else f"{args.config}-eps{num}/{den}",
+        "config": {"workload": workload,
                    "method": args.method, "n": n, "m": m, "nnz": nnz,
                    "eps": f"{num}/{den}", "seed": args.seed, "graph_seed": 1,
                    "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
-                   "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB L2); no flush" %
-                         ((8 * (n + 1) + 4 * nnz) / 1e9)},
-        "colors": K, "rounds": T, "cross_edges": X, "sum_active": sum_active,
+                   "l2": ("inputs larger than L2 (CSR %.2f GB vs 126 MB L2); no flush" %
+                          ((8 * (n + 1) + 4 * nnz) / 1e9)) if 8 * (n + 1) + 4 * nnz > 126e6 else
+                         ("CSR %.1f MB fits the 126 MB L2: steps run back to back with a warm L2 "
+                          "(this small config is latency-bound, not bandwidth-bound)" %
+                          ((8 * (n + 1) + 4 * nnz) / 1e6))},
+        "timing": step_stats(per_step),
+        "colors": K, "rounds": T, "jp_levels": J, "cross_edges": X, "sum_active": sum_active,
         "core_vertices": st["core_vertices"], "core_ctas": st["core_ctas"],
-        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "bytes_per_launch": kbytes, "ms_per_launch": kms,
-                     "path_bytes": path_bytes,
-                     "path_frac": path_bytes / (ms * 1e-3) / 1e9 / peak,
+        "roofline": {"bound": "hbm",
+                     "kernel": "ADG UPDATE with fused JP Part 1 (k_update_light + k_update_heavy + "
+                               "k_update_heavy_f, every round of one step)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes": upd_bytes, "ms_per_launch": t_upd,
+                     "bytes_model": ("SURVEY 8(d) rows a4: 8 nnz + 8X, plus the 16n per-removed-"
+                                     "vertex term" if args.method != "adg-pull" else
+                                     "pull: 8 bytes per rescanned arc + 8 per survivor-round"),
+                     "path": {"bytes": path_bytes, "model": path_model,
+                              "achieved_gbs": path_bytes / (ms * 1e-3) / 1e9,
+                              "frac": path_bytes / (ms * 1e-3) / 1e9 / peak,
+                              "frac_8tbs": path_bytes / (ms * 1e-3) / 8e12},
+                     "builder_model": {"update_bytes": model["update"],
+                                       "path_bytes": sum(model.values()),
+                                       "note": "round-1 builder model incl. pred-list stores (4m); "
+                                               "context only"},
                      "random_access": ra},
         "breakdown_ms": {k[2:-3]: v for k, v in gmean.items()},
         "gpu_launches": launches,
@@ -445,8 +512,13 @@ def run_pgc(args):
         else:
             c_or, K_or = O.jp_rho(g, rho) if sortedR else O.jp(g, r_or, args.seed)
         t2 = time.perf_counter()
+        t3 = time.perf_counter()
+        out["degeneracy"] = O.degeneracy(g)     # d (exact, Matula-Beck peel)
+        t_d = time.perf_counter() - t3
         out["cpu_baseline"] = {"value": m / (t2 - t0), "unit": "edges/s", "cores": 1,
-                               "kind": "oracle",
+                               "kind": "oracle", "host": host_info(),
+                               "oracle_ms": {"adg": (t1 - t0) * 1e3, "jp": (t2 - t1) * 1e3,
+                                             "degeneracy": t_d * 1e3},
                                "sample": f"full {args.config} workload, one "
                                          f"{'ADG' if adgonly else 'JP-ADG'} run of the "
                                          f"sequential C oracle (ADG {t1 - t0:.1f}s + greedy JP "
@@ -454,6 +526,9 @@ def run_pgc(args):
         out["parity"] = {"round": True if baseline else bool(np.array_equal(rnd.cpu().numpy(), r_or)),
                          "color": bool(np.array_equal(color.cpu().numpy(), c_or)),
                          "K": K == K_or}
+        if J is not None and not sortedR:   # J of the oracle's greedy (untimed, after the baseline)
+            _, _, _, J_or = O.jp(g, r_or, args.seed, levels=True)
+            out["parity"]["J"] = J == J_or
 
     if rank == 0:
         print(json.dumps(out), flush=True)

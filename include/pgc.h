@@ -57,21 +57,25 @@
 extern "C" {
 #endif
 
-#define PGC_VERSION 2
+#define PGC_VERSION 3
 
 enum pgc_status {
   PGC_OK = 0,          /* success                                                  */
-  PGC_EINVAL = 1,      /* NULL pointer, n < 0, n >= INT32_MAX, nnz < 0, nnz >= 2^40,
+  PGC_EINVAL = 1,      /* NULL pointer, n < 0, n >= 2^29, nnz < 0, nnz >= 2^40,
                           eps_num == 0 or eps_den == 0, bad round[] range           */
   PGC_EWORKSPACE = 2,  /* workspace too small or not 256-byte aligned              */
   PGC_ECUDA = 3,       /* a CUDA runtime error (message in pgc_last_error)         */
   PGC_EINTERNAL = 4    /* an internal invariant failed (a bug): e.g. an empty ADG
-                          round or an inconsistent compaction count                */
+                          round, a round that broke Lemma 1's exact shrink
+                          n_{l+1}(den+num) < n_l den, more
+                          rounds than T0 = min{t : (den+num)^t >= n den^t}, an
+                          inconsistent compaction count, or a JP stall         */
 };
 
 /* Graph in caller-owned DEVICE memory (see "Graph input" above). */
 typedef struct pgc_graph {
-  int64_t n;                   /* number of vertices, 0 <= n < INT32_MAX              */
+  int64_t n;                   /* number of vertices, 0 <= n < 2^29 (the workspace
+                                  layout indexes 2n + 65536 entries with int32)       */
   int64_t nnz;                 /* number of arcs = 2m = row_offsets[n], < 2^40        */
   const int64_t* row_offsets;  /* device, n+1 entries                                 */
   const int32_t* col_indices;  /* device, nnz entries                                 */
@@ -90,6 +94,11 @@ typedef struct pgc_stats {
   int32_t host_syncs;      /* stream synchronisations this call performed                 */
   int32_t core_ctas;       /* JP: thread-block cluster size of the core engine (0 = none) */
   int32_t sim_col_passes;  /* DEC-ADG-ITR: SIM-COL passes over all partitions (else 0)    */
+  int32_t jp_levels;       /* J = the number of vertices on a longest path of the JP DAG
+                              G_rho (level[v] = 1 + max level over pred(v); Alg. 3's
+                              depth term, Lemma 6 1192-1294).
+                              Computed only with pgc_set_tuning("levels", 1) (an extra
+                              dataflow pass after JP; off in timed runs), else 0.      */
   /* Device time per kernel group, from CUDA events on the call's stream; all -1
    * unless pgc_set_tuning("timing", 1).  Groups: ADG select (a2/a3), ADG UPDATE
    * with fused JP Part 1 (a4/a7), other ADG kernels (init, finalize), the

@@ -45,6 +45,7 @@ class Stats(ctypes.Structure):
                 ("pred_arcs", ctypes.c_int64), ("core_vertices", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int32), ("host_syncs", ctypes.c_int32),
                 ("core_ctas", ctypes.c_int32), ("sim_col_passes", ctypes.c_int32),
+                ("jp_levels", ctypes.c_int32),
                 ("t_select_ms", ctypes.c_float), ("t_update_ms", ctypes.c_float),
                 ("t_adg_other_ms", ctypes.c_float), ("t_order_ms", ctypes.c_float),
                 ("t_core_ms", ctypes.c_float), ("t_jp_ms", ctypes.c_float),
@@ -104,6 +105,14 @@ class PGCError(RuntimeError):
 def _check(rc: int):
     if rc != PGC_OK:
         raise PGCError(rc, _lib.pgc_last_error().decode(errors="replace"))
+
+
+def _run(dev, fn, *args):
+    """Call a library entry point with `dev` as the current CUDA device: the
+    library takes the SM count, side streams and events from the current
+    device, which must be the one the tensors and the stream live on."""
+    with torch.cuda.device(dev):
+        _check(fn(*args))
 
 
 def lib():
@@ -199,9 +208,9 @@ def adg_order(row_offsets, col_indices, eps_num: int, eps_den: int, *, update="p
     ws = _workspace(nb, dev)
     T = ctypes.c_int32(0)
     mode = UPDATE_MODES[update]
-    _check(_lib.pgc_adg_order_mode(ctypes.byref(g), eps_num, eps_den, mode,
+    _run(dev, _lib.pgc_adg_order_mode, ctypes.byref(g), eps_num, eps_den, mode,
                                    rnd.data_ptr() if g.n else None, ctypes.byref(T),
-                                   ws.data_ptr(), ws.numel(), _stream(dev)))
+                                   ws.data_ptr(), ws.numel(), _stream(dev))
     return rnd, T.value
 
 
@@ -214,9 +223,9 @@ def jp_color(row_offsets, col_indices, round_key, seed: int, *, color_out=None):
     color = _out(color_out, g.n, dev, "color_out")
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
     K = ctypes.c_int32(0)
-    _check(_lib.pgc_jp_color(ctypes.byref(g), round_key.contiguous().data_ptr() if g.n else None,
+    _run(dev, _lib.pgc_jp_color, ctypes.byref(g), round_key.contiguous().data_ptr() if g.n else None,
                              seed & 0xFFFFFFFFFFFFFFFF, color.data_ptr() if g.n else None,
-                             ctypes.byref(K), ws.data_ptr(), ws.numel(), _stream(dev)))
+                             ctypes.byref(K), ws.data_ptr(), ws.numel(), _stream(dev))
     return color, K.value
 
 
@@ -229,10 +238,10 @@ def color_jp_adg(row_offsets, col_indices, eps_num: int, eps_den: int, seed: int
     color = _out(color_out, g.n, dev, "color_out")
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
     T, K = ctypes.c_int32(0), ctypes.c_int32(0)
-    _check(_lib.pgc_color_jp_adg(ctypes.byref(g), eps_num, eps_den, seed & 0xFFFFFFFFFFFFFFFF,
+    _run(dev, _lib.pgc_color_jp_adg, ctypes.byref(g), eps_num, eps_den, seed & 0xFFFFFFFFFFFFFFFF,
                                  rnd.data_ptr() if g.n else None, color.data_ptr() if g.n else None,
                                  ctypes.byref(T), ctypes.byref(K), ws.data_ptr(), ws.numel(),
-                                 _stream(dev)))
+                                 _stream(dev))
     return rnd, color, T.value, K.value
 
 
@@ -243,8 +252,8 @@ def adg_m_order(row_offsets, col_indices, *, round_out=None):
     rnd = _out(round_out, g.n, dev, "round_out")
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
     T = ctypes.c_int32(0)
-    _check(_lib.pgc_adg_m_order(ctypes.byref(g), rnd.data_ptr() if g.n else None, ctypes.byref(T),
-                                ws.data_ptr(), ws.numel(), _stream(dev)))
+    _run(dev, _lib.pgc_adg_m_order, ctypes.byref(g), rnd.data_ptr() if g.n else None, ctypes.byref(T),
+                                ws.data_ptr(), ws.numel(), _stream(dev))
     return rnd, T.value
 
 
@@ -256,10 +265,10 @@ def color_jp_adg_m(row_offsets, col_indices, seed: int, *, round_out=None, color
     color = _out(color_out, g.n, dev, "color_out")
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
     T, K = ctypes.c_int32(0), ctypes.c_int32(0)
-    _check(_lib.pgc_color_jp_adg_m(ctypes.byref(g), seed & 0xFFFFFFFFFFFFFFFF,
+    _run(dev, _lib.pgc_color_jp_adg_m, ctypes.byref(g), seed & 0xFFFFFFFFFFFFFFFF,
                                    rnd.data_ptr() if g.n else None, color.data_ptr() if g.n else None,
                                    ctypes.byref(T), ctypes.byref(K), ws.data_ptr(), ws.numel(),
-                                   _stream(dev)))
+                                   _stream(dev))
     return rnd, color, T.value, K.value
 
 
@@ -272,10 +281,10 @@ def color_jp_adg_o(row_offsets, col_indices, eps_num: int, eps_den: int, *, roun
     color = _out(color_out, g.n, dev, "color_out")
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
     T, K = ctypes.c_int32(0), ctypes.c_int32(0)
-    _check(_lib.pgc_color_jp_adg_o(ctypes.byref(g), eps_num, eps_den,
+    _run(dev, _lib.pgc_color_jp_adg_o, ctypes.byref(g), eps_num, eps_den,
                                    rnd.data_ptr() if g.n else None, color.data_ptr() if g.n else None,
                                    ctypes.byref(T), ctypes.byref(K), ws.data_ptr(), ws.numel(),
-                                   _stream(dev)))
+                                   _stream(dev))
     return rnd, color, T.value, K.value
 
 
@@ -289,9 +298,9 @@ def jp_baseline(row_offsets, col_indices, kind: str, seed: int, *, color_out=Non
     color = _out(color_out, g.n, dev, "color_out")
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
     K = ctypes.c_int32(0)
-    _check(_lib.pgc_jp_baseline(ctypes.byref(g), JP_KINDS[kind], seed & 0xFFFFFFFFFFFFFFFF,
+    _run(dev, _lib.pgc_jp_baseline, ctypes.byref(g), JP_KINDS[kind], seed & 0xFFFFFFFFFFFFFFFF,
                                 color.data_ptr() if g.n else None, ctypes.byref(K), ws.data_ptr(),
-                                ws.numel(), _stream(dev)))
+                                ws.numel(), _stream(dev))
     return color, K.value
 
 
@@ -304,10 +313,10 @@ def color_dec_adg_itr(row_offsets, col_indices, eps_num: int, eps_den: int, seed
     color = _out(color_out, g.n, dev, "color_out")
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
     T, K = ctypes.c_int32(0), ctypes.c_int32(0)
-    _check(_lib.pgc_color_dec_adg_itr(ctypes.byref(g), eps_num, eps_den, seed & 0xFFFFFFFFFFFFFFFF,
+    _run(dev, _lib.pgc_color_dec_adg_itr, ctypes.byref(g), eps_num, eps_den, seed & 0xFFFFFFFFFFFFFFFF,
                                       rnd.data_ptr() if g.n else None,
                                       color.data_ptr() if g.n else None, ctypes.byref(T),
-                                      ctypes.byref(K), ws.data_ptr(), ws.numel(), _stream(dev)))
+                                      ctypes.byref(K), ws.data_ptr(), ws.numel(), _stream(dev))
     return rnd, color, T.value, K.value
 
 
@@ -323,13 +332,13 @@ def color_jp_adg_host(row_offsets, col_indices, eps_num: int, eps_den: int, seed
     n, nnz = row_offsets.numel() - 1, col_indices.numel()
     ws = _workspace(host_workspace_bytes(n, nnz), dev)
     T, K = ctypes.c_int32(0), ctypes.c_int32(0)
-    _check(_lib.pgc_color_jp_adg_host(n, nnz, row_offsets.data_ptr(),
+    _run(dev, _lib.pgc_color_jp_adg_host, n, nnz, row_offsets.data_ptr(),
                                       col_indices.data_ptr() if nnz else None, eps_num, eps_den,
                                       seed & 0xFFFFFFFFFFFFFFFF,
                                       round_out.data_ptr() if n else None,
                                       color_out.data_ptr() if n else None,
                                       ctypes.byref(T), ctypes.byref(K), ws.data_ptr(), ws.numel(),
-                                      _stream(dev)))
+                                      _stream(dev))
     return T.value, K.value
 
 
@@ -338,4 +347,4 @@ def check_graph(row_offsets, col_indices):
     g = _graph(row_offsets, col_indices)
     dev = row_offsets.device
     ws = _workspace(workspace_bytes(g.n, g.nnz), dev)
-    _check(_lib.pgc_check_graph(ctypes.byref(g), ws.data_ptr(), ws.numel(), _stream(dev)))
+    _run(dev, _lib.pgc_check_graph, ctypes.byref(g), ws.data_ptr(), ws.numel(), _stream(dev))

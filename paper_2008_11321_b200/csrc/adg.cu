@@ -835,9 +835,16 @@ __global__ void k_msel_reset(State* st) {
 // a2/a5: carry the cached degree sum and |U| to the next round (Q5 reading of
 // PAPER.md:2359-2361), record statistics, detect termination.
 // ord_cnt[l-1] = the non-isolated vertices of R_l (capacity cap): the
-// priority order's round histogram, so the order needs no counting pass
-__global__ void k_adg_finalize(int l, State* st, long long* per_round, int32_t* ord_cnt,
-                               int64_t cap) {
+// priority order's round histogram, so the order needs no counting pass.
+// Every round is checked against the exact integer form of Lemma 1's
+// per-round shrink: the mean rule leaves
+// n_{l+1} (den+num) < n_l den survivors (at most a 1/(1+eps) fraction); the
+// median rule (ADG-M) exactly floor(n_l / 2).  A round that
+// breaks it is a bug (err 7 -> PGC_EINTERNAL), which also bounds T by T0.
+// (per_round keeps the first kMaxRoundStats rounds' (|U_l|, S_l, |R_l|): a
+// diagnostic record, never read by the method.)
+__global__ void k_adg_finalize(int l, int rule, uint32_t num, uint32_t den, State* st,
+                               long long* per_round, int32_t* ord_cnt, int64_t cap) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (st->done) return;
   const int nR = st->nR;
@@ -857,6 +864,12 @@ __global__ void k_adg_finalize(int l, State* st, long long* per_round, int32_t* 
   st->nOrdR = 0;
   const long long nU1 = st->nU - nR;
   if (st->nUnext != nU1) st->err = 2;
+  const bool shrink_ok =
+      rule == kRuleMedian
+          ? nU1 == st->nU / 2
+          : (unsigned __int128)nU1 * ((unsigned long long)den + num) <
+                (unsigned __int128)st->nU * den;
+  if (!shrink_ok) st->err = 7;
   st->S = st->S - st->sumDR - st->cut;
   st->nU = nU1;
   st->T = l;
@@ -867,7 +880,31 @@ __global__ void k_adg_finalize(int l, State* st, long long* per_round, int32_t* 
   st->nLight = 0;
   st->nUnext = 0;
   st->nChunks = 0;
-  if (nU1 == 0) st->done = 1;
+  if (nU1 == 0 || st->err) st->done = 1;
+}
+
+// T0 = min{t : (den+num)^t >= n den^t}, the exact round bound implied by
+// Lemma 1's per-round shrink, for the host
+// loop guard; ADG-M: floor(log2 n) + 1.  Exact: ceil(n (den/(den+num))^t)
+// is tracked as a rational bound in 128-bit, rounding up at every step
+// (each round leaves an integer count of survivors).
+static long long round_bound(int64_t n, uint32_t num, uint32_t den, int rule) {
+  if (n <= 0) return 0;
+  if (rule == kRuleMedian) {
+    long long t = 0;
+    for (int64_t x = n; x > 0; x >>= 1) ++t;
+    return t;
+  }
+  // survivors after t rounds <= s_t with s_0 = n, s_{t+1} = max integer s with
+  // s (den+num) < s_t den, i.e. s_{t+1} = ceil(s_t den / (den+num)) - 1
+  long long t = 0;
+  unsigned __int128 s = (unsigned __int128)n;
+  const unsigned __int128 a = den, b = (unsigned __int128)den + num;
+  while (s > 0) {
+    s = (s * a + b - 1) / b - 1;
+    ++t;
+  }
+  return t;
 }
 
 // JP Part 1 work lists for an arbitrary key (pgc_jp_color): every vertex is
@@ -934,7 +971,7 @@ static int launch_update(Ctx& c, const Arc<MODE>& A, const int32_t* Uin = nullpt
                                                         ratio));
   if constexpr (MODE != 2 && MODE != 4) {
     if (ratio > 0) {
-      static bool attr = false;  // per process: the attribute is per function
+      bool& attr = once_flag(c.dev, MODE);  // the attribute is per function AND device
       if (!attr) {
         PGC_CUDA(cudaFuncSetAttribute(k_update_heavy_f<MODE>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -989,6 +1026,7 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
   }
   int l = 1;
   const int batch = c.tune.rounds_per_sync < 1 ? 1 : c.tune.rounds_per_sync;
+  const long long T0 = round_bound(c.n, num, den, rule);
   for (;;) {
     for (int j = 0; j < batch; ++j, ++l) {
       const int32_t* Uin = l == 1 ? nullptr : c.U[l & 1];
@@ -1027,13 +1065,16 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
         if (int e = launch_update(c, Arc<0>{l, seed, round, c.D, c.rs, atom}, Uin)) return e;
       }
       PGC_LAUNCH(c, kGAdgOther, "k_adg_finalize",
-                 k_adg_finalize<<<1, 32, 0, c.st>>>(l, c.state, c.per_round,
+                 k_adg_finalize<<<1, 32, 0, c.st>>>(l, rule, num, den, c.state, c.per_round,
                                                     c.hist1 + c.lay.range_cap, c.lay.range_cap));
     }
     if (int e = sync_state(c)) return e;
+    if (c.h_state->err == 7)
+      return fail(4, "ADG round %d broke Lemma 1's per-round shrink (PAPER.md:761-771)", c.h_state->T);
     if (c.h_state->err) return fail(4, "ADG internal invariant failed (code %d)", c.h_state->err);
     if (c.h_state->done) break;
-    if ((int64_t)l > c.n + 2) return fail(4, "ADG did not terminate within n rounds");
+    if ((long long)l - 1 >= T0)  // rounds 1..l-1 ran, U is not empty: T > T0
+      return fail(4, "ADG did not terminate within T0 = %lld rounds (Lemma 1)", T0);
   }
   return 0;
 }

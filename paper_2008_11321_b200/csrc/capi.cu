@@ -34,18 +34,31 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// Resident blocks per SM of a kernel (cached per thread; a handful of entries).
-int occupancy_cached(const void* kernel, int block, size_t smem) {
-  struct E { const void* k; int block; size_t smem; int occ; };
+// Resident blocks per SM of a kernel on a device (cached per thread; a
+// handful of entries).
+int occupancy_cached(int dev, const void* kernel, int block, size_t smem) {
+  struct E { int dev; const void* k; int block; size_t smem; int occ; };
   static thread_local std::vector<E> cache;
   for (const E& e : cache)
-    if (e.k == kernel && e.block == block && e.smem == smem) return e.occ;
+    if (e.dev == dev && e.k == kernel && e.block == block && e.smem == smem) return e.occ;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem) != cudaSuccess ||
-      occ < 1)
+      occ < 1) {
+    cudaGetLastError();
     occ = 1;
-  cache.push_back({kernel, block, smem, occ});
+  }
+  cache.push_back({dev, kernel, block, smem, occ});
   return occ;
+}
+
+bool& once_flag(int dev, int slot) {
+  static thread_local bool flags[kMaxDevices][kOnceSlots] = {};
+  static thread_local bool spill = false;  // out-of-range ordinals: never "done"
+  if (dev < 0 || dev >= kMaxDevices || slot < 0 || slot >= kOnceSlots) {
+    spill = false;
+    return spill;
+  }
+  return flags[dev][slot];
 }
 
 Layout make_layout(int64_t n, int64_t nnz) {
@@ -120,8 +133,11 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.col = g->col_indices;
   c.st = (cudaStream_t)stream;
   c.tune = g_tune;
+  cudaGetLastError();  // a stale error of earlier, unrelated work must not be blamed on this call
   int dev = 0;
   PGC_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(PGC_EINTERNAL, "device ordinal %d out of range", dev);
+  c.dev = dev;
   PGC_CUDA(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, dev));
   c.lay = make_layout(g->n, g->nnz);
   char* b = (char*)ws;
@@ -143,7 +159,8 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.rec = (int4*)(b + c.lay.rec);
   c.filt = (uint32_t*)(b + c.lay.filt);
   c.lrec = c.rec;  // ADG and JP never use their records at the same time
-  if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocDefault));
+  // pinned host mirror of State (portable: usable from every device's streams)
+  if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocPortable));
   c.h_state = g_hstate;
   if (g_trace_grab && g_trace_n == g->n) {
     c.trace_grab = g_trace_grab;
@@ -153,39 +170,47 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
 }
 
 // Per-group device timing: one event pair around every launch when enabled.
-// Events are pooled per thread and reused across calls.
+// Events are pooled per thread AND device (an event belongs to the device it
+// was created on) and reused across calls.
 struct EventLog {
   bool on = false;
-  cudaStream_t st = nullptr;
   std::vector<cudaEvent_t> pool;
   size_t used = 0;
   std::vector<int> groups;
-  cudaEvent_t get() {
+  cudaEvent_t total[2] = {nullptr, nullptr};
+  cudaError_t get(cudaEvent_t* e) {
     if (used == pool.size()) {
-      cudaEvent_t e = nullptr;
-      cudaEventCreate(&e);
-      pool.push_back(e);
+      cudaEvent_t x = nullptr;
+      if (cudaError_t r = cudaEventCreate(&x)) return r;
+      pool.push_back(x);
     }
-    return pool[used++];
+    *e = pool[used++];
+    return cudaSuccess;
   }
-  void reset(bool on_, cudaStream_t s) {
+  void reset(bool on_) {
     on = on_;
-    st = s;
     used = 0;
     groups.clear();
   }
 };
-static thread_local EventLog g_log;
-static thread_local cudaEvent_t g_total[2] = {nullptr, nullptr};
+static thread_local EventLog g_logs[kMaxDevices];
 
-void log_begin(Ctx& c, int group) {
-  if (!g_log.on) return;
-  g_log.groups.push_back(group);
-  cudaEventRecord(g_log.get(), c.st);
+int log_begin(Ctx& c, int group) {
+  EventLog& L = g_logs[c.dev];
+  if (!L.on) return 0;
+  L.groups.push_back(group);
+  cudaEvent_t e;
+  PGC_CUDA(L.get(&e));
+  PGC_CUDA(cudaEventRecord(e, c.st));
+  return 0;
 }
-void log_end(Ctx& c) {
-  if (!g_log.on) return;
-  cudaEventRecord(g_log.get(), c.st);
+int log_end(Ctx& c) {
+  EventLog& L = g_logs[c.dev];
+  if (!L.on) return 0;
+  cudaEvent_t e;
+  PGC_CUDA(L.get(&e));
+  PGC_CUDA(cudaEventRecord(e, c.st));
+  return 0;
 }
 
 int sync_state(Ctx& c) {
@@ -195,15 +220,17 @@ int sync_state(Ctx& c) {
   return 0;
 }
 
-static void call_begin(Ctx& c) {
-  g_log.reset(c.tune.timing != 0, c.st);
-  if (g_log.on) {
-    if (!g_total[0]) {
-      cudaEventCreate(&g_total[0]);
-      cudaEventCreate(&g_total[1]);
+static int call_begin(Ctx& c) {
+  EventLog& L = g_logs[c.dev];
+  L.reset(c.tune.timing != 0);
+  if (L.on) {
+    if (!L.total[0]) {
+      PGC_CUDA(cudaEventCreate(&L.total[0]));
+      PGC_CUDA(cudaEventCreate(&L.total[1]));
     }
-    cudaEventRecord(g_total[0], c.st);
+    PGC_CUDA(cudaEventRecord(L.total[0], c.st));
   }
+  return 0;
 }
 
 // Called after the call's final synchronisation.
@@ -219,19 +246,21 @@ static void call_end(Ctx& c, int rounds, int colors, long long sum_active,
   g_stats.kernel_launches = c.launches;
   g_stats.host_syncs = c.syncs;
   g_stats.sim_col_passes = 0;
+  g_stats.jp_levels = c.jp_levels;
   float t[kNumGroups] = {-1.f, -1.f, -1.f, -1.f, -1.f, -1.f};
   float total = -1.f;
-  if (g_log.on) {
-    cudaEventRecord(g_total[1], c.st);
-    cudaEventSynchronize(g_total[1]);
+  EventLog& L = g_logs[c.dev];
+  if (L.on && cudaEventRecord(L.total[1], c.st) == cudaSuccess &&
+      cudaEventSynchronize(L.total[1]) == cudaSuccess) {
     for (int g = 0; g < kNumGroups; ++g) t[g] = 0.f;
-    for (size_t i = 0; i < g_log.groups.size(); ++i) {
+    for (size_t i = 0; i < L.groups.size(); ++i) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, g_log.pool[2 * i], g_log.pool[2 * i + 1]);
-      t[g_log.groups[i]] += ms;
+      cudaEventElapsedTime(&ms, L.pool[2 * i], L.pool[2 * i + 1]);
+      t[L.groups[i]] += ms;
     }
-    cudaEventElapsedTime(&total, g_total[0], g_total[1]);
+    cudaEventElapsedTime(&total, L.total[0], L.total[1]);
   }
+  cudaGetLastError();  // timing is best effort: never leave an error behind
   g_stats.t_select_ms = t[kGSelect];
   g_stats.t_update_ms = t[kGUpdate];
   g_stats.t_adg_other_ms = t[kGAdgOther];
@@ -269,7 +298,7 @@ int pgc_adg_order_mode(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, i
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   if (int e = adg_run(c, eps_num, eps_den, 0, round_out,
                       update_mode == PGC_UPDATE_PULL ? kAdgPull : kAdgOnly, nullptr))
     return e;
@@ -286,7 +315,7 @@ int pgc_jp_color(const pgc_graph* g, const int32_t* round, uint64_t seed, int32_
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   c.round_key = round;
   c.seed = seed;
   if (int e = jp_setup_run(c, round, seed, color_out)) return e;
@@ -313,7 +342,7 @@ static int color_jp_adg_impl(const pgc_graph* g, uint32_t eps_num, uint32_t eps_
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
   c.col_ready = col_ready;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   if (int e = adg_run(c, eps_num, eps_den, seed, round_out, kAdgFused, color_out)) return e;
   if (h_round && g->n > 0) {
     PGC_CUDA(cudaEventRecord(adg_done, c.st));
@@ -349,7 +378,7 @@ int pgc_adg_m_order(const pgc_graph* g, int32_t* round_out, int32_t* num_rounds,
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   if (int e = adg_run(c, 1, 1, 0, round_out, kAdgOnly, nullptr, kRuleMedian)) return e;
   *num_rounds = c.h_state->T;
   call_end(c, c.h_state->T, 0, c.h_state->sum_active, c.h_state->cross, 0, 0);
@@ -365,7 +394,7 @@ int pgc_color_jp_adg_m(const pgc_graph* g, uint64_t seed, int32_t* round_out, in
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   if (int e = adg_run(c, 1, 1, seed, round_out, kAdgFused, color_out, kRuleMedian)) return e;
   const int T = c.h_state->T;
   const long long sum_active = c.h_state->sum_active;
@@ -390,7 +419,7 @@ int pgc_color_jp_adg_o(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den, i
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   if (int e = adg_run(c, eps_num, eps_den, 0, round_out, kAdgFusedO, color_out)) return e;
   const int T = c.h_state->T;
   const long long sum_active = c.h_state->sum_active;
@@ -417,7 +446,7 @@ int pgc_jp_baseline(const pgc_graph* g, int kind, uint64_t seed, int32_t* color_
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   int32_t* key = c.U[0];  // free until the bulk split (after the order)
   if (int e = baseline_key_run(c, kind, key)) return e;
   c.round_key = nullptr;  // U0 is reused by the bulk split: the bulk watches by hash alone
@@ -441,7 +470,7 @@ int pgc_color_dec_adg_itr(const pgc_graph* g, uint32_t eps_num, uint32_t eps_den
   if (int e = check_ws(g, workspace, workspace_bytes)) return e;
   Ctx c;
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
-  call_begin(c);
+  if (int e = call_begin(c)) return e;
   if (int e = adg_run(c, eps_num, eps_den, seed, round_out, kAdgOnly, color_out)) return e;
   const int T = c.h_state->T;
   const long long sum_active = c.h_state->sum_active;
@@ -580,6 +609,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"update_atom", 0, 1, nullptr, &g_tune.update_atom},
       {"fuse_init", 0, 1, nullptr, &g_tune.fuse_init},
       {"top_list", 0, 1, nullptr, &g_tune.top_list},
+      {"levels", 0, 1, nullptr, &g_tune.levels},
       {"core_arc_cap", 0, 1ll << 40, &g_tune.core_arc_cap, nullptr},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };

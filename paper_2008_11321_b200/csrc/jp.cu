@@ -1716,11 +1716,63 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
   if (lane == 0 && kmax) atomicMax(&st->K, kmax);
 }
 
+// J, the depth of JP (diagnostics; pgc_set_tuning("levels", 1)): level[v] =
+// 1 + max level over pred(v) (roots: 1), J = max level = the number of
+// vertices on a longest path of G_rho -- the quantity Alg. 3's depth is written
+// in (Lemma 6, 1192-1294).  A dataflow over the priority
+// order after JP has finished (every pred list is final): warp per vertex,
+// tickets in priority order (deadlock-free: the highest-priority unfinished
+// vertex is held by a warp whose preds are all finished, or not yet handed
+// out, and then every warp is free), each lane polls its preds' levels (0 =
+// not yet).  Core positions p < core_n hold u16 core positions in their P slot
+// (k_core_lists), mapped back to ids through rec[].  lvl[] (n ints) starts at 0.
+__global__ void k_jp_levels(const int4* __restrict__ rec, const int32_t* __restrict__ P,
+                            int32_t* lvl, State* st, unsigned long long watchdog_ns) {
+  const int lane = lane_id();
+  const int no = st->n_order, NC = st->core_n;
+  const unsigned long long deadline = globaltimer() + watchdog_ns;
+  int jmax = 0;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&st->ticket_levels, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= no) break;
+    const int4 r = rec[t];
+    const int np = r.y;
+    const int64_t pb = lo_hi(r.z, r.w);
+    int mx = 0;
+    bool stall = false;
+    for (int i0 = 0; i0 < np && !stall; i0 += 32) {
+      const int i = i0 + lane;
+      int u = -1;
+      if (i < np)
+        u = t < NC ? rec[reinterpret_cast<const uint16_t*>(P + pb)[i]].x : P[pb + i];
+      int x = u >= 0 ? ld_relaxed(lvl + u) : 1;
+      while (__any_sync(0xffffffffu, x == 0)) {
+        if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
+          stall = true;
+          break;
+        }
+        __nanosleep(64);
+        if (x == 0) x = ld_relaxed(lvl + u);
+      }
+      mx = max(mx, x);
+    }
+    if (stall) break;
+    mx = warp_max(mx);
+    if (lane == 0) st_relaxed(lvl + r.x, mx + 1);
+    jmax = max(jmax, mx + 1);
+  }
+  if (lane == 0 && jmax) atomicMax(&st->jp_levels, jmax);
+}
+
 // K starts at 1 for a nonempty graph: the highest-priority vertex has no pred
 // and gets color 1 (isolated vertices and roots are colored outside the JP kernels).
 __global__ void k_jp_reset(State* st, int nonempty) {
   st->ticket_heavy = 0;
   st->ticket_light = 0;
+  st->ticket_levels = 0;
+  st->jp_levels = nonempty;  // isolated vertices and roots are level 1
   st->nheavy = 0;
   st->K = nonempty;
   st->core_n = 0;
@@ -1729,11 +1781,14 @@ __global__ void k_jp_reset(State* st, int nonempty) {
 
 // Largest cluster size (power of two <= want) that k_jp_core can launch with
 // `smem` dynamic bytes; 0 if none.
-static int core_cluster_size(int want, size_t smem) {
-  static thread_local int attr_done = 0;
+static int core_cluster_size(int dev, int want, size_t smem) {
+  bool& attr_done = once_flag(dev, 8);  // per device: attributes belong to one device
   if (!attr_done) {
-    cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_done = 1;
+    if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess)
+      attr_done = true;
+    else
+      cudaGetLastError();  // then only portable sizes (<= 8) are found below
   }
   if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
@@ -1792,7 +1847,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
         int want = c.tune.core_ctas > 0 ? c.tune.core_ctas
                                         : (int)(by_arcs > by_verts ? by_arcs : by_verts);
         want = pow2_floor(want < 1 ? 1 : (want > 16 ? 16 : want));
-        C = core_cluster_size(want, core_smem);
+        C = core_cluster_size(c.dev, want, core_smem);
       }
       if (C == 0) {
         PGC_CUDA(cudaMemsetAsync(&c.state->core_n, 0, sizeof(int), c.st));
@@ -1819,10 +1874,8 @@ int jp_color_run(Ctx& c, int32_t* color) {
       // the running kernels: a side-stream kernel the core waits on (the list
       // rewrite) must be loaded before the core starts, or the first call
       // deadlocks until the watchdog.  Querying the attributes loads them.
-      static thread_local bool loaded[64] = {};  // per device: modules are per context
-      int dev = 0;
-      PGC_CUDA(cudaGetDevice(&dev));
-      if (dev < 0 || dev >= 64 || !loaded[dev]) {
+      bool& loaded = once_flag(c.dev, 9);  // per device: modules are per context
+      if (!loaded) {
         cudaFuncAttributes fa;
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_pos));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_lists));
@@ -1834,7 +1887,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_reduce));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_tmp));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scan_down));
-        if (dev >= 0 && dev < 64) loaded[dev] = true;
+        loaded = true;
       }
     }
     // the core's list rewrite: before the core, or beside it with per-vertex
@@ -1903,13 +1956,10 @@ int jp_color_run(Ctx& c, int32_t* color) {
       // the list rewrite, the rest of the order and the bulk split on the side
       // stream; join before the bulk
       // per thread and device (streams and events belong to one device)
-      static thread_local cudaStream_t sides[64] = {};
-      static thread_local cudaEvent_t evs[64][2] = {};
-      int dev = 0;
-      PGC_CUDA(cudaGetDevice(&dev));
-      if (dev < 0 || dev >= 64) return fail(4, "device ordinal %d out of range", dev);
-      cudaStream_t& side = sides[dev];
-      cudaEvent_t* ev = evs[dev];
+      static thread_local cudaStream_t sides[kMaxDevices] = {};
+      static thread_local cudaEvent_t evs[kMaxDevices][2] = {};
+      cudaStream_t& side = sides[c.dev];
+      cudaEvent_t* ev = evs[c.dev];
       if (!side) {
         PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) PGC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
@@ -1946,7 +1996,15 @@ int jp_color_run(Ctx& c, int32_t* color) {
                      (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
     }
   }
+  if (c.tune.levels && n_order > 0) {
+    // lvl[] in D: free once the bulk (its split's prefix counts) has finished
+    PGC_CUDA(cudaMemsetAsync(c.D, 0, 4 * (size_t)c.n, c.st));
+    PGC_LAUNCH(c, kGJp, "k_jp_levels",
+               k_jp_levels<<<c.nsm * 8, 256, 0, c.st>>>(
+                   c.rec, c.P, c.D, c.state, (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
+  }
   if (int e = sync_state(c)) return e;
+  c.jp_levels = c.tune.levels ? c.h_state->jp_levels : 0;
   if (c.h_state->err == 9)
     return fail(4, "JP core stalled: no progress within %d ms (watchdog)", c.tune.jp_watchdog_ms);
   if (c.h_state->err == 8)

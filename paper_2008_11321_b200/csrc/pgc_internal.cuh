@@ -22,6 +22,11 @@ constexpr int kBucketTarget = PGC_BUCKET_TARGET;  // mean bucket occupancy targe
 constexpr int kScanTile = 4096;       // elements per block in the device-wide scan
 
 // Device-resident scalars of one call.  Lives at the head of the workspace.
+// Counters that many blocks or warps hit with atomics sit on their own
+// 128-byte lines (alignas): one L2 slice serves one line, so two hot counters
+// sharing a line would make that slice the bottleneck of both (the JP bulk's
+// light and heavy tickets and K were one line in round 1: 91 % tag rate on
+// the max slice vs 52 % mean).
 struct State {
   // ADG round state (Alg. 1)
   unsigned long long S;        // sum_{v in U} D[v] for the current round
@@ -30,16 +35,21 @@ struct State {
   int err;                     // internal invariant failure code (0 = none)
   int T;                       // rounds completed
   int pad0;
-  // counters of the current round, reset by k_adg_finalize
-  unsigned long long sumDR;    // sum of D over R_l
-  unsigned long long cut;      // arcs from R_l into U_{l+1}
-  int nR, nLight, nUnext, nChunks;
-  int nOrdR;                   // non-isolated vertices of R_l (the priority order's round histogram)
-  int top_n;                   // length of the saved top-round list (k_top_save; 0 = none)
   // totals
   long long sum_active;        // sum_l |U_l|
   unsigned long long cross;    // X
+  // counters of the current round, reset by k_adg_finalize: the compaction
+  // reservations of k_adg_select (one atomic per block step each)
+  alignas(128) int nChunks;
+  int nLight, nUnext;
+  // ... the selection's block sums
+  alignas(128) unsigned long long sumDR;  // sum of D over R_l
+  int nR;
+  int nOrdR;                   // non-isolated vertices of R_l (the priority order's round histogram)
+  // ... UPDATE's block sums
+  alignas(128) unsigned long long cut;    // arcs from R_l into U_{l+1}
   unsigned long long pred_arcs;  // sum_v |pred(v)|
+  alignas(128) int top_n;      // length of the saved top-round list (k_top_save; 0 = none)
   // priority-order sort
   int rmin, rmax;              // range of the first priority key
   int nbuckets;                // buckets in use
@@ -51,13 +61,16 @@ struct State {
   int sorted_bot;              // split order: placed by the bottom part
   // JP
   int core_n;                  // |core| = length of the priority prefix colored by k_jp_core
-  int K;
   long long core_arcs;         // sum of |pred| over the core
   int nheavy;                  // bulk vertices with |pred| > kLightPredMax
   int nlight;                  // bulk vertices with 1 <= |pred| <= kLightPredMax
-  int ticket_heavy, ticket_light;  // next bulk tickets per class
+  int jp_levels;               // J, when the levels knob is on (k_jp_levels)
+  alignas(128) int K;          // max color (atomicMax per warp)
+  alignas(128) int ticket_heavy;  // next bulk tickets per class
+  alignas(128) int ticket_light;
+  alignas(128) int ticket_levels;  // k_jp_levels' tickets
   // ADG-M radix select of the ceil(|U|/2)-th smallest key (D[v] << 32) | v
-  unsigned long long msel_key;   // key bits found so far (the full key after the last pass)
+  alignas(128) unsigned long long msel_key;  // key bits found so far (the full key after the last pass)
   unsigned long long msel_mask;  // which key bits msel_key determines
   long long msel_rank;           // rank still to find among keys matching msel_key (1-based)
   int msel_done;                 // blocks finished in the current pass (last-block pick)
@@ -95,6 +108,8 @@ struct Tuning {
   int top_list = 1;               // JP-ADG: ADG saves the top rounds' list for the split order
   int fuse_init = 1;              // ADG: round 1's selection also initialises D, rs, round, color
   int update_atom = 1;            // ADG round 1: one atomic per arc instead of gather + RED (Arc::atom)
+  int levels = 0;                 // JP: also compute J = the longest path of G_rho (k_jp_levels;
+                                  // diagnostics, off in timed runs)
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
@@ -108,6 +123,8 @@ enum Group { kGSelect = 0, kGUpdate = 1, kGAdgOther = 2, kGOrder = 3, kGCore = 4
 struct Ctx {
   int launches = 0;  // kernels launched by this call
   int syncs = 0;     // host synchronisations by this call
+  int dev = 0;       // the device of this call (cudaGetDevice at entry)
+  int jp_levels = 0; // J of the last JP (levels knob), else 0
   int64_t n, nnz;
   const int64_t* off;
   const int32_t* col;
@@ -177,9 +194,16 @@ int check_graph_run(Ctx& c, int64_t* bad_vertex);
 // error reporting helper implemented in capi.cu
 int fail(int code, const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* where);
-// per-group event timing (no-ops unless timing is enabled); capi.cu
-void log_begin(Ctx& c, int group);
-void log_end(Ctx& c);
+// per-group event timing (no-ops unless timing is enabled; a failed event
+// record returns PGC_ECUDA naming the event, not the next kernel); capi.cu
+int log_begin(Ctx& c, int group);
+int log_end(Ctx& c);
+// A per-thread, per-device "done once" flag (function attributes such as the
+// dynamic shared memory opt-in apply to the device they were set on, so a
+// thread that drives two GPUs must set them on each).  slot < kOnceSlots.
+constexpr int kOnceSlots = 16;
+constexpr int kMaxDevices = 64;
+bool& once_flag(int dev, int slot);
 // copy State to the pinned host mirror and wait for the stream; capi.cu
 int sync_state(Ctx& c);
 
@@ -187,11 +211,11 @@ int sync_state(Ctx& c);
 // account it and time it in `group`.
 #define PGC_LAUNCH(c, group, name, ...)                         \
   do {                                                          \
-    ::pgc::log_begin(c, group);                                 \
+    if (int le_ = ::pgc::log_begin(c, group)) return le_;       \
     __VA_ARGS__;                                                \
     cudaError_t e_ = cudaGetLastError();                        \
     if (e_ != cudaSuccess) return ::pgc::cuda_fail(e_, name);   \
-    ::pgc::log_end(c);                                          \
+    if (int le_ = ::pgc::log_end(c)) return le_;                \
     ++(c).launches;                                             \
   } while (0)
 
@@ -418,12 +442,13 @@ __device__ __forceinline__ T block_sum(T x, T* sm) {
   return t;  // valid in thread 0
 }
 
-// Grid of exactly one wave: SMs x resident blocks of `kernel` (cached per kernel).
-// Grid-stride kernels sized this way never run a second, serialised wave.
-int occupancy_cached(const void* kernel, int block, size_t smem);  // capi.cu
+// Grid of exactly one wave: SMs x resident blocks of `kernel` (cached per
+// kernel and device).  Grid-stride kernels sized this way never run a second,
+// serialised wave.
+int occupancy_cached(int dev, const void* kernel, int block, size_t smem);  // capi.cu
 template <typename K>
 inline int wave_grid(const Ctx& c, K kernel, int block, size_t smem = 0) {
-  return c.nsm * occupancy_cached((const void*)kernel, block, smem);
+  return c.nsm * occupancy_cached(c.dev, (const void*)kernel, block, smem);
 }
 
 // ---- shared kernels (defined in adg.cu) -----------------------------------

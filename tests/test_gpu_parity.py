@@ -574,3 +574,73 @@ def test_serialised_kernels_do_not_deadlock():
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+# ---- J (JP levels, pgc_stats.jp_levels) against the oracle's level[] -------
+def _levels_gpu(fn, *args):
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    pgc.set_tuning("levels", 1)
+    try:
+        out = fn(*args)
+        torch.cuda.synchronize()
+        return out, pgc.last_stats()["jp_levels"]
+    finally:
+        pgc.set_tuning("levels", 0)
+
+
+@pytest.mark.parametrize("name", ["er", "rmat20", "grid"])
+def test_jp_levels_match_oracle(name):
+    # J = 1 + the longest chain of higher-priority neighbours:
+    # on rmat20 the core engine colors the top of the order (u16 lists), the bulk the rest
+    g = gg.config_graph(name)
+    pgc, off, col = dev(g)
+    num, den = gg.CONFIGS[name][1][0]
+    (rnd, color, T, K), J = _levels_gpu(pgc.color_jp_adg, off, col, num, den, 1)
+    r_or, _ = O.adg(g, num, den)
+    c_or, K_or, lvl, J_or = O.jp(g, r_or, 1, levels=True)
+    assert np.array_equal(color.cpu().numpy(), c_or)
+    assert J == J_or, (J, J_or)
+    # the levels pass changes no result and is off by default
+    pgc.color_jp_adg(off, col, num, den, 1)
+    assert pgc.last_stats()["jp_levels"] == 0
+
+
+def test_jp_levels_small_cases():
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    # clique K_n: J = n; star: 2; edgeless: 1; path at eps 1/2
+    for g in (gg.from_edges(50, [(i, j) for i in range(50) for j in range(i + 1, 50)]),
+              gg.from_edges(6, [(0, i) for i in range(1, 6)]),
+              gg.from_edges(5, []),
+              gg.from_edges(9, [(i, i + 1) for i in range(8)]),
+              gg.rmat(12, 16, seed=5)):
+        _, off, col = dev(g)
+        for num, den in [(1, 10), (1, 2)]:
+            (rnd, color, T, K), J = _levels_gpu(pgc.color_jp_adg, off, col, num, den, 3)
+            r_or, _ = O.adg(g, num, den)
+            _, _, _, J_or = O.jp(g, r_or, 3, levels=True)
+            assert J == J_or
+
+
+def test_jp_levels_generic_key():
+    # pgc_jp_color with JP-R (constant key) and the baselines: same J as the oracle
+    g = gg.rmat(13, 8, seed=9)
+    pgc, off, col = dev(g)
+    key = torch.zeros(g.n, dtype=torch.int32, device="cuda")
+    (color, K), J = _levels_gpu(pgc.jp_color, off, col, key, 11)
+    _, _, _, J_or = O.jp(g, np.zeros(g.n, dtype=np.int32), 11, levels=True)
+    assert J == J_or
+
+
+def test_second_device_if_present():
+    # per-device attributes, occupancy and side streams: one process driving two GPUs
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one GPU")
+    g = gg.rmat(14, 16, seed=2)
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    r_or, _ = O.adg(g, 1, 10)
+    c_or, _ = O.jp(g, r_or, 1)
+    for d in (0, 1, 0):
+        off = torch.from_numpy(g.off).to(f"cuda:{d}")
+        col = torch.from_numpy(g.col).to(f"cuda:{d}")
+        rnd, color, T, K = pgc.color_jp_adg(off, col, 1, 10, 1)
+        assert np.array_equal(color.cpu().numpy(), c_or)
