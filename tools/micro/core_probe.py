@@ -97,3 +97,28 @@ det = {"grab-ready_us": pct((A[sl, 0] - ready[sl]) / 1e3), "scan_us": pct((A[sl,
        "np": pct(npred_core[sl]), "fast_np": pct(npred_core[crit[~slow]]),
        "fast_scan_us": pct((A[crit[~slow], 1] - A[crit[~slow], 0]) / 1e3)}
 print(json.dumps(det))
+# slow hops, phase by phase (ns after ready), and whether the critical pred is local
+prev = np.full(n, -1, np.int64)
+prev[crit] = last[crit]
+cta = {}
+C = st["core_ctas"]
+posc = np.full(n, -1, np.int64)
+posc[core] = np.arange(NC)
+def owner(v):
+    p = posc[v]
+    return (p // 32) % C
+loc = np.array([owner(v) == owner(prev[v]) if prev[v] >= 0 else True for v in crit])
+ph = {}
+for nm, k in (("tail_in", 4), ("tail_seen", 5), ("found", 6), ("pub", 7), ("last_pass", 3), ("scanned", 1)):
+    x = A[sl, k] - ready[sl]
+    ph[nm] = pct(x[A[sl, k] != 0])
+ph["local_frac_slow"] = float(loc[slow].mean()) if slow.any() else 0
+ph["local_frac_fast"] = float(loc[~slow].mean())
+ph["fast_step_local_p50"] = float(np.median(step[~slow & loc])) if (~slow & loc).any() else 0
+ph["fast_step_remote_p50"] = float(np.median(step[~slow & ~loc])) if (~slow & ~loc).any() else 0
+gap = posc[crit] - posc[np.maximum(prev[crit], 0)]
+ph["gap_slow"] = pct(gap[slow])
+ph["gap_fast"] = pct(gap[~slow])
+ph["pos_slow"] = pct(posc[crit[slow]])
+ph["pos_all"] = pct(posc[crit])
+print(json.dumps(ph))
