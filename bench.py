@@ -400,11 +400,19 @@ def run_pgc(args):
             upd_arcs = pull_arcs
     peak, peak_kind = peak_gbs()
     t_upd = gmean["t_update_ms"]
+    small = bool(st.get("small_path", 0))
+    if small:
+        # one persistent kernel runs the whole path (csrc/small.cu): its dominant
+        # (only) kernel is charged the whole path's 8(d) bytes
+        t_upd = gmean["t_select_ms"]
+        upd_bytes = path_bytes
     achieved = upd_bytes / (t_upd * 1e-3) / 1e9
     workload = (f"{args.config}-{args.method}" if (baseline or decitr or adgonly) else
                 f"{args.config}-adgm" if median else
                 f"{args.config}-adgo-eps{num}/{den}" if sortedR else f"{args.config}-eps{num}/{den}")
     traffic, traffic_src = measured_traffic(workload)
+    if small:   # the profiles' UPDATE traffic does not apply: the step is one other kernel
+        traffic, traffic_src = measured_traffic(workload + "-small")
     # the builder's uniform-target probe of the gather+RED mix (context, not a ceiling:
     # UPDATE beats it because hub targets hit in L2)
     ra = None
@@ -444,13 +452,18 @@ def run_pgc(args):
         "timing": step_stats(per_step),
         "colors": K, "rounds": T, "jp_levels": J, "cross_edges": X, "sum_active": sum_active,
         "core_vertices": st["core_vertices"], "core_ctas": st["core_ctas"],
+        "small_path": int(st.get("small_path", 0)),
         "roofline": {"bound": "hbm",
-                     "kernel": "ADG UPDATE with fused JP Part 1 (k_update_light + k_update_heavy + "
-                               "k_update_heavy_f, every round of one step)",
+                     "kernel": ("k_small_jp_adg: the whole JP-ADG in ONE persistent cooperative "
+                                "kernel (%d grid barriers: 1 + 2T + J)" % (1 + 2 * T + (J or 0))
+                                if small else
+                                "ADG UPDATE with fused JP Part 1 (k_update_light + k_update_heavy + "
+                                "k_update_heavy_f, every round of one step)"),
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes": upd_bytes, "ms_per_launch": t_upd,
-                     "bytes_model": ("SURVEY 8(d) rows a4: 8 nnz + 8X, plus the 16n per-removed-"
+                     "bytes_model": (path_model if small else
+                                     "SURVEY 8(d) rows a4: 8 nnz + 8X, plus the 16n per-removed-"
                                      "vertex term" if args.method != "adg-pull" else
                                      "pull: 8 bytes per rescanned arc + 8 per survivor-round"),
                      "path": {"bytes": path_bytes, "model": path_model,

@@ -98,13 +98,20 @@ typedef struct pgc_stats {
                               G_rho (level[v] = 1 + max level over pred(v); Alg. 3's
                               depth term, Lemma 6 1192-1294).
                               Computed only with pgc_set_tuning("levels", 1) (an extra
-                              dataflow pass after JP; off in timed runs), else 0.      */
+                              dataflow pass after JP, off in timed runs; the one-kernel
+                              small-graph path counts its levels for free), else 0.  */
   /* Device time per kernel group, from CUDA events on the call's stream; all -1
    * unless pgc_set_tuning("timing", 1).  Groups: ADG select (a2/a3), ADG UPDATE
    * with fused JP Part 1 (a4/a7), other ADG kernels (init, finalize), the
    * priority-order sort, the JP core (selection, list rewrite, cluster kernel),
    * the JP bulk dataflow (a8/a9), and the whole call. */
   float t_select_ms, t_update_ms, t_adg_other_ms, t_order_ms, t_core_ms, t_jp_ms, t_total_ms;
+  int32_t small_path;      /* 1 if pgc_color_jp_adg ran as ONE persistent cooperative kernel
+                              (small / low-degree graphs: nnz <= tuning "small_max_arcs"
+                              and nnz <= "small_max_avg" * n; ADG rounds and JP levels
+                              separated by grid barriers, JP frontier-driven with
+                              count[] decrements, Alg. 3 l.1128-1133); same results.
+                              Its device time is reported in t_select_ms.          */
 } pgc_stats;
 
 /* Bytes of device workspace the entry points below need for a graph with n
@@ -269,7 +276,10 @@ const char* pgc_last_error(void);
  *   default 1), "fuse_init" 0/1 (ADG's first selection also initialises the
  *   per-vertex state; default 1), "top_list" 0/1 (JP-ADG: ADG keeps the top
  *   rounds' vertex list so the split order's top part skips a pass over n;
- *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns".
+ *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns",
+ *   "small_max_arcs" (pgc_color_jp_adg runs as one persistent kernel when
+ *   nnz <= this and nnz <= "small_max_avg" * n; 0 disables; defaults 2^24, 20),
+ *   "small_blocks_per_sm" 0..64 (that kernel's grid; 0 = occupancy).
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

@@ -49,7 +49,7 @@ class Stats(ctypes.Structure):
                 ("t_select_ms", ctypes.c_float), ("t_update_ms", ctypes.c_float),
                 ("t_adg_other_ms", ctypes.c_float), ("t_order_ms", ctypes.c_float),
                 ("t_core_ms", ctypes.c_float), ("t_jp_ms", ctypes.c_float),
-                ("t_total_ms", ctypes.c_float)]
+                ("t_total_ms", ctypes.c_float), ("small_path", ctypes.c_int32)]
 
 
 _vp, _i64, _u32, _u64, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_size_t

@@ -247,6 +247,7 @@ static void call_end(Ctx& c, int rounds, int colors, long long sum_active,
   g_stats.host_syncs = c.syncs;
   g_stats.sim_col_passes = 0;
   g_stats.jp_levels = c.jp_levels;
+  g_stats.small_path = c.small;
   float t[kNumGroups] = {-1.f, -1.f, -1.f, -1.f, -1.f, -1.f};
   float total = -1.f;
   EventLog& L = g_logs[c.dev];
@@ -343,6 +344,15 @@ static int color_jp_adg_impl(const pgc_graph* g, uint32_t eps_num, uint32_t eps_
   if (int e = make_ctx(c, g, workspace, cuda_stream)) return e;
   c.col_ready = col_ready;
   if (int e = call_begin(c)) return e;
+  if (small_path_wanted(c)) {  // the whole method in one launch (small.cu)
+    if (int e = small_run(c, eps_num, eps_den, seed, round_out, color_out)) return e;
+    if (h_round) PGC_CUDA(cudaMemcpyAsync(h_round, round_out, 4 * (size_t)g->n, cudaMemcpyDeviceToHost, c.st));
+    *num_rounds = c.h_state->T;
+    *num_colors = c.h_state->K;
+    call_end(c, c.h_state->T, c.h_state->K, c.h_state->sum_active, c.h_state->cross,
+             c.h_state->pred_arcs, 0);
+    return PGC_OK;
+  }
   if (int e = adg_run(c, eps_num, eps_den, seed, round_out, kAdgFused, color_out)) return e;
   if (h_round && g->n > 0) {
     PGC_CUDA(cudaEventRecord(adg_done, c.st));
@@ -611,6 +621,9 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"top_list", 0, 1, nullptr, &g_tune.top_list},
       {"levels", 0, 1, nullptr, &g_tune.levels},
       {"core_arc_cap", 0, 1ll << 40, &g_tune.core_arc_cap, nullptr},
+      {"small_max_arcs", 0, 1ll << 40, &g_tune.small_max_arcs, nullptr},
+      {"small_max_avg", 0, 1 << 30, nullptr, &g_tune.small_max_avg},
+      {"small_blocks_per_sm", 0, 64, nullptr, &g_tune.small_blocks_per_sm},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };
   for (const Key& k : keys)

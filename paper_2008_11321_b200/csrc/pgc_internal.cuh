@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstddef>
+#include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -110,6 +111,11 @@ struct Tuning {
   int update_atom = 1;            // ADG round 1: one atomic per arc instead of gather + RED (Arc::atom)
   int levels = 0;                 // JP: also compute J = the longest path of G_rho (k_jp_levels;
                                   // diagnostics, off in timed runs)
+  // JP-ADG on small / low-degree graphs: one persistent cooperative kernel
+  // (small.cu) when nnz <= small_max_arcs and nnz <= small_max_avg * n
+  long long small_max_arcs = 1ll << 24;    // 0 disables the one-kernel path
+  int small_max_avg = 20;
+  int small_blocks_per_sm = 0;             // blocks per SM of that kernel (0 = occupancy)
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
@@ -125,6 +131,7 @@ struct Ctx {
   int syncs = 0;     // host synchronisations by this call
   int dev = 0;       // the device of this call (cudaGetDevice at entry)
   int jp_levels = 0; // J of the last JP (levels knob), else 0
+  int small = 0;     // the one-kernel small-graph path ran (small.cu)
   int64_t n, nnz;
   const int64_t* off;
   const int32_t* col;
@@ -190,6 +197,9 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed, bool range_known, 
                  bool defer = false);
 int jp_color_run(Ctx& c, int32_t* color);
 int check_graph_run(Ctx& c, int64_t* bad_vertex);
+// JP-ADG in one persistent kernel for small / low-degree graphs (small.cu)
+bool small_path_wanted(const Ctx& c);
+int small_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int32_t* color);
 
 // error reporting helper implemented in capi.cu
 int fail(int code, const char* fmt, ...);
@@ -230,6 +240,27 @@ int sync_state(Ctx& c);
     cudaError_t e_ = cudaGetLastError();                          \
     if (e_ != cudaSuccess) return ::pgc::cuda_fail(e_, name);     \
   } while (0)
+
+// ---- checked builds ---------------------------------------------------------
+// compute-sanitizer is closed on the GPU pool, so the checked library
+// (tools/micro/build_checked.sh, -DPGC_CHECKED; never the product build)
+// turns every PGC_DCHECK into a device assertion: a failed bound or invariant
+// prints its file, line and values and traps (the call returns PGC_ECUDA).
+#ifdef PGC_CHECKED
+#define PGC_DCHECK(cond, a, b)                                                            \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("PGC_CHECKED failed: %s at %s:%d (%lld, %lld) block %d thread %d\n", #cond, \
+             __FILE__, __LINE__, (long long)(a), (long long)(b), (int)blockIdx.x,         \
+             (int)threadIdx.x);                                                           \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define PGC_DCHECK(cond, a, b) \
+  do {                         \
+  } while (0)
+#endif
 
 // ---- device helpers ---------------------------------------------------------
 // rho_R(v) = splitmix64(seed ^ v): the first output of a SplitMix64 generator

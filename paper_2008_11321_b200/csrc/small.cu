@@ -1,0 +1,548 @@
+// small.cu -- JP-ADG for small and low-degree graphs in ONE persistent
+// cooperative kernel (the latency path).
+//
+// The multi-kernel path (adg.cu + jp.cu) launches ~4 kernels per ADG round,
+// syncs the host every 8 rounds, and spends ~10 launches and 2 host syncs on
+// the priority order and the core/bulk split.  On graphs whose whole step is a
+// few hundred microseconds of work (ER 16K: 0.26 M arcs, the 2048^2 grid:
+// 12 M arcs, J = 16) those launches ARE the step.  Here the whole method runs
+// in one launch, phases separated by grid barriers:
+//
+//   ADG (Algorithm 1), per round l -- 2 barriers:
+//     select   Dmax_l = floor((den+num) S_l / (den |U_l|)) (exact, 128-bit,
+//              readings Q1/Q2); R_l = {v in U_l : D[v] <= Dmax_l} (l.685),
+//              round[v] = l (688-689); R_l and U_{l+1} = U_l \ R_l (687)
+//              compacted with one atomic per warp; round 1 also initialises
+//              D[v] = deg(v), color[v] = 0 (a1, l.676-677).
+//     update   for v in R_l, u in N(v): u alive (round[u] == 0): D[u] -= 1
+//              (l.692-696), cut += 1.  JP Part 1 fused (PAPER.md:2259-2271,
+//              Alg. 3 l.1116-1121): count[v] = |pred(v)| = #alive neighbours
+//              (they get a later round) + #same-round neighbours u with
+//              h(u) > h(v) (Q8/Q10); count[v] == 0 puts v in the first
+//              frontier.  Warp-flattened over the arcs of 32 vertices.
+//     then every thread reads the round's block sums and carries
+//     S_{l+1} = S_l - sum_{R_l} D - cut_l, |U_{l+1}| (degree-sum caching,
+//     PAPER.md:2353-2365; Q5), and checks Lemma 1's per-round shrink exactly.
+//   JP (Algorithm 3) frontier by frontier -- 1 barrier
+//   per level, J levels (J = the JP DAG depth, reported with the levels knob):
+//     for v in the frontier: color[v] = GetColor = the smallest color no pred
+//     uses (l.1135-1138; 64-color bit-mask windows, OR-ed per owner lane in
+//     shared memory); then for every succ u (lower priority): count[u] -= 1,
+//     the vertex that takes it to 0 appends u to the next frontier (the Join
+//     of l.1128-1133).  The next frontier is colored after the barrier, so
+//     every pred color it reads is final.
+//
+// Results are the same integers as the multi-kernel path (the same Alg. 1 and
+// the same priority); the choice is a host heuristic on (n, nnz) with a knob
+// (pgc_set_tuning "small_max_arcs", "small_max_avg"; 0 disables the path).
+// Data that other blocks wrote in an earlier phase is read with ld.cg (the L1
+// is not coherent inside one kernel).
+#include <cooperative_groups.h>
+
+#include "pgc_internal.cuh"
+
+namespace pgc {
+
+namespace cg = cooperative_groups;
+
+constexpr int kSmallBlock = 512;
+constexpr int kSmallWarps = kSmallBlock / 32;
+constexpr int kSmallUnroll = 4;  // flattened arc steps per warp iteration (loads in flight)
+constexpr int kSelK = 4;         // selection: vertices per lane per step
+// counter ring: 4 slots (round or level mod 4) x fields, each field on its own
+// 128-byte line (16 x u64): the fields are hit by one atomic per warp
+constexpr int kSmallSlots = 4;
+enum { kSfUout = 0, kSfR = 1, kSfSumD = 2, kSfCut = 3, kSfPreds = 4, kSfF = 5, kSmallFields = 6 };
+constexpr int kSmallLine = 16;
+constexpr size_t kSmallCtrBytes = sizeof(unsigned long long) * kSmallSlots * kSmallFields * kSmallLine;
+
+struct SmallArgs {
+  int64_t n, nnz;
+  const int64_t* off;
+  const int32_t* col;
+  uint32_t num, den;
+  uint64_t seed;
+  int32_t* round;
+  int32_t* color;
+  int32_t* D;
+  int32_t* cnt;       // count[v] = |pred(v)|, then decremented by JP's Join
+  int32_t* U[2];      // U_l lists (U_1 = every vertex, implicit)
+  int32_t* R;         // R_l
+  int32_t* F[2];      // JP frontiers
+  unsigned long long* ctr;  // [kSmallSlots][kSmallFields][kSmallLine]
+  State* st;
+  long long* per_round;
+};
+
+__device__ __forceinline__ unsigned long long* sctr(unsigned long long* c, int slot, int f) {
+  return c + ((slot & (kSmallSlots - 1)) * kSmallFields + f) * kSmallLine;
+}
+__device__ __forceinline__ unsigned long long ld_ctr(const unsigned long long* p) {
+  return __ldcg(p);
+}
+
+// Per-warp append queues in shared memory: a list append is staged in the
+// warp's queue and the queue goes out with ONE global atomic per kSmallQ
+// entries (per-warp atomics on one list counter made that counter's L2 slice
+// the bottleneck of a phase: ~1 atomic per 32 vertices from every warp).
+// `fill` is warp-uniform; all 32 lanes call.
+constexpr int kSmallQ = 256;
+__device__ __forceinline__ void wq_flush(int32_t* q, int& fill, int32_t* out,
+                                         unsigned long long* counter, int64_t cap) {
+  __syncwarp();
+  if (fill) {
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(counter, (unsigned long long)fill);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    PGC_DCHECK(base + fill <= (unsigned long long)cap, base, fill);
+    for (int i = lane_id(); i < fill; i += 32) out[base + i] = q[i];
+  }
+  fill = 0;
+  __syncwarp();
+}
+__device__ __forceinline__ void wq_push(int32_t* q, int& fill, bool flag, int val, int32_t* out,
+                                        unsigned long long* counter, int64_t cap) {
+  const unsigned b = __ballot_sync(0xffffffffu, flag);
+  if (!b) return;
+  if (fill + __popc(b) > kSmallQ) wq_flush(q, fill, out, counter, cap);
+  if (flag) q[fill + __popc(b & lanemask_lt())] = val;
+  fill += __popc(b);
+}
+
+// Owner lane of flattened arc j: the largest lane s with start_s <= j (lanes
+// with no arcs share the next lane's start and are never picked for j < total).
+__device__ __forceinline__ int owner_of(int start, int j) {
+  int s = 0;
+#pragma unroll
+  for (int b = 16; b; b >>= 1) {
+    const int t = s + b;
+    const int st_t = __shfl_sync(0xffffffffu, start, t);
+    if (st_t <= j) s = t;
+  }
+  return s;
+}
+
+// Vertices per warp for a list of `cnt` vertices (a power of two in 1..32):
+// few enough that every warp of the grid gets work, so a phase costs a few
+// dependent L2 round trips rather than a long per-warp arc loop.
+__device__ __forceinline__ int verts_per_warp(long long cnt, long long nwarps) {
+  const long long per = (cnt + nwarps - 1) / nwarps;
+  int v = 1;
+  while (v < 32 && v < per) v <<= 1;
+  return v;
+}
+
+// Higher JP priority: <round, h> lexicographic (Q8, Q10; h is a bijection).
+__device__ __forceinline__ bool prio_gt(int ra, uint64_t ha, int rb, uint64_t hb) {
+  return ra > rb || (ra == rb && ha > hb);
+}
+
+#ifdef PGC_PROBE
+// phase timeline (probe builds only): block 0 thread 0 stamps %globaltimer
+// after every grid barrier and prints the phase lengths at the end
+#define SMALL_STAMP()                                                   \
+  do {                                                                  \
+    if (tid == 0 && nstamp < 512) stamps[nstamp++] = globaltimer();     \
+  } while (0)
+#else
+#define SMALL_STAMP() \
+  do {                \
+  } while (0)
+#endif
+
+__global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
+  cg::grid_group grid = cg::this_grid();
+#ifdef PGC_PROBE
+  unsigned long long stamps[512];
+  int nstamp = 0;
+#endif
+  __shared__ int s_acc[kSmallWarps][32];
+  __shared__ unsigned long long s_mask[kSmallWarps][32];
+  __shared__ unsigned long long s_red[kSmallWarps];
+  __shared__ int32_t s_q[kSmallWarps][2][kSmallQ];  // per-warp append queues
+  int32_t* q0 = s_q[threadIdx.x >> 5][0];
+  int32_t* q1 = s_q[threadIdx.x >> 5][1];
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const long long tid = (long long)blockIdx.x * kSmallBlock + threadIdx.x;
+  const long long nth = (long long)gridDim.x * kSmallBlock;
+  const long long gwarp = tid >> 5, nwarps = nth >> 5;
+  const int64_t n = a.n;
+  s_acc[warp][lane] = 0;
+  s_mask[warp][lane] = 0;
+  for (long long i = tid; i < kSmallSlots * kSmallFields * kSmallLine; i += nth) a.ctr[i] = 0;
+  if (tid == 0) a.st->K = 0;
+  grid.sync();
+  SMALL_STAMP();
+
+  // ---------------------------------------------------------------- ADG
+  unsigned long long S = (unsigned long long)a.nnz;  // S_1 = sum of degrees
+  long long nU = n, sum_active = 0;
+  unsigned long long cross = 0, preds_total = 0;
+  int l = 0, err = 0;
+  unsigned long long* f_first = sctr(a.ctr, 1, kSfF);  // JP level 1's frontier count
+  while (nU > 0) {
+    ++l;
+    // the round fields of round l+2's slot (last read in round l-2; the
+    // frontier field is JP's, reset per level)
+    if (tid < kSfF) *sctr(a.ctr, l + 2, (int)tid) = 0;
+    // select (a2/a3): exact threshold
+    const unsigned __int128 numer = (unsigned __int128)((unsigned long long)a.den + a.num) * S;
+    const unsigned long long denom = (unsigned long long)a.den * (unsigned long long)nU;
+    const unsigned __int128 q = numer / denom;
+    const long long dmax = q > (unsigned __int128)0x7fffffff ? 0x7fffffffLL : (long long)q;
+    const int32_t* Uin = l == 1 ? nullptr : a.U[l & 1];
+    int32_t* Uout = a.U[(l + 1) & 1];
+    unsigned long long sumD = 0;
+    // kSelK vertices per lane per step, loads first (the step is latency-bound)
+    int fr = 0, fu = 0;
+    for (long long base = gwarp * 32 * kSelK; base < nU; base += nwarps * 32 * kSelK) {
+      int v[kSelK], d[kSelK];
+      bool valid[kSelK];
+#pragma unroll
+      for (int k = 0; k < kSelK; ++k) {
+        const long long i = base + 32 * k + lane;
+        valid[k] = i < nU;
+        v[k] = valid[k] ? (Uin ? __ldcg(Uin + i) : (int)i) : 0;
+        PGC_DCHECK(!valid[k] || (v[k] >= 0 && v[k] < n), v[k], i);
+      }
+      if (l == 1) {
+        int64_t o0[kSelK], o1[kSelK];
+#pragma unroll
+        for (int k = 0; k < kSelK; ++k) {
+          o0[k] = valid[k] ? a.off[v[k]] : 0;
+          o1[k] = valid[k] ? a.off[v[k] + 1] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < kSelK; ++k) {
+          d[k] = (int)(o1[k] - o0[k]);
+          if (valid[k]) {
+            a.D[v[k]] = d[k];
+            a.color[v[k]] = 0;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kSelK; ++k) d[k] = valid[k] ? __ldcg(a.D + v[k]) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < kSelK; ++k) {
+        const bool sel = valid[k] && d[k] <= dmax;
+        if (valid[k] && (sel || l == 1)) a.round[v[k]] = sel ? l : 0;
+        if (sel) sumD += (unsigned long long)d[k];
+        wq_push(q0, fr, sel, v[k], a.R, sctr(a.ctr, l, kSfR), n);
+        wq_push(q1, fu, valid[k] && !sel, v[k], Uout, sctr(a.ctr, l, kSfUout), n);
+      }
+    }
+    wq_flush(q0, fr, a.R, sctr(a.ctr, l, kSfR), n);
+    wq_flush(q1, fu, Uout, sctr(a.ctr, l, kSfUout), n);
+    sumD = warp_sum(sumD);
+    if (lane == 0 && sumD) atomicAdd(sctr(a.ctr, l, kSfSumD), sumD);
+    grid.sync();
+    SMALL_STAMP();
+    // update (a4) with fused JP Part 1 (a7)
+    const long long nR = (long long)ld_ctr(sctr(a.ctr, l, kSfR));
+    unsigned long long cut = 0, preds = 0;
+    const int vpw = verts_per_warp(nR, nwarps);
+    int ff = 0;
+    for (long long base = gwarp * vpw; base < nR; base += nwarps * vpw) {
+      const long long i = base + lane;
+      const bool valid = lane < vpw && i < nR;
+      const int v = valid ? __ldcg(a.R + i) : 0;
+      PGC_DCHECK(!valid || (v >= 0 && v < n), v, i);
+      const int64_t o = valid ? a.off[v] : 0;
+      const int deg = valid ? (int)(a.off[v + 1] - o) : 0;
+      const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
+      int incl = deg;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, s);
+        if (lane >= s) incl += y;
+      }
+      const int start = incl - deg;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      for (int j0 = 0; j0 < total; j0 += 32 * kSmallUnroll) {
+        int own[kSmallUnroll], u[kSmallUnroll], ru[kSmallUnroll];
+#pragma unroll
+        for (int k = 0; k < kSmallUnroll; ++k) {
+          const int j = j0 + 32 * k + lane;
+          own[k] = owner_of(start, j);
+          const int64_t os = __shfl_sync(0xffffffffu, o, own[k]);
+          const int ss = __shfl_sync(0xffffffffu, start, own[k]);
+          PGC_DCHECK(j >= total || (os + (j - ss) >= 0 && os + (j - ss) < a.nnz), os + (j - ss), j);
+          u[k] = j < total ? __ldg(a.col + os + (j - ss)) : -1;
+          PGC_DCHECK(u[k] < n, u[k], j);
+        }
+#pragma unroll
+        for (int k = 0; k < kSmallUnroll; ++k) ru[k] = u[k] >= 0 ? __ldcg(a.round + u[k]) : -1;
+#pragma unroll
+        for (int k = 0; k < kSmallUnroll; ++k) {
+          const uint64_t hs = __shfl_sync(0xffffffffu, hv, own[k]);
+          bool pred = false;
+          PGC_DCHECK(ru[k] <= l, u[k], ru[k] * 1000000ll + l);  // no round from the future
+          if (ru[k] == 0) {  // alive: D[u] -= 1, u is a pred of v (later round)
+            atomicSub(a.D + u[k], 1);
+            ++cut;
+            pred = true;
+          } else if (ru[k] == l) {
+            pred = prio_hash(a.seed, (uint32_t)u[k]) > hs;
+          }
+          // one shared add per (owner, step): owners hold contiguous lanes (an
+          // atomic: the leaders of one owner in consecutive steps are different lanes)
+          const unsigned same = __match_any_sync(0xffffffffu, own[k]);
+          const int c = __popc(__ballot_sync(0xffffffffu, pred) & same);
+          if (c && lane == __ffs(same) - 1) atomicAdd(&s_acc[warp][own[k]], c);
+        }
+      }
+      __syncwarp();
+      const int p = s_acc[warp][lane];
+      s_acc[warp][lane] = 0;
+      if (valid) {
+        a.cnt[v] = p;
+        preds += (unsigned long long)p;
+      }
+      wq_push(q0, ff, valid && p == 0, v, a.F[1], f_first, n);
+      __syncwarp();
+    }
+    wq_flush(q0, ff, a.F[1], f_first, n);
+    cut = warp_sum(cut);
+    preds = warp_sum(preds);
+    if (lane == 0) {
+      if (cut) atomicAdd(sctr(a.ctr, l, kSfCut), cut);
+      if (preds) atomicAdd(sctr(a.ctr, l, kSfPreds), preds);
+    }
+    grid.sync();
+    SMALL_STAMP();
+    // finalize (every thread, same values): S_{l+1}, |U_{l+1}|, Lemma 1
+    const long long nU1 = (long long)ld_ctr(sctr(a.ctr, l, kSfUout));
+    const unsigned long long sumDR = ld_ctr(sctr(a.ctr, l, kSfSumD));
+    const unsigned long long cut_l = ld_ctr(sctr(a.ctr, l, kSfCut));
+    preds_total += ld_ctr(sctr(a.ctr, l, kSfPreds));
+    if (tid == 0 && l - 1 < kMaxRoundStats) {
+      a.per_round[3 * (l - 1) + 0] = nU;
+      a.per_round[3 * (l - 1) + 1] = (long long)S;
+      a.per_round[3 * (l - 1) + 2] = nR;
+    }
+    sum_active += nU;
+    cross += cut_l;
+    if (nR == 0) err = 1;
+    if (nU1 != nU - nR) err = 2;
+    if (!((unsigned __int128)nU1 * ((unsigned long long)a.den + a.num) <
+          (unsigned __int128)nU * a.den))
+      err = 7;  // Lemma 1
+    S = S - sumDR - cut_l;
+    nU = nU1;
+    if (err) break;
+  }
+
+  // ---------------------------------------------------------------- JP
+  int J = 0, kmax = 0;
+#ifdef PGC_CHECKED
+  // count[v] == |pred(v)| recomputed from the final rounds, vertex by vertex
+  for (long long v = tid; v < n && !err; v += nth) {  // (err is uniform)
+    int p = 0;
+    const int rv = __ldcg(a.round + v);
+    const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
+    for (int64_t e = a.off[v]; e < a.off[v + 1]; ++e) {
+      const int u = a.col[e];
+      p += prio_gt(__ldcg(a.round + u), prio_hash(a.seed, (uint32_t)u), rv, hv);
+    }
+    if (p != __ldcg(a.cnt + v)) {
+      printf("count mismatch v=%lld round=%d deg=%lld cnt=%d p=%d\n", v, rv,
+             (long long)(a.off[v + 1] - a.off[v]), __ldcg(a.cnt + v), p);
+      __trap();
+    }
+  }
+  grid.sync();  // JP's Join decrements count[]: the check must finish first
+  SMALL_STAMP();
+#endif
+  if (!err) {
+    long long nF = (long long)ld_ctr(f_first);
+    for (int j = 1; nF > 0; ++j) {
+      J = j;
+      if (tid < 1) *sctr(a.ctr, j + 2, kSfF) = 0;  // frontier counter of level j+2 (last read at level j-2)
+      const int32_t* Fin = a.F[j & 1];
+      int32_t* Fout = a.F[(j + 1) & 1];
+      unsigned long long* fnext = sctr(a.ctr, j + 1, kSfF);
+      const int vpw = verts_per_warp(nF, nwarps);
+      int ff = 0;
+      for (long long base = gwarp * vpw; base < nF; base += nwarps * vpw) {
+        const long long i = base + lane;
+        const bool valid = lane < vpw && i < nF;
+        const int v = valid ? __ldcg(Fin + i) : 0;
+        PGC_DCHECK(!valid || (v >= 0 && v < n), v, i);
+        PGC_DCHECK(!valid || __ldcg(a.cnt + v) == 0, v, __ldcg(a.cnt + v));
+        const int64_t o = valid ? a.off[v] : 0;
+        const int deg = valid ? (int)(a.off[v + 1] - o) : 0;
+        const int rv = valid ? __ldcg(a.round + v) : 0;
+        const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
+        int incl = deg;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, s);
+          if (lane >= s) incl += y;
+        }
+        const int start = incl - deg;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        // One pass over the arcs does both halves of the level: a pred's color
+        // goes into the owner's GetColor window, a succ's
+        // count is decremented (the Join, l.1128-1133) -- v's color is read by
+        // its succs only after the barrier.  Level 1 holds exactly the
+        // vertices with no pred: color 1, nothing to mark.  A vertex whose
+        // first 64-color window is full rescans its preds for the next window.
+        bool need = valid && j > 1;
+        int mycolor = valid ? 1 : 0;
+        for (int wbase = 0, first = 1; first || __ballot_sync(0xffffffffu, need); wbase += 64, first = 0) {
+          for (int j0 = 0; j0 < total; j0 += 32 * kSmallUnroll) {
+            int own[kSmallUnroll], u[kSmallUnroll], ru[kSmallUnroll], on[kSmallUnroll];
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              const int jj = j0 + 32 * k + lane;
+              own[k] = owner_of(start, jj);
+              const int64_t os = __shfl_sync(0xffffffffu, o, own[k]);
+              const int ss = __shfl_sync(0xffffffffu, start, own[k]);
+              on[k] = __shfl_sync(0xffffffffu, (int)need, own[k]);  // every lane shuffles
+              const bool scan = jj < total && (first || on[k]);
+              PGC_DCHECK(!scan || os + (jj - ss) < a.nnz, os + (jj - ss), jj);
+              u[k] = scan ? __ldg(a.col + os + (jj - ss)) : -1;
+              PGC_DCHECK(u[k] < n, u[k], jj);
+            }
+            // the neighbour's color is loaded beside its round (one dependent
+            // L2 trip less; used only if it turns out to be a pred)
+            int cu[kSmallUnroll];
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              ru[k] = u[k] >= 0 ? __ldcg(a.round + u[k]) : -1;
+              cu[k] = u[k] >= 0 && on[k] ? __ldcg(a.color + u[k]) : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              const int rs = __shfl_sync(0xffffffffu, rv, own[k]);
+              const uint64_t hs = __shfl_sync(0xffffffffu, hv, own[k]);
+              bool freed = false;
+              if (u[k] >= 0) {
+                if (prio_gt(ru[k], prio_hash(a.seed, (uint32_t)u[k]), rs, hs)) {
+                  if (on[k]) {  // pred: colored in an earlier level
+                    const int cb = cu[k] - 1 - wbase;
+                    PGC_DCHECK(cb + wbase >= 0, u[k], cb + wbase);
+                    if (cb >= 0 && cb < 64) atomicOr(&s_mask[warp][own[k]], 1ull << cb);
+                  }
+                } else if (first) {  // succ: count[u] -= 1; the last pred frees u
+                  const int old = atomicSub(a.cnt + u[k], 1);
+                  PGC_DCHECK(old >= 1, u[k], old);
+                  freed = old == 1;
+                }
+              }
+              wq_push(q0, ff, freed, u[k], Fout, fnext, n);
+            }
+          }
+          __syncwarp();
+          const unsigned long long m = s_mask[warp][lane];
+          s_mask[warp][lane] = 0;
+          if (need && ~m) {
+            mycolor = wbase + __ffsll((long long)~m);
+            need = false;
+          }
+          __syncwarp();
+        }
+        if (valid) {
+          a.color[v] = mycolor;
+          kmax = max(kmax, mycolor);
+        }
+      }
+      wq_flush(q0, ff, Fout, fnext, n);
+      grid.sync();
+      SMALL_STAMP();
+      nF = (long long)ld_ctr(fnext);
+    }
+  }
+  kmax = warp_max(kmax);
+  if (lane == 0) s_red[warp] = (unsigned long long)kmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int bm = 0;
+    for (int w = 0; w < kSmallWarps; ++w) bm = max(bm, (int)s_red[w]);
+    if (bm) atomicMax(&a.st->K, bm);
+  }
+#ifdef PGC_PROBE
+  if (tid == 0) {
+    printf("small phases (us):");
+    for (int k = 1; k < nstamp; ++k) printf(" %.1f", (stamps[k] - stamps[k - 1]) * 1e-3);
+    printf("\ntotal %.1f us, %d phases, grid %d\n", (stamps[nstamp - 1] - stamps[0]) * 1e-3, nstamp,
+           (int)gridDim.x);
+  }
+#endif
+  if (tid == 0) {
+    State* st = a.st;
+    st->T = l;
+    st->rmax = l;
+    st->sum_active = sum_active;
+    st->cross = cross;
+    st->pred_arcs = preds_total;
+    st->jp_levels = J;
+    st->err = err;
+    st->done = 1;
+    st->nU = nU;
+    st->S = S;
+  }
+}
+
+// Host side: one cooperative launch, one state read-back.
+bool small_path_wanted(const Ctx& c) {
+  if (c.tune.small_max_arcs <= 0 || c.n <= 0) return false;
+  if (c.nnz > c.tune.small_max_arcs) return false;
+  return c.nnz <= (long long)c.tune.small_max_avg * c.n;
+}
+
+static_assert(kSmallCtrBytes <= 2 * (size_t)kFilterBytes, "counter ring must fit the filter region");
+
+int small_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int32_t* color) {
+  if (!once_flag(c.dev, 9)) {  // load the kernel before the first timed launch
+    cudaFuncAttributes fa;
+    PGC_CUDA(cudaFuncGetAttributes(&fa, k_small_jp_adg));
+    once_flag(c.dev, 9) = true;
+  }
+  SmallArgs a;
+  a.n = c.n;
+  a.nnz = c.nnz;
+  a.off = c.off;
+  a.col = c.col;
+  a.num = num;
+  a.den = den;
+  a.seed = seed;
+  a.round = round;
+  a.color = color;
+  a.D = c.D;
+  a.cnt = c.npred;
+  a.U[0] = c.U[0];
+  a.U[1] = c.U[1];
+  a.R = c.Rl;
+  int32_t* fr = reinterpret_cast<int32_t*>(c.rec);  // 16 (2n + ...) bytes: two n-int frontiers
+  a.F[0] = fr;
+  a.F[1] = fr + c.n;
+  a.ctr = reinterpret_cast<unsigned long long*>(c.filt);  // the UPDATE filter is unused here
+  a.st = c.state;
+  a.per_round = c.per_round;
+  // grid: enough warps for a wave of the largest phase, at most one wave of
+  // resident blocks (a grid barrier needs every block resident)
+  const int occ = occupancy_cached(c.dev, (const void*)k_small_jp_adg, kSmallBlock, 0);
+  const int cap = c.nsm * (c.tune.small_blocks_per_sm > 0 && c.tune.small_blocks_per_sm < occ
+                               ? c.tune.small_blocks_per_sm
+                               : occ);
+  const long long want = (c.n + kSmallBlock - 1) / kSmallBlock;
+  const int G = (int)(want < 1 ? 1 : (want < cap ? want : cap));
+  if (c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
+  void* args[] = {&a};
+  PGC_LAUNCH(c, kGSelect, "k_small_jp_adg",
+             PGC_CUDA(cudaLaunchCooperativeKernel((const void*)k_small_jp_adg, dim3(G),
+                                                  dim3(kSmallBlock), args, 0, c.st)));
+  if (int e = sync_state(c)) return e;
+  const State* h = c.h_state;
+  if (h->err == 7)
+    return fail(4, "ADG round %d broke Lemma 1's per-round shrink (PAPER.md:761-771)", h->T);
+  if (h->err) return fail(4, "ADG internal invariant failed (code %d)", h->err);
+  c.jp_levels = c.tune.levels ? h->jp_levels : 0;  // (free here; reported like the other path)
+  c.small = 1;
+  return 0;
+}
+
+}  // namespace pgc

@@ -19,6 +19,18 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
+@pytest.fixture(autouse=True)
+def multi_kernel_path():
+    """These tests cover the multi-kernel path (adg.cu + jp.cu) on every graph
+    size: the one-kernel small-graph path (small.cu), which the default
+    heuristic picks for small low-degree graphs, has its own file
+    (test_gpu_small.py)."""
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    pgc.set_tuning("small_max_arcs", 0)
+    yield
+    pgc.set_tuning("small_max_arcs", 1 << 24)
+
+
 def dev(g):
     pgc = pytest.importorskip("paper_2008_11321_b200")
     off = torch.from_numpy(g.off).cuda()
@@ -562,7 +574,7 @@ def test_serialised_kernels_do_not_deadlock():
         "import sys; sys.path.insert(0, 'tests')\n"
         "import numpy as np, torch\n"
         "import graphgen as gg, oracle as O, paper_2008_11321_b200 as pgc\n"
-        "pgc.set_tuning('jp_watchdog_ms', 5000)\n"
+        "pgc.set_tuning('jp_watchdog_ms', 5000); pgc.set_tuning('small_max_arcs', 0)\n"
         "g = gg.rmat(15, 16, seed=6)\n"
         "off = torch.from_numpy(g.off).cuda(); col = torch.from_numpy(g.col).cuda()\n"
         "r, c, T, K = pgc.color_jp_adg(off, col, 1, 10, 5)\n"
