@@ -276,7 +276,7 @@ const char* pgc_last_error(void);
  *   default 1), "fuse_init" 0/1 (ADG's first selection also initialises the
  *   per-vertex state; default 1), "top_list" 0/1 (JP-ADG: ADG keeps the top
  *   rounds' vertex list so the split order's top part skips a pass over n;
- *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns",
+ *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns", "core_near",
  *   "small_max_arcs" (pgc_color_jp_adg runs as one persistent kernel when
  *   nnz <= this and nnz <= "small_max_avg" * n; 0 disables; defaults 2^24, 20),
  *   "small_blocks_per_sm" 0..64 (that kernel's grid; 0 = occupancy).

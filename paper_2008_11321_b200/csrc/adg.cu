@@ -242,8 +242,13 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
           }
         cpos += nch[j];
       }
+      if (light[j]) PGC_DCHECK_V(lpos);  // light records: at most n
       if (light[j]) __stcs(lrec + lpos++, light_rec(v[j], (int)deg[j], o[j]));
-      if (valid[j] && !sel[j]) Uout[upos++] = v[j];
+      if (valid[j] && !sel[j]) {
+        PGC_DCHECK_V(upos);  // |U_{l+1}| < n
+        PGC_DCHECK_V(v[j]);
+        Uout[upos++] = v[j];
+      }
     }
     __syncthreads();  // s_red / sm are reused by the next step
   }
@@ -419,7 +424,9 @@ __global__ void __launch_bounds__(256, PGC_LIGHT_MINB) k_update_light(Arc<MODE> 
         ow[k] = lo > 31 ? 31 : lo;
         const long long oo = __shfl_sync(0xffffffffu, o, ow[k]);
         const int oe = __shfl_sync(0xffffffffu, excl, ow[k]);
+        if (a < total) PGC_DCHECK_A(oo + (a - oe));
         u[k] = a < total ? ld_stream(col + oo + (a - oe)) : -1;
+        if (a < total) PGC_DCHECK_V(u[k]);
       }
 #pragma unroll
       for (int k = 0; k < kLStrips; ++k) gs[k] = A.raw(u[k]);  // all gathers in flight
@@ -440,8 +447,13 @@ __global__ void __launch_bounds__(256, PGC_LIGHT_MINB) k_update_light(Arc<MODE> 
           const int oe = __shfl_sync(0xffffffffu, excl, ow[k]);
           const long long oo = __shfl_sync(0xffffffffu, o, ow[k]);
           const int seg0 = max(0, oe - ts);  // first lane of the owner's segment
+#ifdef PGC_CHECKED
+          const int odeg = __shfl_sync(0xffffffffu, deg, ow[k]);
+#endif
           if (Arc<MODE>::kPreds && pred) {
             const int rank = __popc(pb & lt & ~((1u << seg0) - 1u));
+            PGC_DCHECK(base + rank < odeg, base + rank, odeg);  // pred(v) fits v's CSR slot
+            PGC_DCHECK_A(oo + base + rank);
             st_stream(P + oo + base + rank, u[k]);
           }
           // own segment in this strip: lanes [lo, hi)
@@ -526,7 +538,9 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) {
           const long long a = a0 + 32 * k + lane;
+          if (a < e0) PGC_DCHECK_A(a);
           u[k] = a < e0 ? ld_stream(col + a) : -1;
+          if (a < e0) PGC_DCHECK_V(u[k]);
         }
 #pragma unroll
         for (int k = 0; k < kStrips; ++k) g[k] = A.raw(u[k]);  // all gathers in flight
@@ -551,7 +565,10 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
         int base = 0;
         if (lane == 0) base = atomicAdd(&npred[v], cnt);
         base = __shfl_sync(0xffffffffu, base, 0);
-        for (int i = lane; i < cnt; i += 32) st_stream(P + o + base + i, s_buf[warp][i]);
+        for (int i = lane; i < cnt; i += 32) {
+          PGC_DCHECK_A(o + base + i);
+          st_stream(P + o + base + i, s_buf[warp][i]);
+        }
         if (lane == 0) preds += (unsigned long long)cnt;
         __syncwarp();
       }
@@ -988,6 +1005,7 @@ static int launch_update(Ctx& c, const Arc<MODE>& A, const int32_t* Uin = nullpt
 
 int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
             int32_t* color_zero, int rule) {
+  PGC_CHK_SIZES(c);
   const int B = 256;
   const int G = grid_for(c, 8);
   // mean rule: round 1's selection does init's per-vertex work (one pass less)
@@ -1140,6 +1158,7 @@ __global__ void k_o_key(int64_t n, const int32_t* __restrict__ round, const int3
 }
 
 int adg_o_keys(Ctx& c, const int32_t* round, int32_t* key1) {
+  PGC_CHK_SIZES(c);
   const int T = c.h_state->T;
   if (c.n == 0) return 0;
   // the order's histogram space (2(n + 65536) ints >= 2(T + 2)) is free until jp_order_run
@@ -1170,6 +1189,7 @@ __global__ void k_baseline_key(int64_t n, const int64_t* __restrict__ off, int k
 }
 
 int baseline_key_run(Ctx& c, int kind, int32_t* key) {
+  PGC_CHK_SIZES(c);
   if (c.n == 0) return 0;
   PGC_LAUNCH(c, kGAdgOther, "k_baseline_key",
              k_baseline_key<<<grid_for(c, 8), 256, 0, c.st>>>(c.n, c.off, kind, key));
@@ -1177,6 +1197,7 @@ int baseline_key_run(Ctx& c, int kind, int32_t* key) {
 }
 
 int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color) {
+  PGC_CHK_SIZES(c);
   const int G = grid_for(c, 8);
   PGC_LAUNCH(c, kGAdgOther, "k_state_reset_jp", k_state_reset_jp<<<1, 1, 0, c.st>>>(c.state));
   if (c.n == 0) return 0;

@@ -614,6 +614,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"core_spin_ns", 0, 100000, nullptr, &g_tune.core_spin_ns},
       {"core_tail_ns", 0, 100000, nullptr, &g_tune.core_tail_ns},
       {"core_pass_ns", 0, 100000, nullptr, &g_tune.core_pass_ns},
+      {"core_near", 0, 512, nullptr, &g_tune.core_near},
       {"itr_blocks_per_sm", 0, 64, nullptr, &g_tune.itr_blocks_per_sm},
       {"jp_split_overlap", 0, 1, nullptr, &g_tune.jp_split_overlap},
       {"update_atom", 0, 1, nullptr, &g_tune.update_atom},

@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(1024) k_order_top(State* st, const int32_t* __
 
 int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known, bool idkey,
                  bool defer) {
+  PGC_CHK_SIZES(c);
   int idshift = 0;
   if (idkey) {
     int bits = 1;
@@ -911,7 +912,7 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
                                                            unsigned long long* tr_grab,
                                                            unsigned long long* tr_done,
                                                            unsigned spin_ns, unsigned tail_ns,
-                                                           unsigned pass_ns,
+                                                           unsigned pass_ns, int near_n,
                                                            unsigned long long watchdog_ns,
                                                            int32_t* ready,
                                                            const int32_t* __restrict__ pos) {
@@ -1058,8 +1059,12 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
             stall = true;
             break;
           }
-          if (sleep_ns) __nanosleep(sleep_ns);
-          sleep_ns = sleep_ns ? min(sleep_ns * 2, (unsigned)spin_ns) : (spin_ns ? 32u : 0u);
+          if (npend <= near_n) {
+            sleep_ns = 0;  // a few preds from the tail: poll without backing off
+          } else {
+            if (sleep_ns) __nanosleep(sleep_ns);
+            sleep_ns = sleep_ns ? min(sleep_ns * 2, (unsigned)spin_ns) : (spin_ns ? 32u : 0u);
+          }
         }
       }
       if (stall) break;
@@ -1152,6 +1157,8 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
                    "h"((unsigned short)found)
                    : "memory");
     PROBE_STAMP(tr_grab, vprobe, 7);
+    PGC_DCHECK(found >= 1 && found <= np + 1, found, np);  // GetColor <= |pred| + 1
+    PGC_DCHECK_V(vcore);
     if (lane == 0) {
       st_relaxed(color + vcore, found);
 #ifndef PGC_PROBE
@@ -1277,6 +1284,7 @@ __device__ __forceinline__ int heavy_scan(const int32_t* __restrict__ P, int64_t
   for (int k = 0; k < kHS; ++k) {
     const int i = from + 32 * k + lane;
     un[k] = i < np ? jp_stream(P + pb + i) : -1;
+    if (i < np) PGC_DCHECK_V(un[k]);
   }
   for (int i0 = from; i0 < np; i0 += 32 * kHS) {
     int u[kHS], cc[kHS];
@@ -1533,6 +1541,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         __syncwarp();
       }
       if (found < 0) break;  // stalled: the host reports PGC_EINTERNAL
+      PGC_DCHECK(found >= 1 && found <= np + 1, found, np);  // GetColor <= |pred| + 1
       if (lane == 0) {
         st_relaxed(color + v, found);
         if (tr_done) tr_done[v] = globaltimer();
@@ -1639,7 +1648,10 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         for (int k = 0; k < 4 * kLV; ++k)
           if (s0 + k < pb || s0 + k >= pe) u[k] = -1;
 #pragma unroll
-        for (int k = 0; k < 4 * kLV; ++k) cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+        for (int k = 0; k < 4 * kLV; ++k) {
+          if (u[k] >= 0) PGC_DCHECK_V(u[k]);
+          cc[k] = u[k] >= 0 ? ld_relaxed(color + u[k]) : 1;
+        }
 #pragma unroll
         for (int k = 0; k < 4 * kLV; ++k) {
           if (u[k] < 0) continue;
@@ -1697,6 +1709,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
       // 3. GetColor once nothing is pending: the smallest color the preds do not use
       if (scanned && watch_u < 0) {
         const int cc = __ffsll((long long)~mask) - 1;
+        PGC_DCHECK(cc >= 1 && cc <= (int)(pe - pb) + 1, cc, pe - pb);  // GetColor <= |pred| + 1
         st_relaxed(color + v, cc);
         if (tr_done) tr_done[v] = globaltimer();
         kmax = max(kmax, cc);
@@ -1822,6 +1835,7 @@ static int pow2_floor(int x) {
 }
 
 int jp_color_run(Ctx& c, int32_t* color) {
+  PGC_CHK_SIZES(c);
   PGC_LAUNCH(c, kGJp, "k_jp_reset", k_jp_reset<<<1, 1, 0, c.st>>>(c.state, c.n > 0 ? 1 : 0));
   int64_t n_order = 0;
   if (c.n > 0) {
@@ -1947,7 +1961,8 @@ int jp_color_run(Ctx& c, int32_t* color) {
                                              c.trace_grab, c.trace_done,
                                              (unsigned)c.tune.core_spin_ns,
                                              (unsigned)c.tune.core_tail_ns,
-                                             (unsigned)c.tune.core_pass_ns, wd, ready,
+                                             (unsigned)c.tune.core_pass_ns, c.tune.core_near, wd,
+                                             ready,
                                              (const int32_t*)pos)));
       return 0;
     };
@@ -2045,6 +2060,7 @@ __global__ void k_check_graph(int64_t n, int64_t nnz, const int64_t* __restrict_
 }
 
 int check_graph_run(Ctx& c, int64_t* bad_vertex) {
+  PGC_CHK_SIZES(c);
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(&c.state->S);
   PGC_CUDA(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), c.st));
   if (c.n > 0)

@@ -104,6 +104,7 @@ struct Tuning {
   int core_spin_ns = 1024;        // JP core: backoff cap (ns) of a warp still several preds away
   int core_tail_ns = 0;           // JP core: sleep (ns) per poll of a warp in the tail
   int core_pass_ns = 0;           // JP core: min sleep (ns) between passes of a warp far from its tail
+  int core_near = 0;              // JP core: warps with at most this many pending preds poll without backoff
   int itr_blocks_per_sm = 0;      // DEC-ADG-ITR: blocks per SM of the cooperative kernel (0 = occupancy)
   int jp_split_overlap = 1;       // JP: run the bulk split on a side stream beside the core kernel
   int top_list = 1;               // JP-ADG: ADG saves the top rounds' list for the split order
@@ -216,6 +217,29 @@ constexpr int kMaxDevices = 64;
 bool& once_flag(int dev, int slot);
 // copy State to the pinned host mirror and wait for the stream; capi.cu
 int sync_state(Ctx& c);
+
+// Checked builds: the graph's sizes in device globals of each translation
+// unit (set by its host phases), for vertex / arc bounds in PGC_DCHECKs.
+#ifdef PGC_CHECKED
+static __device__ long long g_chk_n = 0, g_chk_nnz = 0;
+inline void chk_sizes(const Ctx& c) {
+  cudaMemcpyToSymbolAsync(g_chk_n, &c.n, sizeof(long long), 0, cudaMemcpyHostToDevice, c.st);
+  cudaMemcpyToSymbolAsync(g_chk_nnz, &c.nnz, sizeof(long long), 0, cudaMemcpyHostToDevice, c.st);
+}
+#define PGC_CHK_SIZES(c) ::pgc::chk_sizes(c)
+#define PGC_DCHECK_V(u) PGC_DCHECK((long long)(u) >= 0 && (long long)(u) < ::pgc::g_chk_n, u, ::pgc::g_chk_n)
+#define PGC_DCHECK_A(e) PGC_DCHECK((long long)(e) >= 0 && (long long)(e) < ::pgc::g_chk_nnz, e, ::pgc::g_chk_nnz)
+#else
+#define PGC_CHK_SIZES(c) \
+  do {                   \
+  } while (0)
+#define PGC_DCHECK_V(u) \
+  do {                  \
+  } while (0)
+#define PGC_DCHECK_A(e) \
+  do {                  \
+  } while (0)
+#endif
 
 // Launch a kernel (variadic so the <<<...>>> commas survive), check the launch,
 // account it and time it in `group`.

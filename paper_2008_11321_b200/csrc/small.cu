@@ -496,6 +496,7 @@ bool small_path_wanted(const Ctx& c) {
 static_assert(kSmallCtrBytes <= 2 * (size_t)kFilterBytes, "counter ring must fit the filter region");
 
 int small_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int32_t* color) {
+  PGC_CHK_SIZES(c);
   if (!once_flag(c.dev, 9)) {  // load the kernel before the first timed launch
     cudaFuncAttributes fa;
     PGC_CUDA(cudaFuncGetAttributes(&fa, k_small_jp_adg));

@@ -449,6 +449,26 @@ def test_dec_adg_itr_rmat20():
     assert_parity_dec(gg.config_graph("rmat20"), 1, 10, 1)
 
 
+def test_dec_adg_itr_and_baselines_rmat24():
+    """The headline graph (R-MAT 24, 520 M arcs) on DEC-ADG-ITR and on the JP
+    baselines without a dense priority prefix (JP-R, JP-FF: no core, long
+    chains in the bulk) and with one (JP-LLF)."""
+    import math
+    g = gg.config_graph("rmat24")
+    assert_parity_dec(g, 1, 10, 1)
+    pgc, off, col = dev(g)
+    deg = g.degrees()
+    for kind in ("jp-r", "jp-ff", "jp-llf"):
+        color, K = pgc.jp_baseline(off, col, kind, 1)
+        torch.cuda.synchronize()
+        key = {"jp-r": np.zeros(g.n), "jp-ff": -np.arange(g.n),
+               "jp-llf": np.ceil(np.log2(np.maximum(deg, 1)))}[kind]
+        c_or, K_or = O.jp(g, key.astype(np.int32), 1)
+        bad = np.nonzero(color.cpu().numpy() != c_or)[0]
+        assert len(bad) == 0, f"{kind}: color mismatch at {bad[:10]}"
+        assert K == K_or
+
+
 # ------------------------------------- next rows on the other full-size configs --
 @pytest.mark.parametrize("cfg", ["cl", "grid"])
 def test_next_rows_full_size(cfg):

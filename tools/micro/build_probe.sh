@@ -9,4 +9,4 @@ mkdir -p build/probe
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -c \
   -DPGC_PROBE -I include -o build/probe/jp.o paper_2008_11321_b200/csrc/jp.cu
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tools/micro/libpgc_probe.so \
-  build/pgc/adg.o build/pgc/capi.o build/pgc/dec.o build/probe/jp.o
+  $(ls build/pgc/*.o | grep -v '/jp.o$') build/probe/jp.o

@@ -8,4 +8,4 @@ mkdir -p build/probe
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -c \
   -DPGC_PROBE -I include -o build/probe/small.o paper_2008_11321_b200/csrc/small.cu
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tools/micro/libpgc_small_probe.so \
-  build/pgc/adg.o build/pgc/capi.o build/pgc/dec.o build/pgc/jp.o build/probe/small.o
+  $(ls build/pgc/*.o | grep -v '/small.o$') build/probe/small.o

@@ -27,8 +27,8 @@ import graphgen as gg  # noqa: E402
 import oracle as O  # noqa: E402
 import paper_2008_11321_b200 as pgc  # noqa: E402
 
-ALL = ["jp_adg", "adg_push", "adg_pull", "jp_color", "jp_adg_o", "jp_adg_m", "jp_r", "dec_adg_itr",
-       "host"]
+ALL = ["jp_adg", "jp_adg_small", "jp_adg_multi", "adg_push", "adg_pull", "jp_color", "jp_adg_o",
+       "jp_adg_m", "jp_r", "dec_adg_itr", "host"]
 
 
 def graph(name):
@@ -69,9 +69,19 @@ def main():
     for e in a.entries.split(","):
         t0 = time.time()
         ro, co = outs()
-        if e == "jp_adg":
+        if e in ("jp_adg", "jp_adg_small", "jp_adg_multi"):
+            # default heuristic, then the one-kernel path and the multi-kernel path forced
+            if e == "jp_adg_small":
+                pgc.set_tuning("small_max_arcs", 1 << 40)
+                pgc.set_tuning("small_max_avg", 1 << 30)
+            elif e == "jp_adg_multi":
+                pgc.set_tuning("small_max_arcs", 0)
             r, c, T, K = pgc.color_jp_adg(off, col, num, den, 1, round_out=ro, color_out=co)
-            check(e, np.array_equal(r.cpu().numpy(), r_or) and np.array_equal(c.cpu().numpy(), c_or))
+            path = pgc.last_stats()["small_path"]
+            pgc.set_tuning("small_max_arcs", 1 << 24)
+            pgc.set_tuning("small_max_avg", 20)
+            check(f"{e} (small_path={path})",
+                  np.array_equal(r.cpu().numpy(), r_or) and np.array_equal(c.cpu().numpy(), c_or))
         elif e in ("adg_push", "adg_pull"):
             r, T = pgc.adg_order(off, col, num, den, update=e[4:], round_out=ro)
             check(e, np.array_equal(r.cpu().numpy(), r_or))

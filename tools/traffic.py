@@ -11,7 +11,10 @@
   python tools/traffic.py parse gpurun_out/t.csv --workload rmat24-eps1/10 --source <path>
 
 `run` makes two JP-ADG calls (the first warms up); `parse` sums the second
-call's k_update* launches (half of the captured launches).
+call's k_update* launches (half of the captured launches).  Workloads on the
+one-kernel small-graph path (csrc/small.cu) have no UPDATE launch: capture
+`-k regex:k_small` and parse with `--kernel k_small_jp_adg --workload
+<workload>-small` (the whole path's DRAM bytes, bench.py's `traffic` there).
 """
 import argparse
 import csv
@@ -47,8 +50,9 @@ def parse(a):
     rows = [r for r in csv.reader(open(a.csv)) if len(r) > 10]
     h = rows[0]
     ki, ni, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
-    ids = sorted({int(r[ii]) for r in rows[1:] if r[ki].startswith("void k_update") or
-                  r[ki].startswith("k_update")})
+    kp = a.kernel
+    ids = sorted({int(r[ii]) for r in rows[1:] if r[ki].startswith("void " + kp) or
+                  r[ki].startswith(kp)})
     second = set(ids[len(ids) // 2:])   # the second (profiled) call's launches
     # ncu reports bytes with unit prefixes in some versions: the csv unit column says which
     ui = h.index("Metric Unit")
@@ -75,6 +79,9 @@ def main():
     q.add_argument("csv")
     q.add_argument("--workload", required=True)
     q.add_argument("--source", default=None)
+    q.add_argument("--kernel", default="k_update",
+                   help="kernel name prefix (k_small_jp_adg for the one-kernel path; "
+                        "its workload key gets the suffix -small)")
     a = ap.parse_args()
     return run(a) if a.cmd == "run" else parse(a)
 
