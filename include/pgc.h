@@ -107,6 +107,8 @@ typedef struct pgc_stats {
    * the JP bulk dataflow (a8/a9), and the whole call. */
   float t_select_ms, t_update_ms, t_adg_other_ms, t_order_ms, t_core_ms, t_jp_ms, t_total_ms;
   int32_t small_path;      /* 1 if pgc_color_jp_adg ran as ONE persistent cooperative kernel
+                              (2: as ONE thread-block cluster, state in DSMEM; core_ctas
+                              then holds its size)
                               (small / low-degree graphs: nnz <= tuning "small_max_arcs"
                               and nnz <= "small_max_avg" * n; ADG rounds and JP levels
                               separated by grid barriers, JP frontier-driven with
@@ -279,7 +281,10 @@ const char* pgc_last_error(void);
  *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns", "core_near",
  *   "small_max_arcs" (pgc_color_jp_adg runs as one persistent kernel when
  *   nnz <= this and nnz <= "small_max_avg" * n; 0 disables; defaults 2^24, 20),
- *   "small_blocks_per_sm" 0..64 (that kernel's grid; 0 = occupancy).
+ *   "small_blocks_per_sm" 0..64 (that kernel's grid; 0 = occupancy),
+ *   "tiny_max_n" / "tiny_max_arcs" (that path runs on ONE thread-block cluster
+ *   with the per-vertex state in distributed shared memory when n and nnz are
+ *   at most these and the state fits; tiny_max_n = 0 disables; 2^17, 2^22).
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

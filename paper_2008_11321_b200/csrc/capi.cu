@@ -625,6 +625,8 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"small_max_arcs", 0, 1ll << 40, &g_tune.small_max_arcs, nullptr},
       {"small_max_avg", 0, 1 << 30, nullptr, &g_tune.small_max_avg},
       {"small_blocks_per_sm", 0, 64, nullptr, &g_tune.small_blocks_per_sm},
+      {"tiny_max_n", 0, 1ll << 30, &g_tune.tiny_max_n, nullptr},
+      {"tiny_max_arcs", 0, 1ll << 40, &g_tune.tiny_max_arcs, nullptr},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };
   for (const Key& k : keys)

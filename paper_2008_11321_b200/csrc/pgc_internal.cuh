@@ -117,6 +117,11 @@ struct Tuning {
   long long small_max_arcs = 1ll << 24;    // 0 disables the one-kernel path
   int small_max_avg = 20;
   int small_blocks_per_sm = 0;             // blocks per SM of that kernel (0 = occupancy)
+  // ... on ONE thread-block cluster with the per-vertex state in distributed
+  // shared memory (k_tiny_jp_adg) when n <= tiny_max_n (and it fits) and
+  // nnz <= tiny_max_arcs; tiny_max_n = 0 disables
+  long long tiny_max_n = 1ll << 17;
+  long long tiny_max_arcs = 1ll << 22;
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
@@ -132,7 +137,7 @@ struct Ctx {
   int syncs = 0;     // host synchronisations by this call
   int dev = 0;       // the device of this call (cudaGetDevice at entry)
   int jp_levels = 0; // J of the last JP (levels knob), else 0
-  int small = 0;     // the one-kernel small-graph path ran (small.cu)
+  int small = 0;     // the one-kernel small-graph path ran (small.cu): 1 grid, 2 one cluster
   int64_t n, nnz;
   const int64_t* off;
   const int32_t* col;

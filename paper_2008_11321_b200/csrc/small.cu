@@ -132,6 +132,23 @@ __device__ __forceinline__ int verts_per_warp(long long cnt, long long nwarps) {
   return v;
 }
 
+// Dmax = floor((den+num) S / (den |U|)) exactly (readings Q1/Q2), clamped to
+// INT32_MAX; 64-bit division when the numerator fits (the software 128-bit
+// division costs microseconds on a latency-bound phase).
+__device__ __forceinline__ long long dmax_of(uint32_t num, uint32_t den, unsigned long long S,
+                                             long long nU) {
+  const unsigned long long dn = (unsigned long long)den + num;
+  const unsigned long long denom = (unsigned long long)den * (unsigned long long)nU;
+  unsigned long long q;
+  if (S <= 0xffffffffffffffffull / dn) {
+    q = (S * dn) / denom;
+  } else {
+    const unsigned __int128 q128 = ((unsigned __int128)dn * S) / denom;
+    q = q128 > (unsigned __int128)0x7fffffff ? 0x7fffffffull : (unsigned long long)q128;
+  }
+  return q > 0x7fffffffull ? 0x7fffffffLL : (long long)q;
+}
+
 // Higher JP priority: <round, h> lexicographic (Q8, Q10; h is a bijection).
 __device__ __forceinline__ bool prio_gt(int ra, uint64_t ha, int rb, uint64_t hb) {
   return ra > rb || (ra == rb && ha > hb);
@@ -186,10 +203,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
     // frontier field is JP's, reset per level)
     if (tid < kSfF) *sctr(a.ctr, l + 2, (int)tid) = 0;
     // select (a2/a3): exact threshold
-    const unsigned __int128 numer = (unsigned __int128)((unsigned long long)a.den + a.num) * S;
-    const unsigned long long denom = (unsigned long long)a.den * (unsigned long long)nU;
-    const unsigned __int128 q = numer / denom;
-    const long long dmax = q > (unsigned __int128)0x7fffffff ? 0x7fffffffLL : (long long)q;
+    const long long dmax = dmax_of(a.num, a.den, S, nU);
     const int32_t* Uin = l == 1 ? nullptr : a.U[l & 1];
     int32_t* Uout = a.U[(l + 1) & 1];
     unsigned long long sumD = 0;
@@ -486,6 +500,461 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
   }
 }
 
+
+// ============================================================ tiny graphs
+// The same method on ONE thread-block cluster (<= 16 CTAs x 1024 threads) with
+// every per-vertex array in distributed shared memory: vertex v lives in CTA
+// v mod C at index v / C (D, round, count, color, the U/R lists and the JP
+// frontiers).  A phase then costs a cluster barrier (hardware, well under a
+// microsecond) and DSMEM / L1 accesses instead of a grid barrier and L2 round
+// trips; the CSR is read through the read-only path (each CTA's rows stay in
+// its L1 across the phases).  Rounds and levels run as in k_small_jp_adg:
+// select (own vertices, local lists) | cluster barrier | UPDATE + JP Part 1
+// (decrements into the owners' D by DSMEM atomics) | cluster barrier; JP
+// levels push a freed succ into its OWNER's next frontier (one DSMEM atomic
+// per owner group of a warp).  Global sums (|U|, S terms) are per-CTA
+// partials in a 2-slot ring read by warp 0 of every CTA after the barrier.
+constexpr int kTinyBlock = 1024;
+constexpr int kTinyWarps = kTinyBlock / 32;
+constexpr int kTinyMaxC = 16;
+constexpr int kTinyArrays = 9;  // D, rnd, cnt, clr, U0, U1, R, F0, F1 (+ row starts, rows)
+enum { kTpUout = 0, kTpR = 1, kTpSumD = 2, kTpCut = 3, kTpPreds = 4, kTpFields = 5 };
+
+struct TinyArgs {
+  int64_t n, nnz;
+  const int64_t* off;
+  const int32_t* col;
+  uint32_t num, den;
+  uint64_t seed;
+  int32_t* round;
+  int32_t* color;
+  State* st;
+  long long* per_round;
+  int nloc;     // per-CTA capacity of every array (>= ceil(n / C))
+  int cshift;   // C = 1 << cshift
+  long long adj_cap;  // per-CTA capacity of the copied rows (ints)
+};
+
+__global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+#ifdef PGC_PROBE
+  unsigned long long stamps[512];
+  int nstamp = 0;
+  const long long tid = (long long)cl.block_rank() * kTinyBlock + threadIdx.x;
+#endif
+  extern __shared__ __align__(16) int32_t t_dyn[];
+  __shared__ unsigned long long s_part[2][kTpFields];  // this CTA's partial sums (ring: round parity)
+  __shared__ unsigned long long s_tot[kTpFields];
+  __shared__ int s_nR, s_nUo, s_nown;
+  __shared__ int s_fcnt[3];  // frontier lengths (ring: level mod 3); other CTAs push into them
+  __shared__ int s_acc[kTinyWarps][32];
+  __shared__ unsigned long long s_mask[kTinyWarps][32];
+  const int C = 1 << a.cshift, cs = a.cshift, me = (int)cl.block_rank();
+  const int nloc = a.nloc;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  int32_t* D = t_dyn;
+  int32_t* rnd = D + nloc;
+  int32_t* cnt = rnd + nloc;
+  int32_t* clr = cnt + nloc;
+  int32_t* Ul[2] = {clr + nloc, clr + 2 * nloc};
+  int32_t* Rl = clr + 3 * nloc;
+  int32_t* Fb[2] = {clr + 4 * nloc, clr + 5 * nloc};
+  // the own rows of the CSR, copied once: cluster.sync invalidates the L1, so
+  // a row read from global memory would cost an L2 round trip in every phase
+  int32_t* loff = clr + 6 * nloc;  // [nloc + 1] local row starts into ladj
+  int32_t* ladj = loff + nloc + 1; // [a.adj_cap]
+  // an array element of vertex u in its owner's shared memory (generic address)
+  auto at = [&](int32_t* local_array, int u) -> int32_t* {
+    return cl.map_shared_rank(local_array, u & (C - 1)) + (u >> cs);
+  };
+  const int nown = me < n ? (int)((n - me + C - 1) >> cs) : 0;  // own vertices me, me + C, ...
+  if (threadIdx.x == 0) {
+    s_fcnt[0] = s_fcnt[1] = s_fcnt[2] = 0;
+    s_nR = s_nUo = 0;
+    s_nown = nown;
+    if (me == 0) a.st->K = 0;
+  }
+  s_acc[warp][lane] = 0;
+  s_mask[warp][lane] = 0;
+  // local row starts: a block scan of the own degrees (thread t: a contiguous chunk)
+  {
+    const int per = (nown + kTinyBlock - 1) / kTinyBlock;
+    const int b0 = min(nown, (int)threadIdx.x * per), b1 = min(nown, b0 + per);
+    long long sum = 0;
+    for (int i = b0; i < b1; ++i) {
+      const int v = (i << cs) + me;
+      sum += __ldg(a.off + v + 1) - __ldg(a.off + v);
+    }
+    long long incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __shared__ long long s_w[kTinyWarps + 1];
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const long long w = s_w[lane];
+      long long wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_w[lane] = wi - w;
+      if (lane == 31) s_w[kTinyWarps] = wi;
+    }
+    __syncthreads();
+    const long long tot = s_w[kTinyWarps];
+    long long run = s_w[warp] + incl - sum;
+    if (tot <= a.adj_cap) {
+      for (int i = b0; i < b1; ++i) {
+        const int v = (i << cs) + me;
+        loff[i] = (int)run;
+        const int d = (int)(__ldg(a.off + v + 1) - __ldg(a.off + v));
+        D[i] = d;
+        clr[i] = 0;
+        run += d;
+      }
+      if (threadIdx.x == 0) loff[nown] = (int)tot;
+    }
+    if (threadIdx.x == 0) s_part[0][0] = tot > a.adj_cap ? 1ull : 0ull;  // does not fit
+    __syncthreads();
+    // copy the rows: a warp per row, coalesced
+    if (tot <= a.adj_cap)
+      for (int i = warp; i < nown; i += kTinyWarps) {
+        const int v = (i << cs) + me;
+        const int64_t o = __ldg(a.off + v);
+        const int d = loff[i + 1] - loff[i];
+        for (int k = lane; k < d; k += 32) ladj[loff[i] + k] = __ldg(a.col + o + k);
+      }
+  }
+  cl.sync();
+  SMALL_STAMP();
+  // every CTA's rows must fit: otherwise all leave, the host runs the grid kernel
+  {
+    int bad = 0;
+    if (warp == 0) bad = __any_sync(0xffffffffu, lane < C && *cl.map_shared_rank(&s_part[0][0], lane) != 0);
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = bad;
+    __syncthreads();
+    if (s_bad) {
+      if (me == 0 && threadIdx.x == 0) a.st->err = 11;
+      cl.sync();  // the peers' flags are read before anyone leaves
+      return;
+    }
+  }
+  cl.sync();  // the flags are read before round 1 reuses s_part
+
+  unsigned long long S = (unsigned long long)a.nnz;
+  long long nU = n, sum_active = 0;
+  unsigned long long cross = 0, preds_total = 0;
+  int l = 0, err = 0, nUloc = nown;
+  while (nU > 0) {
+    ++l;
+    const int par = l & 1;
+    const long long dmax = dmax_of(a.num, a.den, S, nU);
+    const int32_t* Uin = Ul[l & 1];
+    int32_t* Uout = Ul[(l + 1) & 1];
+    // this round's partial-sum slot: last read by the peers in round l-2
+    if (threadIdx.x < kTpFields) s_part[par][threadIdx.x] = 0;
+    __syncthreads();
+    // select (own vertices; local lists)
+    unsigned long long sumD = 0;
+    for (int base = warp * 32; base < nUloc; base += kTinyBlock) {
+      const int i = base + lane;
+      const bool valid = i < nUloc;
+      const int v = valid ? (l == 1 ? (i << cs) + me : Uin[i]) : 0;
+      const int iv = v >> cs;
+      int d = 0;
+      if (valid) d = D[iv];
+      const bool sel = valid && d <= dmax;
+      if (valid && (sel || l == 1)) rnd[iv] = sel ? l : 0;
+      if (sel) sumD += (unsigned long long)d;
+      const unsigned bs = __ballot_sync(0xffffffffu, sel), bu = __ballot_sync(0xffffffffu, valid && !sel);
+      int ps = 0, pu = 0;
+      if (lane == 0) {
+        if (bs) ps = atomicAdd(&s_nR, __popc(bs));
+        if (bu) pu = atomicAdd(&s_nUo, __popc(bu));
+      }
+      ps = __shfl_sync(0xffffffffu, ps, 0);
+      pu = __shfl_sync(0xffffffffu, pu, 0);
+      if (sel) Rl[ps + __popc(bs & lanemask_lt())] = v;
+      if (valid && !sel) Uout[pu + __popc(bu & lanemask_lt())] = v;
+    }
+    sumD = warp_sum(sumD);
+    if (lane == 0 && sumD) atomicAdd(&s_part[par][kTpSumD], sumD);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_part[par][kTpR] = (unsigned long long)s_nR;
+      s_part[par][kTpUout] = (unsigned long long)s_nUo;
+    }
+    cl.sync();
+    SMALL_STAMP();
+    // UPDATE + JP Part 1 over the own R_l; decrements go to the owners' D
+    const int nR = s_nR;
+    unsigned long long cut = 0, preds = 0;
+    const int vpwR = verts_per_warp(nR, kTinyWarps);
+    for (int base = warp * vpwR; base < nR; base += kTinyWarps * vpwR) {
+      const int i = base + lane;
+      const bool valid = lane < vpwR && i < nR;
+      const int v = valid ? Rl[i] : 0;
+      const int o = valid ? loff[v >> cs] : 0;
+      const int deg = valid ? loff[(v >> cs) + 1] - o : 0;
+      const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
+      int incl = deg;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, s);
+        if (lane >= s) incl += y;
+      }
+      const int start = incl - deg;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      for (int j0 = 0; j0 < total; j0 += 32 * kSmallUnroll) {
+        int own[kSmallUnroll], u[kSmallUnroll], ru[kSmallUnroll];
+#pragma unroll
+        for (int k = 0; k < kSmallUnroll; ++k) {
+          const int j = j0 + 32 * k + lane;
+          own[k] = owner_of(start, j);
+          const int os = __shfl_sync(0xffffffffu, o, own[k]);
+          const int ss = __shfl_sync(0xffffffffu, start, own[k]);
+          u[k] = j < total ? ladj[os + (j - ss)] : -1;
+          PGC_DCHECK(j >= total || (u[k] >= 0 && u[k] < n), u[k], j);
+        }
+#pragma unroll
+        for (int k = 0; k < kSmallUnroll; ++k) ru[k] = u[k] >= 0 ? *at(rnd, u[k]) : -1;
+#pragma unroll
+        for (int k = 0; k < kSmallUnroll; ++k) {
+          const uint64_t hs = __shfl_sync(0xffffffffu, hv, own[k]);
+          bool pred = false;
+          if (ru[k] == 0) {
+            atomicSub(at(D, u[k]), 1);
+            ++cut;
+            pred = true;
+          } else if (ru[k] == l) {
+            pred = prio_hash(a.seed, (uint32_t)u[k]) > hs;
+          }
+          const unsigned same = __match_any_sync(0xffffffffu, own[k]);
+          const int c = __popc(__ballot_sync(0xffffffffu, pred) & same);
+          if (c && lane == __ffs(same) - 1) atomicAdd(&s_acc[warp][own[k]], c);
+        }
+      }
+      __syncwarp();
+      const int p = s_acc[warp][lane];
+      s_acc[warp][lane] = 0;
+      if (valid) {
+        cnt[v >> cs] = p;
+        preds += (unsigned long long)p;
+      }
+      const unsigned bf = __ballot_sync(0xffffffffu, valid && p == 0);
+      int pf = 0;
+      if (lane == 0 && bf) pf = atomicAdd(&s_fcnt[1], __popc(bf));
+      pf = __shfl_sync(0xffffffffu, pf, 0);
+      if (valid && p == 0) Fb[1][pf + __popc(bf & lanemask_lt())] = v;
+      __syncwarp();
+    }
+    cut = warp_sum(cut);
+    preds = warp_sum(preds);
+    if (lane == 0) {
+      if (cut) atomicAdd(&s_part[par][kTpCut], cut);
+      if (preds) atomicAdd(&s_part[par][kTpPreds], preds);
+    }
+    cl.sync();
+    SMALL_STAMP();
+    // every CTA sums the C partials (warp 0, one lane per CTA)
+    if (warp == 0) {
+      unsigned long long x[kTpFields];
+#pragma unroll
+      for (int f = 0; f < kTpFields; ++f)  // all C x fields loads in flight
+        x[f] = lane < C ? *cl.map_shared_rank(&s_part[par][f], lane) : 0ull;
+#pragma unroll
+      for (int f = 0; f < kTpFields; ++f) {
+        x[f] = warp_sum(x[f]);
+        if (lane == 0) s_tot[f] = x[f];
+      }
+    }
+    __syncthreads();
+    const long long nU1 = (long long)s_tot[kTpUout];
+    const long long nRg = (long long)s_tot[kTpR];
+    const unsigned long long sumDR = s_tot[kTpSumD], cut_l = s_tot[kTpCut];
+    preds_total += s_tot[kTpPreds];
+    if (me == 0 && threadIdx.x == 0 && l - 1 < kMaxRoundStats) {
+      a.per_round[3 * (l - 1) + 0] = nU;
+      a.per_round[3 * (l - 1) + 1] = (long long)S;
+      a.per_round[3 * (l - 1) + 2] = nRg;
+    }
+    sum_active += nU;
+    cross += cut_l;
+    if (nRg == 0) err = 1;
+    if (nU1 != nU - nRg) err = 2;
+    if (!((unsigned __int128)nU1 * ((unsigned long long)a.den + a.num) <
+          (unsigned __int128)nU * a.den))
+      err = 7;
+    S = S - sumDR - cut_l;
+    nU = nU1;
+    nUloc = s_nUo;
+    __syncthreads();  // every thread has read s_nR / s_nUo / s_tot
+    if (threadIdx.x == 0) {
+      s_nR = 0;
+      s_nUo = 0;
+    }
+    __syncthreads();
+    if (err) break;
+  }
+
+  // ---------------------------------------------------------------- JP
+  int J = 0, kmax = 0;
+  if (!err) {
+    long long nF = 0;
+    if (warp == 0) {
+      long long x = lane < C ? *cl.map_shared_rank(&s_fcnt[1], lane) : 0;
+      x = warp_sum(x);
+      if (lane == 0) s_tot[0] = (unsigned long long)x;
+    }
+    __syncthreads();
+    nF = (long long)s_tot[0];
+    for (int j = 1; nF > 0; ++j) {
+      J = j;
+      const int nFl = s_fcnt[j % 3];
+      const int32_t* Fin = Fb[j & 1];
+      int32_t* Fout = Fb[(j + 1) & 1];
+      const int nslot = (j + 1) % 3;
+      __syncthreads();  // every thread has read s_fcnt[j % 3] and s_tot
+      if (threadIdx.x == 0) s_fcnt[(j + 2) % 3] = 0;  // level j+2's (pushed into at level j+1)
+      const int vpwF = verts_per_warp(nFl, kTinyWarps);
+      for (int base = warp * vpwF; base < nFl; base += kTinyWarps * vpwF) {
+        const int i = base + lane;
+        const bool valid = lane < vpwF && i < nFl;
+        const int v = valid ? Fin[i] : 0;
+        const int o = valid ? loff[v >> cs] : 0;
+        const int deg = valid ? loff[(v >> cs) + 1] - o : 0;
+        const int rv = valid ? rnd[v >> cs] : 0;
+        const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
+        int incl = deg;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, s);
+          if (lane >= s) incl += y;
+        }
+        const int start = incl - deg;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        bool need = valid && j > 1;
+        int mycolor = valid ? 1 : 0;
+        for (int wbase = 0, first = 1; first || __ballot_sync(0xffffffffu, need); wbase += 64, first = 0) {
+          for (int j0 = 0; j0 < total; j0 += 32 * kSmallUnroll) {
+            int own[kSmallUnroll], u[kSmallUnroll], ru[kSmallUnroll], cu[kSmallUnroll], on[kSmallUnroll];
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              const int jj = j0 + 32 * k + lane;
+              own[k] = owner_of(start, jj);
+              const int os = __shfl_sync(0xffffffffu, o, own[k]);
+              const int ss = __shfl_sync(0xffffffffu, start, own[k]);
+              on[k] = __shfl_sync(0xffffffffu, (int)need, own[k]);
+              const bool scan = jj < total && (first || on[k]);
+              u[k] = scan ? ladj[os + (jj - ss)] : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              ru[k] = u[k] >= 0 ? *at(rnd, u[k]) : -1;
+              cu[k] = u[k] >= 0 && on[k] ? *at(clr, u[k]) : 0;
+            }
+            // classify every step, all count decrements in flight together
+            int oldc[kSmallUnroll];
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              const int rs = __shfl_sync(0xffffffffu, rv, own[k]);
+              const uint64_t hs = __shfl_sync(0xffffffffu, hv, own[k]);
+              oldc[k] = 0;
+              if (u[k] >= 0) {
+                if (prio_gt(ru[k], prio_hash(a.seed, (uint32_t)u[k]), rs, hs)) {
+                  if (on[k]) {
+                    const int cb = cu[k] - 1 - wbase;
+                    PGC_DCHECK(cb + wbase >= 0, u[k], cb + wbase);
+                    if (cb >= 0 && cb < 64) atomicOr(&s_mask[warp][own[k]], 1ull << cb);
+                  }
+                } else if (first) {
+                  oldc[k] = atomicSub(at(cnt, u[k]), 1);
+                  PGC_DCHECK(oldc[k] >= 1, u[k], oldc[k]);
+                }
+              }
+            }
+            // a freed u goes to its owner's next frontier: one DSMEM atomic per
+            // (step, owner) group, all issued before any position is used
+            unsigned grp[kSmallUnroll];
+            int pos[kSmallUnroll], key[kSmallUnroll];
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              key[k] = oldc[k] == 1 ? (u[k] & (C - 1)) : -1;
+              grp[k] = __match_any_sync(0xffffffffu, key[k]);
+              pos[k] = 0;
+              if (key[k] >= 0 && lane == __ffs(grp[k]) - 1)
+                pos[k] = atomicAdd(cl.map_shared_rank(&s_fcnt[nslot], key[k]), __popc(grp[k]));
+            }
+#pragma unroll
+            for (int k = 0; k < kSmallUnroll; ++k) {
+              const int p0 = __shfl_sync(0xffffffffu, pos[k], __ffs(grp[k]) - 1);
+              if (key[k] >= 0)
+                *cl.map_shared_rank(Fout + p0 + __popc(grp[k] & lanemask_lt()), key[k]) = u[k];
+            }
+          }
+          __syncwarp();
+          const unsigned long long m = s_mask[warp][lane];
+          s_mask[warp][lane] = 0;
+          if (need && ~m) {
+            mycolor = wbase + __ffsll((long long)~m);
+            need = false;
+          }
+          __syncwarp();
+        }
+        if (valid) {
+          clr[v >> cs] = mycolor;
+          kmax = max(kmax, mycolor);
+        }
+      }
+      cl.sync();
+      SMALL_STAMP();
+      if (warp == 0) {
+        long long x = lane < C ? *cl.map_shared_rank(&s_fcnt[nslot], lane) : 0;
+        x = warp_sum(x);
+        if (lane == 0) s_tot[0] = (unsigned long long)x;
+      }
+      __syncthreads();
+      nF = (long long)s_tot[0];
+    }
+  }
+#ifdef PGC_PROBE
+  if (tid == 0) {
+    printf("tiny phases (us):");
+    for (int k = 1; k < nstamp; ++k) printf(" %.1f", (stamps[k] - stamps[k - 1]) * 1e-3);
+    printf("\ntotal %.1f us, %d phases, cluster %d\n", (stamps[nstamp - 1] - stamps[0]) * 1e-3, nstamp, C);
+  }
+#endif
+  // outputs: every CTA writes its own vertices
+  for (int i = threadIdx.x; i < nown; i += kTinyBlock) {
+    const int v = (i << cs) + me;
+    a.round[v] = rnd[i];
+    a.color[v] = err ? 0 : clr[i];
+  }
+  kmax = warp_max(kmax);
+  if (lane == 0 && kmax) atomicMax(&a.st->K, kmax);
+  if (me == 0 && threadIdx.x == 0) {
+    State* st = a.st;
+    st->T = l;
+    st->rmax = l;
+    st->sum_active = sum_active;
+    st->cross = cross;
+    st->pred_arcs = preds_total;
+    st->jp_levels = J;
+    st->err = err;
+    st->done = 1;
+    st->nU = nU;
+    st->S = S;
+  }
+  cl.sync();  // no CTA leaves while a peer may still access its shared memory
+}
+
 // Host side: one cooperative launch, one state read-back.
 bool small_path_wanted(const Ctx& c) {
   if (c.tune.small_max_arcs <= 0 || c.n <= 0) return false;
@@ -495,6 +964,98 @@ bool small_path_wanted(const Ctx& c) {
 
 static_assert(kSmallCtrBytes <= 2 * (size_t)kFilterBytes, "counter ring must fit the filter region");
 
+// The one-cluster variant when the graph fits the cluster's shared memory:
+// returns -1 when it ran (and succeeded), 0 when not applicable, else an error.
+static int tiny_try(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int32_t* color) {
+  if (c.tune.tiny_max_n <= 0 || c.n > c.tune.tiny_max_n || c.nnz > c.tune.tiny_max_arcs) return 0;
+  if (c.n >= (1ll << 30)) return 0;
+  bool& attr = once_flag(c.dev, 10);
+  static thread_local int max_smem[kMaxDevices] = {};
+  if (!attr) {
+    int optin = 0;
+    PGC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.dev));
+    cudaFuncAttributes fa;
+    PGC_CUDA(cudaFuncGetAttributes(&fa, k_tiny_jp_adg));
+    max_smem[c.dev] = optin - (int)fa.sharedSizeBytes;
+    if (cudaFuncSetAttribute(k_tiny_jp_adg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             max_smem[c.dev]) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tiny_jp_adg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      max_smem[c.dev] = 0;  // no tiny path on this device
+    }
+    attr = true;
+  }
+  int C = 0;
+  size_t smem = 0;
+  int nloc = 0;
+  for (int cand = kTinyMaxC; cand >= 2; cand >>= 1) {
+    nloc = (int)((c.n + cand - 1) / cand);
+    // the arrays, the row starts and at least the mean row share of the CSR
+    const long long need = 4ll * ((long long)kTinyArrays * (nloc > 0 ? nloc : 1) + nloc + 1) +
+                           4ll * ((c.nnz + cand - 1) / cand);
+    if (need > max_smem[c.dev]) break;  // a smaller cluster holds less per cluster
+    smem = (size_t)max_smem[c.dev];
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cand);
+    cfg.blockDim = dim3(kTinyBlock);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cand;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_tiny_jp_adg, &cfg) == cudaSuccess && ncl >= 1) {
+      C = cand;
+      break;
+    }
+    cudaGetLastError();
+  }
+  if (!C) return 0;
+  TinyArgs a;
+  a.n = c.n;
+  a.nnz = c.nnz;
+  a.off = c.off;
+  a.col = c.col;
+  a.num = num;
+  a.den = den;
+  a.seed = seed;
+  a.round = round;
+  a.color = color;
+  a.st = c.state;
+  a.per_round = c.per_round;
+  a.nloc = nloc;
+  a.cshift = __builtin_ctz((unsigned)C);
+  a.adj_cap = ((long long)smem - 4ll * ((long long)kTinyArrays * nloc + nloc + 1)) / 4;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kTinyBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
+  PGC_LAUNCH(c, kGSelect, "k_tiny_jp_adg", PGC_CUDA(cudaLaunchKernelEx(&cfg, k_tiny_jp_adg, a)));
+  if (int e = sync_state(c)) return e;
+  const State* h = c.h_state;
+  if (h->err == 11) return 0;  // a CTA's rows did not fit its shared memory: the grid kernel
+  if (h->err == 7)
+    return fail(4, "ADG round %d broke Lemma 1's per-round shrink (PAPER.md:761-771)", h->T);
+  if (h->err) return fail(4, "ADG internal invariant failed (code %d)", h->err);
+  c.jp_levels = c.tune.levels ? h->jp_levels : 0;
+  c.small = 2;
+  c.core_ctas = C;
+  return -1;
+}
+
 int small_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int32_t* color) {
   PGC_CHK_SIZES(c);
   if (!once_flag(c.dev, 9)) {  // load the kernel before the first timed launch
@@ -502,6 +1063,7 @@ int small_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round,
     PGC_CUDA(cudaFuncGetAttributes(&fa, k_small_jp_adg));
     once_flag(c.dev, 9) = true;
   }
+  if (int e = tiny_try(c, num, den, seed, round, color)) return e < 0 ? 0 : e;  // done on one cluster
   SmallArgs a;
   a.n = c.n;
   a.nnz = c.nnz;

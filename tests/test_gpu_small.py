@@ -24,15 +24,29 @@ pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
-@pytest.fixture(autouse=True)
-def small_path():
+VARIANT = {"v": None}
+
+
+@pytest.fixture(autouse=True, params=["grid", "cluster"])
+def small_path(request):
+    """Both variants of the path: the cooperative grid kernel (k_small_jp_adg)
+    and the one-cluster kernel with the state in distributed shared memory
+    (k_tiny_jp_adg, taken whenever the graph fits the cluster)."""
     pgc = pytest.importorskip("paper_2008_11321_b200")
     pgc.set_tuning("small_max_arcs", 1 << 40)
     pgc.set_tuning("small_max_avg", 1 << 30)
+    if request.param == "grid":
+        pgc.set_tuning("tiny_max_n", 0)
+    else:
+        pgc.set_tuning("tiny_max_n", 1 << 30)
+        pgc.set_tuning("tiny_max_arcs", 1 << 40)
+    VARIANT["v"] = request.param
     yield pgc
     pgc.set_tuning("small_max_arcs", 1 << 24)
     pgc.set_tuning("small_max_avg", 20)
     pgc.set_tuning("small_blocks_per_sm", 0)
+    pgc.set_tuning("tiny_max_n", 1 << 17)
+    pgc.set_tuning("tiny_max_arcs", 1 << 22)
     pgc.set_tuning("levels", 0)
 
 
@@ -48,7 +62,14 @@ def assert_parity(pgc, g, num, den, seed, levels=True):
     rnd, color, T, K = pgc.color_jp_adg(off, col, num, den, seed)
     torch.cuda.synchronize()
     st = pgc.last_stats()
-    assert st["small_path"] == (1 if g.n > 0 else 0)
+    if g.n == 0:
+        assert st["small_path"] == 0
+    elif VARIANT["v"] == "grid":
+        assert st["small_path"] == 1
+    elif g.n <= 20000 and g.nnz <= 300000:   # fits 16 CTAs' shared memory (arrays + own rows)
+        assert st["small_path"] == 2 and st["core_ctas"] >= 2
+    else:   # the cluster kernel when it fits, else the grid kernel
+        assert st["small_path"] in (1, 2)
     r_or, st_or = O.adg(g, num, den)
     c_or, K_or, _, J_or = O.jp(g, r_or, seed, levels=True)
     r_gpu, c_gpu = rnd.cpu().numpy(), color.cpu().numpy()
@@ -144,14 +165,17 @@ def test_config_parity(small_path, name):
         assert_parity(small_path, g, num, den, 1)
 
 
-def test_default_heuristic_and_host_api():
-    """Defaults: ER and the grid take the one-kernel path, R-MAT 20 (mean
-    degree 30, a deep dense core) the multi-kernel one; the host-buffer entry
-    point gives the same result on the small path."""
-    pgc = pytest.importorskip("paper_2008_11321_b200")
-    pgc.set_tuning("small_max_arcs", 1 << 24)
-    pgc.set_tuning("small_max_avg", 20)
-    for name, want in (("er", 1), ("grid", 1), ("rmat20", 0)):
+def test_default_heuristic_and_host_api(small_path):
+    """Defaults: ER takes the one-cluster kernel, the grid the cooperative grid
+    kernel, R-MAT 20 (mean degree 30, a deep dense core) the multi-kernel
+    path; the host-buffer entry point gives the same result on the small path."""
+    if VARIANT["v"] != "grid":
+        pytest.skip("defaults: checked once")
+    pgc = small_path
+    for k, v in (("small_max_arcs", 1 << 24), ("small_max_avg", 20), ("tiny_max_n", 1 << 17),
+                 ("tiny_max_arcs", 1 << 22)):
+        pgc.set_tuning(k, v)
+    for name, want in (("er", 2), ("grid", 1), ("rmat20", 0)):
         g = gg.config_graph(name)
         off, col = dev(g)
         num, den = gg.CONFIGS[name][1][0]
@@ -163,7 +187,7 @@ def test_default_heuristic_and_host_api():
             h_c = torch.zeros(g.n, dtype=torch.int32).pin_memory()
             T2, K2 = pgc.color_jp_adg_host(torch.from_numpy(g.off), torch.from_numpy(g.col), num, den,
                                            1, h_r, h_c)
-            assert pgc.last_stats()["small_path"] == 1
+            assert pgc.last_stats()["small_path"] == 2
             assert (T2, K2) == (T, K)
             assert np.array_equal(h_r.numpy(), rnd.cpu().numpy())
             assert np.array_equal(h_c.numpy(), color.cpu().numpy())
