@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
   int nstamp = 0;
 #endif
   __shared__ int s_acc[kSmallWarps][32];
-  __shared__ unsigned long long s_mask[kSmallWarps][32];
+  __shared__ unsigned s_mask[kSmallWarps][32][2];  // GetColor windows (two 32-bit halves: native smem atomics)
   __shared__ unsigned long long s_red[kSmallWarps];
   __shared__ int32_t s_q[kSmallWarps][2][kSmallQ];  // per-warp append queues
   int32_t* q0 = s_q[threadIdx.x >> 5][0];
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
   const long long gwarp = tid >> 5, nwarps = nth >> 5;
   const int64_t n = a.n;
   s_acc[warp][lane] = 0;
-  s_mask[warp][lane] = 0;
+  s_mask[warp][lane][0] = s_mask[warp][lane][1] = 0;
   for (long long i = tid; i < kSmallSlots * kSmallFields * kSmallLine; i += nth) a.ctr[i] = 0;
   if (tid == 0) a.st->K = 0;
   grid.sync();
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
                   if (on[k]) {  // pred: colored in an earlier level
                     const int cb = cu[k] - 1 - wbase;
                     PGC_DCHECK(cb + wbase >= 0, u[k], cb + wbase);
-                    if (cb >= 0 && cb < 64) atomicOr(&s_mask[warp][own[k]], 1ull << cb);
+                    if (cb >= 0 && cb < 64) atomicOr(&s_mask[warp][own[k]][cb >> 5], 1u << (cb & 31));
                   }
                 } else if (first) {  // succ: count[u] -= 1; the last pred frees u
                   const int old = atomicSub(a.cnt + u[k], 1);
@@ -450,8 +450,9 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
             }
           }
           __syncwarp();
-          const unsigned long long m = s_mask[warp][lane];
-          s_mask[warp][lane] = 0;
+          const unsigned long long m =
+              ((unsigned long long)s_mask[warp][lane][1] << 32) | s_mask[warp][lane][0];
+          s_mask[warp][lane][0] = s_mask[warp][lane][1] = 0;
           if (need && ~m) {
             mycolor = wbase + __ffsll((long long)~m);
             need = false;
@@ -516,6 +517,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
 // partials in a 2-slot ring read by warp 0 of every CTA after the barrier.
 constexpr int kTinyBlock = 1024;
 constexpr int kTinyWarps = kTinyBlock / 32;
+static_assert(kTinyWarps == 32, "block sums: one lane of warp 0 per warp");
 constexpr int kTinyMaxC = 16;
 constexpr int kTinyArrays = 9;  // D, rnd, cnt, clr, U0, U1, R, F0, F1 (+ row starts, rows)
 enum { kTpUout = 0, kTpR = 1, kTpSumD = 2, kTpCut = 3, kTpPreds = 4, kTpFields = 5 };
@@ -548,7 +550,8 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
   __shared__ int s_nR, s_nUo, s_nown;
   __shared__ int s_fcnt[3];  // frontier lengths (ring: level mod 3); other CTAs push into them
   __shared__ int s_acc[kTinyWarps][32];
-  __shared__ unsigned long long s_mask[kTinyWarps][32];
+  __shared__ unsigned s_mask[kTinyWarps][32][2];
+  __shared__ unsigned long long s_wsum[kTinyWarps][2];
   const int C = 1 << a.cshift, cs = a.cshift, me = (int)cl.block_rank();
   const int nloc = a.nloc;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
@@ -576,7 +579,7 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
     if (me == 0) a.st->K = 0;
   }
   s_acc[warp][lane] = 0;
-  s_mask[warp][lane] = 0;
+  s_mask[warp][lane][0] = s_mask[warp][lane][1] = 0;
   // local row starts: a block scan of the own degrees (thread t: a contiguous chunk)
   {
     const int per = (nown + kTinyBlock - 1) / kTinyBlock;
@@ -685,11 +688,15 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
       if (valid && !sel) Uout[pu + __popc(bu & lanemask_lt())] = v;
     }
     sumD = warp_sum(sumD);
-    if (lane == 0 && sumD) atomicAdd(&s_part[par][kTpSumD], sumD);
+    if (lane == 0) s_wsum[warp][0] = sumD;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      s_part[par][kTpR] = (unsigned long long)s_nR;
-      s_part[par][kTpUout] = (unsigned long long)s_nUo;
+    if (warp == 0) {  // the warp sums of the block, one lane each
+      const unsigned long long t = warp_sum(s_wsum[lane][0]);
+      if (lane == 0) {
+        s_part[par][kTpSumD] = t;
+        s_part[par][kTpR] = (unsigned long long)s_nR;
+        s_part[par][kTpUout] = (unsigned long long)s_nUo;
+      }
     }
     cl.sync();
     SMALL_STAMP();
@@ -758,8 +765,16 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
     cut = warp_sum(cut);
     preds = warp_sum(preds);
     if (lane == 0) {
-      if (cut) atomicAdd(&s_part[par][kTpCut], cut);
-      if (preds) atomicAdd(&s_part[par][kTpPreds], preds);
+      s_wsum[warp][0] = cut;
+      s_wsum[warp][1] = preds;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned long long t0 = warp_sum(s_wsum[lane][0]), t1 = warp_sum(s_wsum[lane][1]);
+      if (lane == 0) {
+        s_part[par][kTpCut] = t0;
+        s_part[par][kTpPreds] = t1;
+      }
     }
     cl.sync();
     SMALL_STAMP();
@@ -872,7 +887,7 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
                   if (on[k]) {
                     const int cb = cu[k] - 1 - wbase;
                     PGC_DCHECK(cb + wbase >= 0, u[k], cb + wbase);
-                    if (cb >= 0 && cb < 64) atomicOr(&s_mask[warp][own[k]], 1ull << cb);
+                    if (cb >= 0 && cb < 64) atomicOr(&s_mask[warp][own[k]][cb >> 5], 1u << (cb & 31));
                   }
                 } else if (first) {
                   oldc[k] = atomicSub(at(cnt, u[k]), 1);
@@ -900,8 +915,9 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
             }
           }
           __syncwarp();
-          const unsigned long long m = s_mask[warp][lane];
-          s_mask[warp][lane] = 0;
+          const unsigned long long m =
+              ((unsigned long long)s_mask[warp][lane][1] << 32) | s_mask[warp][lane][0];
+          s_mask[warp][lane][0] = s_mask[warp][lane][1] = 0;
           if (need && ~m) {
             mycolor = wbase + __ffsll((long long)~m);
             need = false;
