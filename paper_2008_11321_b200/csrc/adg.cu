@@ -1005,6 +1005,7 @@ static int launch_update(Ctx& c, const Arc<MODE>& A, const int32_t* Uin = nullpt
 
 int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, int mode,
             int32_t* color_zero, int rule) {
+  NvtxRange nvtx_("pgc ADG (Alg. 1)");
   PGC_CHK_SIZES(c);
   const int B = 256;
   const int G = grid_for(c, 8);
@@ -1197,6 +1198,7 @@ int baseline_key_run(Ctx& c, int kind, int32_t* key) {
 }
 
 int jp_setup_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color) {
+  NvtxRange nvtx_("pgc JP Part 1");
   PGC_CHK_SIZES(c);
   const int G = grid_for(c, 8);
   PGC_LAUNCH(c, kGAdgOther, "k_state_reset_jp", k_state_reset_jp<<<1, 1, 0, c.st>>>(c.state));

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kItrBlock) k_itr_partition(ItrArgs a) {
 }
 
 int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, long long* passes) {
+  NvtxRange nvtx_("pgc DEC-ADG-ITR partitions");
   PGC_CHK_SIZES(c);
   *passes = 0;
   if (c.n == 0) return 0;

@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(1024) k_order_top(State* st, const int32_t* __
 
 int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known, bool idkey,
                  bool defer) {
+  NvtxRange nvtx_("pgc JP priority order");
   PGC_CHK_SIZES(c);
   int idshift = 0;
   if (idkey) {
@@ -755,10 +756,15 @@ __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ r
   }
 }
 
-__global__ void k_core_pos(const int4* __restrict__ rec, const State* st, int32_t* __restrict__ pos) {
+// pos[v] = core position of v; also clears the per-vertex list states of the
+// list rewrite beside the core (`ready`, when it runs there): one launch, no memset
+__global__ void k_core_pos(const int4* __restrict__ rec, const State* st, int32_t* __restrict__ pos,
+                           int32_t* __restrict__ ready) {
   const int NC = st->core_n;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < NC; p += gridDim.x * blockDim.x)
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < NC; p += gridDim.x * blockDim.x) {
     pos[rec[p].x] = p;
+    if (ready) ready[p] = 0;
+  }
 }
 
 // One warp rewrites core vertex p's pred list in place (P slot, int32 ids ->
@@ -1794,21 +1800,32 @@ __global__ void k_jp_reset(State* st, int nonempty) {
 
 // Largest cluster size (power of two <= want) that k_jp_core can launch with
 // `smem` dynamic bytes; 0 if none.
+// The attributes are set once per device (the dynamic shared memory opt-in at
+// the largest core's size) and the answer is cached per (device, want, smem):
+// the occupancy query sat on the critical path of every call (the host is
+// between k_core_select's read-back and the core launch; 35 us gap in the
+// kernel timeline, profiles/r2_b/timeline_rmat24.json).
 static int core_cluster_size(int dev, int want, size_t smem) {
   bool& attr_done = once_flag(dev, 8);  // per device: attributes belong to one device
   if (!attr_done) {
-    if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+    if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
         cudaSuccess)
-      attr_done = true;
-    else
       cudaGetLastError();  // then only portable sizes (<= 8) are found below
+    // the largest core's size (64 KB + 2 x 65 536 B): every later launch fits under it
+    if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kCoreFixedSmem + 2 * (size_t)kCoreCap)) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;  // (retried on the next call)
+    }
+    attr_done = true;
   }
-  if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  for (int C = want; C >= 1; C >>= 1) {
+  struct E { int dev, want; size_t smem; int C; };
+  static thread_local E cache[16];
+  static thread_local int ncache = 0;
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].dev == dev && cache[i].want == want && cache[i].smem == smem) return cache[i].C;
+  int found = 0;
+  for (int C = want; C >= 1 && !found; C >>= 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(kCoreBlock);
@@ -1822,10 +1839,12 @@ static int core_cluster_size(int dev, int want, size_t smem) {
     cfg.numAttrs = 1;
     int nclusters = 0;
     if (cudaOccupancyMaxActiveClusters(&nclusters, k_jp_core, &cfg) == cudaSuccess && nclusters >= 1)
-      return C;
-    cudaGetLastError();
+      found = C;
+    else
+      cudaGetLastError();
   }
-  return 0;
+  cache[ncache < 16 ? ncache++ : 15] = {dev, want, smem, found};
+  return found;
 }
 
 static int pow2_floor(int x) {
@@ -1835,6 +1854,7 @@ static int pow2_floor(int x) {
 }
 
 int jp_color_run(Ctx& c, int32_t* color) {
+  NvtxRange nvtx_("pgc JP Part 2 (core + bulk)");
   PGC_CHK_SIZES(c);
   PGC_LAUNCH(c, kGJp, "k_jp_reset", k_jp_reset<<<1, 1, 0, c.st>>>(c.state, c.n > 0 ? 1 : 0));
   int64_t n_order = 0;
@@ -1913,7 +1933,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
     int32_t* pos = c.hist1 + c.lay.range_cap;
     if (C > 0)
       PGC_LAUNCH(c, kGCore, "k_core_pos",
-                 k_core_pos<<<c.nsm * 4, 256, 0, c.st>>>(c.rec, c.state, pos));
+                 k_core_pos<<<c.nsm * 4, 256, 0, c.st>>>(c.rec, c.state, pos, ready));
     auto lists = [&]() -> int {
       PGC_LAUNCH(c, kGCore, "k_core_lists",
                  k_core_lists<<<c.nsm * 8, 256, 0, c.st>>>(c.rec, pos, c.P, c.state, ready));
@@ -1980,8 +2000,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
         for (int i = 0; i < 2; ++i) PGC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
       }
       static_assert(65535 * 4 <= 2 * kFilterBytes, "list states fit the filter buffers");
-      PGC_CUDA(cudaMemsetAsync(ready, 0, 4 * (size_t)NC, c.st));
-      PGC_CUDA(cudaEventRecord(ev[0], c.st));
+      PGC_CUDA(cudaEventRecord(ev[0], c.st));  // (ready[] was cleared by k_core_pos)
       if (int e = core()) return e;
       PGC_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
       const cudaStream_t main = c.st;

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys/ncu (no-ops without a tool)
 
 namespace pgc {
 
@@ -217,6 +218,9 @@ int log_end(Ctx& c);
 // A per-thread, per-device "done once" flag (function attributes such as the
 // dynamic shared memory opt-in apply to the device they were set on, so a
 // thread that drives two GPUs must set them on each).  slot < kOnceSlots.
+// Slots: 0-4 k_update_heavy_f per Arc mode (adg.cu), 8 k_jp_core attributes,
+// 9 side-stream kernels loaded (jp.cu), 10 k_tiny_jp_adg attributes,
+// 11 k_small_jp_adg loaded (small.cu).
 constexpr int kOnceSlots = 16;
 constexpr int kMaxDevices = 64;
 bool& once_flag(int dev, int slot);
@@ -245,6 +249,15 @@ inline void chk_sizes(const Ctx& c) {
   do {                  \
   } while (0)
 #endif
+
+// An NVTX range over a host phase (entry points, ADG, the priority order,
+// the JP kernels): the phases show up by name in nsys / ncu --nvtx.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Launch a kernel (variadic so the <<<...>>> commas survive), check the launch,
 // account it and time it in `group`.
