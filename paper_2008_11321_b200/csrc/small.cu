@@ -109,6 +109,34 @@ __device__ __forceinline__ void wq_push(int32_t* q, int& fill, bool flag, int va
   fill += __popc(b);
 }
 
+// L2 policy for the grid kernel: the per-vertex state it gathers at random
+// (round, color, D, count) is kept (evict-last) and the arrays it streams
+// through (col, the lists) go first -- on the 2048^2 grid the state plus the
+// CSR exceed the 126 MB L2 (ncu: 1.4 GB DRAM per step against 0.59 GB of
+// algorithmic bytes before the hints).  Loads bypass L1 (.cg): other blocks
+// wrote the state in earlier phases.
+__device__ __forceinline__ int ldcg_keep(const int32_t* a) {
+#ifdef PGC_NO_L2HINT
+  return __ldcg(a);
+#else
+  int v;
+  asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(l2_keep_policy()));
+  return v;
+#endif
+}
+__device__ __forceinline__ int atom_sub_keep(int32_t* a) {
+#ifdef PGC_NO_L2HINT
+  return atomicSub(a, 1);
+#else
+  int v;
+  asm volatile("atom.global.add.L2::cache_hint.s32 %0, [%1], %2, %3;"
+               : "=r"(v)
+               : "l"(a), "r"(-1), "l"(l2_keep_policy())
+               : "memory");
+  return v;
+#endif
+}
+
 // Owner lane of flattened arc j: the largest lane s with start_s <= j (lanes
 // with no arcs share the next lane's start and are never picked for j < total).
 __device__ __forceinline__ int owner_of(int start, int j) {
@@ -230,18 +258,18 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
         for (int k = 0; k < kSelK; ++k) {
           d[k] = (int)(o1[k] - o0[k]);
           if (valid[k]) {
-            a.D[v[k]] = d[k];
-            a.color[v[k]] = 0;
+            st_i32_keep(a.D + v[k], d[k]);
+            st_i32_keep(a.color + v[k], 0);
           }
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < kSelK; ++k) d[k] = valid[k] ? __ldcg(a.D + v[k]) : 0;
+        for (int k = 0; k < kSelK; ++k) d[k] = valid[k] ? ldcg_keep(a.D + v[k]) : 0;
       }
 #pragma unroll
       for (int k = 0; k < kSelK; ++k) {
         const bool sel = valid[k] && d[k] <= dmax;
-        if (valid[k] && (sel || l == 1)) a.round[v[k]] = sel ? l : 0;
+        if (valid[k] && (sel || l == 1)) st_i32_keep(a.round + v[k], sel ? l : 0);
         if (sel) sumD += (unsigned long long)d[k];
         wq_push(q0, fr, sel, v[k], a.R, sctr(a.ctr, l, kSfR), n);
         wq_push(q1, fu, valid[k] && !sel, v[k], Uout, sctr(a.ctr, l, kSfUout), n);
@@ -283,18 +311,18 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
           const int64_t os = __shfl_sync(0xffffffffu, o, own[k]);
           const int ss = __shfl_sync(0xffffffffu, start, own[k]);
           PGC_DCHECK(j >= total || (os + (j - ss) >= 0 && os + (j - ss) < a.nnz), os + (j - ss), j);
-          u[k] = j < total ? __ldg(a.col + os + (j - ss)) : -1;
+          u[k] = j < total ? __ldcs(a.col + os + (j - ss)) : -1;
           PGC_DCHECK(u[k] < n, u[k], j);
         }
 #pragma unroll
-        for (int k = 0; k < kSmallUnroll; ++k) ru[k] = u[k] >= 0 ? __ldcg(a.round + u[k]) : -1;
+        for (int k = 0; k < kSmallUnroll; ++k) ru[k] = u[k] >= 0 ? ldcg_keep(a.round + u[k]) : -1;
 #pragma unroll
         for (int k = 0; k < kSmallUnroll; ++k) {
           const uint64_t hs = __shfl_sync(0xffffffffu, hv, own[k]);
           bool pred = false;
           PGC_DCHECK(ru[k] <= l, u[k], ru[k] * 1000000ll + l);  // no round from the future
           if (ru[k] == 0) {  // alive: D[u] -= 1, u is a pred of v (later round)
-            atomicSub(a.D + u[k], 1);
+            red_dec_keep(a.D + u[k]);
             ++cut;
             pred = true;
           } else if (ru[k] == l) {
@@ -311,7 +339,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
       const int p = s_acc[warp][lane];
       s_acc[warp][lane] = 0;
       if (valid) {
-        a.cnt[v] = p;
+        st_i32_keep(a.cnt + v, p);
         preds += (unsigned long long)p;
       }
       wq_push(q0, ff, valid && p == 0, v, a.F[1], f_first, n);
@@ -387,7 +415,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
         PGC_DCHECK(!valid || __ldcg(a.cnt + v) == 0, v, __ldcg(a.cnt + v));
         const int64_t o = valid ? a.off[v] : 0;
         const int deg = valid ? (int)(a.off[v + 1] - o) : 0;
-        const int rv = valid ? __ldcg(a.round + v) : 0;
+        const int rv = valid ? ldcg_keep(a.round + v) : 0;
         const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
         int incl = deg;
 #pragma unroll
@@ -417,7 +445,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
               on[k] = __shfl_sync(0xffffffffu, (int)need, own[k]);  // every lane shuffles
               const bool scan = jj < total && (first || on[k]);
               PGC_DCHECK(!scan || os + (jj - ss) < a.nnz, os + (jj - ss), jj);
-              u[k] = scan ? __ldg(a.col + os + (jj - ss)) : -1;
+              u[k] = scan ? __ldcs(a.col + os + (jj - ss)) : -1;
               PGC_DCHECK(u[k] < n, u[k], jj);
             }
             // the neighbour's color is loaded beside its round (one dependent
@@ -425,8 +453,8 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
             int cu[kSmallUnroll];
 #pragma unroll
             for (int k = 0; k < kSmallUnroll; ++k) {
-              ru[k] = u[k] >= 0 ? __ldcg(a.round + u[k]) : -1;
-              cu[k] = u[k] >= 0 && on[k] ? __ldcg(a.color + u[k]) : 0;
+              ru[k] = u[k] >= 0 ? ldcg_keep(a.round + u[k]) : -1;
+              cu[k] = u[k] >= 0 && on[k] ? ldcg_keep(a.color + u[k]) : 0;
             }
 #pragma unroll
             for (int k = 0; k < kSmallUnroll; ++k) {
@@ -441,7 +469,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
                     if (cb >= 0 && cb < 64) atomicOr(&s_mask[warp][own[k]][cb >> 5], 1u << (cb & 31));
                   }
                 } else if (first) {  // succ: count[u] -= 1; the last pred frees u
-                  const int old = atomicSub(a.cnt + u[k], 1);
+                  const int old = atom_sub_keep(a.cnt + u[k]);
                   PGC_DCHECK(old >= 1, u[k], old);
                   freed = old == 1;
                 }
@@ -460,7 +488,7 @@ __global__ void __launch_bounds__(kSmallBlock) k_small_jp_adg(SmallArgs a) {
           __syncwarp();
         }
         if (valid) {
-          a.color[v] = mycolor;
+          st_i32_keep(a.color + v, mycolor);
           kmax = max(kmax, mycolor);
         }
       }

@@ -72,10 +72,14 @@ def main():
     lp = os.path.join(src, "launches.csv")
     if os.path.exists(lp):
         steps = launches(lp)
-        last = steps[-1]
+        # the last TIMED step: bench.py's extra untimed call with the levels
+        # pass (k_jp_levels, J) comes after the timed steps and is skipped
+        timed = [st for st in steps if "k_jp_levels" not in st]
+        last = (timed or steps)[-1]
         tot = sum(v[0] for v in last.values())
-        md.append(f"## Launch list (last full step of `{os.path.basename(src)}`; ncu "
-                  f"gpu__time_duration, cold-cache, serialised)\n")
+        md.append(f"## Launch list (last timed step of `{os.path.basename(src)}`; ncu "
+                  f"gpu__time_duration, cold-cache, serialised; the untimed levels call "
+                  f"is excluded)\n")
         md.append("| kernel | launches | ms | share |\n|---|---|---|---|")
         for k, (t, c) in sorted(last.items(), key=lambda x: -x[1][0]):
             md.append(f"| {k} | {c} | {t / 1e6:.3f} | {100 * t / tot:.1f}% |")

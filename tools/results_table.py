@@ -40,7 +40,8 @@ def main():
         cb = d.get("cpu_baseline", {})
         om = cb.get("oracle_ms", {})
         osec = (om.get("adg", 0) + om.get("jp", 0)) / 1e3 if om else None
-        e = tr.get(w)
+        small = bool(d.get("small_path"))
+        e = tr.get(w + "-small") if small else tr.get(w)
         dram = e["update_dram_bytes_per_step"] / (rf["ms_per_launch"] * 1e-3) / 1e9 if e else None
         par = d.get("parity", {})
         ok = all(par.get(k) for k in ("round", "color", "K")) if par else None
@@ -49,9 +50,13 @@ def main():
             f"| {name} | {c['n']:,} | {c['m']:,} | {c['eps']} | {d['rounds']} | {d['jp_levels']} | "
             f"{d['colors']} | {d.get('degeneracy')} | {t:.3f} | {d['value'] / 1e9:.2f} G | "
             f"{100 * rf['path']['frac_8tbs']:.1f}% | {100 * rf['path']['frac']:.1f}% | "
-            f"{100 * rf['frac']:.1f}% | {dram:.0f} | " if dram is not None else "— | ")
+            f"{100 * rf['frac']:.1f}%{'¹' if small else ''} | "
+            f"{(f'{dram:.0f}' + ('¹' if small else '')) if dram is not None else '—'} | ")
         out[-1] += (f"{osec:.2f} | {cb.get('value', 0) / 1e6:.1f} M | "
                     f"{'bit-exact' if ok else ('MISMATCH' if ok is False else '—')} |") if osec else "— | — | — |"
+    out.append("")
+    out.append("¹ one-kernel path (csrc/small.cu): the column is that kernel (the whole path), "
+               "not UPDATE.")
     print("\n".join(out))
 
 
