@@ -193,6 +193,16 @@ def test_default_heuristic_and_host_api(small_path):
             assert np.array_equal(h_c.numpy(), color.cpu().numpy())
 
 
+def test_cluster_fallback_when_rows_do_not_fit(small_path):
+    """A hub whose row does not fit its CTA's shared memory: the one-cluster
+    kernel leaves (every CTA checks every peer's fit) and the grid kernel runs;
+    the result is the same."""
+    n = 120001
+    g = gg.from_edges(n, [(0, i) for i in range(1, n)] + [(i, i + 1) for i in range(1, n - 1, 2)])
+    T, K = assert_parity(small_path, g, 1, 10, 4)
+    assert small_path.last_stats()["small_path"] == 1
+
+
 def test_repeats_identical(small_path):
     g = gg.config_graph("er")
     off, col = dev(g)
