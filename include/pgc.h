@@ -263,7 +263,8 @@ const char* pgc_last_error(void);
  *   "heavy_degree" >= 128 (ADG UPDATE edge-chunks rows longer than this),
  *   "chunk_arcs" >= 256, "block_threads" 64..1024 (multiple of 32),
  *   "jp_heavy_warps" 1..4 (warps per 8-warp bulk JP block serving vertices with
- *   more than 62 preds), "jp_heavy_sleep_max" / "jp_light_sleep_max" ns >= 0
+ *   more than 62 preds), "jp_heavy_batch" 1..64 (heavy tickets per atomic),
+ *   "jp_heavy_sleep_max" / "jp_light_sleep_max" ns >= 0
  *   (backoff caps of waiting bulk JP warps), "jp_watchdog_ms"
  *   (a stalled JP kernel returns PGC_EINTERNAL after this long; default 20000),
  *   "core_max" 0..65535 (JP core size cap; 0 disables the core engine),
@@ -279,6 +280,8 @@ const char* pgc_last_error(void);
  *   per-vertex state; default 1), "top_list" 0/1 (JP-ADG: ADG keeps the top
  *   rounds' vertex list so the split order's top part skips a pass over n;
  *   default 1), "filter_ratio", "core_tail_ns", "core_pass_ns", "core_near",
+ *   "core_tier2" 0..65535 (JP core: when the first cluster pass is capped at
+ *   core_max, a second pass over the next <= core_tier2 positions; 0 = off),
  *   "small_max_arcs" (pgc_color_jp_adg runs as one persistent kernel when
  *   nnz <= this and nnz <= "small_max_avg" * n; 0 disables; defaults 2^24, 20),
  *   "small_blocks_per_sm" 0..64 (that kernel's grid; 0 = occupancy),

@@ -1068,7 +1068,7 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                                  c.tune.filter_ratio > 0 ? c.filt : nullptr));
       if (save_top)
         PGC_LAUNCH(c, kGAdgOther, "k_top_save",
-                   k_top_save<<<c.nsm * 4, 256, 0, c.st>>>(l, Uin, c.state, c.Rl, c.tune.core_max));
+                   k_top_save<<<c.nsm * 4, 256, 0, c.st>>>(l, Uin, c.state, c.Rl, core_reach(c.tune)));
       if (l == 1 && c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
       if (c.tune.filter_ratio > 0 && mode != kAdgPull)
         PGC_LAUNCH(c, kGUpdate, "k_filter_build",

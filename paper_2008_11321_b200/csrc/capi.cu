@@ -605,6 +605,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"jp_watchdog_ms", 1, 3600000, nullptr, &g_tune.jp_watchdog_ms},
       {"filter_ratio", 0, 1 << 20, nullptr, &g_tune.filter_ratio},
       {"jp_heavy_warps", 1, 4, nullptr, &g_tune.jp_heavy_warps},
+      {"jp_heavy_batch", 1, 64, nullptr, &g_tune.jp_heavy_batch},
       {"jp_heavy_sleep_max", 0, 1000000, nullptr, &g_tune.jp_heavy_sleep_max},
       {"jp_light_sleep_max", 0, 1000000, nullptr, &g_tune.jp_light_sleep_max},
       {"core_max", 0, 65535, nullptr, &g_tune.core_max},
@@ -615,6 +616,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"core_tail_ns", 0, 100000, nullptr, &g_tune.core_tail_ns},
       {"core_pass_ns", 0, 100000, nullptr, &g_tune.core_pass_ns},
       {"core_near", 0, 512, nullptr, &g_tune.core_near},
+      {"core_tier2", 0, 65535, nullptr, &g_tune.core_tier2},
       {"itr_blocks_per_sm", 0, 64, nullptr, &g_tune.itr_blocks_per_sm},
       {"jp_split_overlap", 0, 1, nullptr, &g_tune.jp_split_overlap},
       {"update_atom", 0, 1, nullptr, &g_tune.update_atom},

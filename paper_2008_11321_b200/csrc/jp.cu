@@ -566,7 +566,7 @@ int jp_order_run(Ctx& c, const int32_t* round, uint64_t seed_, bool range_known,
   const int32_t* top_list = defer && range_known && c.top_list ? c.Rl : nullptr;
   if (defer)
     PGC_LAUNCH(c, kGOrder, "k_order_top",
-               k_order_top<<<1, 1024, 0, c.st>>>(c.state, c.hist1, c.base1, L, c.tune.core_max));
+               k_order_top<<<1, 1024, 0, c.st>>>(c.state, c.hist1, c.base1, L, core_reach(c.tune)));
   PGC_LAUNCH(c, kGOrder, "k_zero_i32_dev",
              k_zero_i32_dev<<<G, 256, 0, c.st>>>(c.bcnt, &c.state->nbuckets, 1));
   PGC_LAUNCH(c, kGOrder, "k_hist2",
@@ -684,7 +684,7 @@ constexpr int kCoreFixedSmem = kCoreWarps * kCoreWin + kCoreWarps * kCorePend * 
 __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ rec,
                                                       State* st,
                                                       int core_max, int min_avg,
-                                                      long long arc_cap) {
+                                                      long long arc_cap, int tier2_max) {
   // warp w scans the contiguous chunk [wb, we) of the prefix, lanes reading
   // consecutive records, kCsU strips in flight: pass 1 sums the chunk, a
   // block scan of the warp sums gives each chunk's base, pass 2 evaluates
@@ -751,7 +751,13 @@ __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ r
   atomicMax(&s_best, best);
   __syncthreads();
   if (threadIdx.x == 0) {
-    st->core_n = (int)(s_best >> 32);
+    // tier 2: when the dense prefix runs into the cap, the next <= tier2_max
+    // positions get a second cluster pass after the first (the priority
+    // prefix of length NC1 + NC2 is closed under pred as well)
+    const int nc1 = (int)(s_best >> 32);
+    const int nc2 = (nc1 == core_max && tier2_max > 0) ? min(tier2_max, no - nc1) : 0;
+    st->core_n1 = nc1;
+    st->core_n = nc1 + nc2;
     st->core_arcs = (long long)(s_best & 0xffffffffull);
   }
 }
@@ -763,7 +769,7 @@ __global__ void k_core_pos(const int4* __restrict__ rec, const State* st, int32_
   const int NC = st->core_n;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < NC; p += gridDim.x * blockDim.x) {
     pos[rec[p].x] = p;
-    if (ready) ready[p] = 0;
+    if (ready && p < st->core_n1) ready[p] = 0;
   }
 }
 
@@ -814,7 +820,7 @@ __device__ __forceinline__ void list_release(int32_t* ready, int p) {
 __global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __restrict__ pos,
                              int32_t* P, const State* st, int32_t* ready) {
   const int lane = lane_id();
-  const int NC = st->core_n;
+  const int NC = st->core_n1;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < NC; p += nw) {
     if (ready) {
@@ -824,6 +830,39 @@ __global__ void k_core_lists(const int4* __restrict__ rec, const int32_t* __rest
     }
     core_list_rewrite(rec[p], pos, P);
     if (ready && lane == 0) list_release(ready, p);
+  }
+}
+
+// Tier 2's lists (positions [core_n1, core_n)), rewritten in place to int32
+// codes: a pred in tier 2 -> its tier-2 position (>= 0), a pred in tier 1 ->
+// -(id + 1) (its color is final when tier 2 runs: read from color[] once).
+// Warp per vertex, strips of loads then pos gathers in flight.
+__global__ void k_core2_lists(const int4* __restrict__ rec, const int32_t* __restrict__ pos,
+                              int32_t* P, const State* st) {
+  const int lane = lane_id();
+  const int N1 = st->core_n1, NC = st->core_n;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  constexpr int kS = 8;
+  for (int p = N1 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); p < NC; p += nw) {
+    const int4 r = rec[p];
+    const int np = r.y;
+    int32_t* L = P + lo_hi(r.z, r.w);
+    for (int i0 = 0; i0 < np; i0 += 32 * kS) {
+      int x[kS], y[kS];
+#pragma unroll
+      for (int k = 0; k < kS; ++k) {
+        const int i = i0 + 32 * k + lane;
+        x[k] = i < np ? L[i] : -1;
+      }
+#pragma unroll
+      for (int k = 0; k < kS; ++k) y[k] = x[k] >= 0 ? pos[x[k]] : 0;
+#pragma unroll
+      for (int k = 0; k < kS; ++k) {
+        const int i = i0 + 32 * k + lane;
+        PGC_DCHECK(i >= np || (y[k] >= 0 && y[k] < p), y[k], p);  // a pred precedes p
+        if (i < np) L[i] = y[k] >= N1 ? y[k] - N1 : -(x[k] + 1);
+      }
+    }
   }
 }
 
@@ -912,6 +951,52 @@ __device__ __forceinline__ int core_scan(const uint16_t* __restrict__ L, int np,
   return np;
 }
 
+// Tier 2's scan: int32 codes (k_core2_lists), one per lane and strip; a
+// tier-1 pred's color comes from color[] (final), a tier-2 pred's from the
+// replica (pending while 0).  Same contract as core_scan.
+__device__ __forceinline__ int core_scan2(const int32_t* __restrict__ L, int np, int from,
+                                          const uint16_t* cc, const int32_t* color, uint8_t* bm,
+                                          int wbase, uint16_t* plist, int& npend, int& qmax) {
+  const int lane = lane_id();
+  const unsigned lt = lanemask_lt();
+  constexpr int kStep = 32 * kScanStrips;
+  constexpr int kNone = (int)0x80000000;
+  int w[kScanStrips];
+#pragma unroll
+  for (int k = 0; k < kScanStrips; ++k) {
+    const int i = from + 32 * k + lane;
+    w[k] = i < np ? __ldcg(L + i) : kNone;
+  }
+  for (int i0 = from; i0 < np; i0 += kStep) {
+    int wn[kScanStrips], cv[kScanStrips];
+#pragma unroll
+    for (int k = 0; k < kScanStrips; ++k) {
+      const int i = i0 + kStep + 32 * k + lane;
+      wn[k] = i < np ? __ldcg(L + i) : kNone;
+    }
+#pragma unroll
+    for (int k = 0; k < kScanStrips; ++k)
+      cv[k] = w[k] >= 0 ? ld_vol_u16(cc + w[k]) : (w[k] != kNone ? ld_relaxed(color + (-w[k] - 1)) : 1);
+#pragma unroll
+    for (int k = 0; k < kScanStrips; ++k) {
+      const bool pend = w[k] >= 0 && cv[k] == 0;
+      PGC_DCHECK(w[k] >= 0 || w[k] == kNone || cv[k] > 0, -w[k] - 1, cv[k]);  // tier 1 is final
+      const unsigned b = __ballot_sync(0xffffffffu, pend);
+      if (npend + __popc(b) > kCorePend) return i0 + 32 * k;  // strips before k are complete
+      if (w[k] != kNone && cv[k]) bmap_mark(bm, cv[k], wbase, kCoreWin);
+      if (pend) {
+        plist[npend + __popc(b & lt)] = (uint16_t)w[k];
+        qmax = max(qmax, w[k]);
+      }
+      npend += __popc(b);
+    }
+#pragma unroll
+    for (int k = 0; k < kScanStrips; ++k) w[k] = wn[k];
+  }
+  return np;
+}
+
+template <bool T2>
 __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restrict__ rec,
                                                            int32_t* P,  // pred lists (u16 core positions; rewritten here if claimed)
                                                            int32_t* color, State* st,
@@ -921,7 +1006,8 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
                                                            unsigned pass_ns, int near_n,
                                                            unsigned long long watchdog_ns,
                                                            int32_t* ready,
-                                                           const int32_t* __restrict__ pos) {
+                                                           const int32_t* __restrict__ pos,
+                                                           int NC, int base) {
   // dynamic shared memory: bitmaps | pending lists | color replica [NC] (0 = uncolored)
   extern __shared__ __align__(16) unsigned char s_dyn[];
   uint8_t* s_bm = s_dyn;
@@ -932,7 +1018,6 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
   cg::cluster_group cl = cg::this_cluster();
   const int C = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
-  const int NC = st->core_n;
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
   for (int i = threadIdx.x; i < NC; i += blockDim.x) s_cc[i] = 0;
@@ -960,11 +1045,12 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
     // chain hops inside a run stay in local shared memory
     const int p = (rank + C * (k / kCoreRun)) * kCoreRun + (k % kCoreRun);
     if (p >= NC) break;
-    const int4 r = rec[p];
+    const int4 r = rec[base + p];
     const int np = r.y;
     const uint16_t* L = reinterpret_cast<const uint16_t*>(P + lo_hi(r.z, r.w));
+    const int32_t* L32 = P + lo_hi(r.z, r.w);  // tier 2: int32 codes
     const int vcore = r.x;
-    if (ready) {  // k_core_lists runs beside this kernel: p's list must be done
+    if (!T2 && ready) {  // k_core_lists runs beside this kernel: p's list must be done
       int act = 0;  // 0: done, 1: rewrite it here, 2: watchdog
       if (lane == 0) {
         const unsigned long long t_give = globaltimer() + 20000;  // 20 us
@@ -1009,7 +1095,8 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
       bmap_clear(bm, kCoreWin);
       __syncwarp();
       int npend = 0, qmax = -1;
-      int over = core_scan(L, np, 0, s_cc, bm, wbase, plist, npend, qmax);
+      int over = T2 ? core_scan2(L32, np, 0, s_cc, color, bm, wbase, plist, npend, qmax)
+                    : core_scan(L, np, 0, s_cc, bm, wbase, plist, npend, qmax);
       __syncwarp();
       // zi = the GetColor candidate (first unused color of the window, 0-based),
       // kept current as pending colors arrive so that the last arrival costs
@@ -1023,7 +1110,8 @@ __global__ void __launch_bounds__(kCoreBlock, 1) k_jp_core(const int4* __restric
       for (;;) {
         if (npend == 0) {
           if (over >= np) break;
-          over = core_scan(L, np, over, s_cc, bm, wbase, plist, npend, qmax);
+          over = T2 ? core_scan2(L32, np, over, s_cc, color, bm, wbase, plist, npend, qmax)
+                    : core_scan(L, np, over, s_cc, bm, wbase, plist, npend, qmax);
           __syncwarp();
           zi = bmap_next_zero<kCoreWin>(bm, zi);
           continue;
@@ -1377,7 +1465,8 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
                                                      const int4* __restrict__ lrec,
                                                      const int32_t* __restrict__ round,
                                                      uint64_t seed, int32_t* color,
-                                                     State* st, int heavy_warps, unsigned heavy_sleep_max,
+                                                     State* st, int heavy_warps, int heavy_batch,
+                                                     unsigned heavy_sleep_max,
                                                      unsigned light_sleep_max,
                                                      unsigned long long* tr_grab,
                                                      unsigned long long* tr_done,
@@ -1396,10 +1485,18 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
     unsigned long long* pkey = s_pkey[warp];
     // the next ticket and its (vertex, |pred|, P slot) are fetched one vertex
     // ahead, so their dependent loads overlap the current vertex
+    // tickets come `heavy_batch` at a time per warp (consecutive, so a held
+    // ticket is always of lower priority than the current one: the
+    // deadlock-freedom argument of the one-ahead prefetch holds for any batch)
+    int q_next = 0, q_end = 0;
     auto fetch = [&](int& t, int& v, int& np, int64_t& pb) {
-      t = 0;
-      if (lane == 0) t = atomicAdd(&st->ticket_heavy, 1);
-      t = __shfl_sync(0xffffffffu, t, 0);
+      if (q_next == q_end) {
+        int b = 0;
+        if (lane == 0) b = atomicAdd(&st->ticket_heavy, heavy_batch);
+        q_next = __shfl_sync(0xffffffffu, b, 0);
+        q_end = q_next + heavy_batch;
+      }
+      t = q_next++;
       if (t < nheavy) {
         const int4 r = __ldcs(hrec + t);
         v = r.x;
@@ -1743,12 +1840,13 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
 // tickets in priority order (deadlock-free: the highest-priority unfinished
 // vertex is held by a warp whose preds are all finished, or not yet handed
 // out, and then every warp is free), each lane polls its preds' levels (0 =
-// not yet).  Core positions p < core_n hold u16 core positions in their P slot
-// (k_core_lists), mapped back to ids through rec[].  lvl[] (n ints) starts at 0.
+// not yet).  Core positions p < core_n1 hold u16 core positions in their P slot
+// (k_core_lists), tier-2 positions int32 codes (k_core2_lists), both mapped
+// back to ids through rec[].  lvl[] (n ints) starts at 0.
 __global__ void k_jp_levels(const int4* __restrict__ rec, const int32_t* __restrict__ P,
                             int32_t* lvl, State* st, unsigned long long watchdog_ns) {
   const int lane = lane_id();
-  const int no = st->n_order, NC = st->core_n;
+  const int no = st->n_order, NC = st->core_n, N1 = st->core_n1;
   const unsigned long long deadline = globaltimer() + watchdog_ns;
   int jmax = 0;
   for (;;) {
@@ -1764,8 +1862,16 @@ __global__ void k_jp_levels(const int4* __restrict__ rec, const int32_t* __restr
     for (int i0 = 0; i0 < np && !stall; i0 += 32) {
       const int i = i0 + lane;
       int u = -1;
-      if (i < np)
-        u = t < NC ? rec[reinterpret_cast<const uint16_t*>(P + pb)[i]].x : P[pb + i];
+      if (i < np) {
+        if (t < N1) {  // tier 1: u16 core positions
+          u = rec[reinterpret_cast<const uint16_t*>(P + pb)[i]].x;
+        } else if (t < NC) {  // tier 2: int32 codes
+          const int code = P[pb + i];
+          u = code >= 0 ? rec[N1 + code].x : -code - 1;
+        } else {
+          u = P[pb + i];
+        }
+      }
       int x = u >= 0 ? ld_relaxed(lvl + u) : 1;
       while (__any_sync(0xffffffffu, x == 0)) {
         if (__shfl_sync(0xffffffffu, (int)stalled(st, deadline), 0)) {
@@ -1795,6 +1901,7 @@ __global__ void k_jp_reset(State* st, int nonempty) {
   st->nheavy = 0;
   st->K = nonempty;
   st->core_n = 0;
+  st->core_n1 = 0;
   st->core_arcs = 0;
 }
 
@@ -1808,14 +1915,16 @@ __global__ void k_jp_reset(State* st, int nonempty) {
 static int core_cluster_size(int dev, int want, size_t smem) {
   bool& attr_done = once_flag(dev, 8);  // per device: attributes belong to one device
   if (!attr_done) {
-    if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-        cudaSuccess)
-      cudaGetLastError();  // then only portable sizes (<= 8) are found below
-    // the largest core's size (64 KB + 2 x 65 536 B): every later launch fits under it
-    if (cudaFuncSetAttribute(k_jp_core, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kCoreFixedSmem + 2 * (size_t)kCoreCap)) != cudaSuccess) {
-      cudaGetLastError();
-      return 0;  // (retried on the next call)
+    // both tiers' instantiations (attributes are per function)
+    for (const void* f : {(const void*)k_jp_core<false>, (const void*)k_jp_core<true>}) {
+      if (cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        cudaGetLastError();  // then only portable sizes (<= 8) are found below
+      // the largest core's size (64 KB + 2 x 65 536 B): every later launch fits under it
+      if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(kCoreFixedSmem + 2 * (size_t)kCoreCap)) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;  // (retried on the next call)
+      }
     }
     attr_done = true;
   }
@@ -1838,7 +1947,8 @@ static int core_cluster_size(int dev, int want, size_t smem) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, k_jp_core, &cfg) == cudaSuccess && nclusters >= 1)
+    if (cudaOccupancyMaxActiveClusters(&nclusters, k_jp_core<false>, &cfg) == cudaSuccess &&
+        nclusters >= 1)
       found = C;
     else
       cudaGetLastError();
@@ -1846,6 +1956,8 @@ static int core_cluster_size(int dev, int want, size_t smem) {
   cache[ncache < 16 ? ncache++ : 15] = {dev, want, smem, found};
   return found;
 }
+
+static int cuda_ok(cudaError_t e, const char* where) { return e == cudaSuccess ? 0 : cuda_fail(e, where); }
 
 static int pow2_floor(int x) {
   int p = 1;
@@ -1860,17 +1972,19 @@ int jp_color_run(Ctx& c, int32_t* color) {
   int64_t n_order = 0;
   if (c.n > 0) {
     // --- core selection and its pred-list rewrite ---
-    int C = 0;
-    size_t core_smem = 0;
+    int C = 0, C2 = 0, NC1 = 0, NC2 = 0;
+    size_t core_smem = 0, core_smem2 = 0;
     if (c.tune.core_max > 0) {
       PGC_LAUNCH(c, kGCore, "k_core_select",
                  k_core_select<<<1, 1024, 0, c.st>>>(c.rec, c.state,
                                                       c.tune.core_max, c.tune.core_min_avg,
-                                                      c.tune.core_arc_cap));
+                                                      c.tune.core_arc_cap, c.tune.core_tier2));
       if (int e = sync_state(c)) return e;
-      const int NC = c.h_state->core_n;
+      const int NC = c.h_state->core_n1;
+      NC2 = c.h_state->core_n - NC;
       const long long arcs = c.h_state->core_arcs;
       core_smem = kCoreFixedSmem + (((size_t)NC * 2 + 15) & ~(size_t)15);
+      core_smem2 = kCoreFixedSmem + (((size_t)NC2 * 2 + 15) & ~(size_t)15);
       if (NC >= c.tune.core_min_n) {
         // CTAs for the arcs AND for the chain: each CTA keeps 32 vertices in
         // flight, and a long prefix needs many in flight even when its lists
@@ -1882,12 +1996,22 @@ int jp_color_run(Ctx& c, int32_t* color) {
                                         : (int)(by_arcs > by_verts ? by_arcs : by_verts);
         want = pow2_floor(want < 1 ? 1 : (want > 16 ? 16 : want));
         C = core_cluster_size(c.dev, want, core_smem);
+        if (C > 0 && NC2 > 0) C2 = core_cluster_size(c.dev, want, core_smem2);
       }
       if (C == 0) {
-        PGC_CUDA(cudaMemsetAsync(&c.state->core_n, 0, sizeof(int), c.st));
+        static_assert(offsetof(State, core_n1) == offsetof(State, core_n) + sizeof(int),
+                      "core_n, core_n1 adjacent");
+        PGC_CUDA(cudaMemsetAsync(&c.state->core_n, 0, 2 * sizeof(int), c.st));
+        NC1 = NC2 = 0;
       } else {
+        if (C2 == 0 && NC2 > 0) {  // no cluster for tier 2: the bulk takes its positions
+          PGC_CUDA(cudaMemcpyAsync(&c.state->core_n, &c.state->core_n1, sizeof(int),
+                                   cudaMemcpyDeviceToDevice, c.st));
+          NC2 = 0;
+        }
+        NC1 = NC;
         c.core_ctas = C;
-        c.core_n = NC;
+        c.core_n = NC + NC2;
       }
     }
     // --- bulk split of positions [core_n, n_order) (needs only the records)
@@ -1913,6 +2037,8 @@ int jp_color_run(Ctx& c, int32_t* color) {
         cudaFuncAttributes fa;
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_pos));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_core_lists));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_core2_lists));
+        PGC_CUDA(cudaFuncGetAttributes(&fa, k_jp_core<true>));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_hist2));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_scatter));
         PGC_CUDA(cudaFuncGetAttributes(&fa, k_bucket_sort));
@@ -1941,6 +2067,12 @@ int jp_color_run(Ctx& c, int32_t* color) {
     };
     if (C > 0 && !fork)
       if (int e = lists()) return e;
+    // tier 2's lists -> int32 codes (needs only pos[]: beside tier 1 when forked)
+    auto lists2 = [&]() -> int {
+      PGC_LAUNCH(c, kGCore, "k_core2_lists",
+                 k_core2_lists<<<c.nsm * 8, 256, 0, c.st>>>(c.rec, pos, c.P, c.state));
+      return 0;
+    };
     auto split = [&]() -> int {
       if (c.ord_pending)  // the rest of the priority order first (same stream)
         if (int e = jp_order_bottom(c)) return e;
@@ -1961,29 +2093,39 @@ int jp_color_run(Ctx& c, int32_t* color) {
                                                      color));
       return 0;
     };
-    auto core = [&]() -> int {
+    // tier 1: positions [0, NC1) with u16 lists (rewritten beside it when
+    // forked); tier 2: [NC1, NC1 + NC2) with int32 codes, after tier 1
+    auto core = [&](bool t2) -> int {
+      const int CC = t2 ? C2 : C;
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(C);
+      cfg.gridDim = dim3(CC);
       cfg.blockDim = dim3(kCoreBlock);
-      cfg.dynamicSmemBytes = core_smem;
+      cfg.dynamicSmemBytes = t2 ? core_smem2 : core_smem;
       cfg.stream = c.st;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.x = CC;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
       const unsigned long long wd = (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull;
-      PGC_LAUNCH(c, kGCore, "k_jp_core",
-                 PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core, (const int4*)c.rec, c.P, color,
-                                             c.state,
-                                             c.trace_grab, c.trace_done,
-                                             (unsigned)c.tune.core_spin_ns,
-                                             (unsigned)c.tune.core_tail_ns,
-                                             (unsigned)c.tune.core_pass_ns, c.tune.core_near, wd,
-                                             ready,
-                                             (const int32_t*)pos)));
+      if (t2)
+        PGC_LAUNCH(c, kGCore, "k_jp_core<tier2>",
+                   PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core<true>, (const int4*)c.rec, c.P, color,
+                                               c.state, c.trace_grab, c.trace_done,
+                                               (unsigned)c.tune.core_spin_ns,
+                                               (unsigned)c.tune.core_tail_ns,
+                                               (unsigned)c.tune.core_pass_ns, c.tune.core_near, wd,
+                                               (int32_t*)nullptr, (const int32_t*)pos, NC2, NC1)));
+      else
+        PGC_LAUNCH(c, kGCore, "k_jp_core",
+                   PGC_CUDA(cudaLaunchKernelEx(&cfg, k_jp_core<false>, (const int4*)c.rec, c.P, color,
+                                               c.state, c.trace_grab, c.trace_done,
+                                               (unsigned)c.tune.core_spin_ns,
+                                               (unsigned)c.tune.core_tail_ns,
+                                               (unsigned)c.tune.core_pass_ns, c.tune.core_near, wd,
+                                               ready, (const int32_t*)pos, NC1, 0)));
       return 0;
     };
     if (fork) {
@@ -1992,22 +2134,30 @@ int jp_color_run(Ctx& c, int32_t* color) {
       // stream; join before the bulk
       // per thread and device (streams and events belong to one device)
       static thread_local cudaStream_t sides[kMaxDevices] = {};
-      static thread_local cudaEvent_t evs[kMaxDevices][2] = {};
+      static thread_local cudaEvent_t evs[kMaxDevices][3] = {};
       cudaStream_t& side = sides[c.dev];
       cudaEvent_t* ev = evs[c.dev];
       if (!side) {
         PGC_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-        for (int i = 0; i < 2; ++i) PGC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        for (int i = 0; i < 3; ++i) PGC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
       }
       static_assert(65535 * 4 <= 2 * kFilterBytes, "list states fit the filter buffers");
       PGC_CUDA(cudaEventRecord(ev[0], c.st));  // (ready[] was cleared by k_core_pos)
-      if (int e = core()) return e;
+      if (int e = core(false)) return e;
       PGC_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
       const cudaStream_t main = c.st;
       c.st = side;
       int e = lists();
+      if (!e && NC2 > 0) {  // tier 2's lists next on the side stream; tier 2 waits for them
+        e = lists2();
+        if (!e) e = cuda_ok(cudaEventRecord(ev[2], side), "cudaEventRecord(tier2 lists)");
+      }
       if (!e) e = split();
       c.st = main;
+      if (!e && NC2 > 0) {
+        e = cuda_ok(cudaStreamWaitEvent(c.st, ev[2], 0), "cudaStreamWaitEvent(tier2 lists)");
+        if (!e) e = core(true);
+      }
       if (e) {
         cudaStreamSynchronize(side);  // nothing may stay in flight on the error path
         return e;
@@ -2015,9 +2165,15 @@ int jp_color_run(Ctx& c, int32_t* color) {
       PGC_CUDA(cudaEventRecord(ev[1], side));
       PGC_CUDA(cudaStreamWaitEvent(c.st, ev[1], 0));
     } else {
+      // (pos[] is read by the list rewrites: both before the split, which
+      // may reuse its space)
+      if (NC2 > 0)
+        if (int e = lists2()) return e;
       if (int e = split()) return e;
       if (C > 0)
-        if (int e = core()) return e;
+        if (int e = core(false)) return e;
+      if (NC2 > 0)
+        if (int e = core(true)) return e;
     }
     // --- bulk dataflow ---
     if (nbulk > 0) {
@@ -2025,7 +2181,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
       PGC_LAUNCH(c, kGJp, "k_jp_bulk",
                  k_jp_bulk<<<GB, kJpBlock, 0, c.st>>>(
                      c.off, c.P, c.npred, hrec, lrec, c.round_key, c.seed, color, c.state,
-                     c.tune.jp_heavy_warps, (unsigned)c.tune.jp_heavy_sleep_max,
+                     c.tune.jp_heavy_warps, c.tune.jp_heavy_batch, (unsigned)c.tune.jp_heavy_sleep_max,
                      (unsigned)c.tune.jp_light_sleep_max, c.trace_grab, c.trace_done,
                      (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
     }

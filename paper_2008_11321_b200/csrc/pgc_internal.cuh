@@ -63,6 +63,9 @@ struct State {
   int sorted_bot;              // split order: placed by the bottom part
   // JP
   int core_n;                  // |core| = length of the priority prefix colored by k_jp_core
+                               // (both tiers)
+  int core_n1;                 // tier 1 of the core: positions [0, core_n1) (u16 lists);
+                               // tier 2: [core_n1, core_n) (int32 codes, after tier 1)
   long long core_arcs;         // sum of |pred| over the core
   int nheavy;                  // bulk vertices with |pred| > kLightPredMax
   int nlight;                  // bulk vertices with 1 <= |pred| <= kLightPredMax
@@ -95,6 +98,7 @@ struct Tuning {
   int chunk_arcs = 1024;    // arcs per chunk work item
   int filter_ratio = 4;     // UPDATE: filtered heavy kernel once |U_l| * ratio <= filter bits (0 = off)
   int jp_heavy_warps = 4;         // warps per 8-warp bulk JP block serving heavy vertices (1..4)
+  int jp_heavy_batch = 1;         // heavy tickets per atomic (consecutive, per warp)
   int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
   int jp_light_sleep_max = 8192;  // ns, same for light warps
   int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
@@ -106,6 +110,9 @@ struct Tuning {
   int core_tail_ns = 0;           // JP core: sleep (ns) per poll of a warp in the tail
   int core_pass_ns = 0;           // JP core: min sleep (ns) between passes of a warp far from its tail
   int core_near = 0;              // JP core: warps with at most this many pending preds poll without backoff
+  int core_tier2 = 0;             // JP core: a second cluster pass over the next <= this many
+                                  // positions when tier 1 is capped (0 = off; measured slower
+                                  // on R-MAT 24 / Chung-Lu / R-MAT 20)
   int itr_blocks_per_sm = 0;      // DEC-ADG-ITR: blocks per SM of the cooperative kernel (0 = occupancy)
   int jp_split_overlap = 1;       // JP: run the bulk split on a side stream beside the core kernel
   int top_list = 1;               // JP-ADG: ADG saves the top rounds' list for the split order
@@ -127,6 +134,13 @@ struct Tuning {
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;
 };
+
+// Positions the JP core engine may cover (tier 1 + tier 2): the split
+// priority order sorts at least this many before the core starts.
+inline int core_reach(const Tuning& t) {
+  const long long r = (long long)t.core_max + (t.core_max > 0 ? t.core_tier2 : 0);
+  return r > 0x7fffffff ? 0x7fffffff : (int)r;
+}
 
 // Kernel groups for per-group device timing (pgc_stats.t_*_ms).
 enum Group { kGSelect = 0, kGUpdate = 1, kGAdgOther = 2, kGOrder = 3, kGCore = 4, kGJp = 5,

@@ -141,7 +141,8 @@ def tuning():
     defaults = {"core_max": 65535, "core_min_avg": 32, "core_min_n": 256, "core_ctas": 0,
                 "core_arc_cap": 1 << 30, "core_arcs_per_cta": 2 << 20, "jp_heavy_warps": 4,
                 "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
-                "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1, "top_list": 1}
+                "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1, "top_list": 1,
+                "core_tier2": 0}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
 
@@ -171,6 +172,29 @@ def test_core_engine_whole_graph_and_windows(tuning):
         tuning("core_max", cap)
         assert_parity(gg.rmat(12, 16, seed=2), 1, 10, 4)
         assert pgc_stats()["core_vertices"] == cap
+
+
+def test_core_engine_tier2(tuning):
+    """The second cluster pass (tier 2: int32 codes, tier-1 pred colors read
+    from color[]) after a capped tier 1, forked and serial, with J."""
+    for split in (1, 0):
+        tuning("jp_split_overlap", split)
+        for cap, t2 in ((1000, 2000), (300, 65535), (4096, 1)):
+            tuning("core_max", cap)
+            tuning("core_tier2", t2)
+            tuning("core_min_n", 1)
+            tuning("core_min_avg", 0)
+            for g in (gg.rmat(14, 16, seed=5), gg.rmat(13, 32, seed=8)):
+                assert_parity(g, 1, 10, 11)
+                st = pgc_stats()
+                assert st["core_vertices"] == min(cap + t2, g.n - int((g.degrees() == 0).sum()))
+    pgc = pytest.importorskip("paper_2008_11321_b200")
+    g = gg.rmat(14, 16, seed=5)
+    _, off, col = dev(g)
+    (rnd, color, T, K), J = _levels_gpu(pgc.color_jp_adg, off, col, 1, 10, 3)
+    r_or, _ = O.adg(g, 1, 10)
+    _, _, _, J_or = O.jp(g, r_or, 3, levels=True)
+    assert J == J_or
 
 
 def pgc_stats():

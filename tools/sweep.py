@@ -21,7 +21,7 @@ import graphgen as gg  # noqa: E402
 KEYS = {"hw": "jp_heavy_warps", "hsleep": "jp_heavy_sleep_max", "lsleep": "jp_light_sleep_max", "chunk": "chunk_arcs", "heavy_deg": "heavy_degree",
         "rps": "rounds_per_sync", "core": "core_max", "ctas": "core_ctas", "avg": "core_min_avg",
         "apc": "core_arcs_per_cta", "spin": "core_spin_ns", "near": "core_near", "pass": "core_pass_ns",
-        "tail": "core_tail_ns"}
+        "tail": "core_tail_ns", "hb": "jp_heavy_batch", "t2": "core_tier2"}
 
 
 def main():
