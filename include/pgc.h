@@ -287,7 +287,9 @@ const char* pgc_last_error(void);
  *   "small_blocks_per_sm" 0..64 (that kernel's grid; 0 = occupancy),
  *   "tiny_max_n" / "tiny_max_arcs" (that path runs on ONE thread-block cluster
  *   with the per-vertex state in distributed shared memory when n and nnz are
- *   at most these and the state fits; tiny_max_n = 0 disables; 2^17, 2^22).
+ *   at most these and the state fits; tiny_max_n = 0 disables; 2^17, 2^22),
+ *   "tiny_dataflow" 0/1 (that kernel's JP as a barrier-free dataflow, a thread
+ *   per own vertex; 0: frontier levels with cluster barriers; default 1).
  * Returns PGC_EINVAL for an unknown key or out-of-range value. */
 int pgc_set_tuning(const char* key, int64_t value);
 

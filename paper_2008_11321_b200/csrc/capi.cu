@@ -629,6 +629,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"small_blocks_per_sm", 0, 64, nullptr, &g_tune.small_blocks_per_sm},
       {"tiny_max_n", 0, 1ll << 30, &g_tune.tiny_max_n, nullptr},
       {"tiny_max_arcs", 0, 1ll << 40, &g_tune.tiny_max_arcs, nullptr},
+      {"tiny_dataflow", 0, 1, nullptr, &g_tune.tiny_dataflow},
       {"core_arcs_per_cta", 1, 1ll << 40, &g_tune.core_arcs_per_cta, nullptr},
   };
   for (const Key& k : keys)

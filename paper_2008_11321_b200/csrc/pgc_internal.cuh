@@ -130,6 +130,7 @@ struct Tuning {
   // nnz <= tiny_max_arcs; tiny_max_n = 0 disables
   long long tiny_max_n = 1ll << 17;
   long long tiny_max_arcs = 1ll << 22;
+  int tiny_dataflow = 1;                   // ... its JP as a barrier-free dataflow (else by levels)
   long long core_arc_cap = 1ll << 30;      // JP core: max sum |pred|
   long long core_arcs_per_cta = 2 << 20;   // JP core: pred arcs per cluster CTA
   int block_threads = 256;

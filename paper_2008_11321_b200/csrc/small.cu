@@ -547,6 +547,7 @@ constexpr int kTinyBlock = 1024;
 constexpr int kTinyWarps = kTinyBlock / 32;
 static_assert(kTinyWarps == 32, "block sums: one lane of warp 0 per warp");
 constexpr int kTinyMaxC = 16;
+constexpr int kTinyPer = 8;     // dataflow JP: own vertices per thread (nloc <= 8 x 1024)
 constexpr int kTinyArrays = 9;  // D, rnd, cnt, clr, U0, U1, R, F0, F1 (+ row starts, rows)
 enum { kTpUout = 0, kTpR = 1, kTpSumD = 2, kTpCut = 3, kTpPreds = 4, kTpFields = 5 };
 
@@ -563,6 +564,9 @@ struct TinyArgs {
   int nloc;     // per-CTA capacity of every array (>= ceil(n / C))
   int cshift;   // C = 1 << cshift
   long long adj_cap;  // per-CTA capacity of the copied rows (ints)
+  int dataflow;       // JP as a barrier-free dataflow (thread per own vertex), else by levels
+  int levels;         // compute J (the levels knob)
+  unsigned long long watchdog_ns;
 };
 
 __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
@@ -603,7 +607,10 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
   if (threadIdx.x == 0) {
     s_fcnt[0] = s_fcnt[1] = s_fcnt[2] = 0;
     s_nR = s_nUo = 0;
-    if (me == 0) a.st->K = 0;
+    if (me == 0) {
+      a.st->K = 0;
+      a.st->jp_levels = 0;
+    }
   }
   s_acc[warp][lane] = 0;
   s_mask[warp][lane][0] = s_mask[warp][lane][1] = 0;
@@ -848,7 +855,136 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
 
   // ---------------------------------------------------------------- JP
   int J = 0, kmax = 0;
-  if (!err) {
+  __shared__ int s_stall;
+  if (threadIdx.x == 0) s_stall = 0;
+  __syncthreads();
+  if (!err && a.dataflow) {
+    // Dataflow JP (Alg. 3 with its count[] Join, no level barriers): thread t
+    // owns the local vertices t, t + 1024, ... and colors them in decreasing
+    // priority, each once its count reaches 0 -- deadlock-free: the
+    // highest-priority uncolored vertex always has all preds colored and is
+    // the current vertex of its thread (a thread's earlier vertices have
+    // higher priority, so they are colored).  A pred's color (and level) is
+    // released before its decrement (cluster-scope fences); the decrement
+    // is a DSMEM atomic on the succ's count.
+    int32_t* lvl = Ul[0];  // JP levels (free after ADG)
+    int mine[kTinyPer];
+    int nm = 0;
+    for (int i = threadIdx.x; i < nown && nm < kTinyPer; i += kTinyBlock) mine[nm++] = i;
+    for (int x = 1; x < nm; ++x) {  // insertion sort, priority descending
+      const int y = mine[x];
+      const int ry = rnd[y];
+      const uint64_t hy = prio_hash(a.seed, (uint32_t)((y << cs) + me));
+      int z = x - 1;
+      while (z >= 0 && prio_gt(ry, hy, rnd[mine[z]], prio_hash(a.seed, (uint32_t)((mine[z] << cs) + me)))) {
+        mine[z + 1] = mine[z];
+        --z;
+      }
+      mine[z + 1] = y;
+    }
+    // warp-synchronous: every lane checks its current vertex's count, then the
+    // whole warp processes the ready ones one by one (lanes over the arcs):
+    // no divergent spinning inside a warp
+    const unsigned long long deadline = globaltimer() + a.watchdog_ns;
+    int q = 0;
+    unsigned ns = 0;
+    for (;;) {
+      const bool have = q < nm;
+      bool ready = false;
+      if (have) {  // acquire: a pred's color precedes its (release) decrement
+        int cv;
+        asm volatile("ld.acquire.cluster.b32 %0, [%1];" : "=r"(cv) : "l"(cnt + mine[q]) : "memory");
+        ready = cv == 0;
+      }
+      unsigned rb = __ballot_sync(0xffffffffu, ready);
+      if (!__any_sync(0xffffffffu, have)) break;
+      if (!rb) {
+        if (__shfl_sync(0xffffffffu, (int)(globaltimer() > deadline), 0)) {
+          if (lane == 0) s_stall = 1;
+          break;
+        }
+        if (ns) __nanosleep(ns);
+        ns = ns ? min(ns * 2, 128u) : 16u;
+        continue;
+      }
+      ns = 0;
+      while (rb) {
+        const int src = __ffs(rb) - 1;
+        rb &= rb - 1;
+        const int i = __shfl_sync(0xffffffffu, have ? mine[q < nm ? q : 0] : 0, src);
+        const int v = (i << cs) + me;
+        const int rv = rnd[i];
+        const uint64_t hv = prio_hash(a.seed, (uint32_t)v);
+        const int o = loff[i], d = loff[i + 1] - o;
+        int color = 0, lv = 0;
+        // the first 32 arcs' (u, pred?) stay in registers for the Join below
+        int u0 = -1;
+        bool pr0 = false;
+        for (int wbase = 0; !color; wbase += 64) {
+          unsigned long long m = 0;
+          for (int e0 = 0; e0 < d; e0 += 32) {
+            const int e = e0 + lane;
+            const int u = e < d ? ladj[o + e] : -1;
+            // round and color loaded together (one DSMEM round trip; the color
+            // is used only if u turns out to be a pred)
+            const int ru = u >= 0 ? *at(rnd, u) : -1;
+            const int cl_u = u >= 0 ? *at(clr, u) : 0;
+            const bool pr = u >= 0 && prio_gt(ru, prio_hash(a.seed, (uint32_t)u), rv, hv);
+            if (e0 == 0 && wbase == 0) {
+              u0 = u;
+              pr0 = pr;
+            }
+            const int cu = pr ? cl_u : 0;
+            if (pr && a.levels && wbase == 0) lv = max(lv, *at(lvl, u));
+            PGC_DCHECK(!pr || cu > 0, u, cu);  // every pred is colored
+            const int cb = cu - 1 - wbase;
+            const bool in = pr && cb >= 0 && cb < 64;
+            // OR of the lanes' color bits: shuffle-reduce the 64-bit word
+            unsigned long long bit = in ? (1ull << cb) : 0ull;
+#pragma unroll
+            for (int s2 = 16; s2 > 0; s2 >>= 1) bit |= __shfl_xor_sync(0xffffffffu, bit, s2);
+            m |= bit;
+          }
+          if (~m) color = wbase + __ffsll((long long)~m);
+        }
+        lv = warp_max(lv);
+        if (lane == src) {
+          clr[i] = color;
+          if (a.levels) lvl[i] = lv + 1;
+        }
+        kmax = max(kmax, color);
+        J = max(J, lv + 1);
+        // Join: release decrements (the color store above precedes them)
+        __syncwarp();
+        for (int e0 = 0; e0 < d; e0 += 32) {
+          const int e = e0 + lane;
+          int u;
+          bool succ;
+          if (e0 == 0) {
+            u = u0;
+            succ = u0 >= 0 && !pr0;
+          } else {
+            u = e < d ? ladj[o + e] : -1;
+            const int ru = u >= 0 ? *at(rnd, u) : -1;
+            succ = u >= 0 && prio_gt(rv, hv, ru, prio_hash(a.seed, (uint32_t)u));
+          }
+          if (succ)
+            asm volatile("red.release.cluster.add.s32 [%0], %1;" ::"l"(at(cnt, u)), "r"(-1) : "memory");
+        }
+        if (lane == src) ++q;
+      }
+    }
+    J = a.levels ? J : 0;
+    cl.sync();  // every vertex colored; the peers' stall flags below
+    SMALL_STAMP();
+    if (threadIdx.x < 32) {
+      const int x = lane < C ? *cl.map_shared_rank(&s_stall, lane) : 0;
+      if (__any_sync(0xffffffffu, x != 0) && lane == 0) err = 9;
+    }
+    if (threadIdx.x == 0 && err == 9) s_stall = 2;
+    __syncthreads();
+    if (s_stall == 2) err = 9;
+  } else if (!err) {
     long long nF = 0;
     if (warp == 0) {
       long long x = lane < C ? *cl.map_shared_rank(&s_fcnt[1], lane) : 0;
@@ -982,6 +1118,10 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
   }
   kmax = warp_max(kmax);
   if (lane == 0 && kmax) atomicMax(&a.st->K, kmax);
+  if (a.dataflow) {  // J: a per-thread max here
+    J = warp_max(J);
+    if (lane == 0 && J) atomicMax(&a.st->jp_levels, J);
+  }
   if (me == 0 && threadIdx.x == 0) {
     State* st = a.st;
     st->T = l;
@@ -989,7 +1129,7 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_tiny_jp_adg(TinyArgs a) {
     st->sum_active = sum_active;
     st->cross = cross;
     st->pred_arcs = preds_total;
-    st->jp_levels = J;
+    if (!a.dataflow) st->jp_levels = J;
     st->err = err;
     st->done = 1;
     st->nU = nU;
@@ -1073,6 +1213,9 @@ static int tiny_try(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* 
   a.nloc = nloc;
   a.cshift = __builtin_ctz((unsigned)C);
   a.adj_cap = ((long long)smem - 4ll * ((long long)kTinyArrays * nloc + nloc + 1)) / 4;
+  a.dataflow = c.tune.tiny_dataflow && nloc <= kTinyPer * kTinyBlock;
+  a.levels = c.tune.levels;
+  a.watchdog_ns = (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(kTinyBlock);
@@ -1090,6 +1233,9 @@ static int tiny_try(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* 
   if (int e = sync_state(c)) return e;
   const State* h = c.h_state;
   if (h->err == 11) return 0;  // a CTA's rows did not fit its shared memory: the grid kernel
+  if (h->err == 9)
+    return fail(4, "JP (one-cluster dataflow) stalled: no progress within %d ms (watchdog)",
+                c.tune.jp_watchdog_ms);
   if (h->err == 7)
     return fail(4, "ADG round %d broke Lemma 1's per-round shrink (PAPER.md:761-771)", h->T);
   if (h->err) return fail(4, "ADG internal invariant failed (code %d)", h->err);

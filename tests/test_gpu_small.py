@@ -27,7 +27,7 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 VARIANT = {"v": None}
 
 
-@pytest.fixture(autouse=True, params=["grid", "cluster"])
+@pytest.fixture(autouse=True, params=["grid", "cluster", "cluster-levels"])
 def small_path(request):
     """Both variants of the path: the cooperative grid kernel (k_small_jp_adg)
     and the one-cluster kernel with the state in distributed shared memory
@@ -40,6 +40,8 @@ def small_path(request):
     else:
         pgc.set_tuning("tiny_max_n", 1 << 30)
         pgc.set_tuning("tiny_max_arcs", 1 << 40)
+        # the cluster kernel's JP: barrier-free dataflow (default) or frontier levels
+        pgc.set_tuning("tiny_dataflow", 0 if request.param == "cluster-levels" else 1)
     VARIANT["v"] = request.param
     yield pgc
     pgc.set_tuning("small_max_arcs", 1 << 24)
@@ -47,6 +49,7 @@ def small_path(request):
     pgc.set_tuning("small_blocks_per_sm", 0)
     pgc.set_tuning("tiny_max_n", 1 << 17)
     pgc.set_tuning("tiny_max_arcs", 1 << 22)
+    pgc.set_tuning("tiny_dataflow", 1)
     pgc.set_tuning("levels", 0)
 
 

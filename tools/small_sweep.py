@@ -40,5 +40,11 @@ for name in (sys.argv[1:] or ["er", "grid", "rmat20"]):
         st = pgc.last_stats()
         print(name, "small bps=%d" % bps, "%.3f ms" % t, "T", st["rounds"], "small", st["small_path"], flush=True)
     pgc.set_tuning("small_blocks_per_sm", 0)
+    for df in (0, 1):
+        pgc.set_tuning("tiny_dataflow", df)
+        t = timed(off, col, num, den)
+        st = pgc.last_stats()
+        print(name, "tiny_dataflow=%d" % df, "%.3f ms" % t, "small", st["small_path"], flush=True)
+    pgc.set_tuning("tiny_dataflow", 1)
     pgc.set_tuning("small_max_arcs", 1 << 24)
     pgc.set_tuning("small_max_avg", 20)
