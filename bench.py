@@ -331,6 +331,10 @@ def run_pgc(args):
         return pgc.color_jp_adg(off, col, num, den, args.seed, round_out=rnd, color_out=color)
 
     pgc.set_tuning("timing", 0)
+    # ablation hook: PGC_TUNE="key=value,key=value" (library tuning knobs)
+    for kv in filter(None, os.environ.get("PGC_TUNE", "").split(",")):
+        k, v = kv.split("=")
+        pgc.set_tuning(k.strip(), int(v))
     if args.serial_schedule:
         pgc.set_tuning("jp_split_overlap", 0)
     for _ in range(args.warmup):

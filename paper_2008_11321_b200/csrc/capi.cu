@@ -94,10 +94,16 @@ Layout make_layout(int64_t n, int64_t nnz) {
   const int64_t big = L.nb_cap > 2 * L.range_cap + 1 ? L.nb_cap : 2 * L.range_cap + 1;
   L.scan_tmp_cap = big / kScanTile + 4;
   L.scan_tmp = take(4 * (size_t)L.scan_tmp_cap);
-  // JP records: n in priority order, then the bulk's heavy list (> 62 preds,
-  // so at most nnz / 63 of them) and light list (< n)
-  L.rec_heavy_cap = (nnz / 63 < n ? nnz / 63 : n) + 1;
+  // JP records: n in priority order, then the bulk's heavy work
+  // list (> 62 preds, so at most nnz / 63 of them; a mega vertex adds at most
+  // |pred| / jp_mega_chunk items, nnz / kMinMegaChunk in all) and light list (< n)
+  L.rec_heavy_cap = (nnz / 63 < n ? nnz / 63 : n) + nnz / kMinMegaChunk + 1;
   L.rec = take(16 * (size_t)(L.rec_heavy_cap + 2 * n));
+  // per heavy item {mega index or -1, chunks}; per mega vertex (> kMinMegaPred
+  // preds: at most nnz / (kMinMegaPred + 1)) its used-color words and a counter
+  L.hmeta = take(8 * (size_t)L.rec_heavy_cap);
+  L.mega_cap = nnz / (kMinMegaPred + 1) + 1;
+  L.mega = take(4 * (size_t)(kMegaWords + 1) * L.mega_cap);
   L.filt = take(2 * (size_t)kFilterBytes);
   L.total = a;
   return L;
@@ -158,6 +164,8 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.scan_tmp = (int32_t*)(b + c.lay.scan_tmp);
   c.rec = (int4*)(b + c.lay.rec);
   c.filt = (uint32_t*)(b + c.lay.filt);
+  c.hmeta = (int2*)(b + c.lay.hmeta);
+  c.mega = (uint32_t*)(b + c.lay.mega);
   c.lrec = c.rec;  // ADG and JP never use their records at the same time
   // pinned host mirror of State (portable: usable from every device's streams)
   if (!g_hstate) PGC_CUDA(cudaHostAlloc((void**)&g_hstate, sizeof(State), cudaHostAllocPortable));
@@ -596,6 +604,10 @@ int pgc_set_tuning(const char* key, int64_t value) {
     g_tune.heavy_degree = (int)value;
     return PGC_OK;
   }
+  if (!strcmp(key, "jp_mega_pred") && (value == 0 || (value >= kMinMegaPred && value <= (1 << 30)))) {
+    g_tune.jp_mega_pred = (int)value;
+    return PGC_OK;
+  }
   if (!strcmp(key, "chunk_arcs") && value >= kMinChunk && value <= (1 << 24)) {
     g_tune.chunk_arcs = (int)value;
     return PGC_OK;
@@ -606,6 +618,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"filter_ratio", 0, 1 << 20, nullptr, &g_tune.filter_ratio},
       {"jp_heavy_warps", 1, 4, nullptr, &g_tune.jp_heavy_warps},
       {"jp_heavy_batch", 1, 64, nullptr, &g_tune.jp_heavy_batch},
+      {"jp_mega_chunk", kMinMegaChunk, kMegaBits, nullptr, &g_tune.jp_mega_chunk},
       {"jp_heavy_sleep_max", 0, 1000000, nullptr, &g_tune.jp_heavy_sleep_max},
       {"jp_light_sleep_max", 0, 1000000, nullptr, &g_tune.jp_light_sleep_max},
       {"core_max", 0, 65535, nullptr, &g_tune.core_max},
@@ -618,6 +631,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"core_near", 0, 512, nullptr, &g_tune.core_near},
       {"core_tier2", 0, 65535, nullptr, &g_tune.core_tier2},
       {"itr_blocks_per_sm", 0, 64, nullptr, &g_tune.itr_blocks_per_sm},
+      {"itr_members_per_warp", 1, 1024, nullptr, &g_tune.itr_members_per_warp},
       {"jp_split_overlap", 0, 1, nullptr, &g_tune.jp_split_overlap},
       {"update_atom", 0, 1, nullptr, &g_tune.update_atom},
       {"fuse_init", 0, 1, nullptr, &g_tune.fuse_init},

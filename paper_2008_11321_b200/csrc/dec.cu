@@ -37,6 +37,10 @@ namespace cg = cooperative_groups;
 
 constexpr int kItrWin = 1024;  // colors per byte-map window
 constexpr int kItrBlock = 256;
+#ifndef PGC_ITR_STRIPS
+#define PGC_ITR_STRIPS 4
+#endif
+constexpr int kItrStrips = PGC_ITR_STRIPS;  // strips of 32 neighbour loads in flight per pass step
 
 __device__ __forceinline__ int ldcg(const int32_t* p) { return __ldcg(p); }
 
@@ -185,11 +189,24 @@ __global__ void __launch_bounds__(kItrBlock) k_itr_partition(ItrArgs a) {
       const int64_t b = a.off[v];
       const int ni = ldcg(a.icnt + v), bs = ldcg(a.base + v);
       unsigned long long taken = 0;
-      for (int j0 = 0; j0 < ni; j0 += 32) {
-        const int j = j0 + lane;
-        const int c = j < ni ? ldcg(a.color + ldcg(a.P + b + j)) : 0;
-        const int d = c - bs;
-        if (c > 0 && d >= 0 && d < 64) taken |= 1ull << d;
+      // kItrStrips strips of 32 neighbours per step, all loads in flight (a
+      // dense partition's lists are hundreds long: one L2 round trip per
+      // strip would make every pass a chain of dependent loads)
+      for (int j0 = 0; j0 < ni; j0 += 32 * kItrStrips) {
+        int u[kItrStrips];
+#pragma unroll
+        for (int k = 0; k < kItrStrips; ++k) {
+          const int j = j0 + 32 * k + lane;
+          u[k] = j < ni ? ldcg(a.P + b + j) : -1;
+        }
+        int c[kItrStrips];
+#pragma unroll
+        for (int k = 0; k < kItrStrips; ++k) c[k] = u[k] >= 0 ? ldcg(a.color + u[k]) : 0;
+#pragma unroll
+        for (int k = 0; k < kItrStrips; ++k) {
+          const int d = c[k] - bs;
+          if (c[k] > 0 && d >= 0 && d < 64) taken |= 1ull << d;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) taken |= __shfl_xor_sync(0xffffffffu, taken, o);
@@ -217,13 +234,23 @@ __global__ void __launch_bounds__(kItrBlock) k_itr_partition(ItrArgs a) {
       const int64_t b = a.off[v];
       const int ni = ldcg(a.icnt + v);
       bool lose = false;
-      for (int j0 = 0; j0 < ni && !lose; j0 += 32) {
-        const int j = j0 + lane;
-        bool x = false;
-        if (j < ni) {
-          const int u = ldcg(a.P + b + j);
-          if (ldcg(a.color + u) == 0 && ldcg(a.tent + u) == tv) x = prio_hash(a.seed, (uint32_t)u) > hv;
+      for (int j0 = 0; j0 < ni && !lose; j0 += 32 * kItrStrips) {
+        int u[kItrStrips];
+#pragma unroll
+        for (int k = 0; k < kItrStrips; ++k) {
+          const int j = j0 + 32 * k + lane;
+          u[k] = j < ni ? ldcg(a.P + b + j) : -1;
         }
+        int c[kItrStrips], t[kItrStrips];
+#pragma unroll
+        for (int k = 0; k < kItrStrips; ++k) {
+          c[k] = u[k] >= 0 ? ldcg(a.color + u[k]) : 1;
+          t[k] = u[k] >= 0 ? ldcg(a.tent + u[k]) : 0;
+        }
+        bool x = false;
+#pragma unroll
+        for (int k = 0; k < kItrStrips; ++k)
+          if (c[k] == 0 && t[k] == tv) x |= prio_hash(a.seed, (uint32_t)u[k]) > hv;
         lose = __any_sync(0xffffffffu, x);
       }
       if (lane == 0) a.won[v] = lose ? 0 : 1;
@@ -303,8 +330,10 @@ int dec_itr_run(Ctx& c, const int32_t* round, uint64_t seed, int32_t* color, lon
     a.cl = cl;
     pbase += cl;
     PGC_LAUNCH(c, kGJp, "k_itr_prep", k_itr_prep<<<G, kItrBlock, 0, c.st>>>(a));
-    // passes: about one warp per 4 active vertices of the partition's start
-    const int want = (cl + 4 * (kItrBlock / 32) - 1) / (4 * (kItrBlock / 32));
+    // passes: about one warp per itr_members_per_warp active vertices of the
+    // partition's start
+    const int mpw = c.tune.itr_members_per_warp;
+    const int want = (cl + mpw * (kItrBlock / 32) - 1) / (mpw * (kItrBlock / 32));
     const int GP = want < G ? (want < 1 ? 1 : want) : G;
     void* args[] = {&a};
     PGC_LAUNCH(c, kGJp, "k_itr_partition",

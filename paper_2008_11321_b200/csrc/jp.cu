@@ -1310,13 +1310,19 @@ constexpr int kLV = PGC_LIGHT_VEC;  // 16-byte pred-id loads per first-pass step
 #endif
 constexpr int kLightSteps = PGC_LIGHT_STEPS;  // first-pass steps per lane per loop iteration
 
+// hflag = heavy work items of the vertex (1, or its pred chunks when it is a
+// mega vertex), lflag = 1 for a light vertex
+__device__ __forceinline__ int mega_chunks(int np, int mega_pred, int mega_chunk) {
+  return mega_pred > 0 && np > mega_pred ? (np + mega_chunk - 1) / mega_chunk : 1;
+}
 __global__ void k_bulk_flags(int64_t n, const int4* __restrict__ rec, const State* st,
-                             int32_t* __restrict__ hflag, int32_t* __restrict__ lflag) {
+                             int32_t* __restrict__ hflag, int32_t* __restrict__ lflag,
+                             int mega_pred, int mega_chunk) {
   const int NC = st->core_n;
   for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int np = rec[p].y;
-    hflag[p - NC] = np > kLightPredMax ? 1 : 0;
+    hflag[p - NC] = np > kLightPredMax ? mega_chunks(np, mega_pred, mega_chunk) : 0;
     lflag[p - NC] = np > 0 && np <= kLightPredMax ? 1 : 0;
   }
 }
@@ -1328,15 +1334,39 @@ __global__ void k_bulk_flags(int64_t n, const int4* __restrict__ rec, const Stat
 // counts of the heavy / light flags.
 __global__ void k_bulk_scatter(int64_t n, const int4* __restrict__ rec, State* st,
                                const int32_t* __restrict__ hpos, const int32_t* __restrict__ lpos,
-                               int4* __restrict__ hrec, int4* __restrict__ lrec, int32_t* color) {
+                               int4* __restrict__ hrec, int4* __restrict__ lrec, int32_t* color,
+                               int2* __restrict__ hmeta, uint32_t* __restrict__ mega,
+                               int64_t mega_cap, int mega_pred, int mega_chunk) {
   const int NC = st->core_n;
   bool root = false;
   for (int64_t p = NC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int4 r = rec[p];
     const int64_t i = p - NC;
-    if (r.y > kLightPredMax) hrec[hpos[i]] = r;
-    else if (r.y > 0) lrec[lpos[i]] = r;
+    if (r.y > kLightPredMax) {
+      const int nch = mega_chunks(r.y, mega_pred, mega_chunk);
+      const int h = hpos[i];
+      if (nch == 1) {
+        hrec[h] = r;
+        hmeta[h] = make_int2(-1, 1);
+      } else {
+        // a mega vertex: its own used-color set and counter (cleared here, the
+        // bulk kernel runs after this one), then one item per pred chunk, in
+        // place of the vertex in the priority order (equal priority: no chunk
+        // waits on another chunk, so the ticket order stays deadlock-free)
+        const int m = atomicAdd(&st->nmega, 1);
+        PGC_DCHECK(m < mega_cap, m, mega_cap);
+        for (int w = 0; w < kMegaWords; ++w) mega[(int64_t)m * kMegaWords + w] = 0u;
+        mega[mega_cap * kMegaWords + m] = 0u;
+        const uint64_t slot = ((uint64_t)(uint32_t)r.w << 32) | (uint32_t)r.z;
+        for (int k = 0; k < nch; ++k) {
+          const uint64_t sk = slot + (uint64_t)k * mega_chunk;
+          hrec[h + k] = make_int4(r.x, min(mega_chunk, r.y - k * mega_chunk), (int)(uint32_t)sk,
+                                  (int)(uint32_t)(sk >> 32));
+          hmeta[h + k] = make_int2(m, nch);
+        }
+      }
+    } else if (r.y > 0) lrec[lpos[i]] = r;
     else {
       st_relaxed(color + r.x, 1);
       root = true;
@@ -1470,7 +1500,9 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
                                                      unsigned light_sleep_max,
                                                      unsigned long long* tr_grab,
                                                      unsigned long long* tr_done,
-                                                     unsigned long long watchdog_ns) {
+                                                     unsigned long long watchdog_ns,
+                                                     const int2* __restrict__ hmeta,
+                                                     uint32_t* mega, int64_t mega_cap) {
   const unsigned long long deadline = globaltimer() + watchdog_ns;
   __shared__ __align__(16) uint8_t s_bm[kMaxHeavyWarps][kHeavyWin];
   __shared__ int s_pend[kMaxHeavyWarps][kPendCap];
@@ -1489,7 +1521,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
     // ticket is always of lower priority than the current one: the
     // deadlock-freedom argument of the one-ahead prefetch holds for any batch)
     int q_next = 0, q_end = 0;
-    auto fetch = [&](int& t, int& v, int& np, int64_t& pb) {
+    auto fetch = [&](int& t, int& v, int& np, int64_t& pb, int2& mm) {
       if (q_next == q_end) {
         int b = 0;
         if (lane == 0) b = atomicAdd(&st->ticket_heavy, heavy_batch);
@@ -1502,18 +1534,26 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         v = r.x;
         np = r.y;
         pb = rec_slot(r);
+        mm = __ldcs(hmeta + t);
       }
     };
     int t_next, v_next = 0, np_next = 0;
     int64_t pb_next = 0;
-    fetch(t_next, v_next, np_next, pb_next);
+    int2 mm_next = make_int2(-1, 1);
+    fetch(t_next, v_next, np_next, pb_next, mm_next);
     for (;;) {
       const int t = t_next;
       if (t >= nheavy) break;
       const int v = v_next;
-      const int np = np_next;
-      const int64_t pb = pb_next;
-      fetch(t_next, v_next, np_next, pb_next);
+      int np = np_next;
+      int64_t pb = pb_next;
+      // a chunk of a mega vertex's preds (m >= 0): window 0 only, every pred
+      // waited for, its colors ORed into the vertex's set; the last of the
+      // vertex's nch chunks to finish takes GetColor from the union
+      int m = mm_next.x;
+      const int nch = mm_next.y;
+      bool publish = true;
+      fetch(t_next, v_next, np_next, pb_next, mm_next);
 #ifndef PGC_PROBE
       if (tr_grab && lane == 0) tr_grab[v] = globaltimer();
 #endif
@@ -1536,7 +1576,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
             zi = bmap_next_zero<kHeavyWin>(bm, zi);
             continue;
           }
-          if (npend <= kHeavyTail && over >= np) break;  // the tail below takes them
+          if (npend <= kHeavyTail && over >= np && m < 0) break;  // the tail below takes them
           // Several pending: watch the second-to-last expected (one load per
           // poll, exponential backoff), then one pass drops the colored entries.
           int u1, u2;
@@ -1640,10 +1680,67 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
           zi = res;
           npend = 0;
         }
+        if (m >= 0) {
+          // (npend == 0 and every pred of the chunk examined: bm holds all of
+          // the chunk's colors <= kMegaBits) byte map -> bits, OR into the set
+          static_assert(kMegaBits == kHeavyWin, "one window per chunk");
+          uint32_t* mbits = mega + (int64_t)m * kMegaWords;
+#pragma unroll
+          for (int h = 0; h < kMegaWords / 32; ++h) {
+            const int w = lane + 32 * h;
+            const uint4 b0 = *reinterpret_cast<const uint4*>(bm + 32 * w);
+            const uint4 b1 = *reinterpret_cast<const uint4*>(bm + 32 * w + 16);
+            const uint32_t by[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            uint32_t bits = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+              for (int y = 0; y < 4; ++y)
+                if ((by[q] >> (8 * y)) & 0xffu) bits |= 1u << (4 * q + y);
+            if (bits) atomicOr(mbits + w, bits);
+          }
+          __threadfence();
+          __syncwarp();
+          int last = 0;
+          if (lane == 0)
+            last = atomicAdd(mega + mega_cap * kMegaWords + m, 1) == nch - 1;
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (!last) {
+            publish = false;
+            break;
+          }
+          __threadfence();  // every other chunk's ORs precede its count
+          int z = kMegaBits;
+#pragma unroll
+          for (int h = 0; h < kMegaWords / 32; ++h) {
+            const uint32_t free_bits = ~__ldcg(mbits + lane + 32 * h);
+            const unsigned any = __ballot_sync(0xffffffffu, free_bits != 0u);
+            if (any && z == kMegaBits) {  // (warp-uniform)
+              const int wl = __ffs(any) - 1;
+              const uint32_t fb = __shfl_sync(0xffffffffu, free_bits, wl);
+              z = 32 * (wl + 32 * h) + __ffs(fb) - 1;
+            }
+          }
+          if (z < kMegaBits) {
+            found = z + 1;  // GetColor over all of v's preds
+            break;
+          }
+          // colors 1..kMegaBits all taken (every pred is colored by now): the
+          // whole-vertex window loop over v's full list from the next window
+          m = -1;
+          pb = off[v];
+          np = npred[v];
+          __syncwarp();
+          continue;
+        }
         if (zi < kHeavyWin) found = wbase + zi + 1;  // GetColor (else: next window)
         __syncwarp();
       }
       if (found < 0) break;  // stalled: the host reports PGC_EINTERNAL
+      if (!publish) continue;  // a chunk of a mega vertex another warp finishes
+#ifdef PGC_CHECKED
+      if (nch > 1) np = npred[v];
+#endif
       PGC_DCHECK(found >= 1 && found <= np + 1, found, np);  // GetColor <= |pred| + 1
       if (lane == 0) {
         st_relaxed(color + v, found);
@@ -1899,6 +1996,7 @@ __global__ void k_jp_reset(State* st, int nonempty) {
   st->ticket_levels = 0;
   st->jp_levels = nonempty;  // isolated vertices and roots are level 1
   st->nheavy = 0;
+  st->nmega = 0;
   st->K = nonempty;
   st->core_n = 0;
   st->core_n1 = 0;
@@ -2085,12 +2183,14 @@ int jp_color_run(Ctx& c, int32_t* color) {
       int32_t* hpos = c.Rl;
       int32_t* lpos = c.D;
       PGC_LAUNCH(c, kGJp, "k_bulk_flags",
-                 k_bulk_flags<<<G, 256, 0, c.st>>>(n_order, c.rec, c.state, hflag, lflag));
+                 k_bulk_flags<<<G, 256, 0, c.st>>>(n_order, c.rec, c.state, hflag, lflag,
+                                                   c.tune.jp_mega_pred, c.tune.jp_mega_chunk));
       if (int e = scan_ex(c, hflag, hpos, nullptr, nbulk, nbulk, &c.state->nheavy, kGJp)) return e;
       if (int e = scan_ex(c, lflag, lpos, nullptr, nbulk, nbulk, &c.state->nlight, kGJp)) return e;
       PGC_LAUNCH(c, kGJp, "k_bulk_scatter",
                  k_bulk_scatter<<<G, 256, 0, c.st>>>(n_order, c.rec, c.state, hpos, lpos, hrec, lrec,
-                                                     color));
+                                                     color, c.hmeta, c.mega, c.lay.mega_cap,
+                                                     c.tune.jp_mega_pred, c.tune.jp_mega_chunk));
       return 0;
     };
     // tier 1: positions [0, NC1) with u16 lists (rewritten beside it when
@@ -2183,7 +2283,8 @@ int jp_color_run(Ctx& c, int32_t* color) {
                      c.off, c.P, c.npred, hrec, lrec, c.round_key, c.seed, color, c.state,
                      c.tune.jp_heavy_warps, c.tune.jp_heavy_batch, (unsigned)c.tune.jp_heavy_sleep_max,
                      (unsigned)c.tune.jp_light_sleep_max, c.trace_grab, c.trace_done,
-                     (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull));
+                     (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull, c.hmeta, c.mega,
+                     c.lay.mega_cap));
     }
   }
   if (c.tune.levels && n_order > 0) {

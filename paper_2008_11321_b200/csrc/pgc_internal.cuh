@@ -15,6 +15,13 @@ namespace pgc {
 constexpr int kWarp = 32;
 constexpr int kMinChunk = 256;        // smallest allowed arcs-per-work-item for chunked vertices
 constexpr int kMinHeavyDeg = 128;     // smallest allowed heavy_degree (sizes the chunk records)
+// JP bulk mega vertices (jp.cu): a vertex with more than jp_mega_pred preds is
+// colored by ceil(|pred| / jp_mega_chunk) warps, one per chunk of its pred
+// list, which OR their preds' colors into a kMegaBits-bit used-color set
+constexpr int kMegaBits = 2048;       // = the heavy byte-map window: colors 1..2048
+constexpr int kMegaWords = kMegaBits / 32;
+constexpr int kMinMegaPred = 1024;    // smallest allowed jp_mega_pred (sizes the mega state)
+constexpr int kMinMegaChunk = 256;    // smallest allowed jp_mega_chunk (sizes the heavy list)
 constexpr int kMaxRoundStats = 4096;  // per-round statistics kept in the workspace
 constexpr int kCoreCap = 65536;       // JP core: at most this many vertices (u16 positions)
 #ifndef PGC_BUCKET_TARGET
@@ -67,7 +74,9 @@ struct State {
   int core_n1;                 // tier 1 of the core: positions [0, core_n1) (u16 lists);
                                // tier 2: [core_n1, core_n) (int32 codes, after tier 1)
   long long core_arcs;         // sum of |pred| over the core
-  int nheavy;                  // bulk vertices with |pred| > kLightPredMax
+  int nheavy;                  // bulk heavy work items (vertices with |pred| > kLightPredMax;
+                               // a mega vertex counts once per pred chunk)
+  int nmega;                   // bulk mega vertices (|pred| > jp_mega_pred), split into chunks
   int nlight;                  // bulk vertices with 1 <= |pred| <= kLightPredMax
   int jp_levels;               // J, when the levels knob is on (k_jp_levels)
   alignas(128) int K;          // max color (atomicMax per warp)
@@ -85,8 +94,8 @@ struct State {
 // Byte offsets of every workspace region (each 256-byte aligned).
 struct Layout {
   size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, hist1, base1, bcnt, bstart,
-      scan_tmp, rec, filt, total;
-  int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap, rec_heavy_cap;
+      scan_tmp, rec, hmeta, mega, filt, total;
+  int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap, rec_heavy_cap, mega_cap;
 };
 
 Layout make_layout(int64_t n, int64_t nnz);
@@ -99,6 +108,9 @@ struct Tuning {
   int filter_ratio = 4;     // UPDATE: filtered heavy kernel once |U_l| * ratio <= filter bits (0 = off)
   int jp_heavy_warps = 4;         // warps per 8-warp bulk JP block serving heavy vertices (1..4)
   int jp_heavy_batch = 1;         // heavy tickets per atomic (consecutive, per warp)
+  int jp_mega_pred = 2048;        // bulk vertices with more preds are split into pred chunks,
+                                  // colored by several warps (0 = off; else >= kMinMegaPred)
+  int jp_mega_chunk = 512;        // preds per chunk (kMinMegaChunk .. kMegaBits)
   int jp_heavy_sleep_max = 256;   // ns, exponential backoff cap of waiting heavy warps
   int jp_light_sleep_max = 8192;  // ns, same for light warps
   int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
@@ -114,6 +126,7 @@ struct Tuning {
                                   // positions when tier 1 is capped (0 = off; measured slower
                                   // on R-MAT 24 / Chung-Lu / R-MAT 20)
   int itr_blocks_per_sm = 0;      // DEC-ADG-ITR: blocks per SM of the cooperative kernel (0 = occupancy)
+  int itr_members_per_warp = 4;   // DEC-ADG-ITR: partition members per warp of the pass grid
   int jp_split_overlap = 1;       // JP: run the bulk split on a side stream beside the core kernel
   int top_list = 1;               // JP-ADG: ADG saves the top rounds' list for the split order
   int fuse_init = 1;              // ADG: round 1's selection also initialises D, rs, round, color
@@ -179,6 +192,9 @@ struct Ctx {
   int32_t* scan_tmp;
   int4* rec;       // JP records {v, |pred|, P slot}: n in priority order, then the
                    // bulk's heavy and light lists
+  int2* hmeta;     // per heavy item: {mega index (-1: a whole vertex), chunks}
+  uint32_t* mega;  // per mega vertex: kMegaWords used-color words, then (after all
+                   // mega_cap of them) one finished-chunk counter each
   const int32_t* round_key = nullptr;  // JP first priority key (rho_ADG for JP-ADG)
   uint64_t seed = 0;                   // JP tie-break seed
   int core_ctas = 0;                   // cluster size used by the last k_jp_core (0 = none)

@@ -142,7 +142,8 @@ def tuning():
                 "core_arc_cap": 1 << 30, "core_arcs_per_cta": 2 << 20, "jp_heavy_warps": 4,
                 "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
                 "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1, "top_list": 1,
-                "core_tier2": 0}
+                "core_tier2": 0, "jp_mega_pred": 2048, "jp_mega_chunk": 512,
+                "itr_members_per_warp": 4}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
 
@@ -172,6 +173,32 @@ def test_core_engine_whole_graph_and_windows(tuning):
         tuning("core_max", cap)
         assert_parity(gg.rmat(12, 16, seed=2), 1, 10, 4)
         assert pgc_stats()["core_vertices"] == cap
+
+
+@pytest.mark.parametrize("mega", [(1024, 256), (1024, 1024), (4096, 2048), (0, 1024)])
+def test_bulk_mega_vertices(mega, tuning):
+    """Bulk vertices with more than jp_mega_pred preds are colored by one warp
+    per pred chunk (the chunks OR their colors into one used-color set, the
+    last one takes GetColor): no core (core_max 0), so K_2100's vertices of
+    rank > 1024 are mega vertices and those of rank > 2048 find colors
+    1..2048 all taken (the whole-list fallback from the second window); hubs
+    and R-MAT under JP-ADG and JP-R; (0, .) = off."""
+    pred, chunk = mega
+    tuning("core_max", 0)
+    tuning("jp_mega_pred", pred)
+    tuning("jp_mega_chunk", chunk)
+    n = 2100
+    g = gg.from_edges(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+    T, K = assert_parity(g, 1, 10, 3)
+    assert K == n
+    edges = [(i, j) for i in range(1, 400) for j in range(i + 1, 400)] + [(0, i) for i in range(1, 20000)]
+    for g in (gg.from_edges(20000, edges), gg.rmat(15, 16, seed=2)):
+        assert_parity(g, 1, 100, 5)
+        pgc, off, col = dev(g)
+        color, K = pgc.jp_baseline(off, col, "jp-r", 7)
+        torch.cuda.synchronize()
+        c_or, K_or = O.jp(g, np.zeros(g.n, dtype=np.int32), 7)
+        assert np.array_equal(color.cpu().numpy(), c_or) and K == K_or
 
 
 def test_core_engine_tier2(tuning):
@@ -467,6 +494,19 @@ def test_dec_adg_itr_random(name):
          "grid": lambda: gg.grid(256, seed=4), "edgeless": lambda: gg.from_edges(1000, [])}[name]()
     for num, den in [(1, 100), (1, 10), (1, 2)]:
         assert_parity_dec(g, num, den, 7)
+
+
+@pytest.mark.parametrize("mpw", [1, 64])
+def test_dec_adg_itr_pass_grid_sizes(mpw, tuning):
+    """The SIM-COL pass grid sized at 1 and 64 partition members per warp (one
+    block for most partitions: the grid barrier among one block), on a clique
+    (one vertex fixed per pass) and R-MAT."""
+    tuning("itr_members_per_warp", mpw)
+    n = 300
+    g = gg.from_edges(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+    T, K = assert_parity_dec(g, 1, 10, 3)
+    assert K == n
+    assert_parity_dec(gg.rmat(15, 16, seed=2), 1, 10, 7)
 
 
 def test_dec_adg_itr_rmat20():
