@@ -126,7 +126,7 @@ struct Tuning {
                                   // positions when tier 1 is capped (0 = off; measured slower
                                   // on R-MAT 24 / Chung-Lu / R-MAT 20)
   int itr_blocks_per_sm = 0;      // DEC-ADG-ITR: blocks per SM of the cooperative kernel (0 = occupancy)
-  int itr_members_per_warp = 4;   // DEC-ADG-ITR: partition members per warp of the pass grid
+  int itr_members_per_warp = 1;   // DEC-ADG-ITR: partition members per warp of the pass grid
   int jp_split_overlap = 1;       // JP: run the bulk split on a side stream beside the core kernel
   int top_list = 1;               // JP-ADG: ADG saves the top rounds' list for the split order
   int fuse_init = 1;              // ADG: round 1's selection also initialises D, rs, round, color

@@ -143,7 +143,7 @@ def tuning():
                 "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
                 "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1, "top_list": 1,
                 "core_tier2": 0, "jp_mega_pred": 2048, "jp_mega_chunk": 512,
-                "itr_members_per_warp": 4}
+                "itr_members_per_warp": 1, "jp_heavy_stripes": 1}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
 
@@ -198,6 +198,26 @@ def test_bulk_mega_vertices(mega, tuning):
         color, K = pgc.jp_baseline(off, col, "jp-r", 7)
         torch.cuda.synchronize()
         c_or, K_or = O.jp(g, np.zeros(g.n, dtype=np.int32), 7)
+        assert np.array_equal(color.cpu().numpy(), c_or) and K == K_or
+
+
+@pytest.mark.parametrize("stripes", [3, 8])
+def test_bulk_heavy_ticket_stripes(stripes, tuning):
+    """The heavy list dealt round-robin to several ticket counters (each
+    stripe handed out in priority order): JP-ADG with and without the core,
+    JP-R with mega vertices."""
+    tuning("jp_heavy_stripes", stripes)
+    g = gg.rmat(15, 16, seed=2)
+    assert_parity(g, 1, 10, 5)
+    tuning("core_max", 0)
+    assert_parity(g, 1, 100, 6)
+    n = 2100
+    gk = gg.from_edges(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+    for h in (g, gk):
+        pgc, off, col = dev(h)
+        color, K = pgc.jp_baseline(off, col, "jp-r", 7)
+        torch.cuda.synchronize()
+        c_or, K_or = O.jp(h, np.zeros(h.n, dtype=np.int32), 7)
         assert np.array_equal(color.cpu().numpy(), c_or) and K == K_or
 
 
@@ -496,9 +516,9 @@ def test_dec_adg_itr_random(name):
         assert_parity_dec(g, num, den, 7)
 
 
-@pytest.mark.parametrize("mpw", [1, 64])
+@pytest.mark.parametrize("mpw", [4, 64])
 def test_dec_adg_itr_pass_grid_sizes(mpw, tuning):
-    """The SIM-COL pass grid sized at 1 and 64 partition members per warp (one
+    """The SIM-COL pass grid sized at 4 and 64 partition members per warp (one
     block for most partitions: the grid barrier among one block), on a clique
     (one vertex fixed per pass) and R-MAT."""
     tuning("itr_members_per_warp", mpw)
