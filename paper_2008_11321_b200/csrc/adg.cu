@@ -759,6 +759,10 @@ __global__ void k_maxdeg(int64_t n, const int64_t* __restrict__ off, State* st) 
   m = warp_max(m);
   if (lane_id() == 0 && m) atomicMax(&st->maxdeg, m);
 }
+// first == 2: the round's first pass bins min(D, kMselBins - 1) (the median's
+// D is exact after one pass unless it is >= kMselBins - 1, which leaves the
+// key undetermined for the digit passes); a digit pass whose bits are already
+// determined returns at once.
 __global__ void __launch_bounds__(1024) k_msel_pass(int first, int shift, int bits,
                                                     const int32_t* __restrict__ Uin,
                                                     const int32_t* __restrict__ D,
@@ -770,6 +774,8 @@ __global__ void __launch_bounds__(1024) k_msel_pass(int first, int shift, int bi
   if (st->done) return;
   const unsigned long long pkey = st->msel_key, pmask = st->msel_mask;
   const unsigned dmask = (1u << bits) - 1u;
+  const bool clampD = first == 2;
+  if (!clampD && ((pmask >> shift) & dmask) == dmask) return;  // digit known
   for (int i = threadIdx.x; i < kMselBins; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const long long nU = st->nU;
@@ -779,7 +785,8 @@ __global__ void __launch_bounds__(1024) k_msel_pass(int first, int shift, int bi
     if (i < nU) {
       const int v = Uin ? Uin[i] : (int)i;
       const unsigned long long key = (((unsigned long long)(uint32_t)ld_i32_keep(D + v)) << 32) | (uint32_t)v;
-      if ((key & pmask) == pkey) bin = (int)((unsigned)(key >> shift) & dmask);
+      if (clampD) bin = (int)min((uint32_t)(key >> 32), (uint32_t)(kMselBins - 1));
+      else if ((key & pmask) == pkey) bin = (int)((unsigned)(key >> shift) & dmask);
     }
     // degrees concentrate on few bins: one shared atomic per distinct bin per warp
     const unsigned peers = __match_any_sync(0xffffffffu, bin);
@@ -836,9 +843,19 @@ __global__ void __launch_bounds__(1024) k_msel_pass(int first, int shift, int bi
   for (int k = 0; k < 4; ++k) hist[4 * t + k] = 0;
   __syncthreads();
   if (t == 0) {
-    st->msel_key = pkey | ((unsigned long long)s_digit << shift);
-    st->msel_mask = pmask | ((unsigned long long)dmask << shift);
-    st->msel_rank = rank - s_before;
+    if (clampD && s_digit == kMselBins - 1) {  // D >= kMselBins - 1: digit passes from scratch
+      st->msel_key = 0;
+      st->msel_mask = 0;
+      st->msel_rank = rank;
+    } else if (clampD) {                         // D = s_digit exactly
+      st->msel_key = (unsigned long long)s_digit << 32;
+      st->msel_mask = 0xffffffffull << 32;
+      st->msel_rank = rank - s_before;
+    } else {
+      st->msel_key = pkey | ((unsigned long long)s_digit << shift);
+      st->msel_mask = pmask | ((unsigned long long)dmask << shift);
+      st->msel_rank = rank - s_before;
+    }
     st->msel_done = 0;
   }
 }
@@ -1053,9 +1070,14 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
       const int atom = l == 1 && c.tune.update_atom && (mode == kAdgOnly || mode == kAdgFused);
       if (rule == kRuleMedian) {
         PGC_LAUNCH(c, kGSelect, "k_msel_reset", k_msel_reset<<<1, 1, 0, c.st>>>(c.state));
+        // the clamped-D pass first, then the digit passes (those of D return
+        // at once when the clamped pass fixed D)
+        PGC_LAUNCH(c, kGSelect, "k_msel_pass",
+                   k_msel_pass<<<c.nsm * 2, 1024, 0, c.st>>>(2, 32, kMselBits, Uin, c.D, mhist,
+                                                            c.state));
         for (size_t p = 0; p < digits.size(); ++p)
           PGC_LAUNCH(c, kGSelect, "k_msel_pass",
-                     k_msel_pass<<<c.nsm * 2, 1024, 0, c.st>>>(p == 0, digits[p].first,
+                     k_msel_pass<<<c.nsm * 2, 1024, 0, c.st>>>(0, digits[p].first,
                                                               digits[p].second, Uin, c.D, mhist,
                                                               c.state));
       }

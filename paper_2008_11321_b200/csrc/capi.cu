@@ -618,6 +618,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"filter_ratio", 0, 1 << 20, nullptr, &g_tune.filter_ratio},
       {"jp_heavy_warps", 1, 4, nullptr, &g_tune.jp_heavy_warps},
       {"jp_heavy_batch", 1, 64, nullptr, &g_tune.jp_heavy_batch},
+      {"jp_heavy_stripes", 1, kMaxHeavyStripes, nullptr, &g_tune.jp_heavy_stripes},
       {"jp_mega_chunk", kMinMegaChunk, kMegaBits, nullptr, &g_tune.jp_mega_chunk},
       {"jp_heavy_sleep_max", 0, 1000000, nullptr, &g_tune.jp_heavy_sleep_max},
       {"jp_light_sleep_max", 0, 1000000, nullptr, &g_tune.jp_light_sleep_max},

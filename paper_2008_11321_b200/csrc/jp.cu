@@ -1496,6 +1496,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
                                                      const int32_t* __restrict__ round,
                                                      uint64_t seed, int32_t* color,
                                                      State* st, int heavy_warps, int heavy_batch,
+                                                     int heavy_stripes,
                                                      unsigned heavy_sleep_max,
                                                      unsigned light_sleep_max,
                                                      unsigned long long* tr_grab,
@@ -1521,14 +1522,25 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
     // ticket is always of lower priority than the current one: the
     // deadlock-freedom argument of the one-ahead prefetch holds for any batch)
     int q_next = 0, q_end = 0;
+    // heavy_stripes > 1: item t belongs to stripe t mod S, each stripe has its
+    // own ticket counter on its own line (one counter took ~1 atomic per heavy
+    // item on one L2 slice) and its own warps; every stripe is handed out in
+    // priority order, so the deadlock-freedom argument holds per stripe (the
+    // highest-priority uncolored item, if not held, has no later item of its
+    // stripe handed out, and the stripe's earlier items are colored: a warp of
+    // its stripe is free)
+    const int S = heavy_stripes;
+    const int stripe = (blockIdx.x * heavy_warps + warp) % S;
+    int* tick = stripe == 0 ? &st->ticket_heavy : &st->ticket_hs[32 * (stripe - 1)];
     auto fetch = [&](int& t, int& v, int& np, int64_t& pb, int2& mm) {
       if (q_next == q_end) {
         int b = 0;
-        if (lane == 0) b = atomicAdd(&st->ticket_heavy, heavy_batch);
+        if (lane == 0) b = atomicAdd(tick, heavy_batch);
         q_next = __shfl_sync(0xffffffffu, b, 0);
         q_end = q_next + heavy_batch;
       }
-      t = q_next++;
+      const int k = q_next++;
+      t = k >= nheavy ? nheavy : stripe + S * k;
       if (t < nheavy) {
         const int4 r = __ldcs(hrec + t);
         v = r.x;
@@ -1992,6 +2004,7 @@ __global__ void k_jp_levels(const int4* __restrict__ rec, const int32_t* __restr
 // and gets color 1 (isolated vertices and roots are colored outside the JP kernels).
 __global__ void k_jp_reset(State* st, int nonempty) {
   st->ticket_heavy = 0;
+  for (int k = 0; k < kMaxHeavyStripes - 1; ++k) st->ticket_hs[32 * k] = 0;
   st->ticket_light = 0;
   st->ticket_levels = 0;
   st->jp_levels = nonempty;  // isolated vertices and roots are level 1
@@ -2281,7 +2294,8 @@ int jp_color_run(Ctx& c, int32_t* color) {
       PGC_LAUNCH(c, kGJp, "k_jp_bulk",
                  k_jp_bulk<<<GB, kJpBlock, 0, c.st>>>(
                      c.off, c.P, c.npred, hrec, lrec, c.round_key, c.seed, color, c.state,
-                     c.tune.jp_heavy_warps, c.tune.jp_heavy_batch, (unsigned)c.tune.jp_heavy_sleep_max,
+                     c.tune.jp_heavy_warps, c.tune.jp_heavy_batch, c.tune.jp_heavy_stripes,
+                     (unsigned)c.tune.jp_heavy_sleep_max,
                      (unsigned)c.tune.jp_light_sleep_max, c.trace_grab, c.trace_done,
                      (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull, c.hmeta, c.mega,
                      c.lay.mega_cap));

@@ -21,6 +21,7 @@ constexpr int kMinHeavyDeg = 128;     // smallest allowed heavy_degree (sizes th
 constexpr int kMegaBits = 2048;       // = the heavy byte-map window: colors 1..2048
 constexpr int kMegaWords = kMegaBits / 32;
 constexpr int kMinMegaPred = 1024;    // smallest allowed jp_mega_pred (sizes the mega state)
+constexpr int kMaxHeavyStripes = 8;   // JP bulk: heavy ticket counters (jp_heavy_stripes)
 constexpr int kMinMegaChunk = 256;    // smallest allowed jp_mega_chunk (sizes the heavy list)
 constexpr int kMaxRoundStats = 4096;  // per-round statistics kept in the workspace
 constexpr int kCoreCap = 65536;       // JP core: at most this many vertices (u16 positions)
@@ -80,7 +81,9 @@ struct State {
   int nlight;                  // bulk vertices with 1 <= |pred| <= kLightPredMax
   int jp_levels;               // J, when the levels knob is on (k_jp_levels)
   alignas(128) int K;          // max color (atomicMax per warp)
-  alignas(128) int ticket_heavy;  // next bulk tickets per class
+  alignas(128) int ticket_heavy;  // next bulk tickets per class (heavy: stripe 0)
+  // heavy stripes 1..kMaxHeavyStripes-1 (jp_heavy_stripes), 128 bytes apart
+  alignas(128) int ticket_hs[(kMaxHeavyStripes - 1) * 32];
   alignas(128) int ticket_light;
   alignas(128) int ticket_levels;  // k_jp_levels' tickets
   // ADG-M radix select of the ceil(|U|/2)-th smallest key (D[v] << 32) | v
@@ -108,6 +111,7 @@ struct Tuning {
   int filter_ratio = 4;     // UPDATE: filtered heavy kernel once |U_l| * ratio <= filter bits (0 = off)
   int jp_heavy_warps = 4;         // warps per 8-warp bulk JP block serving heavy vertices (1..4)
   int jp_heavy_batch = 1;         // heavy tickets per atomic (consecutive, per warp)
+  int jp_heavy_stripes = 1;       // heavy list dealt round-robin to this many ticket counters
   int jp_mega_pred = 2048;        // bulk vertices with more preds are split into pred chunks,
                                   // colored by several warps (0 = off; else >= kMinMegaPred)
   int jp_mega_chunk = 512;        // preds per chunk (kMinMegaChunk .. kMegaBits)
