@@ -1488,6 +1488,13 @@ __device__ __forceinline__ void lowest_two(const int* plist, const unsigned long
 #ifndef PGC_BULK_MINB
 #define PGC_BULK_MINB 5
 #endif
+// MEGA: the heavy warps also serve pred chunks of mega vertices.  Two
+// instantiations, both launched: each returns at once unless the split found
+// mega vertices (nmega > 0) iff it is the MEGA one -- the chunk bookkeeping
+// (item meta loads, the set union, the live registers across the pending
+// loop) cost the JP-ADG bulk 6 % (1.92 -> 2.04 ms on R-MAT 24) although its
+// hubs are in the core and it has no mega vertex.
+template <bool MEGA>
 __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64_t* __restrict__ off,
                                                      const int32_t* __restrict__ P,
                                                      const int32_t* __restrict__ npred,
@@ -1504,6 +1511,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
                                                      unsigned long long watchdog_ns,
                                                      const int2* __restrict__ hmeta,
                                                      uint32_t* mega, int64_t mega_cap) {
+  if ((st->nmega > 0) != MEGA) return;
   const unsigned long long deadline = globaltimer() + watchdog_ns;
   __shared__ __align__(16) uint8_t s_bm[kMaxHeavyWarps][kHeavyWin];
   __shared__ int s_pend[kMaxHeavyWarps][kPendCap];
@@ -1546,7 +1554,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         v = r.x;
         np = r.y;
         pb = rec_slot(r);
-        mm = __ldcs(hmeta + t);
+        if (MEGA) mm = __ldcs(hmeta + t);
       }
     };
     int t_next, v_next = 0, np_next = 0;
@@ -1562,8 +1570,8 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
       // a chunk of a mega vertex's preds (m >= 0): window 0 only, every pred
       // waited for, its colors ORed into the vertex's set; the last of the
       // vertex's nch chunks to finish takes GetColor from the union
-      int m = mm_next.x;
-      const int nch = mm_next.y;
+      int m = MEGA ? mm_next.x : -1;
+      const int nch = MEGA ? mm_next.y : 1;
       bool publish = true;
       fetch(t_next, v_next, np_next, pb_next, mm_next);
 #ifndef PGC_PROBE
@@ -1588,7 +1596,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
             zi = bmap_next_zero<kHeavyWin>(bm, zi);
             continue;
           }
-          if (npend <= kHeavyTail && over >= np && m < 0) break;  // the tail below takes them
+          if (npend <= kHeavyTail && over >= np && (!MEGA || m < 0)) break;  // the tail below takes them
           // Several pending: watch the second-to-last expected (one load per
           // poll, exponential backoff), then one pass drops the colored entries.
           int u1, u2;
@@ -1692,7 +1700,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
           zi = res;
           npend = 0;
         }
-        if (m >= 0) {
+        if (MEGA && m >= 0) {
           // (npend == 0 and every pred of the chunk examined: bm holds all of
           // the chunk's colors <= kMegaBits) byte map -> bits, OR into the set
           static_assert(kMegaBits == kHeavyWin, "one window per chunk");
@@ -1749,7 +1757,7 @@ __global__ void __launch_bounds__(kJpBlock, PGC_BULK_MINB) k_jp_bulk(const int64
         __syncwarp();
       }
       if (found < 0) break;  // stalled: the host reports PGC_EINTERNAL
-      if (!publish) continue;  // a chunk of a mega vertex another warp finishes
+      if (MEGA && !publish) continue;  // a chunk of a mega vertex another warp finishes
 #ifdef PGC_CHECKED
       if (nch > 1) np = npred[v];
 #endif
@@ -2290,15 +2298,26 @@ int jp_color_run(Ctx& c, int32_t* color) {
     }
     // --- bulk dataflow ---
     if (nbulk > 0) {
-      const int GB = wave_grid(c, k_jp_bulk, kJpBlock);
+      const int GB = wave_grid(c, k_jp_bulk<false>, kJpBlock);
       PGC_LAUNCH(c, kGJp, "k_jp_bulk",
-                 k_jp_bulk<<<GB, kJpBlock, 0, c.st>>>(
+                 k_jp_bulk<false><<<GB, kJpBlock, 0, c.st>>>(
                      c.off, c.P, c.npred, hrec, lrec, c.round_key, c.seed, color, c.state,
                      c.tune.jp_heavy_warps, c.tune.jp_heavy_batch, c.tune.jp_heavy_stripes,
                      (unsigned)c.tune.jp_heavy_sleep_max,
                      (unsigned)c.tune.jp_light_sleep_max, c.trace_grab, c.trace_done,
                      (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull, c.hmeta, c.mega,
                      c.lay.mega_cap));
+      if (c.tune.jp_mega_pred > 0) {  // (nmega > 0 needs the knob: else no launch at all)
+        const int GM = wave_grid(c, k_jp_bulk<true>, kJpBlock);
+        PGC_LAUNCH(c, kGJp, "k_jp_bulk_mega",
+                   k_jp_bulk<true><<<GM, kJpBlock, 0, c.st>>>(
+                       c.off, c.P, c.npred, hrec, lrec, c.round_key, c.seed, color, c.state,
+                       c.tune.jp_heavy_warps, c.tune.jp_heavy_batch, c.tune.jp_heavy_stripes,
+                       (unsigned)c.tune.jp_heavy_sleep_max,
+                       (unsigned)c.tune.jp_light_sleep_max, c.trace_grab, c.trace_done,
+                       (unsigned long long)c.tune.jp_watchdog_ms * 1000000ull, c.hmeta, c.mega,
+                       c.lay.mega_cap));
+      }
     }
   }
   if (c.tune.levels && n_order > 0) {

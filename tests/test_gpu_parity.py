@@ -143,7 +143,8 @@ def tuning():
                 "jp_heavy_sleep_max": 256, "jp_light_sleep_max": 8192,
                 "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1, "top_list": 1,
                 "core_tier2": 0, "jp_mega_pred": 2048, "jp_mega_chunk": 512,
-                "itr_members_per_warp": 1, "jp_heavy_stripes": 1}
+                "itr_members_per_warp": 1, "jp_heavy_stripes": 1,
+                "filter_ratio": 4, "chunk_arcs": 1024}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
 
@@ -280,6 +281,26 @@ def test_jp_key_range_error():
     with pytest.raises(pgc.PGCError) as e:
         pgc.jp_color(off, col, key, 1)
     assert e.value.code == pgc.PGC_EINVAL
+
+
+def test_filtered_update_chunk_and_ratio_sweep(tuning):
+    """The filtered late-round UPDATE (k_update_heavy_f; Alg. 1 UPDATE,
+    PAPER.md:692-696, with the fused JP Part 1) against the oracle through
+    JP-ADG, ADG only and JP-ADG-O: 256- and 300-arc chunks give ragged last
+    steps and many chunk changes per warp, filter_ratio 1 / 2 start the filter
+    in an earlier round (many hits per step)."""
+    for hd, chunk, ratio in ((128, 1024, 4), (128, 256, 1), (160, 300, 2)):
+        tuning("heavy_degree", hd)
+        tuning("chunk_arcs", chunk)
+        tuning("filter_ratio", ratio)
+        for g, (num, den) in ((gg.rmat(15, 16, seed=4), (1, 10)), (gg.rmat(13, 32, seed=6), (1, 100)),
+                              (gg.chung_lu(1 << 14, 32.0, 2.1, 1000.0, seed=3), (1, 2))):
+            assert_parity(g, num, den, 5)
+            pgc, off, col = dev(g)
+            rnd, T = pgc.adg_order(off, col, num, den)
+            r_or, st_or = O.adg(g, num, den)
+            assert T == st_or["T"] and np.array_equal(rnd.cpu().numpy(), r_or)
+            assert_parity_o(g, num, den)
 
 
 def test_determinism_across_tuning(tuning):
