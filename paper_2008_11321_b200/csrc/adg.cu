@@ -84,21 +84,6 @@ __global__ void k_adg_state_init(int64_t n, int64_t nnz, State* st) {
   *st = s;
 }
 
-// After round l's selection: in the round where |U| drops below target
-// (|U_l| >= target > |U_{l+1}|), keep a copy of U_l -- the smallest U holding
-// every vertex of the top rounds the JP core's prefix is drawn from (with the
-// mean rule U_l, l >= 2, holds no isolated vertex) -- so the priority order's
-// top part need not pass over all n vertices.  U_1 (every vertex) is not kept.
-__global__ void k_top_save(int l, const int32_t* __restrict__ Uin, State* st,
-                           int32_t* __restrict__ save, int target) {
-  if (st->done || l < 2) return;
-  const long long cnt = st->nU;
-  if (cnt < target || st->nUnext >= target) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->top_n = (int)cnt;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
-    save[i] = Uin[i];
-}
-
 // a2+a3: threshold, select, compact.
 constexpr int kSelItems = 4;
 __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const int64_t* __restrict__ off,
@@ -108,7 +93,8 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
                              int4* __restrict__ lrec, int4* __restrict__ chunks,
                              int32_t* __restrict__ npred, State* st, int heavy_deg, int chunk,
                              int64_t chunk_cap, int pull, int mark_removed, int first,
-                             int32_t* __restrict__ color, uint32_t* __restrict__ filt) {
+                             int32_t* __restrict__ color, uint32_t* __restrict__ filt,
+                             int4* __restrict__ cexp) {
   __shared__ int sm[33];
   __shared__ long long s_dmax;
   __shared__ unsigned long long s_red[32];
@@ -233,7 +219,14 @@ __global__ void k_adg_select(int l, int rule, uint32_t num, uint32_t den, const 
     for (int j = 0; j < K; ++j) {
       if (nch[j]) {
         if (cpos + nch[j] > chunk_cap) st->err = 3;
-        else
+        else if (nch[j] > kExpandMin) {
+          // a hub: one descriptor; k_round_aux writes its records, a warp per
+          // hub (one thread writing a late round's ~10^2 records per hub made
+          // the selection of the last rounds 20-40 us each)
+          const int e = atomicAdd(&st->nExp, 1);
+          cexp[2 * e] = make_int4(v[j], nch[j], (int)cpos, (int)deg[j]);
+          cexp[2 * e + 1] = make_int4((int)(uint32_t)o[j], (int)(o[j] >> 32), 0, 0);
+        } else
           for (int k = 0; k < nch[j]; ++k) {
             const long long s0 = o[j] + (long long)k * chunk;
             const int len = (int)min((long long)chunk, o[j] + deg[j] - s0);
@@ -590,7 +583,7 @@ __global__ void __launch_bounds__(256) k_update_heavy(Arc<MODE> A, const int32_t
 // gather is a wasted random access, and UPDATE is bound by the random-access
 // rate.  Each CTA (one per SM, 1024 threads) copies a one-hash Bloom filter of
 // U_l (the round's input list: alive or removed this round; built once per
-// round by k_filter_build) into shared memory; an arc whose target misses the
+// round by k_round_aux) into shared memory; an arc whose target misses the
 // filter is "removed earlier" for certain.  A warp first filters a 256-arc
 // step and compacts the hits (members of U_l plus <= 1/ratio false positives)
 // into shared memory, then gathers, classifies and decrements only those, 32
@@ -607,23 +600,55 @@ __device__ __forceinline__ uint32_t filter_slot(int u) {
   return __umulhi((uint32_t)u * 0x9E3779B1u, kFilterBits);
 }
 
-// Before UPDATE of round l: set the bits of U_l (the round's input list) in the
-// global filter buffer l&1 -- one RED per member, once per round, not per CTA
-// -- and clear buffer (l+1)&1 for the next round (its last reader, UPDATE of
-// round l-1, has finished).  Buffers start zeroed (k_adg_init).
-__global__ void k_filter_build(int l, const int32_t* __restrict__ Uin, uint32_t* __restrict__ filt,
-                               const State* st, int ratio) {
+// Between round l's selection and its UPDATE, one launch (k_round_aux):
+// (a) the membership filter: set the bits of U_l (the round's input list) in
+//     the global filter buffer l&1 -- one RED per member, once per round, not
+//     per CTA -- and clear buffer (l+1)&1 for the next round (its last reader,
+//     UPDATE of round l-1, has finished).  Buffers start zeroed (k_adg_init).
+// (b) the saved top list: in the round where |U| drops below target (|U_l| >=
+//     target > |U_{l+1}|), keep a copy of U_l -- the smallest U holding every
+//     vertex of the top rounds the JP core's prefix is drawn from (with the
+//     mean rule U_l, l >= 2, holds no isolated vertex) -- so the priority
+//     order's top part need not pass over all n vertices.  U_1 (every vertex)
+//     is not kept.
+// (c) the chunk records of this round's hubs (k_adg_select's descriptors), a
+//     warp per hub.
+__global__ void __launch_bounds__(1024) k_round_aux(int l, const int32_t* __restrict__ Uin,
+                                                    uint32_t* __restrict__ filt, State* st, int ratio,
+                                                    int32_t* __restrict__ save, int target,
+                                                    int4* __restrict__ chunks,
+                                                    const int4* __restrict__ cexp, int chunk) {
   if (st->done) return;
-  uint32_t* nxt = filt + (size_t)((l + 1) & 1) * kFilterWords;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
-  for (int i = tid; i < kFilterWords / 4; i += nt) reinterpret_cast<uint4*>(nxt)[i] = make_uint4(0, 0, 0, 0);
-  if (!filter_round(st, ratio)) return;
-  uint32_t* cur = filt + (size_t)(l & 1) * kFilterWords;
   const long long nU = st->nU;
-  for (long long i = tid; i < nU; i += nt) {
-    const int u = Uin ? Uin[i] : (int)i;
-    const uint32_t b = filter_slot(u);
-    atomicOr(&cur[b >> 5], 1u << (b & 31));
+  if (filt) {
+    uint32_t* nxt = filt + (size_t)((l + 1) & 1) * kFilterWords;
+    for (int i = tid; i < kFilterWords / 4; i += nt) reinterpret_cast<uint4*>(nxt)[i] = make_uint4(0, 0, 0, 0);
+    if (filter_round(st, ratio)) {
+      uint32_t* cur = filt + (size_t)(l & 1) * kFilterWords;
+      for (long long i = tid; i < nU; i += nt) {
+        const int u = Uin ? Uin[i] : (int)i;
+        const uint32_t b = filter_slot(u);
+        atomicOr(&cur[b >> 5], 1u << (b & 31));
+      }
+    }
+  }
+  if (save && l >= 2 && nU >= target && st->nUnext < target) {
+    if (tid == 0) st->top_n = (int)nU;
+    for (long long i = tid; i < nU; i += nt) save[i] = Uin[i];
+  }
+  const int nE = st->nExp;
+  const int lane = lane_id();
+  for (int e = tid >> 5; e < nE; e += nt >> 5) {
+    const int4 d0 = cexp[2 * e], d1 = cexp[2 * e + 1];
+    const long long o = lo_hi(d1.x, d1.y);
+    const int4 tail = make_int4(d1.x, d1.y, 0, 0);
+    for (int k = lane; k < d0.y; k += 32) {
+      const long long s0 = o + (long long)k * chunk;
+      const int len = (int)min((long long)chunk, o + d0.w - s0);
+      __stcs(chunks + 2 * ((long long)d0.z + k), make_int4(d0.x, len, (int)(uint32_t)s0, (int)(s0 >> 32)));
+      __stcs(chunks + 2 * ((long long)d0.z + k) + 1, tail);
+    }
   }
 }
 
@@ -644,7 +669,7 @@ __global__ void __launch_bounds__(kFilterThreads, 1)
   const unsigned lt = lanemask_lt();
   int* s_buf = s_buf_all + warp * kFilterSub;
   int* s_hit = s_buf_all + (kFilterThreads / 32 + warp) * kFilterSub;
-  {  // the round's filter (built by k_filter_build) -> shared memory
+  {  // the round's filter (built by k_round_aux) -> shared memory
     const uint4* src = reinterpret_cast<const uint4*>(gfilt + (size_t)(A.l & 1) * kFilterWords);
     uint4* dst = reinterpret_cast<uint4*>(filt);
     for (int i = threadIdx.x; i < kFilterWords / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
@@ -916,6 +941,7 @@ __global__ void k_adg_finalize(int l, int rule, uint32_t num, uint32_t den, Stat
   st->nLight = 0;
   st->nUnext = 0;
   st->nChunks = 0;
+  st->nExp = 0;
   if (nU1 == 0 || st->err) st->done = 1;
 }
 
@@ -1089,15 +1115,14 @@ int adg_run(Ctx& c, uint32_t num, uint32_t den, uint64_t seed, int32_t* round, i
                                                  c.tune.heavy_degree, c.tune.chunk_arcs,
                                                  c.lay.chunk_cap, mode == kAdgPull, atom,
                                                  fuse_init && l == 1, color_zero,
-                                                 c.tune.filter_ratio > 0 ? c.filt : nullptr));
-      if (save_top)
-        PGC_LAUNCH(c, kGAdgOther, "k_top_save",
-                   k_top_save<<<c.nsm * 4, 256, 0, c.st>>>(l, Uin, c.state, c.Rl, core_reach(c.tune)));
+                                                 c.tune.filter_ratio > 0 ? c.filt : nullptr,
+                                                 c.cexp));
       if (l == 1 && c.col_ready) PGC_CUDA(cudaStreamWaitEvent(c.st, c.col_ready, 0));
-      if (c.tune.filter_ratio > 0 && mode != kAdgPull)
-        PGC_LAUNCH(c, kGUpdate, "k_filter_build",
-                   k_filter_build<<<c.nsm * 2, 1024, 0, c.st>>>(l, Uin, c.filt, c.state,
-                                                                c.tune.filter_ratio));
+      PGC_LAUNCH(c, kGUpdate, "k_round_aux",
+                 k_round_aux<<<c.nsm * 2, 1024, 0, c.st>>>(
+                     l, Uin, c.tune.filter_ratio > 0 && mode != kAdgPull ? c.filt : nullptr, c.state,
+                     c.tune.filter_ratio, save_top ? c.Rl : nullptr, core_reach(c.tune), c.chunks,
+                     c.cexp, c.tune.chunk_arcs));
       if (mode == kAdgFused) {
         if (int e = launch_update(c, Arc<1>{l, seed, round, c.D, c.rs, atom}, Uin)) return e;
       } else if (mode == kAdgFusedO) {

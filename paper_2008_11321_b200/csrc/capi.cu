@@ -84,6 +84,10 @@ Layout make_layout(int64_t n, int64_t nnz) {
   // items each; a chunk record is 2 x int4
   L.chunk_cap = nnz / kMinChunk + (nnz / (kMinHeavyDeg + 1) < n ? nnz / (kMinHeavyDeg + 1) : n) + 2;
   L.chunks = take(32 * (size_t)L.chunk_cap);
+  // hub descriptors: vertices with more than kExpandMin chunks have degree
+  // > kExpandMin * kMinChunk
+  L.cexp_cap = nnz / ((int64_t)kExpandMin * kMinChunk) + 2;
+  L.cexp = take(32 * (size_t)L.cexp_cap);
   L.range_cap = n + 65536;
   L.hist1 = take(4 * (size_t)(2 * L.range_cap));
   L.base1 = take(4 * (size_t)(2 * L.range_cap + 1));
@@ -157,6 +161,7 @@ static int make_ctx(Ctx& c, const pgc_graph* g, void* ws, void* stream) {
   c.U[1] = (int32_t*)(b + c.lay.U1);
   c.Rl = (int32_t*)(b + c.lay.Rl);
   c.chunks = (int4*)(b + c.lay.chunks);
+  c.cexp = (int4*)(b + c.lay.cexp);
   c.hist1 = (int32_t*)(b + c.lay.hist1);
   c.base1 = (int32_t*)(b + c.lay.base1);
   c.bcnt = (int32_t*)(b + c.lay.bcnt);

@@ -299,7 +299,7 @@ __global__ void k_hist2(int64_t n, const int32_t* __restrict__ round, Key2 seed,
                         int part, const int32_t* __restrict__ list) {
   const int rmax = st->rmax;
   const int ktop = st->ord_ktop;
-  // `list` (part 0): a superset of the top rounds saved by ADG (k_top_save)
+  // `list` (part 0): a superset of the top rounds saved by ADG (k_round_aux)
   const bool use_list = list && st->top_n > 0;
   const int64_t cnt = use_list ? st->top_n : n;
   // kOrdItems vertices per thread per step, all loads before any use

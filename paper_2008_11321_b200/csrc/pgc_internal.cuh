@@ -13,6 +13,7 @@
 namespace pgc {
 
 constexpr int kWarp = 32;
+constexpr int kExpandMin = 8;        // a vertex with more chunks gets one descriptor; k_round_aux writes its records
 constexpr int kMinChunk = 256;        // smallest allowed arcs-per-work-item for chunked vertices
 constexpr int kMinHeavyDeg = 128;     // smallest allowed heavy_degree (sizes the chunk records)
 // JP bulk mega vertices (jp.cu): a vertex with more than jp_mega_pred preds is
@@ -52,6 +53,7 @@ struct State {
   // reservations of k_adg_select (one atomic per block step each)
   alignas(128) int nChunks;
   int nLight, nUnext;
+  int nExp;                    // hub descriptors of this round (k_round_aux writes their chunk records)
   // ... the selection's block sums
   alignas(128) unsigned long long sumDR;  // sum of D over R_l
   int nR;
@@ -59,7 +61,7 @@ struct State {
   // ... UPDATE's block sums
   alignas(128) unsigned long long cut;    // arcs from R_l into U_{l+1}
   unsigned long long pred_arcs;  // sum_v |pred(v)|
-  alignas(128) int top_n;      // length of the saved top-round list (k_top_save; 0 = none)
+  alignas(128) int top_n;      // length of the saved top-round list (k_round_aux; 0 = none)
   // priority-order sort
   int rmin, rmax;              // range of the first priority key
   int nbuckets;                // buckets in use
@@ -96,9 +98,9 @@ struct State {
 
 // Byte offsets of every workspace region (each 256-byte aligned).
 struct Layout {
-  size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, hist1, base1, bcnt, bstart,
+  size_t state, per_round, D, rs, npred, P, U0, U1, Rl, chunks, cexp, hist1, base1, bcnt, bstart,
       scan_tmp, rec, hmeta, mega, filt, total;
-  int64_t chunk_cap, range_cap, nb_cap, scan_tmp_cap, rec_heavy_cap, mega_cap;
+  int64_t chunk_cap, cexp_cap, range_cap, nb_cap, scan_tmp_cap, rec_heavy_cap, mega_cap;
 };
 
 Layout make_layout(int64_t n, int64_t nnz);
@@ -189,6 +191,7 @@ struct Ctx {
   uint32_t* filt;  // 2 x kFilterWords: UPDATE membership filters of U_l (double-buffered)
   int4* lrec;      // UPDATE light work records (aliases the JP bulk record region)
   int4* chunks;    // UPDATE edge-chunk records, 2 x int4 each
+  int4* cexp;      // hub descriptors (2 x int4 each) of vertices with > kExpandMin chunks
   int32_t* hist1;
   int32_t* base1;
   int32_t* bcnt;

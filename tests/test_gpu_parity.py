@@ -303,6 +303,31 @@ def test_filtered_update_chunk_and_ratio_sweep(tuning):
             assert_parity_o(g, num, den)
 
 
+def test_hub_chunk_descriptors(tuning):
+    """Vertices with more than 8 edge chunks get one descriptor in the selection
+    and their chunk records from k_round_aux (a warp per hub): hubs of degree
+    2 100 .. 60 000 on a sparse background, removed in late rounds (UPDATE,
+    PAPER.md:692-696), through JP-ADG, ADG push / pull and JP-ADG-M, with 256-
+    and 1024-arc chunks (9 chunks = the first descriptor, a ragged last chunk)."""
+    rng = np.random.default_rng(7)
+    n = 70000
+    edges = set()
+    for hub, deg in ((0, 60000), (1, 2305), (2, 2100), (3, 9217), (4, 30001)):
+        for u in rng.choice(np.arange(5, n), size=deg, replace=False):
+            edges.add((hub, int(u)))
+    for a, b in rng.integers(5, n, size=(150000, 2)):
+        if a != b:
+            edges.add((int(min(a, b)), int(max(a, b))))
+    edges.update({(0, 1), (0, 2), (1, 3), (2, 4), (3, 4)})
+    g = gg.from_edges(n, sorted(edges))
+    for chunk in (256, 1024):
+        tuning("chunk_arcs", chunk)
+        for num, den in ((1, 10), (1, 2)):
+            assert_parity(g, num, den, 3)
+            assert_parity_pull(g, num, den)
+        assert_parity_m(g, 3)
+
+
 def test_determinism_across_tuning(tuning):
     g = gg.rmat(14, 16, seed=2)
     pgc, off, col = dev(g)

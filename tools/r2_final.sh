@@ -62,7 +62,7 @@ full)
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_update_heavy_f -s 10 -c 2 -o $OUT/upd_heavy_f python tools/launch_times.py > $OUT/f2.log 2>&1
   echo "full heavy_f rc=$?" >> $OUT/status.txt
   python tools/launch_times.py jp_split_overlap=0 > /dev/null 2>&1
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_jp_core|k_jp_bulk" -s 2 -c 2 -o $OUT/jp python tools/launch_times.py jp_split_overlap=0 > $OUT/f3.log 2>&1
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_jp_core|k_jp_bulk" -s 3 -c 2 -o $OUT/jp python tools/launch_times.py jp_split_overlap=0 > $OUT/f3.log 2>&1
   echo "full jp rc=$?" >> $OUT/status.txt
   timeout 600 python tools/traffic.py run --config grid > /dev/null 2>&1 && \
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_small -s 1 -c 1 -o $OUT/small_grid python tools/traffic.py run --config grid > $OUT/f4.log 2>&1
