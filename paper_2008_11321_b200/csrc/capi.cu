@@ -629,6 +629,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"jp_light_sleep_max", 0, 1000000, nullptr, &g_tune.jp_light_sleep_max},
       {"core_max", 0, 65535, nullptr, &g_tune.core_max},
       {"core_min_avg", 0, 1 << 30, nullptr, &g_tune.core_min_avg},
+      {"core_div", 0, 1 << 30, nullptr, &g_tune.core_div},
       {"core_min_n", 1, 65535, nullptr, &g_tune.core_min_n},
       {"core_ctas", 0, 16, nullptr, &g_tune.core_ctas},
       {"core_spin_ns", 0, 100000, nullptr, &g_tune.core_spin_ns},

@@ -672,6 +672,7 @@ constexpr int kCoreWin = 1024;   // colors per byte-map window
 constexpr int kCorePend = 512;   // pending-pred list capacity per warp
 constexpr int kCoreVertsPerCta = 1024;  // cluster sizing: core vertices per CTA
 constexpr int kCoreRun = 32;     // consecutive core positions per CTA run
+constexpr int kCoreFloor = 16384;  // core_div never caps the prefix below this
 #ifndef PGC_CORE_TAIL
 #define PGC_CORE_TAIL 4
 #endif
@@ -684,7 +685,8 @@ constexpr int kCoreFixedSmem = kCoreWarps * kCoreWin + kCoreWarps * kCorePend * 
 __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ rec,
                                                       State* st,
                                                       int core_max, int min_avg,
-                                                      long long arc_cap, int tier2_max) {
+                                                      long long arc_cap, int tier2_max,
+                                                      int core_div) {
   // warp w scans the contiguous chunk [wb, we) of the prefix, lanes reading
   // consecutive records, kCsU strips in flight: pass 1 sums the chunk, a
   // block scan of the warp sums gives each chunk's base, pass 2 evaluates
@@ -694,7 +696,13 @@ __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ r
   __shared__ unsigned long long s_best;
   const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int no = st->n_order;
-  const int L = no < core_max ? no : core_max;
+  // the prefix is also capped at max(kCoreFloor, n_order / core_div): each
+  // core vertex costs the one cluster ~6 ns, which only the chain's top
+  // repays (R-MAT 20, 0.55 M ordered vertices: 65 535 core vertices 1.73 ms
+  // per step, 32 768 1.71, 16 384 1.59, 8 192 1.65; R-MAT 24 and Chung-Lu,
+  // 8 M ordered vertices, keep 65 535)
+  const int capn = core_div > 0 ? max(kCoreFloor, no / core_div) : core_max;
+  const int L = min(no, min(core_max, capn));
   const int cw = ((L + nw - 1) / nw + 31) & ~31;
   const int wb = min(L, warp * cw), we = min(L, wb + cw);
   if (threadIdx.x == 0) s_best = 0;
@@ -2097,7 +2105,8 @@ int jp_color_run(Ctx& c, int32_t* color) {
       PGC_LAUNCH(c, kGCore, "k_core_select",
                  k_core_select<<<1, 1024, 0, c.st>>>(c.rec, c.state,
                                                       c.tune.core_max, c.tune.core_min_avg,
-                                                      c.tune.core_arc_cap, c.tune.core_tier2));
+                                                      c.tune.core_arc_cap, c.tune.core_tier2,
+                                                      c.tune.core_div));
       if (int e = sync_state(c)) return e;
       const int NC = c.h_state->core_n1;
       NC2 = c.h_state->core_n - NC;

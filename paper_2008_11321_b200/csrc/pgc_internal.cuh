@@ -121,6 +121,7 @@ struct Tuning {
   int jp_light_sleep_max = 8192;  // ns, same for light warps
   int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
   int core_max = 65535;           // JP core: max vertices (0 disables the core engine)
+  int core_div = 32;              // JP core: at most max(16 384, n_order / core_div) vertices (0 = no such cap)
   int core_min_avg = 32;          // JP core: min mean |pred| over the prefix
   int core_min_n = 256;           // JP core: smaller cores are left to the bulk kernel
   int core_ctas = 0;              // JP core: cluster size (0 = from core_arcs_per_cta)
