@@ -919,6 +919,10 @@ __global__ void k_adg_finalize(int l, int rule, uint32_t num, uint32_t den, Stat
     per_round[3 * (l - 1) + 1] = (long long)st->S;
     per_round[3 * (l - 1) + 2] = nR;
   }
+  {  // the mean degree of G[U_l]: S_l = 2 |E[U_l]| (Q3); its maximum sizes the JP core
+    const long long a = (long long)(st->S / (unsigned long long)(st->nU > 0 ? st->nU : 1));
+    if (a > st->avg_max) st->avg_max = a;
+  }
   st->sum_active += st->nU;
   st->cross += st->cut;
   if (l - 1 < cap) ord_cnt[l - 1] = st->nOrdR;

@@ -630,6 +630,7 @@ int pgc_set_tuning(const char* key, int64_t value) {
       {"core_max", 0, 65535, nullptr, &g_tune.core_max},
       {"core_min_avg", 0, 1 << 30, nullptr, &g_tune.core_min_avg},
       {"core_div", 0, 1 << 30, nullptr, &g_tune.core_div},
+      {"core_dmul", 0, 1 << 20, nullptr, &g_tune.core_dmul},
       {"core_min_n", 1, 65535, nullptr, &g_tune.core_min_n},
       {"core_ctas", 0, 16, nullptr, &g_tune.core_ctas},
       {"core_spin_ns", 0, 100000, nullptr, &g_tune.core_spin_ns},

@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ r
                                                       State* st,
                                                       int core_max, int min_avg,
                                                       long long arc_cap, int tier2_max,
-                                                      int core_div) {
+                                                      int core_div, int core_dmul) {
   // warp w scans the contiguous chunk [wb, we) of the prefix, lanes reading
   // consecutive records, kCsU strips in flight: pass 1 sums the chunk, a
   // block scan of the warp sums gives each chunk's base, pass 2 evaluates
@@ -701,7 +701,13 @@ __global__ void __launch_bounds__(1024) k_core_select(const int4* __restrict__ r
   // repays (R-MAT 20, 0.55 M ordered vertices: 65 535 core vertices 1.73 ms
   // per step, 32 768 1.71, 16 384 1.59, 8 192 1.65; R-MAT 24 and Chung-Lu,
   // 8 M ordered vertices, keep 65 535)
-  const int capn = core_div > 0 ? max(kCoreFloor, no / core_div) : core_max;
+  // ... and, after ADG, at core_dmul x the largest mean degree of a G[U_l]
+  // (ADG's peel is a 2-approximate densest-subgraph peel; that mean degree is
+  // within 2x of the degeneracy): the best core sizes measured were 16 K / 24-32 K
+  // / 49 K vertices at 808 / 1 603 / 2 287 (R-MAT 20 / Chung-Lu / R-MAT 24)
+  long long capl = core_div > 0 ? (long long)(no / core_div) : (long long)core_max;
+  if (core_dmul > 0 && st->avg_max > 0) capl = min(capl, (long long)core_dmul * st->avg_max);
+  const int capn = (int)max((long long)kCoreFloor, min(capl, (long long)core_max));
   const int L = min(no, min(core_max, capn));
   const int cw = ((L + nw - 1) / nw + 31) & ~31;
   const int wb = min(L, warp * cw), we = min(L, wb + cw);
@@ -2106,7 +2112,7 @@ int jp_color_run(Ctx& c, int32_t* color) {
                  k_core_select<<<1, 1024, 0, c.st>>>(c.rec, c.state,
                                                       c.tune.core_max, c.tune.core_min_avg,
                                                       c.tune.core_arc_cap, c.tune.core_tier2,
-                                                      c.tune.core_div));
+                                                      c.tune.core_div, c.tune.core_dmul));
       if (int e = sync_state(c)) return e;
       const int NC = c.h_state->core_n1;
       NC2 = c.h_state->core_n - NC;

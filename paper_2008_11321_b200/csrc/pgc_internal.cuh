@@ -49,6 +49,7 @@ struct State {
   // totals
   long long sum_active;        // sum_l |U_l|
   unsigned long long cross;    // X
+  long long avg_max;           // max over the rounds so far of floor(S_l / |U_l|): the densest U_l's mean degree
   // counters of the current round, reset by k_adg_finalize: the compaction
   // reservations of k_adg_select (one atomic per block step each)
   alignas(128) int nChunks;
@@ -121,6 +122,7 @@ struct Tuning {
   int jp_light_sleep_max = 8192;  // ns, same for light warps
   int jp_watchdog_ms = 20000;     // JP kernel reports a stall after this long
   int core_max = 65535;           // JP core: max vertices (0 disables the core engine)
+  int core_dmul = 20;             // JP core (after ADG): at most max(16 384, core_dmul * max_l mean degree of G[U_l]) vertices (0 = off)
   int core_div = 32;              // JP core: at most max(16 384, n_order / core_div) vertices (0 = no such cap)
   int core_min_avg = 32;          // JP core: min mean |pred| over the prefix
   int core_min_n = 256;           // JP core: smaller cores are left to the bulk kernel

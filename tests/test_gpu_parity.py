@@ -144,7 +144,7 @@ def tuning():
                 "heavy_degree": 128, "rounds_per_sync": 8, "jp_split_overlap": 1, "update_atom": 1, "fuse_init": 1, "top_list": 1,
                 "core_tier2": 0, "jp_mega_pred": 2048, "jp_mega_chunk": 512,
                 "itr_members_per_warp": 1, "jp_heavy_stripes": 1,
-                "filter_ratio": 4, "chunk_arcs": 1024, "core_div": 32}
+                "filter_ratio": 4, "chunk_arcs": 1024, "core_div": 32, "core_dmul": 20}
     for k in touched:
         pgc.set_tuning(k, defaults[k])
 
